@@ -1,0 +1,67 @@
+"""Exception types of the drop-in API.
+
+Same names, hierarchy and meaning as the reference's
+``pkg/src/leorzf/errors.py:8-54``, so callers that catch
+``leorzf.errors.X`` can catch ``paper_2512_16543_b200.errors.X`` instead.
+
+Device kernels never raise: they write a per-item status code into an
+``int32 info[B]`` array (see ``include/leorzf_b200.h``) and the Python
+layer maps the codes below onto these exceptions for single-item calls.
+"""
+
+
+class ConfigError(Exception):
+    """Invalid scenario configuration (reference errors.py:8)."""
+
+
+class ParseError(ConfigError):
+    """Config text could not be parsed (reference errors.py:12)."""
+
+
+class UnknownKeyError(ConfigError):
+    """Unknown configuration key (reference errors.py:16)."""
+
+
+class RangeError(ConfigError):
+    """Configuration value out of range (reference errors.py:20)."""
+
+
+class SimulationError(Exception):
+    """Numerical failure while running the precoder update (errors.py:24)."""
+
+
+class DimensionMismatchError(SimulationError):
+    """Operands have incompatible shapes (errors.py:28)."""
+
+
+class SingularMatrixError(SimulationError):
+    """Condition estimate above 1e14 or non-finite (errors.py:32)."""
+
+
+class SingularAuxiliaryError(SimulationError):
+    """Woodbury r x r auxiliary matrix condition above 1e12 (errors.py:36)."""
+
+
+class UnsupportedGeometryError(SimulationError):
+    """Array geometry outside what an operation supports (errors.py:41)."""
+
+
+class ZeroPrecoderError(SimulationError):
+    """Precoder has zero Frobenius norm (errors.py:49)."""
+
+
+class EmptyInputError(SimulationError):
+    """Operation requires a non-empty input (errors.py:53)."""
+
+
+class NativeLibraryError(RuntimeError):
+    """The sm_100a library is missing, was built for another target, or a
+    launch failed. There is deliberately no CPU fallback."""
+
+
+# Per-item status codes written by the kernels (include/leorzf_b200.h).
+INFO_OK = 0
+INFO_SINGULAR = 1            # not PD / cond > 1e14 / non-finite  -> SingularMatrixError
+INFO_SINGULAR_AUX = 2        # cond(aux) > 1e12                    -> SingularAuxiliaryError
+INFO_ZERO_PRECODER = 3       # ||F_RF F_raw||_F == 0              -> ZeroPrecoderError
+INFO_INDEFINITE = 4          # Hermitian, not PD, inverted by the pivoted path (not an error)

@@ -1,0 +1,114 @@
+"""Host-side Gaussian sketch streams (Omega) for the device arSVD.
+
+The reference draws each sketch inside ``arsvd`` from the caller's
+``np.random.Generator`` as sqrt(1/2) * (N(K x d) + j N(K x d)), real block
+first, both row-major (``lowrank.py:284-286``), and the harness shares one
+Generator per (method, trial) across all time steps (``harness.py:206-211,
+236-237``).  Because ``Generator.standard_normal`` is chunking-invariant
+(the n-th normal does not depend on how the draws were batched), one flat
+float64 normal stream per trial plus a device-side cursor reproduces the
+reference's Omega bit for bit: an arSVD iteration of width d starting at
+cursor c reads the real block at [c, c + K d) and the imaginary block at
+[c + K d, c + 2 K d), then advances the cursor by 2 K d.
+
+Consumption is data dependent (it depends on the number of arSVD
+iterations), so each trial keeps a FIFO: normals are generated ahead in
+chunks, the device reports the cursor it reached, and consumed normals
+are dropped.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+from .scenario import method_label, stream_seed
+
+
+def sketch_widths(K: int, k_init: int, p: int, i_max: int) -> list[int]:
+    """Widths d_i = min(k0_i + p, K), k0_i = k_init * 2^i (lowrank.py:279-302)."""
+    out, k0 = [], k_init
+    for _ in range(i_max):
+        out.append(min(k0 + p, K))
+        k0 *= 2
+    return out
+
+
+def normals_per_call_max(K: int, k_init: int, p: int, i_max: int) -> int:
+    """Upper bound on normals one arsvd call consumes (all i_max iterations)."""
+    return sum(2 * K * d for d in sketch_widths(K, k_init, p, i_max))
+
+
+def consumed_by(iters: np.ndarray, K: int, k_init: int, p: int, i_max: int) -> np.ndarray:
+    """Normals consumed by a call that ran ``iters`` iterations (0 = none)."""
+    cum = np.concatenate([[0], np.cumsum([2 * K * d for d in
+                                          sketch_widths(K, k_init, p, i_max)])])
+    return cum[np.asarray(iters, dtype=np.int64)]
+
+
+class OmegaStreams:
+    """One sequential standard-normal stream per trial.
+
+    ``window(n)`` returns a (B, n) float64 array whose row b starts at that
+    trial's first unconsumed normal; ``advance(consumed)`` drops the
+    normals a device pass consumed.  The same object drives the oracle
+    (``oracle/``) and the GPU path, so both see identical sketches.
+    """
+
+    def __init__(self, generators):
+        self._gens = list(generators)
+        self._buf = [np.empty(0) for _ in self._gens]
+        self.consumed_total = np.zeros(len(self._gens), dtype=np.int64)
+
+    @classmethod
+    def for_method(cls, master_seed: int, eta: float, trials) -> "OmegaStreams":
+        """Streams keyed exactly like the reference harness's per-(method,
+        trial) sketch Generator (harness.py:88-92,206-211)."""
+        label = method_label(eta)
+        return cls(np.random.default_rng(stream_seed(master_seed, label, t)) for t in trials)
+
+    @property
+    def B(self) -> int:
+        return len(self._gens)
+
+    def _fill(self, b: int, n: int) -> None:
+        have = self._buf[b].size
+        if have < n:
+            extra = self._gens[b].standard_normal(max(n - have, 1 << 12))
+            self._buf[b] = np.concatenate([self._buf[b], extra])
+
+    def window(self, n: int, out: np.ndarray | None = None) -> np.ndarray:
+        """(B, n) block of the next n unconsumed normals of every trial."""
+        if out is None:
+            out = np.empty((self.B, n), dtype=np.float64)
+        for b in range(self.B):
+            self._fill(b, n)
+            out[b] = self._buf[b][:n]
+        return out
+
+    def advance(self, consumed) -> None:
+        consumed = np.broadcast_to(np.asarray(consumed, dtype=np.int64), (self.B,))
+        for b in range(self.B):
+            c = int(consumed[b])
+            self._fill(b, c)
+            self._buf[b] = self._buf[b][c:]
+        self.consumed_total += consumed
+
+
+class GeneratorBudget:
+    """Adapter for the single-call API, which receives a bare
+    ``np.random.Generator`` like the reference's ``arsvd(dA, cfg, rng)``.
+
+    Draws a worst-case block from a snapshot of the generator state, and
+    after the device reports how many normals it used, rewinds and redraws
+    exactly that many so the caller's generator ends in the same state as
+    after the reference call."""
+
+    def __init__(self, rng: np.random.Generator, n_max: int):
+        self.rng = rng
+        self._state = rng.bit_generator.state
+        self.block = rng.standard_normal(n_max)
+
+    def commit(self, consumed: int) -> None:
+        self.rng.bit_generator.state = self._state
+        if consumed:
+            self.rng.standard_normal(int(consumed))
