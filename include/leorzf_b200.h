@@ -1,0 +1,186 @@
+/*
+ * leorzf_b200 -- C ABI of the B200-native (sm_100a) RZF precoder update.
+ *
+ * Drop-in boundary for the numerical core of the reference package
+ * leorzf 0.1.0 (pkg/src/leorzf/__init__.py:17-31).  The reference is pure
+ * Python; its public functions are re-exposed by the Python package
+ * paper_2512_16543_b200 (same names/signatures/exceptions) which calls the
+ * entry points below through ctypes.  Foreign callers can bind them the
+ * same way.
+ *
+ * Conventions
+ *  - All pointers are DEVICE pointers (caller-allocated, e.g. torch tensors)
+ *    unless stated; `stream` is a cudaStream_t (NULL = legacy default).
+ *  - Complex data is interleaved (re, im); dtype LRZ_C64 = float2,
+ *    LRZ_C128 = double2.  Matrices are row-major like numpy unless stated;
+ *    low-rank factors U, V are stored column-major per item ([D][K]: column
+ *    j contiguous) with D = d_max columns reserved.
+ *  - Batched calls take an item count and an element stride per item.
+ *  - Return value: LRZ_OK, or < 0 (bad argument / launch error; message in
+ *    lrz_last_error()).  Per-item numerical outcomes go to `info[item]`
+ *    (LRZ_INFO_*), which the Python layer maps to the reference exceptions
+ *    (pkg/src/leorzf/errors.py:28-50).
+ *  - No host synchronisation inside calls except lrz_traj_* (see below), no
+ *    allocation, deterministic (fixed reduction orders, no atomics on
+ *    values).
+ */
+#ifndef LEORZF_B200_H
+#define LEORZF_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define LRZ_C64 0
+#define LRZ_C128 1
+
+#define LRZ_OK 0
+#define LRZ_EINVAL (-1)
+#define LRZ_ELAUNCH (-2)
+#define LRZ_EDEVICE (-3)
+
+#define LRZ_INFO_OK 0
+#define LRZ_INFO_SINGULAR 1          /* SingularMatrixError      lowrank.py:136-137 */
+#define LRZ_INFO_SINGULAR_AUX 2      /* SingularAuxiliaryError   lowrank.py:213-216 */
+#define LRZ_INFO_ZERO_PRECODER 3     /* ZeroPrecoderError        precoding.py:49-50 */
+#define LRZ_INFO_INDEFINITE 4        /* not PD: pivoted path used (lowrank.py:142-144) */
+
+/* method codes, same as harness._DECISION_CODES (harness.py:29) */
+#define LRZ_METHOD_FULL 0
+#define LRZ_METHOD_WOODBURY 1
+#define LRZ_METHOD_NONE 2
+
+int lrz_version(void);
+const char *lrz_last_error(void);
+/* 0 if `device` is a compute-capability 10.0 part this library was built for. */
+int lrz_device_check(int device);
+
+/* K1  Gram + regularisation: A[i] = 0.5 (H H^H + (H H^H)^H) + alpha I.
+ *     Replaces lowrank.py:160-162 (and :365-366).  H: [B][K][N] dtype,
+ *     A: [B][K][K] complex128 (always: the reference promotes via alpha I). */
+int lrz_gram(int dtype, int64_t B, int K, int N, const void *H, int64_t h_stride,
+             double alpha, void *A, int64_t a_stride, void *stream);
+
+/* K1' Gram correction (lowrank.py:167-179):
+ *     dA = H dH^H + dH H^H + dH dH^H  computed as X dH^H + dH X^H,
+ *     X = H + dH/2.  mode 0: P = H, Q = dH.  mode 1: P = H_prev, Q = H_cur
+ *     (dH = Q - P formed on the fly, exactly harness.py:235).
+ *     dA: [B][K][K] complex128, exactly Hermitian. */
+int lrz_gram_delta(int dtype, int64_t B, int K, int N, const void *P, int64_t p_stride,
+                   const void *Q, int64_t q_stride, int mode, void *dA, int64_t a_stride,
+                   void *stream);
+
+/* K5  Hermitian inverse with the reference's condition guard
+ *     (lowrank.py:127-144): Gauss-Jordan without pivoting while PD, pivoted
+ *     otherwise; info = SINGULAR when cond_2 > cond_limit or non-finite.
+ *     A, A_inv: complex128 [B][K][K].  item_mask (nullable): skip items with 0.
+ *     workspace: lrz_workspace_bytes(LRZ_WS_INVERSE, ...) bytes. */
+int lrz_herm_inverse(int64_t B, int K, const void *A, int64_t a_stride, void *A_inv,
+                     int64_t ai_stride, int32_t *info, double cond_limit,
+                     const uint8_t *item_mask, void *workspace, void *stream);
+
+/* K2+K3 adaptive randomised SVD (lowrank.py:243-316, Alg. 1).
+ *   item i reads dA[i] (complex128 K x K), sketch normals
+ *   omega + omega_row[i] * omega_stride starting at cursor[i] (the real block
+ *   of width d then the imaginary block, lowrank.py:284-286).
+ *   Writes U, V ([D][K] column-major, complex128), S (D, descending),
+ *   k_est, iters (sketch iterations run), fallback (1 = iteration-cap
+ *   tail), consumed (normals used).  omega_row / item_mask nullable. */
+typedef struct {
+  double eta;
+  int k_init, p, i_max;
+  int d_max;               /* >= min(k_init * 2^(i_max-1) + p, K) */
+} lrz_arsvd_cfg;
+
+int lrz_arsvd(int64_t B, int K, const void *dA, int64_t a_stride, const double *omega,
+              int64_t omega_stride, const int32_t *omega_row, const int64_t *cursor,
+              const lrz_arsvd_cfg *cfg, void *U, void *V, double *S, int32_t *k_est,
+              int32_t *iters, int32_t *fallback, int64_t *consumed,
+              const uint8_t *item_mask, void *workspace, void *stream);
+
+/* K4  Woodbury update (lowrank.py:182-227):
+ *     A_inv_out = A_inv - (A_inv U aux^-1)(V^H A_inv), aux = S^-1 + V^H A_inv U,
+ *     A_out = A + U S V^H (skipped when A/A_out are NULL).
+ *     info = SINGULAR_AUX (outputs untouched) when cond_2(aux) > 1e12.
+ *     r[i] <= d_max <= 256. */
+int lrz_woodbury(int64_t B, int K, int d_max, const void *A, const void *A_inv,
+                 int64_t a_stride, const void *U, const void *V, const double *S,
+                 const int32_t *r, void *A_out, void *A_inv_out, int32_t *info,
+                 void *workspace, void *stream);
+
+/* Chain step of the batched runner (harness.py:228-241 per trial): walks the
+ * T steps of each trial in order.  plan[b][t]: 0 = full (A_inv_seq[b][t]
+ * already holds inv(G[b][t])), 1 = Woodbury candidate (factor in U/V/S/r),
+ * 2 = none.  A_inv_seq[b][t] <- state after step t; A_state updated in
+ * place when non-NULL.  On SingularAuxiliary the step falls back to
+ * inv(G[b][t]) (lowrank.py:353-367).  method/info per (b,t). */
+int lrz_chain(int64_t B, int T, int K, int d_max, const uint8_t *plan, const void *G,
+              const void *A_inv_prev, void *A_inv_seq, void *A_state, const void *U,
+              const void *V, const double *S, const int32_t *r, uint8_t *method,
+              int32_t *info, void *workspace, void *stream);
+
+/* Dispatcher decision (lowrank.py:345-359) for n steps: plan = 2 (none,
+ * k_est == 0), 1 (Woodbury, k_est/K <= 0.5), 0 (full); is_sketch == 0 -> 0. */
+int lrz_plan(int64_t n, int K, const uint8_t *is_sketch, const int32_t *k_est, uint8_t *plan,
+             void *stream);
+
+/* K6  fully-digital precoder + rate (precoding.py:37-80 with F_RF = I):
+ *     W = H^H A_inv (N x K, dtype of H, UNSCALED), scale = sqrt(P_t)/||W||_F,
+ *     G = scale * H W, SINR_n = |G_nn|^2 / (sum_{i != n}|G_ni|^2 + noise_n),
+ *     rates = log2(1 + SINR), sum.  noise row = item / noise_div.
+ *     W may be NULL (then kept in workspace).  info = ZERO_PRECODER if ||W||=0. */
+int lrz_precode_rate(int dtype, int64_t B, int K, int N, const void *H, int64_t h_stride,
+                     const void *A_inv, int64_t ai_stride, double P_t, const double *noise,
+                     int64_t noise_div, void *W, int64_t w_stride, double *scale,
+                     double *rates, double *sinr, double *sum_rate, int32_t *info,
+                     void *workspace, void *stream);
+
+/* Batched complex GEMM C[i] = op(A[i]) op(B[i]) (op: 0 = N, 1 = T, 2 = C^H),
+ * all operands of `dtype`, row-major with leading dims.  Used by the
+ * single-call precoder/rate with an explicit F_RF (precoding.py:47-48,74). */
+int lrz_cgemm(int dtype, int64_t batch, int M, int N, int Kd, int opA, const void *A,
+              int64_t lda, int64_t sA, int opB, const void *Bm, int64_t ldb, int64_t sB,
+              void *C, int64_t ldc, int64_t sC, void *stream);
+
+/* Z = a X + b Y elementwise over n complex elements (Y nullable); used for
+ * F_BB = scale * F_raw (precoding.py:51) and H_new = H + dH (lowrank.py:364). */
+int lrz_axpby(int dtype, int64_t n, double a, const void *X, double b, const void *Y, void *Z,
+              void *stream);
+
+/* ||X[i]||_F^2 in fp64 for `n` complex elements per item. */
+int lrz_fro2(int dtype, int64_t batch, int64_t n, const void *X, int64_t sX, double *out,
+             void *stream);
+
+/* SINR / rate from a K x K coupling matrix G (dtype), scaled by scale[i]
+ * (nullable = 1): precoding.py:74-80. */
+int lrz_sinr_rate(int dtype, int64_t batch, int K, const void *G, int64_t sG,
+                  const double *scale, const double *noise, int64_t noise_div, double *rates,
+                  double *sinr, double *sum_rate, void *stream);
+
+/* Workspace sizing for the calls that take one. */
+#define LRZ_WS_INVERSE 0
+#define LRZ_WS_ARSVD 1
+#define LRZ_WS_WOODBURY 2
+#define LRZ_WS_CHAIN 3
+#define LRZ_WS_PRECODE 4
+size_t lrz_workspace_bytes(int op, int dtype, int64_t B, int K, int N, int d_max);
+
+/* Speculative sketch-cursor resolution for the batched runner: one thread
+ * per trial walks its T steps, accepts every step whose observed iteration
+ * count matches the prediction, and re-predicts the suffix after the first
+ * mismatch.  Adds, to
+ * *pending (device int32), the number of trials with unverified steps.
+ * iters_act == NULL: initialise cursors/active from iters_pred only. */
+int lrz_spec_verify(int64_t B, int T, int K, const lrz_arsvd_cfg *cfg,
+                    const uint8_t *is_sketch, int32_t *iters_pred,
+                    const int32_t *iters_act, int64_t *cursor, const int64_t *cursor0,
+                    int32_t *first_unverified, uint8_t *active, int32_t *pending,
+                    void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LEORZF_B200_H */

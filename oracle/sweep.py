@@ -44,9 +44,11 @@ def _margin(f: port.Factor) -> float:
 
 
 def sweep_trial(H_seq, alpha, noise, P_t, cfg: port.Cfg | None, sketch,
-                n_reset: int = 1200, keep_state: bool = False) -> SweepRecord:
+                n_reset: int = 1200, keep_state: bool = False, F_RF=None) -> SweepRecord:
     """Run one method (cfg None = conventional) over one trial's channels
-    H_seq (T, K, N).  ``sketch`` is that trial's Generator or FlatNormals."""
+    H_seq (T, K, N).  ``sketch`` is that trial's Generator or FlatNormals.
+    F_RF None is the identity-elided fully digital form; pass np.eye(N) for
+    the reference's verbatim F_RF = I_N products."""
     T, K, _ = H_seq.shape
     rec = SweepRecord(np.zeros(T), np.zeros((T, K)), np.zeros(T, np.uint8),
                       np.zeros(T, np.int64), np.zeros(T), np.zeros(T, np.int64),
@@ -62,8 +64,8 @@ def sweep_trial(H_seq, alpha, noise, P_t, cfg: port.Cfg | None, sketch,
             st, method, k, cost, f = port.update_inverse(st, prev, H - prev, cfg, sketch)
             rec.iters[i], rec.consumed[i] = f.iters, f.consumed
             rec.fallback[i], rec.margin[i] = f.used_fallback, _margin(f)
-        F_BB, _ = port.rzf_precoder(H, st.A_inv, None, P_t)
-        rates, total, _ = port.sum_rate(H, None, F_BB, noise)
+        F_BB, _ = port.rzf_precoder(H, st.A_inv, F_RF, P_t)
+        rates, total, _ = port.sum_rate(H, F_RF, F_BB, noise)
         rec.rates[i], rec.per_ut[i] = total, rates
         rec.method[i], rec.k_est[i], rec.cost[i] = DECISION[method], k, cost
         if keep_state:

@@ -1,0 +1,62 @@
+// C-ABI plumbing: error reporting, device check, workspace sizing.
+#include <stdarg.h>
+#include <stdio.h>
+
+#include "common.cuh"
+
+static thread_local char g_err[512] = "";
+
+void lrz_set_error(const char *fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+}
+
+int lrz_launch_status(const char *what) {
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    lrz_set_error("%s: launch failed: %s", what, cudaGetErrorString(e));
+    return LRZ_ELAUNCH;
+  }
+  return LRZ_OK;
+}
+
+size_t lrz_arsvd_ws(int64_t B, int K, int D);
+size_t lrz_precode_ws(int dtype, int64_t B, int K, int N);
+size_t lrz_wb_ws(int64_t B, int K, int D);
+
+extern "C" int lrz_version(void) { return 1; }
+
+extern "C" const char *lrz_last_error(void) { return g_err; }
+
+extern "C" int lrz_device_check(int device) {
+  cudaDeviceProp p;
+  const cudaError_t e = cudaGetDeviceProperties(&p, device);
+  if (e != cudaSuccess) {
+    lrz_set_error("cudaGetDeviceProperties: %s", cudaGetErrorString(e));
+    return LRZ_EDEVICE;
+  }
+  if (p.major != 10 || p.minor != 0) {
+    lrz_set_error("device %d is sm_%d%d; this library is built for sm_100a only", device,
+                  p.major, p.minor);
+    return LRZ_EDEVICE;
+  }
+  return LRZ_OK;
+}
+
+extern "C" size_t lrz_workspace_bytes(int op, int dtype, int64_t B, int K, int N, int d_max) {
+  switch (op) {
+    case LRZ_WS_INVERSE:
+      return 0;
+    case LRZ_WS_ARSVD:
+      return lrz_arsvd_ws(B, K, d_max);
+    case LRZ_WS_WOODBURY:
+    case LRZ_WS_CHAIN:
+      return lrz_wb_ws(B, K, d_max);
+    case LRZ_WS_PRECODE:
+      return lrz_precode_ws(dtype, B, K, N);
+    default:
+      return 0;
+  }
+}

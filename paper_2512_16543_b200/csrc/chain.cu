@@ -1,0 +1,316 @@
+// K5 batched Hermitian inverse, K4 Woodbury update, the per-trial chain of
+// the batched runner, and the speculative sketch-cursor verifier.
+
+#include "linalg.cuh"
+
+namespace lrz {
+
+constexpr int INV_THREADS = 256;
+constexpr int INV_SMEM_KMAX = 64;   // K <= 64: factorise in shared memory
+
+struct InvSmem {
+  // layout inside dynamic shared memory
+  __host__ __device__ static size_t bytes(int K, int rmax, bool matrix) {
+    const int n = K > rmax ? K : rmax;
+    size_t b = 4 * size_t(n) * sizeof(c128) + size_t(n) * sizeof(int) +
+               (INV_THREADS / 32) * (sizeof(double) * 2 + sizeof(int));
+    b = (b + 15) & ~size_t(15);
+    if (matrix) b += size_t(K) * K * sizeof(c128);
+    return b;
+  }
+};
+
+LRZ_DEV InvScratch carve_inv(char *sm, int n, c128 **matrix, int K, bool want_matrix) {
+  InvScratch s;
+  s.colbuf = (c128 *)sm;
+  s.rowbuf = s.colbuf + n;
+  s.v = s.rowbuf + n;
+  s.w = s.v + n;
+  s.red = (double *)(s.w + n);
+  s.ired = (int *)(s.red + 2 * (INV_THREADS / 32));
+  s.perm = s.ired + (INV_THREADS / 32);
+  size_t off = size_t((char *)(s.perm + n) - sm);
+  off = (off + 15) & ~size_t(15);
+  *matrix = want_matrix ? (c128 *)(sm + off) : nullptr;
+  return s;
+}
+
+constexpr int WB_SMEM_DMAX = 40;  // aux / aux^-1 in shared memory up to this rank
+
+__host__ __device__ inline int64_t wb_ws_elems(int K, int D) {
+  return 3 * int64_t(K) * D + (D > WB_SMEM_DMAX ? 2 * int64_t(D) * D : 0);
+}
+__host__ __device__ inline size_t wb_aux_smem(int D) {
+  return D > WB_SMEM_DMAX ? 0 : 2 * size_t(D) * D * sizeof(c128);
+}
+LRZ_DEV void carve_wb(WbScratch &sc, char *aux_smem, c128 *w, int K, int D) {
+  sc.AiU = w;
+  sc.T = w + int64_t(K) * D;
+  sc.VhAi = w + 2 * int64_t(K) * D;
+  sc.aux = D > WB_SMEM_DMAX ? w + 3 * int64_t(K) * D : (c128 *)aux_smem;
+  sc.auxinv = sc.aux + D * D;
+}
+
+__global__ void __launch_bounds__(INV_THREADS)
+    herm_inverse_kernel(int K, const c128 *A, int64_t as, c128 *Ainv, int64_t ais,
+                        int32_t *info, double limit, const uint8_t *mask) {
+  extern __shared__ __align__(16) char smem[];
+  const int64_t item = blockIdx.x;
+  if (mask && !mask[item]) return;
+  c128 *M;
+  const InvScratch sc = carve_inv(smem, K, &M, K, K <= INV_SMEM_KMAX);
+  const int st = cta_herm_inverse(A + item * as, Ainv + item * ais, K, M, limit, sc);
+  if (threadIdx.x == 0 && info) info[item] = st;
+}
+
+// Batched Woodbury (single step per item).
+__global__ void __launch_bounds__(INV_THREADS)
+    woodbury_kernel(int K, int D, const c128 *A, const c128 *Ainv, int64_t as, const c128 *U,
+                    const c128 *V, const double *S, const int32_t *r, c128 *A_out,
+                    c128 *Ainv_out, int32_t *info, c128 *ws) {
+  extern __shared__ __align__(16) char smem[];
+  const int64_t item = blockIdx.x;
+  const int rr = r[item];
+  WbScratch sc;
+  c128 *unused;
+  sc.inv = carve_inv(smem, D, &unused, D, false);
+  c128 *w = ws + item * wb_ws_elems(K, D);
+  carve_wb(sc, smem + InvSmem::bytes(D, D, false), w, K, D);
+  if (rr < 1 || rr > D) {
+    if (threadIdx.x == 0) info[item] = LRZ_INFO_SINGULAR_AUX;
+    return;
+  }
+  const int st = cta_woodbury(K, rr, Ainv + item * as, Ainv_out + item * as,
+                              A ? A + item * as : nullptr, A_out ? A_out + item * as : nullptr,
+                              U + item * int64_t(D) * K, V + item * int64_t(D) * K,
+                              S + item * D, sc);
+  if (threadIdx.x == 0) info[item] = st;
+}
+
+// Per-trial chain over T steps (harness.py:228-241 semantics):
+//   plan 0 (full):     A_inv_seq[t] already holds inv(G_t); A_state = G_t
+//   plan 1 (Woodbury): A_inv_seq[t] = woodbury(A_inv_seq[t-1]); on SingularAux
+//                      fall back to inv(G_t) (lowrank.py:353-367)
+//   plan 2 (none):     A_inv_seq[t] = A_inv_seq[t-1] (lowrank.py:345-351)
+__global__ void __launch_bounds__(INV_THREADS)
+    chain_kernel(int T, int K, int D, const uint8_t *plan, const c128 *G, const c128 *Ainv_prev,
+                 c128 *Ainv_seq, c128 *A_state, const c128 *U, const c128 *V, const double *S,
+                 const int32_t *r, uint8_t *method, int32_t *info, c128 *ws) {
+  extern __shared__ __align__(16) char smem[];
+  const int64_t b = blockIdx.x;
+  const int64_t KK = int64_t(K) * K;
+  const int n = K > D ? K : D;
+  c128 *M;
+  WbScratch sc;
+  sc.inv = carve_inv(smem, n, &M, K, K <= INV_SMEM_KMAX);
+  c128 *w = ws + b * wb_ws_elems(K, D);
+  carve_wb(sc, smem + InvSmem::bytes(K, D, K <= INV_SMEM_KMAX), w, K, D);
+  c128 *Ast = A_state ? A_state + b * KK : nullptr;
+  for (int t = 0; t < T; ++t) {
+    const int64_t bt = b * T + t;
+    const int pl = plan[bt];
+    c128 *out = Ainv_seq + bt * KK;
+    const c128 *prev = (t == 0) ? Ainv_prev + b * KK : out - KK;
+    int m = LRZ_METHOD_FULL, st = LRZ_INFO_OK;
+    if (pl == 1) {
+      st = cta_woodbury(K, r[bt], prev, out, Ast, Ast, U + bt * int64_t(D) * K,
+                        V + bt * int64_t(D) * K, S + bt * D, sc);
+      if (st == LRZ_INFO_OK) {
+        m = LRZ_METHOD_WOODBURY;
+      } else {
+        // full branch: invert the true Gram of the new channel
+        st = cta_herm_inverse(G + bt * KK, out, K, M, 1e14, sc.inv);
+        if (Ast)
+          for (int64_t e = threadIdx.x; e < KK; e += blockDim.x) Ast[e] = G[bt * KK + e];
+        m = LRZ_METHOD_FULL;
+      }
+    } else if (pl == 2) {
+      for (int64_t e = threadIdx.x; e < KK; e += blockDim.x) out[e] = prev[e];
+      m = LRZ_METHOD_NONE;
+    } else {
+      if (Ast)
+        for (int64_t e = threadIdx.x; e < KK; e += blockDim.x) Ast[e] = G[bt * KK + e];
+      st = info ? info[bt] : LRZ_INFO_OK;  // written by the batched inverse
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      method[bt] = uint8_t(m);
+      if (info) info[bt] = st;
+    }
+  }
+}
+
+// Speculative cursor verification: one thread per trial.
+//   is_sketch[b][t]: step runs arsvd.  iters_pred: iterations assumed when the
+//   cursor of every later step was computed; iters_act: what the last pass saw.
+struct ConsumedTab {
+  int64_t v[33];
+};
+
+__global__ void spec_verify_kernel(int64_t B, int T, int K, ConsumedTab consumed_tab,
+                                   const uint8_t *is_sketch, int32_t *iters_pred,
+                                   const int32_t *iters_act, int64_t *cursor,
+                                   const int64_t *cursor0, int32_t *first_unverified,
+                                   uint8_t *active, int32_t *pending) {
+  const int64_t b = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (b >= B) return;
+  int t = first_unverified[b];
+  const int64_t base = b * T;
+  // accept the verified prefix (init mode, iters_act == NULL: nothing to accept)
+  while (iters_act && t < T) {
+    const int64_t bt = base + t;
+    if (!is_sketch[bt]) {
+      ++t;
+      continue;
+    }
+    const int pa = iters_act[bt];
+    if (pa == iters_pred[bt]) {
+      ++t;
+      continue;
+    }
+    iters_pred[bt] = pa;  // cursor was right -> result right; consumption differs
+    ++t;
+    break;
+  }
+  // skip trailing non-sketch steps
+  while (t < T && !is_sketch[base + t]) ++t;
+  first_unverified[b] = t;
+  // re-predict the unverified suffix from the last observation and recompute cursors
+  int64_t c = cursor0[b];
+  for (int s = 0; s < T; ++s) {
+    const int64_t bt = base + s;
+    if (iters_act && s >= t && is_sketch[bt]) iters_pred[bt] = iters_act[bt];
+    cursor[bt] = c;
+    active[bt] = (s >= t && is_sketch[bt]) ? 1 : 0;
+    if (is_sketch[bt]) c += consumed_tab.v[iters_pred[bt]];
+  }
+  if (t < T) atomicAdd(pending, 1);
+}
+
+// Dispatcher decision per step (lowrank.py:345-359): 2 = none (k_est == 0),
+// 1 = Woodbury candidate (k_est / K <= 0.5), 0 = full; non-sketch steps are
+// full (step 0 / n_reset, harness.py:229-233).
+__global__ void plan_kernel(int64_t n, int K, const uint8_t *is_sketch, const int32_t *k_est,
+                            uint8_t *plan) {
+  const int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (i >= n) return;
+  uint8_t pl = 0;
+  if (is_sketch[i]) {
+    const int k = k_est[i];
+    pl = (k == 0) ? 2 : ((double(k) / double(K) <= 0.5) ? 1 : 0);
+  }
+  plan[i] = pl;
+}
+
+}  // namespace lrz
+
+using namespace lrz;
+
+extern "C" int lrz_plan(int64_t n, int K, const uint8_t *is_sketch, const int32_t *k_est,
+                        uint8_t *plan, void *stream) {
+  if (n < 0 || K < 1 || !is_sketch || !k_est || !plan) {
+    lrz_set_error("lrz_plan: bad arguments");
+    return LRZ_EINVAL;
+  }
+  if (n == 0) return LRZ_OK;
+  plan_kernel<<<unsigned((n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(n, K, is_sketch,
+                                                                          k_est, plan);
+  return lrz_launch_status("lrz_plan");
+}
+
+size_t lrz_inverse_smem(int K) { return InvSmem::bytes(K, K, K <= INV_SMEM_KMAX); }
+size_t lrz_woodbury_smem(int D) { return InvSmem::bytes(D, D, false) + wb_aux_smem(D); }
+size_t lrz_chain_smem(int K, int D) {
+  return InvSmem::bytes(K, D, K <= INV_SMEM_KMAX) + wb_aux_smem(D);
+}
+size_t lrz_wb_ws(int64_t B, int K, int D) { return size_t(B) * wb_ws_elems(K, D) * sizeof(c128); }
+
+static int set_smem(const void *fn, size_t bytes) {
+  if (bytes > 48 * 1024) {
+    if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes)) !=
+        cudaSuccess) {
+      lrz_set_error("cudaFuncSetAttribute(%zu bytes) failed", bytes);
+      return LRZ_ELAUNCH;
+    }
+  }
+  return LRZ_OK;
+}
+
+extern "C" int lrz_herm_inverse(int64_t B, int K, const void *A, int64_t a_stride,
+                                void *A_inv, int64_t ai_stride, int32_t *info, double cond_limit,
+                                const uint8_t *item_mask, void *workspace, void *stream) {
+  (void)workspace;
+  if (B < 0 || K < 1 || K > 1024 || !A || !A_inv) {
+    lrz_set_error("lrz_herm_inverse: bad arguments");
+    return LRZ_EINVAL;
+  }
+  if (B == 0) return LRZ_OK;
+  const size_t sm = lrz_inverse_smem(K);
+  if (set_smem((const void *)herm_inverse_kernel, sm)) return LRZ_ELAUNCH;
+  herm_inverse_kernel<<<unsigned(B), INV_THREADS, sm, (cudaStream_t)stream>>>(
+      K, (const c128 *)A, a_stride, (c128 *)A_inv, ai_stride, info, cond_limit, item_mask);
+  return lrz_launch_status("lrz_herm_inverse");
+}
+
+extern "C" int lrz_woodbury(int64_t B, int K, int d_max, const void *A, const void *A_inv,
+                            int64_t a_stride, const void *U, const void *V, const double *S,
+                            const int32_t *r, void *A_out, void *A_inv_out, int32_t *info,
+                            void *workspace, void *stream) {
+  if (B < 0 || K < 1 || d_max < 1 || d_max > 256 || !A_inv || !U || !V || !S || !r ||
+      !A_inv_out || !info || !workspace || ((A == nullptr) != (A_out == nullptr))) {
+    lrz_set_error("lrz_woodbury: bad arguments");
+    return LRZ_EINVAL;
+  }
+  if (B == 0) return LRZ_OK;
+  const size_t sm = lrz_woodbury_smem(d_max);
+  if (set_smem((const void *)woodbury_kernel, sm)) return LRZ_ELAUNCH;
+  woodbury_kernel<<<unsigned(B), INV_THREADS, sm, (cudaStream_t)stream>>>(
+      K, d_max, (const c128 *)A, (const c128 *)A_inv, a_stride, (const c128 *)U,
+      (const c128 *)V, S, r, (c128 *)A_out, (c128 *)A_inv_out, info, (c128 *)workspace);
+  return lrz_launch_status("lrz_woodbury");
+}
+
+extern "C" int lrz_chain(int64_t B, int T, int K, int d_max, const uint8_t *plan, const void *G,
+                         const void *A_inv_prev, void *A_inv_seq, void *A_state, const void *U,
+                         const void *V, const double *S, const int32_t *r, uint8_t *method,
+                         int32_t *info, void *workspace, void *stream) {
+  if (B < 0 || T < 1 || K < 1 || d_max < 1 || d_max > 256 || !plan || !G || !A_inv_prev ||
+      !A_inv_seq || !U || !V || !S || !r || !method || !workspace) {
+    lrz_set_error("lrz_chain: bad arguments");
+    return LRZ_EINVAL;
+  }
+  if (B == 0) return LRZ_OK;
+  const size_t sm = lrz_chain_smem(K, d_max);
+  if (set_smem((const void *)chain_kernel, sm)) return LRZ_ELAUNCH;
+  chain_kernel<<<unsigned(B), INV_THREADS, sm, (cudaStream_t)stream>>>(
+      T, K, d_max, plan, (const c128 *)G, (const c128 *)A_inv_prev, (c128 *)A_inv_seq,
+      (c128 *)A_state, (const c128 *)U, (const c128 *)V, S, r, method, info,
+      (c128 *)workspace);
+  return lrz_launch_status("lrz_chain");
+}
+
+extern "C" int lrz_spec_verify(int64_t B, int T, int K, const lrz_arsvd_cfg *cfg,
+                               const uint8_t *is_sketch, int32_t *iters_pred,
+                               const int32_t *iters_act, int64_t *cursor, const int64_t *cursor0,
+                               int32_t *first_unverified, uint8_t *active, int32_t *pending,
+                               void *stream) {
+  if (B < 0 || T < 1 || K < 1 || !cfg || !is_sketch || !iters_pred || !cursor ||
+      !cursor0 || !first_unverified || !active || !pending || cfg->i_max > 30) {
+    lrz_set_error("lrz_spec_verify: bad arguments");
+    return LRZ_EINVAL;
+  }
+  if (B == 0) return LRZ_OK;
+  ConsumedTab tab;
+  tab.v[0] = 0;
+  long long k0 = cfg->k_init;
+  for (int i = 0; i < cfg->i_max; ++i) {
+    const int d = (int)std::min<long long>(k0 + cfg->p, K);
+    tab.v[i + 1] = tab.v[i] + 2LL * K * d;
+    k0 *= 2;
+  }
+  const unsigned nb = unsigned((B + 127) / 128);
+  spec_verify_kernel<<<nb, 128, 0, (cudaStream_t)stream>>>(B, T, K, tab, is_sketch, iters_pred,
+                                                           iters_act, cursor, cursor0,
+                                                           first_unverified, active, pending);
+  return lrz_launch_status("lrz_spec_verify");
+}

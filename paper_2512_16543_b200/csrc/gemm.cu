@@ -1,0 +1,548 @@
+// N-sized batched complex products: Gram (K1), Gram correction (K1'),
+// precoder / coupling GEMMs (K6) and a generic batched CGEMM.
+//
+// These are the HBM/FP-heavy kernels of the step (8K^2 N-class work).  Round-1
+// design: SIMT tiles of 32x32 outputs per CTA, operands staged through shared
+// memory in BK-wide slabs along the N (antenna) axis, fp32 FMA for complex64
+// inputs and fp64 FMA for complex128 inputs; one CTA per (item, tile) so a
+// B*T batch of small matrices fills all 148 SMs.
+
+#include "common.cuh"
+
+namespace lrz {
+
+constexpr int TM = 32;        // output tile edge
+constexpr int GEMM_THREADS = 128;
+
+// map a lower-triangle tile index to (I, J), I >= J
+LRZ_DEV void tri_tile(int t, int &I, int &J) {
+  int i = int((sqrtf(8.0f * t + 1.0f) - 1.0f) * 0.5f);
+  while ((i + 1) * (i + 2) / 2 <= t) ++i;
+  while (i * (i + 1) / 2 > t) --i;
+  I = i;
+  J = t - i * (i + 1) / 2;
+}
+
+// ---------------------------------------------------------------------------
+// K1: A = H H^H (Hermitian, lower tiles computed, mirrored) + alpha I
+// ---------------------------------------------------------------------------
+template <typename T, int BK>
+__global__ void __launch_bounds__(GEMM_THREADS)
+    gram_kernel(int K, int N, const cplx<T> *__restrict__ H, int64_t hs, double alpha,
+                c128 *__restrict__ A, int64_t as, int ntl) {
+  __shared__ cplx<T> As[BK][TM + 1];
+  __shared__ cplx<T> Bs[BK][TM + 1];
+  const int64_t item = blockIdx.x / ntl;
+  int I, J;
+  tri_tile(int(blockIdx.x % ntl), I, J);
+  const bool diag = (I == J);
+  const cplx<T> *h = H + item * hs;
+  const int tid = threadIdx.x, tx = tid & 7, ty = tid >> 3;
+  cplx<T> acc[2][4];
+#pragma unroll
+  for (int i = 0; i < 2; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j] = czero<T>();
+
+  for (int n0 = 0; n0 < N; n0 += BK) {
+    for (int e = tid; e < TM * BK; e += GEMM_THREADS) {
+      const int r = e / BK, k = e % BK, gk = n0 + k;
+      const int ri = I * TM + r, rj = J * TM + r;
+      As[k][r] = (ri < K && gk < N) ? h[int64_t(ri) * N + gk] : czero<T>();
+      if (!diag) Bs[k][r] = (rj < K && gk < N) ? h[int64_t(rj) * N + gk] : czero<T>();
+    }
+    __syncthreads();
+    const cplx<T>(*Bp)[TM + 1] = diag ? As : Bs;
+#pragma unroll 4
+    for (int k = 0; k < BK; ++k) {
+      cplx<T> a0 = As[k][ty], a1 = As[k][ty + 16];
+      cplx<T> b[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) b[j] = Bp[k][tx + 8 * j];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        cfma_cb(acc[0][j], a0, b[j]);
+        cfma_cb(acc[1][j], a1, b[j]);
+      }
+    }
+    __syncthreads();
+  }
+  c128 *a = A + item * as;
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    const int row = I * TM + ty + 16 * i;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int col = J * TM + tx + 8 * j;
+      if (row < K && col < K && row >= col) {
+        c128 v = ccast<double>(acc[i][j]);
+        if (row == col) {
+          v.im = 0.0;  // 0.5 (A + A^H) has an exactly real diagonal (lowrank.py:161)
+          v.re += alpha;
+          a[int64_t(row) * K + col] = v;
+        } else {
+          a[int64_t(row) * K + col] = v;
+          a[int64_t(col) * K + row] = cconj(v);
+        }
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K1': dA = C + C^H, C = X dH^H, X = H + dH/2  (== H dH^H + dH H^H + dH dH^H)
+// ---------------------------------------------------------------------------
+template <typename T>
+LRZ_DEV void load_xd(const cplx<T> *P, const cplx<T> *Q, int mode, int64_t off, cplx<T> &x,
+                     cplx<T> &d) {
+  const cplx<T> p = P[off], q = Q[off];
+  if (mode == 0) {
+    d = q;
+  } else {
+    d = csub(q, p);  // dH = H_t - H_{t-1}, bit-identical to harness.py:235
+  }
+  x = mk<T>(p.re + T(0.5) * d.re, p.im + T(0.5) * d.im);
+}
+
+template <typename T, int BK>
+__global__ void __launch_bounds__(GEMM_THREADS)
+    gram_delta_kernel(int K, int N, const cplx<T> *__restrict__ P, int64_t ps,
+                      const cplx<T> *__restrict__ Q, int64_t qs, int mode,
+                      c128 *__restrict__ dA, int64_t as, int ntl) {
+  __shared__ cplx<T> XI[BK][TM + 1], DI[BK][TM + 1], XJ[BK][TM + 1], DJ[BK][TM + 1];
+  const int64_t item = blockIdx.x / ntl;
+  int I, J;
+  tri_tile(int(blockIdx.x % ntl), I, J);
+  const bool diag = (I == J);
+  const cplx<T> *p = P + item * ps;
+  const cplx<T> *q = Q + item * qs;
+  const int tid = threadIdx.x, tx = tid & 7, ty = tid >> 3;
+  cplx<T> c1[2][4], c2[2][4];
+#pragma unroll
+  for (int i = 0; i < 2; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) c1[i][j] = c2[i][j] = czero<T>();
+
+  for (int n0 = 0; n0 < N; n0 += BK) {
+    for (int e = tid; e < TM * BK; e += GEMM_THREADS) {
+      const int r = e / BK, k = e % BK, gk = n0 + k;
+      const int ri = I * TM + r, rj = J * TM + r;
+      cplx<T> x = czero<T>(), d = czero<T>();
+      if (ri < K && gk < N) load_xd(p, q, mode, int64_t(ri) * N + gk, x, d);
+      XI[k][r] = x;
+      DI[k][r] = d;
+      if (!diag) {
+        x = czero<T>();
+        d = czero<T>();
+        if (rj < K && gk < N) load_xd(p, q, mode, int64_t(rj) * N + gk, x, d);
+        XJ[k][r] = x;
+        DJ[k][r] = d;
+      }
+    }
+    __syncthreads();
+    const cplx<T>(*xj)[TM + 1] = diag ? XI : XJ;
+    const cplx<T>(*dj)[TM + 1] = diag ? DI : DJ;
+#pragma unroll 2
+    for (int k = 0; k < BK; ++k) {
+      cplx<T> xi[2] = {XI[k][ty], XI[k][ty + 16]};
+      cplx<T> di[2] = {DI[k][ty], DI[k][ty + 16]};
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const cplx<T> xjj = xj[k][tx + 8 * j], djj = dj[k][tx + 8 * j];
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+          cfma_cb(c1[i][j], xi[i], djj);   // X_i dH_j^*
+          cfma_cb(c2[i][j], xjj, di[i]);   // X_j dH_i^*
+        }
+      }
+    }
+    __syncthreads();
+  }
+  c128 *a = dA + item * as;
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    const int row = I * TM + ty + 16 * i;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int col = J * TM + tx + 8 * j;
+      if (row < K && col < K && row >= col) {
+        const c128 u = ccast<double>(c1[i][j]), w = ccast<double>(c2[i][j]);
+        c128 v = mk<double>(u.re + w.re, u.im - w.im);
+        if (row == col) {
+          v.im = 0.0;
+          a[int64_t(row) * K + col] = v;
+        } else {
+          a[int64_t(row) * K + col] = v;
+          a[int64_t(col) * K + row] = cconj(v);
+        }
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Generic batched complex GEMM  C = op(A) op(B), element types TA/TB converted
+// to the accumulation type T on load; optional ||C||_F^2 partial per tile.
+// ---------------------------------------------------------------------------
+template <typename T, typename TA, typename TB, int BK>
+__global__ void __launch_bounds__(GEMM_THREADS)
+    cgemm_kernel(int M, int N, int Kd, int opA, const cplx<TA> *__restrict__ A, int64_t lda,
+                 int64_t sA, int opB, const cplx<TB> *__restrict__ Bm, int64_t ldb, int64_t sB,
+                 cplx<T> *__restrict__ C, int64_t ldc, int64_t sC, double *__restrict__ norm_part,
+                 int tiles_m, int tiles_n) {
+  __shared__ cplx<T> As[BK][TM + 1];
+  __shared__ cplx<T> Bs[BK][TM + 1];
+  __shared__ double red[GEMM_THREADS / 32];
+  const int ntile = tiles_m * tiles_n;
+  const int64_t item = blockIdx.x / ntile;
+  const int tile = int(blockIdx.x % ntile);
+  const int I = tile / tiles_n, J = tile % tiles_n;
+  const cplx<TA> *a = A + item * sA;
+  const cplx<TB> *b = Bm + item * sB;
+  const int tid = threadIdx.x, tx = tid & 7, ty = tid >> 3;
+  cplx<T> acc[2][4];
+#pragma unroll
+  for (int i = 0; i < 2; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j] = czero<T>();
+
+  for (int k0 = 0; k0 < Kd; k0 += BK) {
+    for (int e = tid; e < TM * BK; e += GEMM_THREADS) {
+      // A_eff[m][k]: op 0 -> A[m][k] (k contiguous); op 1/2 -> A[k][m] (m contiguous)
+      int m, k;
+      if (opA == 0) {
+        m = e / BK;
+        k = e % BK;
+      } else {
+        k = e / TM;
+        m = e % TM;
+      }
+      const int gm = I * TM + m, gk = k0 + k;
+      cplx<T> v = czero<T>();
+      if (gm < M && gk < Kd) {
+        cplx<TA> x = (opA == 0) ? a[int64_t(gm) * lda + gk] : a[int64_t(gk) * lda + gm];
+        v = ccast<T>(x);
+        if (opA == 2) v.im = -v.im;
+      }
+      As[k][m] = v;
+    }
+    for (int e = tid; e < TM * BK; e += GEMM_THREADS) {
+      // B_eff[k][n]: op 0 -> B[k][n] (n contiguous); op 1/2 -> B[n][k] (k contiguous)
+      int n, k;
+      if (opB == 0) {
+        k = e / TM;
+        n = e % TM;
+      } else {
+        n = e / BK;
+        k = e % BK;
+      }
+      const int gn = J * TM + n, gk = k0 + k;
+      cplx<T> v = czero<T>();
+      if (gn < N && gk < Kd) {
+        cplx<TB> x = (opB == 0) ? b[int64_t(gk) * ldb + gn] : b[int64_t(gn) * ldb + gk];
+        v = ccast<T>(x);
+        if (opB == 2) v.im = -v.im;
+      }
+      Bs[k][n] = v;
+    }
+    __syncthreads();
+#pragma unroll 4
+    for (int k = 0; k < BK; ++k) {
+      const cplx<T> a0 = As[k][ty], a1 = As[k][ty + 16];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const cplx<T> bj = Bs[k][tx + 8 * j];
+        cfma(acc[0][j], a0, bj);
+        cfma(acc[1][j], a1, bj);
+      }
+    }
+    __syncthreads();
+  }
+  cplx<T> *c = C + item * sC;
+  double nrm = 0.0;
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    const int row = I * TM + ty + 16 * i;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int col = J * TM + tx + 8 * j;
+      if (row < M && col < N) {
+        c[int64_t(row) * ldc + col] = acc[i][j];
+        nrm += double(acc[i][j].re) * double(acc[i][j].re) +
+               double(acc[i][j].im) * double(acc[i][j].im);
+      }
+    }
+  }
+  if (norm_part) {
+    const double s = block_sum(nrm, red);
+    if (tid == 0) norm_part[item * ntile + tile] = s;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// SINR / rate epilogue (precoding.py:74-80) from a K x K coupling matrix.
+// scale: explicit per-item (scale_in) or derived from norm partials
+// (sqrt(P_t)/sqrt(sum of partials), precoding.py:47-51).
+// ---------------------------------------------------------------------------
+template <typename T>
+__global__ void __launch_bounds__(256)
+    sinr_kernel(int K, const cplx<T> *__restrict__ G, int64_t sG, const double *scale_in,
+                const double *__restrict__ norm_part, int nparts, double P_t,
+                double *scale_out, const double *__restrict__ noise, int64_t noise_div,
+                double *rates, double *sinr, double *sum_rate, int32_t *info) {
+  __shared__ double red[8];
+  const int64_t item = blockIdx.x;
+  double s = 1.0;
+  int bad = 0;
+  if (scale_in) {
+    s = scale_in[item];
+  } else if (norm_part) {
+    double n2 = 0.0;
+    for (int i = 0; i < nparts; ++i) n2 += norm_part[item * nparts + i];
+    const double nrm = sqrt(n2);
+    if (!(nrm > 0.0)) {
+      bad = 1;
+      s = 0.0;
+    } else {
+      s = sqrt(P_t) / nrm;
+    }
+    if (threadIdx.x == 0) {
+      if (scale_out) scale_out[item] = s;
+      if (info) info[item] = bad ? LRZ_INFO_ZERO_PRECODER : LRZ_INFO_OK;
+    }
+  }
+  const cplx<T> *g = G + item * sG;
+  const double *nz = noise + (item / noise_div) * K;
+  double my = 0.0;
+  for (int i = threadIdx.x; i < K; i += blockDim.x) {
+    double tot = 0.0, sig = 0.0;
+    for (int j = 0; j < K; ++j) {
+      const c128 v = cscale(ccast<double>(g[int64_t(i) * K + j]), s);
+      const double p = cabs2(v);
+      tot += p;
+      if (j == i) sig = p;
+    }
+    const double q = sig / ((tot - sig) + nz[i]);
+    const double r = log2(1.0 + q);
+    if (rates) rates[item * K + i] = r;
+    if (sinr) sinr[item * K + i] = q;
+    my += r;
+  }
+  const double total = block_sum(my, red);
+  if (threadIdx.x == 0 && sum_rate) sum_rate[item] = total;
+}
+
+template <typename T>
+__global__ void fro2_kernel(int64_t n, const cplx<T> *__restrict__ X, int64_t sX, double *out) {
+  __shared__ double red[8];
+  const cplx<T> *x = X + blockIdx.x * sX;
+  double s = 0.0;
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) s += double(cabs2(x[i]));
+  s = block_sum(s, red);
+  if (threadIdx.x == 0) out[blockIdx.x] = s;
+}
+
+template <typename T>
+__global__ void axpby_kernel(int64_t n, double a, const cplx<T> *__restrict__ X, double b,
+                             const cplx<T> *__restrict__ Y, cplx<T> *__restrict__ Z) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    const cplx<T> x = X[i];
+    cplx<T> z = mk<T>(T(a) * x.re, T(a) * x.im);
+    if (Y) {
+      const cplx<T> y = Y[i];
+      z = (a == 1.0 && b == 1.0) ? mk<T>(x.re + y.re, x.im + y.im)
+                                 : mk<T>(z.re + T(b) * y.re, z.im + T(b) * y.im);
+    }
+    Z[i] = z;
+  }
+}
+
+}  // namespace lrz
+
+using namespace lrz;
+
+extern "C" int lrz_axpby(int dtype, int64_t n, double a, const void *X, double b, const void *Y,
+                         void *Z, void *stream) {
+  if (n < 0 || !X || !Z) {
+    lrz_set_error("lrz_axpby: bad arguments");
+    return LRZ_EINVAL;
+  }
+  if (n == 0) return LRZ_OK;
+  const unsigned nb = unsigned(std::min<int64_t>((n + 255) / 256, 148 * 32));
+  cudaStream_t s = (cudaStream_t)stream;
+  if (dtype == LRZ_C64)
+    axpby_kernel<float><<<nb, 256, 0, s>>>(n, a, (const c64 *)X, b, (const c64 *)Y, (c64 *)Z);
+  else
+    axpby_kernel<double><<<nb, 256, 0, s>>>(n, a, (const c128 *)X, b, (const c128 *)Y,
+                                            (c128 *)Z);
+  return lrz_launch_status("lrz_axpby");
+}
+
+static int ntiles(int K) { return (K + TM - 1) / TM; }
+
+extern "C" int lrz_gram(int dtype, int64_t B, int K, int N, const void *H, int64_t h_stride,
+                        double alpha, void *A, int64_t a_stride, void *stream) {
+  if (B < 0 || K < 1 || N < 1 || !H || !A) {
+    lrz_set_error("lrz_gram: bad arguments");
+    return LRZ_EINVAL;
+  }
+  if (B == 0) return LRZ_OK;
+  const int nt = ntiles(K), ntl = nt * (nt + 1) / 2;
+  const dim3 grid(unsigned(B * ntl));
+  cudaStream_t s = (cudaStream_t)stream;
+  if (dtype == LRZ_C64)
+    gram_kernel<float, 32><<<grid, GEMM_THREADS, 0, s>>>(K, N, (const c64 *)H, h_stride, alpha,
+                                                         (c128 *)A, a_stride, ntl);
+  else
+    gram_kernel<double, 32><<<grid, GEMM_THREADS, 0, s>>>(K, N, (const c128 *)H, h_stride,
+                                                          alpha, (c128 *)A, a_stride, ntl);
+  return lrz_launch_status("lrz_gram");
+}
+
+extern "C" int lrz_gram_delta(int dtype, int64_t B, int K, int N, const void *P,
+                              int64_t p_stride, const void *Q, int64_t q_stride, int mode,
+                              void *dA, int64_t a_stride, void *stream) {
+  if (B < 0 || K < 1 || N < 1 || !P || !Q || !dA || (mode != 0 && mode != 1)) {
+    lrz_set_error("lrz_gram_delta: bad arguments");
+    return LRZ_EINVAL;
+  }
+  if (B == 0) return LRZ_OK;
+  const int nt = ntiles(K), ntl = nt * (nt + 1) / 2;
+  const dim3 grid(unsigned(B * ntl));
+  cudaStream_t s = (cudaStream_t)stream;
+  if (dtype == LRZ_C64)
+    gram_delta_kernel<float, 16><<<grid, GEMM_THREADS, 0, s>>>(
+        K, N, (const c64 *)P, p_stride, (const c64 *)Q, q_stride, mode, (c128 *)dA, a_stride,
+        ntl);
+  else
+    gram_delta_kernel<double, 16><<<grid, GEMM_THREADS, 0, s>>>(
+        K, N, (const c128 *)P, p_stride, (const c128 *)Q, q_stride, mode, (c128 *)dA,
+        a_stride, ntl);
+  return lrz_launch_status("lrz_gram_delta");
+}
+
+extern "C" int lrz_cgemm(int dtype, int64_t batch, int M, int N, int Kd, int opA,
+                         const void *A, int64_t lda, int64_t sA, int opB, const void *Bm,
+                         int64_t ldb, int64_t sB, void *C, int64_t ldc, int64_t sC,
+                         void *stream) {
+  if (batch < 0 || M < 1 || N < 1 || Kd < 1 || !A || !Bm || !C || opA < 0 || opA > 2 ||
+      opB < 0 || opB > 2) {
+    lrz_set_error("lrz_cgemm: bad arguments");
+    return LRZ_EINVAL;
+  }
+  if (batch == 0) return LRZ_OK;
+  const int tm = ntiles(M), tn = ntiles(N);
+  const dim3 grid(unsigned(batch * tm * tn));
+  cudaStream_t s = (cudaStream_t)stream;
+  if (dtype == LRZ_C64)
+    cgemm_kernel<float, float, float, 16><<<grid, GEMM_THREADS, 0, s>>>(
+        M, N, Kd, opA, (const c64 *)A, lda, sA, opB, (const c64 *)Bm, ldb, sB, (c64 *)C, ldc,
+        sC, nullptr, tm, tn);
+  else
+    cgemm_kernel<double, double, double, 16><<<grid, GEMM_THREADS, 0, s>>>(
+        M, N, Kd, opA, (const c128 *)A, lda, sA, opB, (const c128 *)Bm, ldb, sB, (c128 *)C,
+        ldc, sC, nullptr, tm, tn);
+  return lrz_launch_status("lrz_cgemm");
+}
+
+extern "C" int lrz_fro2(int dtype, int64_t batch, int64_t n, const void *X, int64_t sX,
+                        double *out, void *stream) {
+  if (batch < 0 || n < 0 || !X || !out) {
+    lrz_set_error("lrz_fro2: bad arguments");
+    return LRZ_EINVAL;
+  }
+  if (batch == 0) return LRZ_OK;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (dtype == LRZ_C64)
+    fro2_kernel<float><<<unsigned(batch), 256, 0, s>>>(n, (const c64 *)X, sX, out);
+  else
+    fro2_kernel<double><<<unsigned(batch), 256, 0, s>>>(n, (const c128 *)X, sX, out);
+  return lrz_launch_status("lrz_fro2");
+}
+
+extern "C" int lrz_sinr_rate(int dtype, int64_t batch, int K, const void *G, int64_t sG,
+                             const double *scale, const double *noise, int64_t noise_div,
+                             double *rates, double *sinr, double *sum_rate, void *stream) {
+  if (batch < 0 || K < 1 || !G || !noise || noise_div < 1) {
+    lrz_set_error("lrz_sinr_rate: bad arguments");
+    return LRZ_EINVAL;
+  }
+  if (batch == 0) return LRZ_OK;
+  cudaStream_t s = (cudaStream_t)stream;
+  static const double one = 1.0;
+  (void)one;
+  if (dtype == LRZ_C64)
+    sinr_kernel<float><<<unsigned(batch), 256, 0, s>>>(K, (const c64 *)G, sG, scale, nullptr, 0,
+                                                       1.0, nullptr, noise, noise_div, rates,
+                                                       sinr, sum_rate, nullptr);
+  else
+    sinr_kernel<double><<<unsigned(batch), 256, 0, s>>>(K, (const c128 *)G, sG, scale, nullptr,
+                                                        0, 1.0, nullptr, noise, noise_div,
+                                                        rates, sinr, sum_rate, nullptr);
+  return lrz_launch_status("lrz_sinr_rate");
+}
+
+// K6: fully digital precoder + rate for B items.  Workspace layout:
+//   [coupling B*K*K of dtype][norm partials B*tiles doubles][W if W==NULL]
+size_t lrz_precode_ws(int dtype, int64_t B, int K, int N) {
+  const size_t es = dtype == LRZ_C64 ? 8 : 16;
+  const size_t tiles = size_t(ntiles(N)) * ntiles(K);
+  size_t bytes = size_t(B) * K * K * es;
+  bytes = (bytes + 255) & ~size_t(255);
+  bytes += size_t(B) * tiles * sizeof(double);
+  bytes = (bytes + 255) & ~size_t(255);
+  bytes += size_t(B) * N * K * es;
+  return bytes;
+}
+
+extern "C" int lrz_precode_rate(int dtype, int64_t B, int K, int N, const void *H,
+                                int64_t h_stride, const void *A_inv, int64_t ai_stride,
+                                double P_t, const double *noise, int64_t noise_div, void *W,
+                                int64_t w_stride, double *scale, double *rates, double *sinr,
+                                double *sum_rate, int32_t *info, void *workspace,
+                                void *stream) {
+  if (B < 0 || K < 1 || N < 1 || !H || !A_inv || !noise || !workspace || noise_div < 1) {
+    lrz_set_error("lrz_precode_rate: bad arguments");
+    return LRZ_EINVAL;
+  }
+  if (B == 0) return LRZ_OK;
+  const size_t es = dtype == LRZ_C64 ? 8 : 16;
+  char *ws = (char *)workspace;
+  void *Gc = ws;
+  size_t off = (size_t(B) * K * K * es + 255) & ~size_t(255);
+  double *parts = (double *)(ws + off);
+  const int tm = ntiles(N), tn = ntiles(K);
+  off += size_t(B) * tm * tn * sizeof(double);
+  off = (off + 255) & ~size_t(255);
+  if (!W) {
+    W = ws + off;
+    w_stride = int64_t(N) * K;
+  }
+  cudaStream_t s = (cudaStream_t)stream;
+  const dim3 g1(unsigned(B * tm * tn)), g2(unsigned(B * tn * tn));
+  if (dtype == LRZ_C64) {
+    // W[n][j] = sum_k conj(H[k][n]) A_inv[k][j]     (precoding.py:47)
+    cgemm_kernel<float, float, double, 16><<<g1, GEMM_THREADS, 0, s>>>(
+        N, K, K, 2, (const c64 *)H, N, h_stride, 0, (const c128 *)A_inv, K, ai_stride,
+        (c64 *)W, K, w_stride, parts, tm, tn);
+    // G = H W                                           (precoding.py:74)
+    cgemm_kernel<float, float, float, 16><<<g2, GEMM_THREADS, 0, s>>>(
+        K, K, N, 0, (const c64 *)H, N, h_stride, 0, (const c64 *)W, K, w_stride, (c64 *)Gc, K,
+        int64_t(K) * K, nullptr, tn, tn);
+    sinr_kernel<float><<<unsigned(B), 256, 0, s>>>(K, (const c64 *)Gc, int64_t(K) * K, nullptr,
+                                                   parts, tm * tn, P_t, scale, noise, noise_div,
+                                                   rates, sinr, sum_rate, info);
+  } else {
+    cgemm_kernel<double, double, double, 16><<<g1, GEMM_THREADS, 0, s>>>(
+        N, K, K, 2, (const c128 *)H, N, h_stride, 0, (const c128 *)A_inv, K, ai_stride,
+        (c128 *)W, K, w_stride, parts, tm, tn);
+    cgemm_kernel<double, double, double, 16><<<g2, GEMM_THREADS, 0, s>>>(
+        K, K, N, 0, (const c128 *)H, N, h_stride, 0, (const c128 *)W, K, w_stride, (c128 *)Gc,
+        K, int64_t(K) * K, nullptr, tn, tn);
+    sinr_kernel<double><<<unsigned(B), 256, 0, s>>>(K, (const c128 *)Gc, int64_t(K) * K,
+                                                    nullptr, parts, tm * tn, P_t, scale, noise,
+                                                    noise_div, rates, sinr, sum_rate, info);
+  }
+  return lrz_launch_status("lrz_precode_rate");
+}

@@ -1,0 +1,316 @@
+"""Device-tensor operators: one function per C-ABI entry point.
+
+Inputs are torch CUDA tensors (contiguous, batch-major); outputs are new
+CUDA tensors.  Everything is stream-ordered on the current torch stream and
+never synchronises the host.  The drop-in API (lowrank.py / precoding.py)
+and the batched trajectory runner (trajectory.py) are built on these.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import math
+
+import torch
+
+from . import _native as N
+
+_WS: dict = {}
+
+# Kernel launches issued through this module (bench.py reports it as
+# gpu_launches): incremented by the number of kernels each entry point launches.
+LAUNCHES = [0]
+
+
+def _count(n: int = 1) -> None:
+    LAUNCHES[0] += n
+
+
+def workspace(device, nbytes: int, slot: str = "main") -> torch.Tensor:
+    """Grow-only per-(device, slot) scratch buffer."""
+    key = (device.index if device.index is not None else 0, slot)
+    buf = _WS.get(key)
+    if buf is None or buf.numel() < nbytes:
+        buf = torch.empty(max(int(nbytes), 256), dtype=torch.uint8, device=device)
+        _WS[key] = buf
+    return buf
+
+
+def _dt(t: torch.Tensor) -> int:
+    if t.dtype == torch.complex64:
+        return N.C64
+    if t.dtype == torch.complex128:
+        return N.C128
+    raise TypeError(f"expected complex64/complex128, got {t.dtype}")
+
+
+def _chk(t: torch.Tensor, name: str) -> torch.Tensor:
+    if not t.is_cuda:
+        raise TypeError(f"{name} must be a CUDA tensor")
+    if not t.is_contiguous():
+        raise ValueError(f"{name} must be contiguous")
+    return t
+
+
+def _items(t: torch.Tensor, name: str) -> tuple[int, int]:
+    """(count, element stride) of a [B, r, c] batch whose matrices are
+    contiguous but whose batch stride may be larger (views like x[:, 0])."""
+    if not t.is_cuda:
+        raise TypeError(f"{name} must be a CUDA tensor")
+    if t.dim() != 3 or t.stride(2) != 1 or t.stride(1) != t.shape[2]:
+        raise ValueError(f"{name} must be [B, r, c] with contiguous matrices")
+    if t.shape[0] > 1 and t.stride(0) < t.shape[1] * t.shape[2]:
+        raise ValueError(f"{name}: overlapping batch stride")
+    return t.shape[0], (t.stride(0) if t.shape[0] > 1 else t.shape[1] * t.shape[2])
+
+
+def _batch(t: torch.Tensor, tail: int):
+    lead = t.shape[:-tail]
+    return lead, int(math.prod(lead)) if lead else 1
+
+
+def d_max_for(K: int, k_init: int, p: int, i_max: int) -> int:
+    """Widest sketch the schedule can reach (lowrank.py:283,302)."""
+    return min(k_init * 2 ** (i_max - 1) + p, K)
+
+
+def gram(H: torch.Tensor, alpha: float, out: torch.Tensor | None = None) -> torch.Tensor:
+    """K1: H H^H + alpha I (complex128 out) over leading batch dims."""
+    _chk(H, "H")
+    lead, B = _batch(H, 2)
+    K, Nn = H.shape[-2:]
+    A = out if out is not None else torch.empty(*lead, K, K, dtype=torch.complex128,
+                                                 device=H.device)
+    lib = N.lib_for(H.device)
+    N.check(lib.lrz_gram(_dt(H), B, K, Nn, H.data_ptr(), K * Nn, float(alpha), A.data_ptr(),
+                         K * K, N.stream_ptr(H.device)), "lrz_gram")
+    _count(1)
+    return A
+
+
+def gram_delta(P: torch.Tensor, Q: torch.Tensor, mode: int,
+               out: torch.Tensor | None = None) -> torch.Tensor:
+    """K1': Gram correction, complex128 out.  mode 0: (H, dH); mode 1: (H_prev, H_cur).
+    P, Q, out: [B, ., .] batches (matrices contiguous, batch stride free)."""
+    if P.dim() == 2:
+        P, Q = P.unsqueeze(0), Q.unsqueeze(0)
+        if out is not None:
+            out = out.unsqueeze(0)
+    if P.shape != Q.shape or P.dtype != Q.dtype:
+        raise ValueError("P/Q shape or dtype mismatch")
+    B, ps = _items(P, "P")
+    _, qs = _items(Q, "Q")
+    K, Nn = P.shape[-2:]
+    dA = out if out is not None else torch.empty(B, K, K, dtype=torch.complex128,
+                                                  device=P.device)
+    _, as_ = _items(dA, "out")
+    lib = N.lib_for(P.device)
+    N.check(lib.lrz_gram_delta(_dt(P), B, K, Nn, P.data_ptr(), ps, Q.data_ptr(), qs,
+                               mode, dA.data_ptr(), as_, N.stream_ptr(P.device)),
+            "lrz_gram_delta")
+    _count(1)
+    return dA
+
+
+def herm_inverse(A: torch.Tensor, cond_limit: float = 1e14, mask: torch.Tensor | None = None,
+                 out: torch.Tensor | None = None, info: torch.Tensor | None = None):
+    """K5: batched Hermitian inverse with the cond guard; returns (A_inv, info)."""
+    _chk(A, "A")
+    if A.dtype != torch.complex128:
+        raise TypeError("herm_inverse works on complex128")
+    lead, B = _batch(A, 2)
+    K = A.shape[-1]
+    if out is None:
+        out = torch.empty_like(A)
+    if info is None:
+        info = torch.zeros(lead if lead else (1,), dtype=torch.int32, device=A.device)
+    lib = N.lib_for(A.device)
+    N.check(lib.lrz_herm_inverse(B, K, A.data_ptr(), K * K, out.data_ptr(), K * K,
+                                 info.data_ptr(), float(cond_limit), N.ptr(mask), None,
+                                 N.stream_ptr(A.device)), "lrz_herm_inverse")
+    _count(1)
+    return out, info
+
+
+def arsvd(dA: torch.Tensor, omega: torch.Tensor, cursor: torch.Tensor, eta: float, k_init: int,
+          p: int, i_max: int, omega_row: torch.Tensor | None = None,
+          mask: torch.Tensor | None = None, out: dict | None = None) -> dict:
+    """K2+K3 over a flat batch of items.  dA [B,K,K] c128; omega [R,L] f64;
+    cursor [B] int64; omega_row [B] int32 (row of omega per item, default = item)."""
+    _chk(dA, "dA")
+    _chk(omega, "omega")
+    B = dA.shape[0]
+    K = dA.shape[-1]
+    D = d_max_for(K, k_init, p, i_max)
+    dev = dA.device
+    if out is None:
+        out = dict(
+            U=torch.empty(B, D, K, dtype=torch.complex128, device=dev),
+            V=torch.empty(B, D, K, dtype=torch.complex128, device=dev),
+            S=torch.zeros(B, D, dtype=torch.float64, device=dev),
+            k_est=torch.zeros(B, dtype=torch.int32, device=dev),
+            iters=torch.zeros(B, dtype=torch.int32, device=dev),
+            fallback=torch.zeros(B, dtype=torch.int32, device=dev),
+            consumed=torch.zeros(B, dtype=torch.int64, device=dev),
+        )
+    cfg = N.ArsvdCfg(float(eta), int(k_init), int(p), int(i_max), int(D))
+    lib = N.lib_for(dev)
+    nbytes = lib.lrz_workspace_bytes(N.WS_ARSVD, N.C128, B, K, 0, D)
+    ws = workspace(dev, nbytes, "arsvd")
+    N.check(lib.lrz_arsvd(B, K, dA.data_ptr(), K * K, omega.data_ptr(), omega.shape[-1],
+                          N.ptr(omega_row), cursor.data_ptr(), C.byref(cfg), out["U"].data_ptr(),
+                          out["V"].data_ptr(), out["S"].data_ptr(), out["k_est"].data_ptr(),
+                          out["iters"].data_ptr(), out["fallback"].data_ptr(),
+                          out["consumed"].data_ptr(), N.ptr(mask), ws.data_ptr(),
+                          N.stream_ptr(dev)), "lrz_arsvd")
+    _count(1)
+    out["D"] = D
+    return out
+
+
+def woodbury(A: torch.Tensor | None, A_inv: torch.Tensor, U: torch.Tensor, V: torch.Tensor,
+             S: torch.Tensor, r: torch.Tensor):
+    """K4 over a batch: returns (A_out or None, A_inv_out, info)."""
+    B, K = A_inv.shape[0], A_inv.shape[-1]
+    D = U.shape[1]
+    dev = A_inv.device
+    A_inv_out = torch.empty_like(A_inv)
+    A_out = torch.empty_like(A) if A is not None else None
+    info = torch.zeros(B, dtype=torch.int32, device=dev)
+    lib = N.lib_for(dev)
+    ws = workspace(dev, lib.lrz_workspace_bytes(N.WS_WOODBURY, N.C128, B, K, 0, D), "wb")
+    N.check(lib.lrz_woodbury(B, K, D, N.ptr(A), A_inv.data_ptr(), K * K, U.data_ptr(),
+                             V.data_ptr(), S.data_ptr(), r.data_ptr(), N.ptr(A_out),
+                             A_inv_out.data_ptr(), info.data_ptr(), ws.data_ptr(),
+                             N.stream_ptr(dev)), "lrz_woodbury")
+    _count(1)
+    return A_out, A_inv_out, info
+
+
+def chain(plan, G, A_inv_prev, A_inv_seq, A_state, U, V, S, r, method, info):
+    """Per-trial sequential Woodbury chain over [B, T] steps (in place)."""
+    B, T = plan.shape
+    K = A_inv_seq.shape[-1]
+    D = U.shape[-2]
+    dev = plan.device
+    lib = N.lib_for(dev)
+    ws = workspace(dev, lib.lrz_workspace_bytes(N.WS_CHAIN, N.C128, B, K, 0, D), "chain")
+    N.check(lib.lrz_chain(B, T, K, D, plan.data_ptr(), G.data_ptr(), A_inv_prev.data_ptr(),
+                          A_inv_seq.data_ptr(), N.ptr(A_state), U.data_ptr(), V.data_ptr(),
+                          S.data_ptr(), r.data_ptr(), method.data_ptr(), info.data_ptr(),
+                          ws.data_ptr(), N.stream_ptr(dev)), "lrz_chain")
+    _count(1)
+
+
+def precode_rate(H: torch.Tensor, A_inv: torch.Tensor, P_t: float, noise: torch.Tensor,
+                 noise_div: int, W: torch.Tensor | None = None, want_sinr: bool = True):
+    """K6 over a flat batch: H [B,K,N], A_inv [B,K,K] c128, noise [R,K] f64 with
+    row = item // noise_div.  Returns dict(W (unscaled F_raw or None), scale,
+    rates [B,K], sinr, sum [B], info)."""
+    _chk(H, "H")
+    B, K, Nn = H.shape
+    dev = H.device
+    lib = N.lib_for(dev)
+    scale = torch.empty(B, dtype=torch.float64, device=dev)
+    rates = torch.empty(B, K, dtype=torch.float64, device=dev)
+    sinr = torch.empty(B, K, dtype=torch.float64, device=dev) if want_sinr else None
+    total = torch.empty(B, dtype=torch.float64, device=dev)
+    info = torch.zeros(B, dtype=torch.int32, device=dev)
+    ws = workspace(dev, lib.lrz_workspace_bytes(N.WS_PRECODE, _dt(H), B, K, Nn, 0), "precode")
+    N.check(lib.lrz_precode_rate(_dt(H), B, K, Nn, H.data_ptr(), K * Nn, A_inv.data_ptr(), K * K,
+                                 float(P_t), noise.data_ptr(), int(noise_div), N.ptr(W), Nn * K,
+                                 scale.data_ptr(), rates.data_ptr(), N.ptr(sinr),
+                                 total.data_ptr(), info.data_ptr(), ws.data_ptr(),
+                                 N.stream_ptr(dev)), "lrz_precode_rate")
+    _count(3)
+    return dict(W=W, scale=scale, rates=rates, sinr=sinr, sum=total, info=info)
+
+
+_OP = {"N": 0, "T": 1, "H": 2}
+
+
+def cgemm(A: torch.Tensor, opA: str, Bm: torch.Tensor, opB: str) -> torch.Tensor:
+    """Batched C = op(A) op(B) over leading dims (same dtype)."""
+    _chk(A, "A")
+    _chk(Bm, "B")
+    if A.dtype != Bm.dtype:
+        raise TypeError("cgemm operands must share a dtype")
+    lead, nb = _batch(A, 2)
+    ar, ac = A.shape[-2:]
+    br, bc = Bm.shape[-2:]
+    M, Ka = (ar, ac) if opA == "N" else (ac, ar)
+    Kb, Nn = (br, bc) if opB == "N" else (bc, br)
+    if Ka != Kb:
+        raise ValueError("inner dimensions differ")
+    Cm = torch.empty(*lead, M, Nn, dtype=A.dtype, device=A.device)
+    sB = 0 if Bm.dim() == 2 and nb > 1 else br * bc
+    lib = N.lib_for(A.device)
+    N.check(lib.lrz_cgemm(_dt(A), nb, M, Nn, Ka, _OP[opA], A.data_ptr(), ac, ar * ac, _OP[opB],
+                          Bm.data_ptr(), bc, sB, Cm.data_ptr(), Nn, M * Nn,
+                          N.stream_ptr(A.device)), "lrz_cgemm")
+    _count(1)
+    return Cm
+
+
+def axpby(a: float, X: torch.Tensor, b: float = 0.0, Y: torch.Tensor | None = None):
+    _chk(X, "X")
+    Z = torch.empty_like(X)
+    lib = N.lib_for(X.device)
+    N.check(lib.lrz_axpby(_dt(X), X.numel(), float(a), X.data_ptr(), float(b), N.ptr(Y),
+                          Z.data_ptr(), N.stream_ptr(X.device)), "lrz_axpby")
+    _count(1)
+    return Z
+
+
+def fro2(X: torch.Tensor, tail: int = 2) -> torch.Tensor:
+    _chk(X, "X")
+    lead, nb = _batch(X, tail)
+    n = int(math.prod(X.shape[-tail:]))
+    out = torch.empty(lead if lead else (1,), dtype=torch.float64, device=X.device)
+    lib = N.lib_for(X.device)
+    N.check(lib.lrz_fro2(_dt(X), nb, n, X.data_ptr(), n, out.data_ptr(),
+                         N.stream_ptr(X.device)), "lrz_fro2")
+    _count(1)
+    return out
+
+
+def sinr_rate(G: torch.Tensor, noise: torch.Tensor, noise_div: int,
+              scale: torch.Tensor | None = None):
+    _chk(G, "G")
+    lead, nb = _batch(G, 2)
+    K = G.shape[-1]
+    dev = G.device
+    rates = torch.empty(*lead, K, dtype=torch.float64, device=dev)
+    sinr = torch.empty(*lead, K, dtype=torch.float64, device=dev)
+    total = torch.empty(lead if lead else (1,), dtype=torch.float64, device=dev)
+    lib = N.lib_for(dev)
+    N.check(lib.lrz_sinr_rate(_dt(G), nb, K, G.data_ptr(), K * K, N.ptr(scale), noise.data_ptr(),
+                              int(noise_div), rates.data_ptr(), sinr.data_ptr(),
+                              total.data_ptr(), N.stream_ptr(dev)), "lrz_sinr_rate")
+    _count(1)
+    return rates, sinr, total
+
+
+def plan(is_sketch: torch.Tensor, k_est: torch.Tensor, K: int, out: torch.Tensor | None = None):
+    """Dispatcher decision per step (lowrank.py:345-359) as a uint8 plan."""
+    pl = out if out is not None else torch.empty_like(is_sketch)
+    lib = N.lib_for(is_sketch.device)
+    N.check(lib.lrz_plan(is_sketch.numel(), K, is_sketch.data_ptr(), k_est.data_ptr(),
+                         pl.data_ptr(), N.stream_ptr(is_sketch.device)), "lrz_plan")
+    _count(1)
+    return pl
+
+
+def spec_verify(is_sketch, iters_pred, iters_act, cursor, cursor0, first_unverified, active,
+                pending, K, eta, k_init, p, i_max):
+    B, T = is_sketch.shape
+    dev = is_sketch.device
+    cfg = N.ArsvdCfg(float(eta), int(k_init), int(p), int(i_max),
+                     d_max_for(K, k_init, p, i_max))
+    lib = N.lib_for(dev)
+    N.check(lib.lrz_spec_verify(B, T, K, C.byref(cfg), is_sketch.data_ptr(),
+                                iters_pred.data_ptr(), N.ptr(iters_act), cursor.data_ptr(),
+                                cursor0.data_ptr(), first_unverified.data_ptr(),
+                                active.data_ptr(), pending.data_ptr(), N.stream_ptr(dev)),
+            "lrz_spec_verify")
+    _count(1)

@@ -1,0 +1,314 @@
+"""Batched trajectory runner: the B200 replacement of the reference's
+per-trial sweep loop (harness._sweep_trial, harness.py:188-257).
+
+For B Monte-Carlo trials x T time steps it produces, per (trial, step), the
+maintained inverse A^-1_t, the precoder W_t = H_t^H A^-1_t (power
+normalised) and the sum-rate, with the reference's step semantics:
+
+* step 0 and every n_reset-th step: full inversion of the Gram
+  (harness.py:229-233);
+* conventional method: full inversion every step;
+* WB-arSVD: arSVD of the Gram correction between consecutive channels
+  (harness.py:234-241) and the rank-ratio dispatcher (lowrank.py:345-373).
+
+Execution plan per time chunk (all device-resident, stream-ordered):
+
+  1. G[b,t]  = H H^H + alpha I            batched over B*T       (K1)
+  2. dG[b,t] = gram_delta(H_{t-1}, H_t)    batched over B*T       (K1')
+  3. arSVD of every dG with *speculative* sketch cursors, batched over
+     B*T; a verifier re-runs only the steps whose cursor was mispredicted
+     (the sketch stream is the only thing that serialises arSVD across
+     steps, and iteration counts rarely change between passes)  (K2+K3)
+  4. plan[b,t] = full / woodbury / none   (dispatcher, lowrank.py:345-359)
+  5. inv(G) for every full step           batched over B*T        (K5)
+  6. Woodbury recurrence per trial        sequential in t only    (K4)
+  7. precoder + SINR / sum-rate           batched over B*T        (K6)
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import ops
+from .errors import SingularMatrixError
+from .lowrank import cost_full, cost_wb_arsvd, sketch_cost
+from .omega import OmegaStreams, consumed_by, normals_per_call_max
+
+
+@dataclass
+class TrajectoryConfig:
+    """Method and knobs.  eta None = conventional (full inversion every step)."""
+
+    alpha: float
+    P_t: float = 1.0
+    eta: float | None = None
+    k_init: int = 2
+    p: int = 5
+    i_max: int = 3
+    n_reset: int = 1200          # config.py:59
+    maintain_A: bool = True      # keep A = A + U S V^H like GramState.A (lowrank.py:220)
+    max_spec_passes: int = 64
+
+
+@dataclass
+class ChunkResult:
+    rates: torch.Tensor          # [B, T] sum-rate
+    per_ut: torch.Tensor         # [B, T, K]
+    method: torch.Tensor         # [B, T] uint8 (full 0, woodbury 1, none 2)
+    k_est: torch.Tensor          # [B, T] int32 (0 on full-reset steps)
+    iters: torch.Tensor          # [B, T] int32 arSVD iterations
+    info: torch.Tensor           # [B, T] int32 kernel status
+    A_inv: torch.Tensor | None   # [B, T, K, K] complex128
+    W: torch.Tensor | None       # [B, T, N, K] unscaled F_raw
+    scale: torch.Tensor          # [B, T] power normalisation
+    consumed: torch.Tensor       # [B] normals consumed in this chunk
+    spec_passes: int = 0
+
+
+@dataclass
+class TrajectoryResult:
+    rates: np.ndarray
+    per_ut: np.ndarray
+    method: np.ndarray
+    k_est: np.ndarray
+    iters: np.ndarray
+    cost: np.ndarray
+    consumed: np.ndarray
+    spec_passes: list = field(default_factory=list)
+    A_inv: np.ndarray | None = None
+
+
+class TrajectoryRunner:
+    """Stateful runner over consecutive time chunks of B trials."""
+
+    def __init__(self, B: int, K: int, N: int, dtype: torch.dtype, cfg: TrajectoryConfig,
+                 device=None):
+        self.B, self.K, self.N, self.dtype, self.cfg = B, K, N, dtype, cfg
+        self.device = torch.device(device) if device is not None else torch.device("cuda", 0)
+        self.t = 0
+        self.H_prev = None
+        self.A_inv = torch.zeros(B, K, K, dtype=torch.complex128, device=self.device)
+        self.A = torch.zeros(B, K, K, dtype=torch.complex128, device=self.device)
+        self.D = ops.d_max_for(K, cfg.k_init, cfg.p, cfg.i_max)
+        self.prof = None          # list of (stage, start_event, end_event) when profiling
+
+    def _ev(self):
+        if self.prof is None:
+            return None
+        e = torch.cuda.Event(enable_timing=True)
+        e.record(torch.cuda.current_stream(self.device))
+        return e
+
+    def _stage(self, name, e0):
+        if self.prof is not None:
+            self.prof.append((name, e0, self._ev()))
+
+    # -- helpers -------------------------------------------------------------
+    def normals_per_step_max(self) -> int:
+        c = self.cfg
+        return 0 if c.eta is None else normals_per_call_max(self.K, c.k_init, c.p, c.i_max)
+
+    def _is_sketch(self, T: int) -> torch.Tensor:
+        c = self.cfg
+        tg = np.arange(self.t, self.t + T)
+        reset = (tg == 0) | ((c.n_reset > 0) & (tg % max(c.n_reset, 1) == 0))
+        if self.H_prev is None:
+            reset[0] = True
+        if c.eta is None:
+            reset[:] = True
+        row = torch.from_numpy((~reset).astype(np.uint8))
+        return row.to(self.device).reshape(1, T).expand(self.B, T).contiguous()
+
+    # -- one chunk -------------------------------------------------------------
+    def run_chunk(self, H: torch.Tensor, noise: torch.Tensor, omega: torch.Tensor | None = None,
+                  keep_A_inv: bool = False, keep_W: bool = False) -> ChunkResult:
+        """H [B, T, K, N] (device, self.dtype); noise [B, K] float64 (device);
+        omega [B, L] float64 (device; row b = trial b's next unconsumed normals,
+        L >= T * normals_per_step_max())."""
+        c = self.cfg
+        B, T, K, Nn = H.shape
+        assert (B, K, Nn) == (self.B, self.K, self.N) and H.dtype == self.dtype
+        dev = self.device
+        BT = B * T
+        Hf = H.reshape(BT, K, Nn)
+        is_sketch = self._is_sketch(T)
+        n_sketch = int(is_sketch[0].sum().item()) if T else 0
+
+        # 1. true Grams of every step
+        e0 = self._ev()
+        G = ops.gram(Hf, c.alpha).reshape(B, T, K, K)
+        self._stage("gram", e0)
+        plan = torch.zeros(B, T, dtype=torch.uint8, device=dev)
+        k_est = torch.zeros(B, T, dtype=torch.int32, device=dev)
+        iters = torch.zeros(B, T, dtype=torch.int32, device=dev)
+        consumed = torch.zeros(B, dtype=torch.int64, device=dev)
+        D = self.D
+        U = V = S = None
+        passes = 0
+        if n_sketch:
+            # 2. Gram corrections between consecutive channels (dH = H_t - H_{t-1})
+            dA = torch.empty(B, T, K, K, dtype=torch.complex128, device=dev)
+            dAf = dA.reshape(BT, K, K)
+            e0 = self._ev()
+            if T > 1:
+                ops.gram_delta(Hf[:-1], Hf[1:], 1, out=dAf[1:])
+            if self.H_prev is not None:
+                ops.gram_delta(self.H_prev, H[:, 0], 1, out=dA[:, 0])
+            self._stage("gram_delta", e0)
+            # 3. speculative arSVD
+            assert omega is not None and omega.shape[0] == B
+            iters_pred = torch.full((B, T), c.i_max, dtype=torch.int32, device=dev)
+            cursor = torch.zeros(B, T, dtype=torch.int64, device=dev)
+            cursor0 = torch.zeros(B, dtype=torch.int64, device=dev)
+            first = torch.zeros(B, dtype=torch.int32, device=dev)
+            active = torch.zeros(B, T, dtype=torch.uint8, device=dev)
+            pending = torch.zeros(1, dtype=torch.int32, device=dev)
+            ops.spec_verify(is_sketch, iters_pred, None, cursor, cursor0, first, active, pending,
+                            K, c.eta, c.k_init, c.p, c.i_max)
+            row = torch.arange(B, dtype=torch.int32, device=dev).repeat_interleave(T)
+            res = dict(
+                U=torch.empty(BT, D, K, dtype=torch.complex128, device=dev),
+                V=torch.empty(BT, D, K, dtype=torch.complex128, device=dev),
+                S=torch.zeros(BT, D, dtype=torch.float64, device=dev),
+                k_est=k_est.reshape(BT),
+                iters=torch.zeros(BT, dtype=torch.int32, device=dev),
+                fallback=torch.zeros(BT, dtype=torch.int32, device=dev),
+                consumed=torch.zeros(BT, dtype=torch.int64, device=dev),
+            )
+            pinned = torch.zeros(1, dtype=torch.int32).pin_memory()
+            while True:
+                e0 = self._ev()
+                ops.arsvd(dAf, omega, cursor.reshape(BT), c.eta, c.k_init, c.p, c.i_max,
+                          omega_row=row, mask=active.reshape(BT), out=res)
+                self._stage("arsvd", e0)
+                passes += 1
+                pending.zero_()
+                e0 = self._ev()
+                ops.spec_verify(is_sketch, iters_pred, res["iters"], cursor, cursor0, first,
+                                active, pending, K, c.eta, c.k_init, c.p, c.i_max)
+                self._stage("verify", e0)
+                pinned.copy_(pending, non_blocking=True)
+                torch.cuda.current_stream(dev).synchronize()
+                if int(pinned[0]) == 0:
+                    break
+                if passes >= c.max_spec_passes + T:
+                    raise RuntimeError("speculative arSVD did not converge")
+            iters.copy_(iters_pred * is_sketch.to(torch.int32))
+            U, V, S = res["U"], res["V"], res["S"]
+            last = cursor[:, -1] + res["consumed"].reshape(B, T)[:, -1] * is_sketch[:, -1]
+            consumed = last
+            # 4. dispatcher
+            ops.plan(is_sketch, k_est, K, out=plan)
+        # 5. full inversions (plan == 0) batched
+        A_inv_seq = torch.empty(B, T, K, K, dtype=torch.complex128, device=dev)
+        info = torch.zeros(B, T, dtype=torch.int32, device=dev)
+        full_mask = (plan == 0).to(torch.uint8)
+        e0 = self._ev()
+        ops.herm_inverse(G.reshape(BT, K, K), 1e14, mask=full_mask.reshape(BT),
+                         out=A_inv_seq.reshape(BT, K, K), info=info.reshape(BT))
+        self._stage("inverse", e0)
+        # 6. sequential Woodbury recurrence per trial
+        method = torch.zeros(B, T, dtype=torch.uint8, device=dev)
+        if U is None:
+            U = torch.zeros(BT, 1, K, dtype=torch.complex128, device=dev)
+            V = torch.zeros_like(U)
+            S = torch.ones(BT, 1, dtype=torch.float64, device=dev)
+        e0 = self._ev()
+        ops.chain(plan, G, self.A_inv, A_inv_seq, self.A if c.maintain_A else None, U, V, S,
+                  k_est, method, info)
+        self._stage("chain", e0)
+        # 7. precoder and rate
+        W = torch.empty(BT, Nn, K, dtype=self.dtype, device=dev) if keep_W else None
+        e0 = self._ev()
+        pr = ops.precode_rate(Hf, A_inv_seq.reshape(BT, K, K), c.P_t, noise, T, W=W,
+                              want_sinr=False)
+        self._stage("precode_rate", e0)
+        # state for the next chunk
+        self.A_inv = A_inv_seq[:, -1].clone()
+        self.H_prev = H[:, -1].contiguous().clone()
+        self.t += T
+        info = torch.maximum(info, pr["info"].reshape(B, T))
+        return ChunkResult(rates=pr["sum"].reshape(B, T), per_ut=pr["rates"].reshape(B, T, K),
+                           method=method, k_est=k_est, iters=iters, info=info,
+                           A_inv=A_inv_seq if keep_A_inv else None,
+                           W=W.reshape(B, T, Nn, K) if keep_W else None,
+                           scale=pr["scale"].reshape(B, T), consumed=consumed,
+                           spec_passes=passes)
+
+
+def step_costs(method: np.ndarray, k_est: np.ndarray, is_sketch: np.ndarray, K: int) -> np.ndarray:
+    """Cost units per step as the harness records them (harness.py:233,239):
+    resets cost K^3; dispatcher full = K^3 + sketch; woodbury; none."""
+    out = np.empty(method.shape, dtype=float)
+    for idx in np.ndindex(method.shape):
+        m, k, sk = int(method[idx]), int(k_est[idx]), bool(is_sketch[idx])
+        if not sk:
+            out[idx] = cost_full(K)
+        elif m == 0:
+            out[idx] = cost_full(K) + sketch_cost(K, k)
+        elif m == 1:
+            out[idx] = cost_wb_arsvd(K, k)
+        else:
+            out[idx] = cost_wb_arsvd(K, 0)
+    return out
+
+
+def run_trajectory(H, noise, cfg: TrajectoryConfig, streams: OmegaStreams | None = None,
+                   chunk: int | None = None, keep_A_inv: bool = False,
+                   device=None) -> TrajectoryResult:
+    """Run B trials x T steps.  H: numpy or torch [B, T, K, N]; noise [K] or
+    [B, K]; streams: per-trial sketch streams (required for WB)."""
+    dev = torch.device(device) if device is not None else (
+        H.device if isinstance(H, torch.Tensor) and H.is_cuda else torch.device("cuda", 0))
+    if isinstance(H, np.ndarray):
+        tdt = torch.complex64 if H.dtype == np.complex64 else torch.complex128
+    else:
+        tdt = H.dtype
+    B, T, K, Nn = H.shape
+    chunk = T if chunk is None else chunk
+    nz = np.array(np.broadcast_to(np.asarray(noise, dtype=np.float64), (B, K)))
+    noise_d = torch.from_numpy(nz).to(dev)
+    runner = TrajectoryRunner(B, K, Nn, tdt, cfg, dev)
+    outs = []
+    passes = []
+    cons_total = np.zeros(B, dtype=np.int64)
+    for t0 in range(0, T, chunk):
+        t1 = min(T, t0 + chunk)
+        Hc = H[:, t0:t1]
+        Hc = (torch.from_numpy(np.ascontiguousarray(Hc)).to(dev) if isinstance(Hc, np.ndarray)
+              else Hc.to(dev).contiguous())
+        om = None
+        if cfg.eta is not None:
+            L = (t1 - t0) * runner.normals_per_step_max()
+            om = torch.from_numpy(streams.window(L)).to(dev)
+        r = runner.run_chunk(Hc, noise_d, om, keep_A_inv=keep_A_inv)
+        if cfg.eta is not None:
+            used = r.consumed.cpu().numpy()
+            streams.advance(used)
+            cons_total += used
+        passes.append(r.spec_passes)
+        outs.append(r)
+    info = torch.cat([o.info for o in outs], 1).cpu().numpy()
+    if np.any(info == 1):
+        b, t = np.argwhere(info == 1)[0]
+        raise SingularMatrixError(f"trial {b} step {t}: condition estimate exceeds 1e14")
+    method = torch.cat([o.method for o in outs], 1).cpu().numpy()
+    k_est = torch.cat([o.k_est for o in outs], 1).cpu().numpy()
+    iters = torch.cat([o.iters for o in outs], 1).cpu().numpy()
+    sk = iters > 0
+    # steps that ran the dispatcher but consumed nothing (zero perturbation) still count
+    tg = np.arange(T)
+    sk_mask = np.broadcast_to((tg > 0) & ~((cfg.n_reset > 0) & (tg % max(cfg.n_reset, 1) == 0)),
+                              (B, T)) if cfg.eta is not None else np.zeros((B, T), bool)
+    cons = consumed_by(iters, K, cfg.k_init, cfg.p, cfg.i_max) if cfg.eta is not None else \
+        np.zeros((B, T), np.int64)
+    del sk
+    return TrajectoryResult(
+        rates=torch.cat([o.rates for o in outs], 1).cpu().numpy(),
+        per_ut=torch.cat([o.per_ut for o in outs], 1).cpu().numpy(),
+        method=method, k_est=k_est, iters=iters,
+        cost=step_costs(method, k_est, sk_mask, K), consumed=cons, spec_passes=passes,
+        A_inv=(torch.cat([o.A_inv for o in outs], 1).cpu().numpy() if keep_A_inv else None))
