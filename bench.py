@@ -74,12 +74,41 @@ def workload_desc(spec, eta):
 
 # --------------------------------------------------------------------------- CPU legs
 
-def _cpu_init():
+_BLAS_ENV = ("OPENBLAS_NUM_THREADS", "OMP_NUM_THREADS", "MKL_NUM_THREADS",
+             "SCIPY_OPENBLAS_NUM_THREADS")
+
+
+def _cpu_init(spec_kw=None):
+    """Worker initialiser: one BLAS thread (harness.py:284-293) and a short
+    warm-up sweep so first-call library costs stay out of the timed trials."""
     try:
         import threadpoolctl
         threadpoolctl.threadpool_limits(1)
     except Exception:
         pass
+    if spec_kw is not None:
+        kw = dict(spec_kw)
+        kw["T"] = 3
+        _cpu_trial((kw, 0, 1.0 - kw["tol"]))
+        _cpu_trial((kw, 0, None))
+
+
+def _cpu_pool(cores, spec):
+    """Spawned worker pool with BLAS pinned to one thread per process."""
+    import dataclasses
+    import multiprocessing as mp
+    saved = {k: os.environ.get(k) for k in _BLAS_ENV}
+    for k in _BLAS_ENV:
+        os.environ[k] = "1"
+    try:
+        return mp.get_context("spawn").Pool(cores, initializer=_cpu_init,
+                                            initargs=(dataclasses.asdict(spec),))
+    finally:
+        for k, v in saved.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
 
 
 def _cpu_trial(job):
@@ -126,12 +155,10 @@ def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    import multiprocessing as mp
     spec, eta = _spec(args)
     cores = _cores()
     n_trials = min(spec.B, cores)
-    ctx = mp.get_context("spawn")
-    with ctx.Pool(cores, initializer=_cpu_init) as pool:
+    with _cpu_pool(cores, spec) as pool:
         for _ in range(args.warmup):
             cpu_rate(spec.with_(T=min(spec.T, 20)), eta, min(n_trials, cores), pool)
         wb = [cpu_rate(spec, eta, n_trials, pool) for _ in range(args.steps)]
@@ -444,11 +471,9 @@ def run_b200(args):
     # ---- CPU baseline (rank 0, N = 1 only)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        import multiprocessing as mp
         cores = _cores()
         n_trials = min(B, cores)
-        with mp.get_context("spawn").Pool(cores, initializer=_cpu_init) as pool:
-            cpu_rate(spec.with_(T=5), eta, min(n_trials, cores), pool)
+        with _cpu_pool(cores, spec) as pool:
             v_cpu = cpu_rate(spec, eta, n_trials, pool)
         cpu = {"value": v_cpu, "unit": "updates/s", "cores": cores, "kind": "port",
                "sample": f"{n_trials} trials x {spec.T} steps of the WB-arSVD method, one trial "

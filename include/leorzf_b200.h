@@ -88,7 +88,12 @@ int lrz_herm_inverse(int64_t B, int K, const void *A, int64_t a_stride, void *A_
  *   of width d then the imaginary block, lowrank.py:284-286).
  *   Writes U, V ([D][K] column-major, complex128), S (D, descending),
  *   k_est, iters (sketch iterations run), fallback (1 = iteration-cap
- *   tail), consumed (normals used).  omega_row / item_mask nullable. */
+ *   tail), consumed (normals used).  omega_row / item_mask nullable.
+ *   want_factor 1: U/S/V always written; 0: only when 2*k_est <= K (the
+ *   dispatcher's Woodbury candidates) -- the batched runner's mode, which
+ *   lets iterations that cannot reach the energy target skip the SVD.
+ *   hermitian 1 promises dA == dA^H exactly (Gram corrections are): with
+ *   want_factor 0 and K <= 32 a warp-per-item front end runs first. */
 typedef struct {
   double eta;
   int k_init, p, i_max;
@@ -99,7 +104,8 @@ int lrz_arsvd(int64_t B, int K, const void *dA, int64_t a_stride, const double *
               int64_t omega_stride, const int32_t *omega_row, const int64_t *cursor,
               const lrz_arsvd_cfg *cfg, void *U, void *V, double *S, int32_t *k_est,
               int32_t *iters, int32_t *fallback, int64_t *consumed,
-              const uint8_t *item_mask, void *workspace, void *stream);
+              const uint8_t *item_mask, int want_factor, int hermitian, void *workspace,
+              void *stream);
 
 /* K4  Woodbury update (lowrank.py:182-227):
  *     A_inv_out = A_inv - (A_inv U aux^-1)(V^H A_inv), aux = S^-1 + V^H A_inv U,

@@ -39,7 +39,7 @@ _SIGS = {
                                  I64, P]),
     "lrz_herm_inverse": (C.c_int, [I64, C.c_int, P, I64, P, I64, P, F64, P, P, P]),
     "lrz_arsvd": (C.c_int, [I64, C.c_int, P, I64, P, I64, P, P, C.POINTER(ArsvdCfg), P, P, P,
-                            P, P, P, P, P, P, P]),
+                            P, P, P, P, P, C.c_int, C.c_int, P, P]),
     "lrz_woodbury": (C.c_int, [I64, C.c_int, C.c_int, P, P, I64, P, P, P, P, P, P, P, P, P]),
     "lrz_chain": (C.c_int, [I64, C.c_int, C.c_int, C.c_int, P, P, P, P, P, P, P, P, P, P, P, P,
                             P]),

@@ -33,6 +33,8 @@ struct ArsvdArgs {
   const int64_t *cursor;
   double eta;
   int k_init, p, i_max, D;
+  int want;  // 1: always produce U/S/V; 0: only when 2 k_est <= K (Woodbury candidate)
+  const int32_t *start_it;  // nullable: iteration to resume at (warp front end), < 0 = skip
   c128 *U, *V;
   double *S;
   int32_t *k_est, *iters, *fallback;
@@ -58,9 +60,142 @@ LRZ_DEV void rr_pair(int rnd, int pi, int dp, int &a, int &b) {
   }
 }
 
+// One-sided Jacobi (Hestenes) on the d columns of M (length K), rotations
+// accumulated in J (d x d, column-major); parallel round-robin ordering, one
+// warp per column pair.  On exit sval[j] = ||M_j|| and perm sorts them
+// descending (stable).  Block-cooperative; contains barriers.
+LRZ_DEV void jacobi_sv(c128 *M, c128 *J, int K, int d, double *sval, int *perm, int *s_rot) {
+  const int tid = threadIdx.x, NT = blockDim.x, lane = tid & 31, wid = tid >> 5, NW = NT >> 5;
+  for (int e = tid; e < d * d; e += NT) J[e] = mk<double>((e % (d + 1)) == 0 ? 1.0 : 0.0, 0.0);
+  if (tid == 0) s_rot[0] = s_rot[1] = 0;
+  __syncthreads();
+  const int dp = d + (d & 1), npairs = dp / 2;
+  for (int sweep = 0; sweep < JACOBI_MAX_SWEEPS; ++sweep) {
+    for (int rnd = 0; rnd < dp - 1; ++rnd) {
+      for (int pi = wid; pi < npairs; pi += NW) {
+        int a, b;
+        rr_pair(rnd, pi, dp, a, b);
+        if (b >= d) continue;
+        c128 *ma = M + int64_t(a) * K, *mb = M + int64_t(b) * K;
+        double al = 0.0, be = 0.0, gr = 0.0, gi = 0.0;
+        for (int k = lane; k < K; k += 32) {
+          const c128 x = ma[k], y = mb[k];
+          al += cabs2(x);
+          be += cabs2(y);
+          gr = fma(x.re, y.re, fma(x.im, y.im, gr));
+          gi = fma(x.re, y.im, fma(-x.im, y.re, gi));
+        }
+        al = warp_sum(al);
+        be = warp_sum(be);
+        gr = warp_sum(gr);
+        gi = warp_sum(gi);
+        const double gabs = hypot(gr, gi);
+        if (!(gabs > JACOBI_TOL * sqrt(al) * sqrt(be)) || gabs == 0.0) continue;
+        const double zeta = (be - al) / (2.0 * gabs);
+        const double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+        const double c = 1.0 / sqrt(1.0 + t * t), s = c * t;
+        const c128 ph = mk<double>(gr / gabs, -gi / gabs);  // e^{-i phi}
+        for (int k = lane; k < K; k += 32) {
+          const c128 x = ma[k], y = cmul(mb[k], ph);
+          ma[k] = mk<double>(c * x.re - s * y.re, c * x.im - s * y.im);
+          mb[k] = mk<double>(s * x.re + c * y.re, s * x.im + c * y.im);
+        }
+        c128 *ja = J + int64_t(a) * d, *jb = J + int64_t(b) * d;
+        for (int k = lane; k < d; k += 32) {
+          const c128 x = ja[k], y = cmul(jb[k], ph);
+          ja[k] = mk<double>(c * x.re - s * y.re, c * x.im - s * y.im);
+          jb[k] = mk<double>(s * x.re + c * y.re, s * x.im + c * y.im);
+        }
+        if (lane == 0) s_rot[sweep & 1] = 1;
+      }
+      __syncthreads();
+      // the next sweep's flag was last read before this sweep's first barrier
+      if (rnd == 0 && tid == 0) s_rot[(sweep + 1) & 1] = 0;
+    }
+    const int rotated = s_rot[sweep & 1];
+    if (!rotated) break;
+  }
+  for (int j = wid; j < d; j += NW) {
+    const c128 *mj = M + int64_t(j) * K;
+    double s2 = 0.0;
+    for (int k = lane; k < K; k += 32) s2 += cabs2(mj[k]);
+    s2 = warp_sum(s2);
+    if (lane == 0) sval[j] = sqrt(s2);
+  }
+  __syncthreads();
+  if (tid == 0) {
+    for (int j = 0; j < d; ++j) perm[j] = j;
+    for (int j = 1; j < d; ++j) {  // stable insertion sort, descending
+      const int pj = perm[j];
+      int i = j - 1;
+      while (i >= 0 && sval[perm[i]] < sval[pj]) {
+        perm[i + 1] = perm[i];
+        --i;
+      }
+      perm[i + 1] = pj;
+    }
+  }
+  __syncthreads();
+}
+
+// Certificate that every singular value of B (d of them; B^H = M) is far
+// above the fallback floor s_max K eps: C = M^H M = L L^H (Cholesky) and
+// lambda_min(C) >= 1 / ||L^-1||_F^2 >= 1e-9 tr(C).  C lives in Cw (d x d),
+// L^-1 columns in Xw (d x d).  Returns a block-uniform bool.
+LRZ_DEV bool gram_certificate(const c128 *M, int K, int d, double trC, c128 *Cw, c128 *Xw,
+                              double *red) {
+  const int tid = threadIdx.x, NT = blockDim.x;
+  for (int e = tid; e < d * d; e += NT) {
+    const int i = e / d, j = e - i * d;
+    if (i < j) continue;
+    const c128 *mi = M + int64_t(i) * K, *mj = M + int64_t(j) * K;
+    c128 a = czero<double>();
+    for (int k = 0; k < K; ++k) cfma_ca(a, mi[k], mj[k]);  // C_ij = m_i^H m_j
+    Cw[e] = a;
+  }
+  __syncthreads();
+  for (int j = 0; j < d; ++j) {
+    const double piv = Cw[j * d + j].re;
+    if (!(piv > 0.0)) return false;
+    const double l = sqrt(piv), il = 1.0 / l;
+    __syncthreads();
+    for (int i = j + 1 + tid; i < d; i += NT) Cw[i * d + j] = cscale(Cw[i * d + j], il);
+    if (tid == 0) Cw[j * d + j] = mk<double>(l, 0.0);
+    __syncthreads();
+    const int n = d - j - 1;
+    for (int e = tid; e < n * n; e += NT) {
+      const int i = j + 1 + e / n, k = j + 1 + e % n;
+      if (k > i) continue;
+      const c128 a = Cw[i * d + j], b = Cw[k * d + j];
+      c128 &x = Cw[i * d + k];
+      x.re -= a.re * b.re + a.im * b.im;
+      x.im -= a.im * b.re - a.re * b.im;
+    }
+    __syncthreads();
+  }
+  double loc = 0.0;
+  for (int t = tid; t < d; t += NT) {
+    c128 *x = Xw + int64_t(t) * d;
+    for (int i = t; i < d; ++i) {
+      c128 acc = mk<double>(i == t ? 1.0 : 0.0, 0.0);
+      for (int k = t; k < i; ++k) {
+        const c128 lk = Cw[i * d + k], xk = x[k];
+        acc.re -= lk.re * xk.re - lk.im * xk.im;
+        acc.im -= lk.re * xk.im + lk.im * xk.re;
+      }
+      x[i] = cscale(acc, 1.0 / Cw[i * d + i].re);
+      loc += cabs2(x[i]);
+    }
+  }
+  const double F = block_sum(loc, red);
+  return isfinite(F) && F * trC <= 1e9;
+}
+
 __global__ void __launch_bounds__(ARSVD_THREADS) arsvd_kernel(ArsvdArgs g) {
   const int64_t item = blockIdx.x;
   if (g.mask && !g.mask[item]) return;
+  const int it0 = g.start_it ? g.start_it[item] : 0;
+  if (it0 < 0) return;
   const int K = g.K, D = g.D;
   const int tid = threadIdx.x, NT = blockDim.x, lane = tid & 31, wid = tid >> 5, NW = NT >> 5;
 
@@ -100,8 +235,13 @@ __global__ void __launch_bounds__(ARSVD_THREADS) arsvd_kernel(ArsvdArgs g) {
   const double target = g.eta * energy;
   const double SQH = 0.7071067811865476;  // np.sqrt(0.5)
   int k0 = g.k_init, d = 0, it = 0, r = -1;
+  bool have_sv = false, hit_found = false;
+  for (int i = 0; i < it0; ++i) {  // resume: skip iterations the front end already ran
+    cur += int64_t(2) * K * min(k0 + g.p, K);
+    k0 *= 2;
+  }
 
-  for (it = 0; it < g.i_max; ++it) {
+  for (it = it0; it < g.i_max; ++it) {
     d = min(k0 + g.p, K);
     const double *zre = om + cur;
     const double *zim = zre + int64_t(K) * d;
@@ -212,84 +352,37 @@ __global__ void __launch_bounds__(ARSVD_THREADS) arsvd_kernel(ArsvdArgs g) {
     }
     __syncthreads();
     // ---- M = dA^H Q  (B^H; threads: j slow, k fast -> dA row contiguous)
+    double loc2 = 0.0;
     for (int e = tid; e < K * d; e += NT) {
       const int j = e / K, k = e - j * K;
       c128 a = czero<double>();
       const c128 *qj = Q + int64_t(j) * K;
       for (int m = 0; m < K; ++m) cfma_ca(a, dA[int64_t(m) * K + k], qj[m]);
       M[int64_t(j) * K + k] = a;
+      loc2 += cabs2(a);
     }
-    for (int e = tid; e < d * d; e += NT) J[e] = mk<double>((e % (d + 1)) == 0 ? 1.0 : 0.0, 0.0);
-    if (tid == 0) s_rot[0] = s_rot[1] = 0;
-    __syncthreads();
-    // ---- one-sided Jacobi (Hestenes), parallel round-robin ordering
-    const int dp = d + (d & 1), npairs = dp / 2;
-    for (int sweep = 0; sweep < JACOBI_MAX_SWEEPS; ++sweep) {
-      for (int rnd = 0; rnd < dp - 1; ++rnd) {
-        for (int pi = wid; pi < npairs; pi += NW) {
-          int a, b;
-          rr_pair(rnd, pi, dp, a, b);
-          if (b >= d) continue;
-          c128 *ma = M + int64_t(a) * K, *mb = M + int64_t(b) * K;
-          double al = 0.0, be = 0.0, gr = 0.0, gi = 0.0;
-          for (int k = lane; k < K; k += 32) {
-            const c128 x = ma[k], y = mb[k];
-            al += cabs2(x);
-            be += cabs2(y);
-            gr = fma(x.re, y.re, fma(x.im, y.im, gr));
-            gi = fma(x.re, y.im, fma(-x.im, y.re, gi));
-          }
-          al = warp_sum(al);
-          be = warp_sum(be);
-          gr = warp_sum(gr);
-          gi = warp_sum(gi);
-          const double gabs = hypot(gr, gi);
-          if (!(gabs > JACOBI_TOL * sqrt(al) * sqrt(be)) || gabs == 0.0) continue;
-          const double zeta = (be - al) / (2.0 * gabs);
-          const double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
-          const double c = 1.0 / sqrt(1.0 + t * t), s = c * t;
-          const c128 ph = mk<double>(gr / gabs, -gi / gabs);  // e^{-i phi}
-          for (int k = lane; k < K; k += 32) {
-            const c128 x = ma[k], y = cmul(mb[k], ph);
-            ma[k] = mk<double>(c * x.re - s * y.re, c * x.im - s * y.im);
-            mb[k] = mk<double>(s * x.re + c * y.re, s * x.im + c * y.im);
-          }
-          c128 *ja = J + int64_t(a) * d, *jb = J + int64_t(b) * d;
-          for (int k = lane; k < d; k += 32) {
-            const c128 x = ja[k], y = cmul(jb[k], ph);
-            ja[k] = mk<double>(c * x.re - s * y.re, c * x.im - s * y.im);
-            jb[k] = mk<double>(s * x.re + c * y.re, s * x.im + c * y.im);
-          }
-          if (lane == 0) s_rot[sweep & 1] = 1;
-        }
-        __syncthreads();
-        // the next sweep's flag was last read before this sweep's first barrier
-        if (rnd == 0 && tid == 0) s_rot[(sweep + 1) & 1] = 0;
+    // ||B||_F^2 = sum of all d squared singular values = cumsum(s^2)[-1]
+    const double mf = block_sum(loc2, red);
+    const bool last = (it == g.i_max - 1);
+    const bool below = mf < target * (1.0 - 1e-12);  // no prefix can reach the target
+    if (below && !last) {
+      k0 *= 2;
+      continue;
+    }
+    if (below && g.want == 0 && 2 * d > K) {
+      // iteration-cap tail with r > K/2 (full branch, no factor needed): the
+      // count of s > s_max K eps is d whenever sigma_min is certified far above
+      // that floor (lowrank.py:307-309); otherwise fall through to the SVD.
+      if (gram_certificate(M, K, d, mf, J, V, red)) {  // V: scratch for L^-1
+        r = d;
+        have_sv = false;
+        break;
       }
-      if (dp - 1 == 0) __syncthreads();
-      const int rotated = s_rot[sweep & 1];
-      if (!rotated) break;
     }
-    // ---- singular values, descending order, energy test (lowrank.py:290-301)
-    for (int j = wid; j < d; j += NW) {
-      const c128 *mj = M + int64_t(j) * K;
-      double s2 = 0.0;
-      for (int k = lane; k < K; k += 32) s2 += cabs2(mj[k]);
-      s2 = warp_sum(s2);
-      if (lane == 0) sval[j] = sqrt(s2);
-    }
-    __syncthreads();
+    jacobi_sv(M, J, K, d, sval, perm, s_rot);
+    have_sv = true;
+    // ---- energy test on the exact singular values (lowrank.py:290-301)
     if (tid == 0) {
-      for (int j = 0; j < d; ++j) perm[j] = j;
-      for (int j = 1; j < d; ++j) {  // stable insertion sort, descending
-        const int pj = perm[j];
-        int i = j - 1;
-        while (i >= 0 && sval[perm[i]] < sval[pj]) {
-          perm[i + 1] = perm[i];
-          --i;
-        }
-        perm[i + 1] = pj;
-      }
       double cum = 0.0;
       int hit = -1;
       for (int j = 0; j < d; ++j) {
@@ -305,31 +398,39 @@ __global__ void __launch_bounds__(ARSVD_THREADS) arsvd_kernel(ArsvdArgs g) {
     __syncthreads();
     r = s_r;
     __syncthreads();
-    if (r > 0) break;
+    if (r > 0) {
+      hit_found = true;
+      break;
+    }
     k0 *= 2;
   }
   bool fb = false;
-  if (r <= 0) {  // iteration cap: full rank-d factor minus numerical zeros (lowrank.py:304-316)
+  if (!hit_found) {  // iteration cap (lowrank.py:304-316)
     fb = true;
     it = g.i_max - 1;
-    const double floor = sval[perm[0]] * K * EPS64;
-    int cnt = 0;
-    for (int j = 0; j < d; ++j) cnt += sval[perm[j]] > floor ? 1 : 0;
-    r = cnt > 1 ? cnt : 1;
+    if (have_sv) {  // full rank-d factor minus numerical zeros
+      const double floor = sval[perm[0]] * K * EPS64;
+      int cnt = 0;
+      for (int j = 0; j < d; ++j) cnt += sval[perm[j]] > floor ? 1 : 0;
+      r = cnt > 1 ? cnt : 1;
+    }
   }
   // ---- outputs: S, V = M_perm / s, U = Q J_perm (all d columns, sorted)
-  for (int e = tid; e < K * d; e += NT) {
-    const int j = e / K, k = e - j * K;
-    const int pj = perm[j];
-    const double sj = sval[pj];
-    const c128 m = M[int64_t(pj) * K + k];
-    V[int64_t(j) * K + k] = sj > 0.0 ? cscale(m, 1.0 / sj) : czero<double>();
-    c128 a = czero<double>();
-    const c128 *jc = J + int64_t(pj) * d;
-    for (int i = 0; i < d; ++i) cfma(a, Q[int64_t(i) * K + k], jc[i]);
-    U[int64_t(j) * K + k] = a;
+  if (have_sv && (g.want == 1 || 2 * r <= K)) {
+    for (int e = tid; e < K * d; e += NT) {
+      const int j = e / K, k = e - j * K;
+      const int pj = perm[j];
+      const double sj = sval[pj];
+      const c128 m = M[int64_t(pj) * K + k];
+      V[int64_t(j) * K + k] = sj > 0.0 ? cscale(m, 1.0 / sj) : czero<double>();
+      c128 a = czero<double>();
+      const c128 *jc = J + int64_t(pj) * d;
+      for (int i = 0; i < d; ++i) cfma(a, Q[int64_t(i) * K + k], jc[i]);
+      U[int64_t(j) * K + k] = a;
+    }
   }
-  for (int j = tid; j < d; j += NT) S[j] = sval[perm[j]];
+  if (have_sv)
+    for (int j = tid; j < d; j += NT) S[j] = sval[perm[j]];
   if (tid == 0) {
     g.k_est[item] = r;
     g.iters[item] = it + 1;
@@ -338,20 +439,276 @@ __global__ void __launch_bounds__(ARSVD_THREADS) arsvd_kernel(ArsvdArgs g) {
   }
 }
 
+// ---------------------------------------------------------------------------
+// Batched screening front end (hermitian dA, factor not requested, D <= 32).
+//
+// Every sketch iteration i of one arsvd call reads its Omega block at a cursor
+// that does not depend on the outcome of earlier iterations (cursor +
+// sum_{i'<i} 2 K d_i', lowrank.py:284-286), so all i_max sketches are formed
+// at once:   Y_all = dA [Omega_0 ... Omega_{i_max-1}],  W_all = dA Y_all
+// (two batched GEMMs over all items; dA^H = dA).  A warp per item then screens
+// the iterations in order with CholeskyQR: G_i = Y_i^H Y_i = L L^H,
+// X_i = W_i L^-H (= dA^H Q_i for the CholeskyQR basis Q_i = Y_i L^-H), and
+// ||X_i||_F^2 = ||Q_i^H dA||_F^2 = sum of all squared singular values of B_i
+// (basis independent).  If that total is below the energy target
+// by more than the CholeskyQR error bound, no prefix can reach it and the
+// iteration is decided without an SVD.  The iteration-cap tail is decided
+// here too when its rank d > K/2 is certified (lambda_min(X^H X) far above
+// the s_max K eps floor).  Everything else is handed to arsvd_kernel, which
+// redoes that iteration with Householder QR + one-sided Jacobi.
+// ---------------------------------------------------------------------------
+constexpr int SCR_DMAX = 32;
+
+__global__ void omega_gather_kernel(int64_t n_items, int K, int i_max, int k_init, int p,
+                                    int Dtot, const double *__restrict__ omega, int64_t os,
+                                    const int32_t *__restrict__ orow,
+                                    const int64_t *__restrict__ cursor,
+                                    const uint8_t *__restrict__ mask, c128 *__restrict__ Om) {
+  const int64_t per = int64_t(K) * Dtot;
+  const int64_t total = n_items * per;
+  const double SQH = 0.7071067811865476;
+  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < total;
+       e += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t item = e / per;
+    if (mask && !mask[item]) continue;
+    const int rem = int(e - item * per);
+    const int m = rem / Dtot, col = rem - m * Dtot;
+    // locate the iteration block holding this column
+    int o = 0, k0 = k_init;
+    int64_t c = cursor ? cursor[item] : 0;
+    int d = min(k0 + p, K);
+    while (col >= o + d) {
+      o += d;
+      c += int64_t(2) * K * d;
+      k0 *= 2;
+      d = min(k0 + p, K);
+    }
+    const int j = col - o;
+    const double *z = omega + (orow ? int64_t(orow[item]) : item) * os + c;
+    Om[e] = mk<double>(SQH * z[m * d + j], SQH * z[int64_t(K) * d + m * d + j]);
+  }
+}
+
+__global__ void __launch_bounds__(128) arsvd_screen_kernel(ArsvdArgs g, int64_t B, int Dtot,
+                                                           const c128 *__restrict__ Yall,
+                                                           const c128 *__restrict__ Wall,
+                                                           c128 *__restrict__ Xs,
+                                                           int32_t *__restrict__ resume) {
+  extern __shared__ __align__(16) char scr_smem[];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int64_t item = blockIdx.x * int64_t(blockDim.x >> 5) + wib;
+  if (item >= B) return;
+  if (g.mask && !g.mask[item]) return;
+  const int K = g.K, LD = g.D + 1;
+  c128 *L = (c128 *)scr_smem + wib * g.D * LD;
+  const c128 *dA = g.dA + item * g.as;
+  const c128 *Y = Yall + item * int64_t(K) * Dtot;
+  const c128 *W = Wall + item * int64_t(K) * Dtot;
+  c128 *X = Xs + item * int64_t(K) * SCR_DMAX;
+  double e2 = 0.0;
+  for (int i = lane; i < K * K; i += 32) e2 += cabs2(dA[i]);
+  const double energy = warp_sum(e2);
+  if (energy == 0.0) {
+    if (lane == 0) {
+      g.k_est[item] = 0;
+      g.iters[item] = 0;
+      g.fallback[item] = 0;
+      g.consumed[item] = 0;
+      resume[item] = -1;
+    }
+    return;
+  }
+  const double target = g.eta * energy;
+  int k0 = g.k_init, o = 0;
+  int64_t used = 0;
+  for (int it = 0; it < g.i_max; ++it) {
+    const int d = min(k0 + g.p, K);
+    used += int64_t(2) * K * d;
+    const bool last = (it == g.i_max - 1);
+    // G = Y_i^H Y_i (lower triangle)
+    const int ne = d * (d + 1) / 2;
+    for (int e = lane; e < ne; e += 32) {
+      int a = int((sqrtf(8.0f * e + 1.0f) - 1.0f) * 0.5f);
+      while ((a + 1) * (a + 2) / 2 <= e) ++a;
+      while (a * (a + 1) / 2 > e) --a;
+      const int b = e - a * (a + 1) / 2;
+      c128 s = czero<double>();
+      for (int k = 0; k < K; ++k) cfma_ca(s, Y[int64_t(k) * Dtot + o + a], Y[int64_t(k) * Dtot + o + b]);
+      L[a * LD + b] = s;
+    }
+    __syncwarp();
+    // Cholesky G = L L^H, warp-synchronous
+    bool ok = true;
+    double lmin = 1e300, lmax = 0.0;
+    for (int jj = 0; jj < d; ++jj) {
+      const double piv = L[jj * LD + jj].re;
+      if (!(piv > 0.0)) {
+        ok = false;
+        break;
+      }
+      const double l = sqrt(piv), il = 1.0 / l;
+      lmin = fmin(lmin, l);
+      lmax = fmax(lmax, l);
+      __syncwarp();
+      for (int a = jj + 1 + lane; a < d; a += 32) L[a * LD + jj] = cscale(L[a * LD + jj], il);
+      if (lane == 0) L[jj * LD + jj] = mk<double>(l, 0.0);
+      __syncwarp();
+      const int n = d - jj - 1, nt = n * (n + 1) / 2;
+      for (int e = lane; e < nt; e += 32) {
+        int a = int((sqrtf(8.0f * e + 1.0f) - 1.0f) * 0.5f);
+        while ((a + 1) * (a + 2) / 2 <= e) ++a;
+        while (a * (a + 1) / 2 > e) --a;
+        const int b = e - a * (a + 1) / 2;
+        const int ra = jj + 1 + a, rb = jj + 1 + b;  // rb <= ra
+        const c128 x = L[ra * LD + jj], y = L[rb * LD + jj];
+        c128 &t = L[ra * LD + rb];
+        t.re -= x.re * y.re + x.im * y.im;
+        t.im -= x.im * y.re - x.re * y.im;
+      }
+      __syncwarp();
+    }
+    const double kap2 = ok ? (lmax / lmin) * (lmax / lmin) : 1e300;
+    // CholeskyQR error bound on the captured energy (relative)
+    const double tol = 64.0 * d * EPS64 * kap2 + 1e-12;
+    if (!ok || kap2 > 1e8) {
+      if (lane == 0) resume[item] = it;
+      return;
+    }
+    // X = W_i L^-H row by row (lane = row), ||X||_F^2
+    double loc = 0.0;
+    for (int k = lane; k < K; k += 32) {
+      c128 x[SCR_DMAX];
+#pragma unroll
+      for (int j = 0; j < SCR_DMAX; ++j) {
+        if (j < d) {
+          c128 acc = W[int64_t(k) * Dtot + o + j];
+#pragma unroll
+          for (int m = 0; m < SCR_DMAX; ++m)
+            if (m < j) {
+              const c128 lj = L[j * LD + m];  // x_j -= x_m conj(L_jm)
+              acc.re -= x[m].re * lj.re + x[m].im * lj.im;
+              acc.im -= x[m].im * lj.re - x[m].re * lj.im;
+            }
+          x[j] = cscale(acc, 1.0 / L[j * LD + j].re);
+          loc += cabs2(x[j]);
+          X[int64_t(k) * SCR_DMAX + j] = x[j];
+        }
+      }
+    }
+    const double mf = warp_sum(loc);
+    __syncwarp();
+    if (mf < target * (1.0 - tol)) {  // no prefix of the spectrum reaches the target
+      if (!last) {
+        k0 *= 2;
+        o += d;
+        continue;
+      }
+      if (g.want == 0 && 2 * d > K && kap2 < 1e4) {
+        // tail: certify sigma_min(B)^2 = lambda_min(X^H X) >= 1e-6 tr(X^H X)
+        for (int e = lane; e < d * (d + 1) / 2; e += 32) {
+          int a = int((sqrtf(8.0f * e + 1.0f) - 1.0f) * 0.5f);
+          while ((a + 1) * (a + 2) / 2 <= e) ++a;
+          while (a * (a + 1) / 2 > e) --a;
+          const int b = e - a * (a + 1) / 2;
+          c128 s = czero<double>();
+          for (int k = 0; k < K; ++k)
+            cfma_ca(s, X[int64_t(k) * SCR_DMAX + a], X[int64_t(k) * SCR_DMAX + b]);
+          L[a * LD + b] = s;
+        }
+        __syncwarp();
+        bool ok2 = true;
+        for (int jj = 0; jj < d; ++jj) {
+          const double piv = L[jj * LD + jj].re;
+          if (!(piv > 0.0)) {
+            ok2 = false;
+            break;
+          }
+          const double l = sqrt(piv), il = 1.0 / l;
+          __syncwarp();
+          for (int a = jj + 1 + lane; a < d; a += 32) L[a * LD + jj] = cscale(L[a * LD + jj], il);
+          if (lane == 0) L[jj * LD + jj] = mk<double>(l, 0.0);
+          __syncwarp();
+          const int n = d - jj - 1, nt = n * (n + 1) / 2;
+          for (int e = lane; e < nt; e += 32) {
+            int a = int((sqrtf(8.0f * e + 1.0f) - 1.0f) * 0.5f);
+            while ((a + 1) * (a + 2) / 2 <= e) ++a;
+            while (a * (a + 1) / 2 > e) --a;
+            const int b = e - a * (a + 1) / 2;
+            const int ra = jj + 1 + a, rb = jj + 1 + b;
+            const c128 x = L[ra * LD + jj], y = L[rb * LD + jj];
+            c128 &t = L[ra * LD + rb];
+            t.re -= x.re * y.re + x.im * y.im;
+            t.im -= x.im * y.re - x.re * y.im;
+          }
+          __syncwarp();
+        }
+        if (ok2) {
+          // ||L^-1||_F^2, column t per lane (forward substitution, kept in X's rows 0..d-1
+          // is not possible: use registers)
+          double f = 0.0;
+          for (int t = lane; t < d; t += 32) {
+            c128 x[SCR_DMAX];
+#pragma unroll
+            for (int i = 0; i < SCR_DMAX; ++i) {
+              if (i < d) {
+                c128 acc = mk<double>(i == t ? 1.0 : 0.0, 0.0);
+#pragma unroll
+                for (int k = 0; k < SCR_DMAX; ++k)
+                  if (k < i) {
+                    const c128 lk = L[i * LD + k];
+                    acc.re -= lk.re * x[k].re - lk.im * x[k].im;
+                    acc.im -= lk.re * x[k].im + lk.im * x[k].re;
+                  }
+                x[i] = (i < t) ? czero<double>() : cscale(acc, 1.0 / L[i * LD + i].re);
+                f += cabs2(x[i]);
+              }
+            }
+          }
+          const double F = warp_sum(f);
+          if (isfinite(F) && F * mf <= 1e6) {
+            if (lane == 0) {
+              g.k_est[item] = d;
+              g.iters[item] = g.i_max;
+              g.fallback[item] = 1;
+              g.consumed[item] = used;
+              resume[item] = -1;
+            }
+            return;
+          }
+        }
+      }
+      if (lane == 0) resume[item] = it;
+      return;
+    }
+    if (lane == 0) resume[item] = it;  // a hit is possible: exact SVD on this iteration
+    return;
+  }
+}
+
 }  // namespace lrz
 
 using namespace lrz;
 
+extern "C" int lrz_cgemm(int dtype, int64_t batch, int M, int N, int Kd, int opA, const void *A,
+                         int64_t lda, int64_t sA, int opB, const void *Bm, int64_t ldb,
+                         int64_t sB, void *C, int64_t ldc, int64_t sC, void *stream);
+
 size_t lrz_arsvd_ws(int64_t B, int K, int D) {
   return size_t(B) * (size_t(2) * D * K + size_t(D) * D) * sizeof(c128);
+}
+// plus the screening front end: resume index and three [B][K][max(Dtot, 32)] blocks
+size_t lrz_arsvd_ws_total(int64_t B, int K, int D) {
+  const size_t dt = size_t(std::max(4 * D, 32));  // Dtot <= 4 D bound is loose but safe
+  return lrz_arsvd_ws(B, K, D) + ((size_t(B) * sizeof(int32_t) + 255) & ~size_t(255)) +
+         3 * size_t(B) * K * dt * sizeof(c128);
 }
 
 extern "C" int lrz_arsvd(int64_t B, int K, const void *dA, int64_t a_stride,
                          const double *omega, int64_t omega_stride, const int32_t *omega_row,
                          const int64_t *cursor, const lrz_arsvd_cfg *cfg, void *U, void *V,
                          double *S, int32_t *k_est, int32_t *iters, int32_t *fallback,
-                         int64_t *consumed, const uint8_t *item_mask, void *workspace,
-                         void *stream) {
+                         int64_t *consumed, const uint8_t *item_mask, int want_factor,
+                         int hermitian, void *workspace, void *stream) {
   if (B < 0 || K < 1 || !dA || !omega || !cfg || !U || !V || !S || !k_est || !iters ||
       !fallback || !consumed || !workspace) {
     lrz_set_error("lrz_arsvd: bad arguments");
@@ -385,6 +742,8 @@ extern "C" int lrz_arsvd(int64_t B, int K, const void *dA, int64_t a_stride,
   g.p = cfg->p;
   g.i_max = cfg->i_max;
   g.D = cfg->d_max;
+  g.want = want_factor;
+  g.start_it = nullptr;
   g.U = (c128 *)U;
   g.V = (c128 *)V;
   g.S = S;
@@ -394,6 +753,39 @@ extern "C" int lrz_arsvd(int64_t B, int K, const void *dA, int64_t a_stride,
   g.consumed = consumed;
   g.mask = item_mask;
   g.ws = (c128 *)workspace;
-  arsvd_kernel<<<unsigned(B), ARSVD_THREADS, 0, (cudaStream_t)stream>>>(g);
+  cudaStream_t st = (cudaStream_t)stream;
+  int Dtot = 0;
+  {
+    long long kk = cfg->k_init;
+    for (int i = 0; i < cfg->i_max; ++i) {
+      Dtot += (int)std::min<long long>(kk + cfg->p, K);
+      kk *= 2;
+    }
+  }
+  if (hermitian && want_factor == 0 && g.D <= SCR_DMAX && Dtot <= 4 * g.D) {
+    // screening front end (see arsvd_screen_kernel); workspace layout after the
+    // CTA kernel's part: resume[B] int32 | Om/X [B][K][Dtot] | Y [B][K][Dtot] | W
+    char *wp = (char *)workspace + lrz_arsvd_ws(B, K, cfg->d_max);
+    int32_t *resume = (int32_t *)wp;
+    wp += (size_t(B) * sizeof(int32_t) + 255) & ~size_t(255);
+    const size_t blk = size_t(B) * K * std::max(Dtot, (int)SCR_DMAX) * sizeof(c128);
+    c128 *Om = (c128 *)wp;
+    c128 *Ya = (c128 *)(wp + blk);
+    c128 *Wa = (c128 *)(wp + 2 * blk);
+    const int64_t tot = B * int64_t(K) * Dtot;
+    omega_gather_kernel<<<unsigned(std::min<int64_t>((tot + 255) / 256, 148 * 64)), 256, 0, st>>>(
+        B, K, cfg->i_max, cfg->k_init, cfg->p, Dtot, omega, omega_stride, omega_row, cursor,
+        item_mask, Om);
+    int rc = lrz_cgemm(LRZ_C128, B, K, Dtot, K, 0, dA, K, a_stride, 0, Om, Dtot,
+                       int64_t(K) * Dtot, Ya, Dtot, int64_t(K) * Dtot, stream);
+    if (rc) return rc;
+    rc = lrz_cgemm(LRZ_C128, B, K, Dtot, K, 0, dA, K, a_stride, 0, Ya, Dtot, int64_t(K) * Dtot,
+                   Wa, Dtot, int64_t(K) * Dtot, stream);
+    if (rc) return rc;
+    const size_t sm = 4 * size_t(g.D) * (g.D + 1) * sizeof(c128);
+    arsvd_screen_kernel<<<unsigned((B + 3) / 4), 128, sm, st>>>(g, B, Dtot, Ya, Wa, Om, resume);
+    g.start_it = resume;
+  }
+  arsvd_kernel<<<unsigned(B), ARSVD_THREADS, 0, st>>>(g);
   return lrz_launch_status("lrz_arsvd");
 }

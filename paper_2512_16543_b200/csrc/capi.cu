@@ -22,7 +22,7 @@ int lrz_launch_status(const char *what) {
   return LRZ_OK;
 }
 
-size_t lrz_arsvd_ws(int64_t B, int K, int D);
+size_t lrz_arsvd_ws_total(int64_t B, int K, int D);
 size_t lrz_precode_ws(int dtype, int64_t B, int K, int N);
 size_t lrz_wb_ws(int64_t B, int K, int D);
 
@@ -50,7 +50,7 @@ extern "C" size_t lrz_workspace_bytes(int op, int dtype, int64_t B, int K, int N
     case LRZ_WS_INVERSE:
       return 0;
     case LRZ_WS_ARSVD:
-      return lrz_arsvd_ws(B, K, d_max);
+      return lrz_arsvd_ws_total(B, K, d_max);
     case LRZ_WS_WOODBURY:
     case LRZ_WS_CHAIN:
       return lrz_wb_ws(B, K, d_max);

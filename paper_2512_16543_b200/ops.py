@@ -134,7 +134,8 @@ def herm_inverse(A: torch.Tensor, cond_limit: float = 1e14, mask: torch.Tensor |
 
 def arsvd(dA: torch.Tensor, omega: torch.Tensor, cursor: torch.Tensor, eta: float, k_init: int,
           p: int, i_max: int, omega_row: torch.Tensor | None = None,
-          mask: torch.Tensor | None = None, out: dict | None = None) -> dict:
+          mask: torch.Tensor | None = None, out: dict | None = None,
+          want_factor: bool = True, hermitian: bool = False) -> dict:
     """K2+K3 over a flat batch of items.  dA [B,K,K] c128; omega [R,L] f64;
     cursor [B] int64; omega_row [B] int32 (row of omega per item, default = item)."""
     _chk(dA, "dA")
@@ -161,8 +162,8 @@ def arsvd(dA: torch.Tensor, omega: torch.Tensor, cursor: torch.Tensor, eta: floa
                           N.ptr(omega_row), cursor.data_ptr(), C.byref(cfg), out["U"].data_ptr(),
                           out["V"].data_ptr(), out["S"].data_ptr(), out["k_est"].data_ptr(),
                           out["iters"].data_ptr(), out["fallback"].data_ptr(),
-                          out["consumed"].data_ptr(), N.ptr(mask), ws.data_ptr(),
-                          N.stream_ptr(dev)), "lrz_arsvd")
+                          out["consumed"].data_ptr(), N.ptr(mask), int(want_factor),
+                          int(hermitian), ws.data_ptr(), N.stream_ptr(dev)), "lrz_arsvd")
     _count(1)
     out["D"] = D
     return out

@@ -182,7 +182,8 @@ class TrajectoryRunner:
             while True:
                 e0 = self._ev()
                 ops.arsvd(dAf, omega, cursor.reshape(BT), c.eta, c.k_init, c.p, c.i_max,
-                          omega_row=row, mask=active.reshape(BT), out=res)
+                          omega_row=row, mask=active.reshape(BT), out=res, want_factor=False,
+                          hermitian=True)
                 self._stage("arsvd", e0)
                 passes += 1
                 pending.zero_()

@@ -22,7 +22,7 @@ def test_library_exports_every_header_symbol():
     assert lib.lrz_version() == 1
     # workspace sizing is pure host arithmetic
     assert lib.lrz_workspace_bytes(_native.WS_ARSVD, 1, 10, 32, 0, 21) == \
-        10 * (2 * 21 * 32 + 21 * 21) * 16
+        10 * (2 * 21 * 32 + 21 * 21) * 16 + 10 * 4
 
 
 def test_sass_is_sm100a():
