@@ -137,12 +137,15 @@ int lrz_plan(int64_t n, int K, const uint8_t *is_sketch, const int32_t *k_est, u
  *     W = H^H A_inv (N x K, dtype of H, UNSCALED), scale = sqrt(P_t)/||W||_F,
  *     G = scale * H W, SINR_n = |G_nn|^2 / (sum_{i != n}|G_ni|^2 + noise_n),
  *     rates = log2(1 + SINR), sum.  noise row = item / noise_div.
- *     W may be NULL (then kept in workspace).  info = ZERO_PRECODER if ||W||=0. */
+ *     W may be NULL (then kept in workspace).  info = ZERO_PRECODER if ||W||=0.
+ *     G_true (nullable, complex128 [B][K][K]) = H H^H + alpha I of the same H:
+ *     then H W is formed as G_true A^-1 - alpha A^-1 in K^3
+ *     instead of K^2 N work. */
 int lrz_precode_rate(int dtype, int64_t B, int K, int N, const void *H, int64_t h_stride,
                      const void *A_inv, int64_t ai_stride, double P_t, const double *noise,
-                     int64_t noise_div, void *W, int64_t w_stride, double *scale,
-                     double *rates, double *sinr, double *sum_rate, int32_t *info,
-                     void *workspace, void *stream);
+                     int64_t noise_div, void *W, int64_t w_stride, const void *G_true,
+                     double alpha, double *scale, double *rates, double *sinr,
+                     double *sum_rate, int32_t *info, void *workspace, void *stream);
 
 /* Batched complex GEMM C[i] = op(A[i]) op(B[i]) (op: 0 = N, 1 = T, 2 = C^H),
  * all operands of `dtype`, row-major with leading dims.  Used by the

@@ -44,7 +44,7 @@ _SIGS = {
     "lrz_chain": (C.c_int, [I64, C.c_int, C.c_int, C.c_int, P, P, P, P, P, P, P, P, P, P, P, P,
                             P]),
     "lrz_precode_rate": (C.c_int, [C.c_int, I64, C.c_int, C.c_int, P, I64, P, I64, F64, P, I64,
-                                   P, I64, P, P, P, P, P, P, P]),
+                                   P, I64, P, F64, P, P, P, P, P, P, P]),
     "lrz_cgemm": (C.c_int, [C.c_int, I64, C.c_int, C.c_int, C.c_int, C.c_int, P, I64, I64,
                             C.c_int, P, I64, I64, P, I64, I64, P]),
     "lrz_axpby": (C.c_int, [C.c_int, I64, F64, P, F64, P, P, P]),

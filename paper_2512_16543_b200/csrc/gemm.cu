@@ -289,7 +289,8 @@ __global__ void __launch_bounds__(256)
     sinr_kernel(int K, const cplx<T> *__restrict__ G, int64_t sG, const double *scale_in,
                 const double *__restrict__ norm_part, int nparts, double P_t,
                 double *scale_out, const double *__restrict__ noise, int64_t noise_div,
-                double *rates, double *sinr, double *sum_rate, int32_t *info) {
+                double *rates, double *sinr, double *sum_rate, int32_t *info,
+                const c128 *__restrict__ corr = nullptr, int64_t scorr = 0, double alpha = 0.0) {
   __shared__ double red[8];
   const int64_t item = blockIdx.x;
   double s = 1.0;
@@ -312,12 +313,19 @@ __global__ void __launch_bounds__(256)
     }
   }
   const cplx<T> *g = G + item * sG;
+  const c128 *cr = corr ? corr + item * scorr : nullptr;
   const double *nz = noise + (item / noise_div) * K;
   double my = 0.0;
   for (int i = threadIdx.x; i < K; i += blockDim.x) {
     double tot = 0.0, sig = 0.0;
     for (int j = 0; j < K; ++j) {
-      const c128 v = cscale(ccast<double>(g[int64_t(i) * K + j]), s);
+      c128 gv = ccast<double>(g[int64_t(i) * K + j]);
+      if (cr) {  // H W = (G_true - alpha I) A^-1 = G_true A^-1 - alpha A^-1
+        const c128 a = cr[int64_t(i) * K + j];
+        gv.re -= alpha * a.re;
+        gv.im -= alpha * a.im;
+      }
+      const c128 v = cscale(gv, s);
       const double p = cabs2(v);
       tot += p;
       if (j == i) sig = p;
@@ -486,7 +494,7 @@ extern "C" int lrz_sinr_rate(int dtype, int64_t batch, int K, const void *G, int
 // K6: fully digital precoder + rate for B items.  Workspace layout:
 //   [coupling B*K*K of dtype][norm partials B*tiles doubles][W if W==NULL]
 size_t lrz_precode_ws(int dtype, int64_t B, int K, int N) {
-  const size_t es = dtype == LRZ_C64 ? 8 : 16;
+  const size_t es = 16;  // coupling buffer sized for complex128 (Gram shortcut)
   const size_t tiles = size_t(ntiles(N)) * ntiles(K);
   size_t bytes = size_t(B) * K * K * es;
   bytes = (bytes + 255) & ~size_t(255);
@@ -499,18 +507,17 @@ size_t lrz_precode_ws(int dtype, int64_t B, int K, int N) {
 extern "C" int lrz_precode_rate(int dtype, int64_t B, int K, int N, const void *H,
                                 int64_t h_stride, const void *A_inv, int64_t ai_stride,
                                 double P_t, const double *noise, int64_t noise_div, void *W,
-                                int64_t w_stride, double *scale, double *rates, double *sinr,
-                                double *sum_rate, int32_t *info, void *workspace,
-                                void *stream) {
+                                int64_t w_stride, const void *G_true, double alpha,
+                                double *scale, double *rates, double *sinr, double *sum_rate,
+                                int32_t *info, void *workspace, void *stream) {
   if (B < 0 || K < 1 || N < 1 || !H || !A_inv || !noise || !workspace || noise_div < 1) {
     lrz_set_error("lrz_precode_rate: bad arguments");
     return LRZ_EINVAL;
   }
   if (B == 0) return LRZ_OK;
-  const size_t es = dtype == LRZ_C64 ? 8 : 16;
   char *ws = (char *)workspace;
   void *Gc = ws;
-  size_t off = (size_t(B) * K * K * es + 255) & ~size_t(255);
+  size_t off = (size_t(B) * K * K * 16 + 255) & ~size_t(255);
   double *parts = (double *)(ws + off);
   const int tm = ntiles(N), tn = ntiles(K);
   off += size_t(B) * tm * tn * sizeof(double);
@@ -521,6 +528,25 @@ extern "C" int lrz_precode_rate(int dtype, int64_t B, int K, int N, const void *
   }
   cudaStream_t s = (cudaStream_t)stream;
   const dim3 g1(unsigned(B * tm * tn)), g2(unsigned(B * tn * tn));
+  if (G_true) {
+    // W = H^H A^-1 (norm partials in the epilogue), coupling from the Gram:
+    // H W = (G - alpha I) A^-1, K^3 instead of K^2 N work (F_RF = I)
+    if (dtype == LRZ_C64)
+      cgemm_kernel<float, float, double, 16><<<g1, GEMM_THREADS, 0, s>>>(
+          N, K, K, 2, (const c64 *)H, N, h_stride, 0, (const c128 *)A_inv, K, ai_stride,
+          (c64 *)W, K, w_stride, parts, tm, tn);
+    else
+      cgemm_kernel<double, double, double, 16><<<g1, GEMM_THREADS, 0, s>>>(
+          N, K, K, 2, (const c128 *)H, N, h_stride, 0, (const c128 *)A_inv, K, ai_stride,
+          (c128 *)W, K, w_stride, parts, tm, tn);
+    cgemm_kernel<double, double, double, 16><<<g2, GEMM_THREADS, 0, s>>>(
+        K, K, K, 0, (const c128 *)G_true, K, int64_t(K) * K, 0, (const c128 *)A_inv, K,
+        ai_stride, (c128 *)Gc, K, int64_t(K) * K, nullptr, tn, tn);
+    sinr_kernel<double><<<unsigned(B), 256, 0, s>>>(
+        K, (const c128 *)Gc, int64_t(K) * K, nullptr, parts, tm * tn, P_t, scale, noise,
+        noise_div, rates, sinr, sum_rate, info, (const c128 *)A_inv, ai_stride, alpha);
+    return lrz_launch_status("lrz_precode_rate");
+  }
   if (dtype == LRZ_C64) {
     // W[n][j] = sum_k conj(H[k][n]) A_inv[k][j]     (precoding.py:47)
     cgemm_kernel<float, float, double, 16><<<g1, GEMM_THREADS, 0, s>>>(

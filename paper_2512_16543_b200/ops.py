@@ -204,7 +204,8 @@ def chain(plan, G, A_inv_prev, A_inv_seq, A_state, U, V, S, r, method, info):
 
 
 def precode_rate(H: torch.Tensor, A_inv: torch.Tensor, P_t: float, noise: torch.Tensor,
-                 noise_div: int, W: torch.Tensor | None = None, want_sinr: bool = True):
+                 noise_div: int, W: torch.Tensor | None = None, want_sinr: bool = True,
+                 G_true: torch.Tensor | None = None, alpha: float = 0.0):
     """K6 over a flat batch: H [B,K,N], A_inv [B,K,K] c128, noise [R,K] f64 with
     row = item // noise_div.  Returns dict(W (unscaled F_raw or None), scale,
     rates [B,K], sinr, sum [B], info)."""
@@ -220,6 +221,7 @@ def precode_rate(H: torch.Tensor, A_inv: torch.Tensor, P_t: float, noise: torch.
     ws = workspace(dev, lib.lrz_workspace_bytes(N.WS_PRECODE, _dt(H), B, K, Nn, 0), "precode")
     N.check(lib.lrz_precode_rate(_dt(H), B, K, Nn, H.data_ptr(), K * Nn, A_inv.data_ptr(), K * K,
                                  float(P_t), noise.data_ptr(), int(noise_div), N.ptr(W), Nn * K,
+                                 N.ptr(G_true), float(alpha),
                                  scale.data_ptr(), rates.data_ptr(), N.ptr(sinr),
                                  total.data_ptr(), info.data_ptr(), ws.data_ptr(),
                                  N.stream_ptr(dev)), "lrz_precode_rate")
@@ -253,9 +255,14 @@ def cgemm(A: torch.Tensor, opA: str, Bm: torch.Tensor, opB: str) -> torch.Tensor
     return Cm
 
 
-def axpby(a: float, X: torch.Tensor, b: float = 0.0, Y: torch.Tensor | None = None):
+def axpby(a: float, X: torch.Tensor, b: float = 0.0, Y: torch.Tensor | None = None,
+          out: torch.Tensor | None = None):
+    """Z = a X + b Y elementwise (contiguous operands of one dtype)."""
     _chk(X, "X")
-    Z = torch.empty_like(X)
+    if Y is not None:
+        _chk(Y, "Y")
+    Z = out if out is not None else torch.empty_like(X)
+    _chk(Z, "out")
     lib = N.lib_for(X.device)
     N.check(lib.lrz_axpby(_dt(X), X.numel(), float(a), X.data_ptr(), float(b), N.ptr(Y),
                           Z.data_ptr(), N.stream_ptr(X.device)), "lrz_axpby")

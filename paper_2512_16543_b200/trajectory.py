@@ -51,6 +51,12 @@ class TrajectoryConfig:
     n_reset: int = 1200          # config.py:59
     maintain_A: bool = True      # keep A = A + U S V^H like GramState.A (lowrank.py:220)
     max_spec_passes: int = 64
+    # H W for the rate from the Gram: (G - alpha I) A^-1 (exact with F_RF = I)
+    rate_via_gram: bool = True
+    # Gram correction: "diff" = G_t - G_{t-1} from the Grams already formed (complex128:
+    # cancellation error ~1e-14 relative); "formula" = the gram_delta products; "auto" =
+    # diff for complex128, formula for complex64
+    delta: str = "auto"
 
 
 @dataclass
@@ -90,6 +96,7 @@ class TrajectoryRunner:
         self.device = torch.device(device) if device is not None else torch.device("cuda", 0)
         self.t = 0
         self.H_prev = None
+        self.G_prev = None
         self.A_inv = torch.zeros(B, K, K, dtype=torch.complex128, device=self.device)
         self.A = torch.zeros(B, K, K, dtype=torch.complex128, device=self.device)
         self.D = ops.d_max_for(K, cfg.k_init, cfg.p, cfg.i_max)
@@ -153,10 +160,19 @@ class TrajectoryRunner:
             dA = torch.empty(B, T, K, K, dtype=torch.complex128, device=dev)
             dAf = dA.reshape(BT, K, K)
             e0 = self._ev()
-            if T > 1:
-                ops.gram_delta(Hf[:-1], Hf[1:], 1, out=dAf[1:])
-            if self.H_prev is not None:
-                ops.gram_delta(self.H_prev, H[:, 0], 1, out=dA[:, 0])
+            use_diff = c.delta == "diff" or (c.delta == "auto" and self.dtype == torch.complex128)
+            if use_diff:
+                Gf = G.reshape(BT, K, K)
+                if T > 1:
+                    ops.axpby(1.0, Gf[1:], -1.0, Gf[:-1], out=dAf[1:])
+                if self.G_prev is not None:
+                    d0 = ops.axpby(1.0, G[:, 0].contiguous(), -1.0, self.G_prev)
+                    dA[:, 0].copy_(d0)
+            else:
+                if T > 1:
+                    ops.gram_delta(Hf[:-1], Hf[1:], 1, out=dAf[1:])
+                if self.H_prev is not None:
+                    ops.gram_delta(self.H_prev, H[:, 0], 1, out=dA[:, 0])
             self._stage("gram_delta", e0)
             # 3. speculative arSVD
             assert omega is not None and omega.shape[0] == B
@@ -225,11 +241,14 @@ class TrajectoryRunner:
         W = torch.empty(BT, Nn, K, dtype=self.dtype, device=dev) if keep_W else None
         e0 = self._ev()
         pr = ops.precode_rate(Hf, A_inv_seq.reshape(BT, K, K), c.P_t, noise, T, W=W,
-                              want_sinr=False)
+                              want_sinr=False,
+                              G_true=G.reshape(BT, K, K) if c.rate_via_gram else None,
+                              alpha=c.alpha)
         self._stage("precode_rate", e0)
         # state for the next chunk
         self.A_inv = A_inv_seq[:, -1].clone()
         self.H_prev = H[:, -1].contiguous().clone()
+        self.G_prev = G[:, -1].contiguous().clone()
         self.t += T
         info = torch.maximum(info, pr["info"].reshape(B, T))
         return ChunkResult(rates=pr["sum"].reshape(B, T), per_ut=pr["rates"].reshape(B, T, K),

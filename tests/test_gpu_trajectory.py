@@ -110,3 +110,18 @@ def test_C2_eta09_woodbury_chain_vs_oracle(cuda):
             err = max(rel(res.A_inv[b, t], ref.A_inv[t]) for t in range(spec.T))
             assert err < 1e-10, err
             assert np.allclose(res.rates[b], ref.rates, rtol=1e-10)
+
+
+@pytest.mark.parametrize("delta,via_gram", [("formula", False), ("diff", True), ("formula", True)])
+def test_C2_runner_variants_match_reference(cuda, delta, via_gram):
+    """Gram-correction form (formula vs differenced Grams) and rate form
+    (H W vs (G - alpha I) A^-1) all reproduce the reference trajectory."""
+    g = load_golden("traj_C2s")
+    spec = S.C2
+    H = S.channels(spec, trials=[0, 1], t1=24)
+    cfg = _cfg(spec, 0.9)
+    cfg.delta, cfg.rate_via_gram = delta, via_gram
+    res = run_trajectory(H, S.noise_vector(spec), cfg, OmegaStreams.for_method(0, 0.9, [0, 1]),
+                         keep_A_inv=True)
+    for b in (0, 1):
+        _compare(res, b, g, f"t{b}_e900_", 24, 1e-10, 1e-10)
