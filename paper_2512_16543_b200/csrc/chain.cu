@@ -128,9 +128,9 @@ __global__ void __launch_bounds__(INV_THREADS)
       for (int64_t e = threadIdx.x; e < KK; e += blockDim.x) out[e] = prev[e];
       m = LRZ_METHOD_NONE;
     } else {
-      // A = G_t; the copy is only observable if a Woodbury step follows (it
-      // updates A) or this is the chunk's last step (carried state)
-      const bool needed = (t == T - 1) || plan[bt + 1] == 1;
+      // A = G_t; dead if the next step is another full inversion (it overwrites
+      // A); needed before a Woodbury or 'none' step and at the chunk end
+      const bool needed = (t == T - 1) || plan[bt + 1] != 0;
       if (Ast && needed)
         for (int64_t e = threadIdx.x; e < KK; e += blockDim.x) Ast[e] = G[bt * KK + e];
       st = info ? info[bt] : LRZ_INFO_OK;  // written by the batched inverse
