@@ -1,0 +1,76 @@
+"""Summarise ncu output into text for profiles/.
+
+    python scripts/ncu_summary.py launches gpurun_out/launches.csv
+    python scripts/ncu_summary.py report gpurun_out/prof_x.ncu-rep
+"""
+
+import collections
+import csv
+import io
+import subprocess
+import sys
+
+KEYS = ["Duration", "DRAM Throughput", "Memory Throughput", "Compute (SM) Throughput",
+        "L1/TEX Hit Rate", "L2 Hit Rate", "Executed Ipc Active", "Issue Slots Busy",
+        "Registers Per Thread", "Achieved Occupancy", "Theoretical Occupancy",
+        "Achieved Active Warps Per SM", "Executed Instructions", "Block Size", "Grid Size",
+        "Warp Cycles Per Issued Instruction", "Static Shared Memory Per Block",
+        "Dynamic Shared Memory Per Block", "FP64", "Fp64"]
+
+
+def launches(path):
+    rows = list(csv.reader(open(path)))
+    hi = [i for i, r in enumerate(rows) if "Kernel Name" in r][0]
+    h, data = rows[hi], rows[hi + 1:]
+    ki, vi, ui = h.index("Kernel Name"), h.index("Metric Value"), h.index("Metric Unit")
+    agg = collections.OrderedDict()
+    unit = None
+    for r in data:
+        if len(r) <= vi:
+            continue
+        name = r[ki].split("(")[0]
+        agg.setdefault(name, [0, 0.0])
+        agg[name][0] += 1
+        agg[name][1] += float(r[vi].replace(",", ""))
+        unit = r[ui]
+    scale = {"ns": 1e-6, "nsecond": 1e-6, "us": 1e-3, "usecond": 1e-3, "ms": 1.0,
+             "msecond": 1.0}.get(unit, 1e-6)
+    tot = sum(v[1] for k, v in agg.items() if "cutlass" not in k)
+    print(f"{'launches':>8} {'total ms':>10} {'ms/launch':>10} {'share':>6}  kernel "
+          "(cold-cache, serialised; cuBLAS peak-measurement GEMMs excluded from share)")
+    for k, v in sorted(agg.items(), key=lambda x: -x[1][1]):
+        share = "" if "cutlass" in k else f"{100 * v[1] / tot:5.1f}%"
+        print(f"{v[0]:8d} {v[1] * scale:10.3f} {v[1] * scale / v[0]:10.4f} {share:>6}  {k[:90]}")
+
+
+def report(path):
+    out = subprocess.run(["ncu", "-i", path, "--page", "details", "--csv"], capture_output=True,
+                         text=True).stdout
+    rows = list(csv.reader(io.StringIO(out)))
+    h = rows[0]
+    kname = None
+    for r in rows[1:]:
+        d = dict(zip(h, r))
+        if d.get("Kernel Name") != kname:
+            kname = d.get("Kernel Name")
+            print(f"== {kname}")
+        n = d.get("Metric Name", "")
+        if any(k in n for k in KEYS):
+            print(f"  {d.get('Section Name', '')[:28]:28s} {n[:48]:48s} {d.get('Metric Value', '')} "
+                  f"{d.get('Metric Unit', '')}")
+    raw = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True,
+                         text=True).stdout
+    rr = list(csv.reader(io.StringIO(raw)))
+    if len(rr) >= 3:
+        hh, units, vals = rr[0], rr[1], rr[2]
+        for want in ("dram__bytes_read.sum", "dram__bytes_write.sum", "gpu__time_duration.sum",
+                     "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active",
+                     "sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active",
+                     "smsp__inst_executed.sum", "sm__warps_active.avg.pct_of_peak_sustained_active"):
+            for i, name in enumerate(hh):
+                if name == want:
+                    print(f"  raw {name:60s} {vals[i]} {units[i]}")
+
+
+if __name__ == "__main__":
+    {"launches": launches, "report": report}[sys.argv[1]](sys.argv[2])
