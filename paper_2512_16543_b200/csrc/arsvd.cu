@@ -783,6 +783,11 @@ extern "C" int lrz_arsvd(int64_t B, int K, const void *dA, int64_t a_stride,
                    Wa, Dtot, int64_t(K) * Dtot, stream);
     if (rc) return rc;
     const size_t sm = 4 * size_t(g.D) * (g.D + 1) * sizeof(c128);
+    if (cudaFuncSetAttribute(arsvd_screen_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             int(sm)) != cudaSuccess) {
+      lrz_set_error("lrz_arsvd: cannot reserve %zu bytes of shared memory", sm);
+      return LRZ_ELAUNCH;
+    }
     arsvd_screen_kernel<<<unsigned((B + 3) / 4), 128, sm, st>>>(g, B, Dtot, Ya, Wa, Om, resume);
     g.start_it = resume;
   }

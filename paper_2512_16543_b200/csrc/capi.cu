@@ -48,7 +48,7 @@ extern "C" int lrz_device_check(int device) {
 extern "C" size_t lrz_workspace_bytes(int op, int dtype, int64_t B, int K, int N, int d_max) {
   switch (op) {
     case LRZ_WS_INVERSE:
-      return 0;
+      return size_t(B);  // per-item redo flags of the warp fast path
     case LRZ_WS_ARSVD:
       return lrz_arsvd_ws_total(B, K, d_max);
     case LRZ_WS_WOODBURY:

@@ -205,6 +205,92 @@ __global__ void plan_kernel(int64_t n, int K, const uint8_t *is_sketch, const in
   plan[i] = pl;
 }
 
+
+// K5 fast path for K <= 32: one warp per matrix, lane i holds row i in
+// registers (padded to 32 x 32 with the identity), Gauss-Jordan without
+// pivoting; the pivot row is broadcast with shuffles, no shared memory and
+// no block barriers.  Items that are not positive definite or whose
+// ||A||_F ||A^-1||_F bound exceeds the limit are flagged in `redo` for the
+// CTA kernel (pivoted path / power-iteration condition estimate).
+__global__ void __launch_bounds__(128)
+    herm_inverse_warp_kernel(int64_t B, int K, const c128 *__restrict__ A, int64_t as,
+                             c128 *__restrict__ Ainv, int64_t ais, int32_t *__restrict__ info,
+                             double limit, const uint8_t *__restrict__ mask,
+                             uint8_t *__restrict__ redo) {
+  const int lane = threadIdx.x & 31;
+  const int64_t item = blockIdx.x * int64_t(blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (item >= B) return;
+  if (mask && !mask[item]) return;
+  const c128 *a = A + item * as;
+  c128 m[32];
+  double fa = 0.0;
+#pragma unroll
+  for (int j = 0; j < 32; ++j) {
+    if (lane < K && j < K) {
+      m[j] = a[lane * K + j];
+      fa += cabs2(m[j]);
+    } else {
+      m[j] = mk<double>(lane == j ? 1.0 : 0.0, 0.0);
+    }
+  }
+  fa = warp_sum(fa);
+  __shared__ c128 prow[4][32];
+  c128 *pr_s = prow[threadIdx.x >> 5];
+  bool ok = true;
+#pragma unroll 1
+  for (int k = 0; k < K; ++k) {
+    c128 ci = m[0];  // M[lane][k], selected without dynamic register indexing
+#pragma unroll
+    for (int j = 1; j < 32; ++j)
+      if (j == k) ci = m[j];
+    const double pr = __shfl_sync(0xffffffffu, ci.re, k);
+    const double pi = __shfl_sync(0xffffffffu, ci.im, k);
+    if (!(pr > 0.0) || !isfinite(pr) || !isfinite(pi)) {  // warp-uniform
+      ok = false;
+      break;
+    }
+    const c128 pinv = cinv(mk<double>(pr, pi));
+    if (lane == k) {  // scaled pivot row through shared memory (broadcast reads)
+#pragma unroll
+      for (int j = 0; j < 32; ++j) pr_s[j] = cmul(m[j], pinv);
+    }
+    __syncwarp();
+    // uniform update row_i -= c_i r with c_k = p - 1 (so row k becomes r);
+    // column k is then set to -c_i / p (i != k) and 1 / p (i = k)
+    const c128 c = (lane == k) ? mk<double>(ci.re - 1.0, ci.im) : ci;
+    const c128 colv = (lane == k) ? pinv : cmul(mk<double>(-ci.re, -ci.im), pinv);
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+      const c128 r = pr_s[j];
+      c128 u = m[j];
+      u.re = fma(-c.re, r.re, u.re);
+      u.re = fma(c.im, r.im, u.re);
+      u.im = fma(-c.re, r.im, u.im);
+      u.im = fma(-c.im, r.re, u.im);
+      m[j] = (j == k) ? colv : u;
+    }
+    __syncwarp();
+  }
+  double fi = 0.0;
+#pragma unroll
+  for (int j = 0; j < 32; ++j)
+    if (lane < K && j < K) fi += cabs2(m[j]);
+  fi = warp_sum(fi);
+  const bool good = ok && isfinite(fi) && sqrt(fa) * sqrt(fi) <= limit;
+  if (!good) {
+    if (lane == 0) redo[item] = 1;
+    return;
+  }
+  c128 *o = Ainv + item * ais;
+#pragma unroll
+  for (int j = 0; j < 32; ++j)
+    if (lane < K && j < K) o[lane * K + j] = m[j];
+  if (lane == 0) {
+    redo[item] = 0;
+    if (info) info[item] = LRZ_INFO_OK;
+  }
+}
+
 }  // namespace lrz
 
 using namespace lrz;
@@ -229,7 +315,7 @@ size_t lrz_chain_smem(int K, int D) {
 size_t lrz_wb_ws(int64_t B, int K, int D) { return size_t(B) * wb_ws_elems(K, D) * sizeof(c128); }
 
 static int set_smem(const void *fn, size_t bytes) {
-  if (bytes > 48 * 1024) {
+  if (bytes > 32 * 1024) {  // static shared memory counts against the 48 KB default too
     if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes)) !=
         cudaSuccess) {
       lrz_set_error("cudaFuncSetAttribute(%zu bytes) failed", bytes);
@@ -242,7 +328,6 @@ static int set_smem(const void *fn, size_t bytes) {
 extern "C" int lrz_herm_inverse(int64_t B, int K, const void *A, int64_t a_stride,
                                 void *A_inv, int64_t ai_stride, int32_t *info, double cond_limit,
                                 const uint8_t *item_mask, void *workspace, void *stream) {
-  (void)workspace;
   if (B < 0 || K < 1 || K > 1024 || !A || !A_inv) {
     lrz_set_error("lrz_herm_inverse: bad arguments");
     return LRZ_EINVAL;
@@ -250,8 +335,18 @@ extern "C" int lrz_herm_inverse(int64_t B, int K, const void *A, int64_t a_strid
   if (B == 0) return LRZ_OK;
   const size_t sm = lrz_inverse_smem(K);
   if (set_smem((const void *)herm_inverse_kernel, sm)) return LRZ_ELAUNCH;
-  herm_inverse_kernel<<<unsigned(B), INV_THREADS, sm, (cudaStream_t)stream>>>(
-      K, (const c128 *)A, a_stride, (c128 *)A_inv, ai_stride, info, cond_limit, item_mask);
+  cudaStream_t st = (cudaStream_t)stream;
+  const uint8_t *mask = item_mask;
+  if (K <= 32 && workspace) {
+    // warp-per-matrix fast path; the CTA kernel re-does only flagged items
+    uint8_t *redo = (uint8_t *)workspace;
+    herm_inverse_warp_kernel<<<unsigned((B + 3) / 4), 128, 0, st>>>(
+        B, K, (const c128 *)A, a_stride, (c128 *)A_inv, ai_stride, info, cond_limit, item_mask,
+        redo);
+    mask = redo;
+  }
+  herm_inverse_kernel<<<unsigned(B), INV_THREADS, sm, st>>>(
+      K, (const c128 *)A, a_stride, (c128 *)A_inv, ai_stride, info, cond_limit, mask);
   return lrz_launch_status("lrz_herm_inverse");
 }
 

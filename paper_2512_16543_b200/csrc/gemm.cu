@@ -366,6 +366,165 @@ __global__ void axpby_kernel(int64_t n, double a, const cplx<T> *__restrict__ X,
   }
 }
 
+
+// ---------------------------------------------------------------------------
+// K6 precoder W = H^H A^-1 for one item per CTA (K <= 64): A^-1 staged in
+// shared memory (converted to the input precision), one antenna row n per
+// thread with KB register accumulators, H rows read coalesced along n;
+// ||W||_F^2 reduced in the epilogue (precoding.py:47-48).
+// ---------------------------------------------------------------------------
+template <typename T, int KB>
+__global__ void __launch_bounds__(256)
+    precoder_w_kernel(int K, int N, const cplx<T> *__restrict__ H, int64_t hs,
+                      const c128 *__restrict__ Ainv, int64_t ais, cplx<T> *__restrict__ W,
+                      int64_t wst, double *__restrict__ norm2) {
+  extern __shared__ __align__(16) char pw_smem[];
+  cplx<T> *As = (cplx<T> *)pw_smem;
+  __shared__ double red[8];
+  const int64_t item = blockIdx.x;
+  const c128 *ai = Ainv + item * ais;
+  for (int e = threadIdx.x; e < K * K; e += blockDim.x) As[e] = ccast<T>(ai[e]);
+  __syncthreads();
+  const cplx<T> *h = H + item * hs;
+  cplx<T> *w = W + item * wst;
+  double nrm = 0.0;
+  for (int n = threadIdx.x; n < N; n += blockDim.x) {
+    for (int jb = 0; jb < K; jb += KB) {
+      cplx<T> acc[KB];
+#pragma unroll
+      for (int j = 0; j < KB; ++j) acc[j] = czero<T>();
+#pragma unroll 8
+      for (int k = 0; k < K; ++k) {
+        const cplx<T> hv = h[int64_t(k) * N + n];
+        const cplx<T> *ar = As + k * K + jb;
+#pragma unroll
+        for (int j = 0; j < KB; ++j)
+          if (jb + j < K) cfma_ca(acc[j], hv, ar[j]);
+      }
+#pragma unroll
+      for (int j = 0; j < KB; ++j)
+        if (jb + j < K) {
+          w[int64_t(n) * K + jb + j] = acc[j];
+          nrm += double(acc[j].re) * double(acc[j].re) + double(acc[j].im) * double(acc[j].im);
+        }
+    }
+  }
+  nrm = block_sum(nrm, red);
+  if (threadIdx.x == 0) norm2[item] = nrm;
+}
+
+
+// ---------------------------------------------------------------------------
+// K6 precoder W = H^H A^-1, one item per CTA, K <= 32, 256 threads (2 CTAs/SM).
+// Thread (rg, cg): rows {rg, rg + 64} of each 128-row block, columns
+// {cg + 4 c : c < 8}; H streamed through shared memory in 8-row k-slabs
+// with cp.async double buffering, A^-1 staged once.  2 x 8 complex
+// accumulators per thread keep the kernel FP-pipe bound (10 shared-memory
+// wavefronts per 64 warp-FMAs).  ||W||_F^2 reduced in the epilogue.
+// ---------------------------------------------------------------------------
+constexpr int PW_KC = 8;      // k rows per slab
+constexpr int PW_ROWS = 128;  // antenna rows per block pass
+constexpr int PW_THREADS = 256;
+
+template <typename T>
+LRZ_DEV void cp_async16(void *smem, const void *gmem, bool pred) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  if (sizeof(cplx<T>) == 16) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(sa), "l"(gmem),
+                 "r"(pred ? 16 : 0));
+  } else {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(sa), "l"(gmem),
+                 "r"(pred ? 8 : 0));
+  }
+}
+LRZ_DEV void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+LRZ_DEV void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
+template <typename T>
+__global__ void __launch_bounds__(PW_THREADS, 2)
+    precoder_w32_kernel(int K, int N, const cplx<T> *__restrict__ H, int64_t hs,
+                        const c128 *__restrict__ Ainv, int64_t ais, cplx<T> *__restrict__ W,
+                        int64_t wst, double *__restrict__ norm2) {
+  extern __shared__ __align__(16) char pw2_smem[];
+  cplx<T> *As = (cplx<T> *)pw2_smem;               // [32][32]
+  cplx<T> *Hs = As + 32 * 32;                      // [2][PW_KC][PW_ROWS]
+  __shared__ double red[16];
+  const int tid = threadIdx.x, cg = tid & 3, rg = tid >> 2;
+  const int64_t item = blockIdx.x;
+  const c128 *ai = Ainv + item * ais;
+  for (int e = tid; e < 32 * 32; e += PW_THREADS) {
+    const int k = e >> 5, j = e & 31;
+    As[e] = (k < K && j < K) ? ccast<T>(ai[k * K + j]) : czero<T>();
+  }
+  const cplx<T> *h = H + item * hs;
+  cplx<T> *w = W + item * wst;
+  double nrm = 0.0;
+  const int nslab = (K + PW_KC - 1) / PW_KC;
+  for (int n0 = 0; n0 < N; n0 += PW_ROWS) {
+    cplx<T> acc[2][8];
+#pragma unroll
+    for (int r = 0; r < 2; ++r)
+#pragma unroll
+      for (int c = 0; c < 8; ++c) acc[r][c] = czero<T>();
+    auto issue = [&](int slab, int buf) {
+      // PW_KC x PW_ROWS elements, 4 per thread (coalesced along n)
+#pragma unroll
+      for (int q = 0; q < (PW_KC * PW_ROWS) / PW_THREADS; ++q) {
+        const int e = tid + q * PW_THREADS, kk = e / PW_ROWS, nn = e % PW_ROWS;
+        const int k = slab * PW_KC + kk, n = n0 + nn;
+        const bool ok = (k < K) && (n < N);
+        cp_async16<T>(Hs + (buf * PW_KC + kk) * PW_ROWS + nn,
+                      h + (ok ? int64_t(k) * N + n : 0), ok);
+      }
+      cp_async_commit();
+    };
+    issue(0, 0);
+    for (int sl = 0; sl < nslab; ++sl) {
+      if (sl + 1 < nslab) {
+        issue(sl + 1, (sl + 1) & 1);
+        cp_async_wait<1>();
+      } else {
+        cp_async_wait<0>();
+      }
+      __syncthreads();
+      const cplx<T> *hb = Hs + (sl & 1) * PW_KC * PW_ROWS;
+#pragma unroll
+      for (int kk = 0; kk < PW_KC; ++kk) {
+        const int k = sl * PW_KC + kk;
+        const cplx<T> a0 = hb[kk * PW_ROWS + rg], a1 = hb[kk * PW_ROWS + rg + 64];
+        const cplx<T> *br = As + k * 32 + cg;
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          const cplx<T> b = br[4 * c];
+          cfma_ca(acc[0][c], a0, b);
+          cfma_ca(acc[1][c], a1, b);
+        }
+      }
+      __syncthreads();
+    }
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+      const int n = n0 + rg + 64 * r;
+      if (n < N) {
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          const int j = cg + 4 * c;
+          if (j < K) {
+            w[int64_t(n) * K + j] = acc[r][c];
+            nrm += double(acc[r][c].re) * double(acc[r][c].re) +
+                   double(acc[r][c].im) * double(acc[r][c].im);
+          }
+        }
+      }
+    }
+  }
+  nrm = block_sum(nrm, red);
+  if (tid == 0) norm2[item] = nrm;
+}
+
 }  // namespace lrz
 
 using namespace lrz;
@@ -531,7 +690,43 @@ extern "C" int lrz_precode_rate(int dtype, int64_t B, int K, int N, const void *
   if (G_true) {
     // W = H^H A^-1 (norm partials in the epilogue), coupling from the Gram:
     // H W = (G - alpha I) A^-1, K^3 instead of K^2 N work (F_RF = I)
-    if (dtype == LRZ_C64)
+    int nparts = tm * tn;
+    if (K <= 32) {
+      const size_t es = dtype == LRZ_C64 ? 8 : 16;
+      const size_t sm = (32 * 32 + 2 * PW_KC * PW_ROWS) * es;
+      nparts = 1;
+      if (dtype == LRZ_C64) {
+        cudaFuncSetAttribute(precoder_w32_kernel<float>,
+                               cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
+        precoder_w32_kernel<float><<<unsigned(B), PW_THREADS, sm, s>>>(
+            K, N, (const c64 *)H, h_stride, (const c128 *)A_inv, ai_stride, (c64 *)W, w_stride,
+            parts);
+        if (int rc = lrz_launch_status("precoder_w32_kernel<float>")) return rc;
+      } else {
+        cudaFuncSetAttribute(precoder_w32_kernel<double>,
+                               cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
+        precoder_w32_kernel<double><<<unsigned(B), PW_THREADS, sm, s>>>(
+            K, N, (const c128 *)H, h_stride, (const c128 *)A_inv, ai_stride, (c128 *)W,
+            w_stride, parts);
+        if (int rc = lrz_launch_status("precoder_w32_kernel<double>")) return rc;
+      }
+    } else if (K <= 64) {
+      const size_t sm = size_t(K) * K * (dtype == LRZ_C64 ? 8 : 16);
+      nparts = 1;
+      if (dtype == LRZ_C64) {
+        cudaFuncSetAttribute(precoder_w_kernel<float, 16>,
+                               cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
+        precoder_w_kernel<float, 16><<<unsigned(B), 256, sm, s>>>(
+            K, N, (const c64 *)H, h_stride, (const c128 *)A_inv, ai_stride, (c64 *)W, w_stride,
+            parts);
+      } else {
+        cudaFuncSetAttribute(precoder_w_kernel<double, 16>,
+                               cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
+        precoder_w_kernel<double, 16><<<unsigned(B), 256, sm, s>>>(
+            K, N, (const c128 *)H, h_stride, (const c128 *)A_inv, ai_stride, (c128 *)W,
+            w_stride, parts);
+      }
+    } else if (dtype == LRZ_C64)
       cgemm_kernel<float, float, double, 16><<<g1, GEMM_THREADS, 0, s>>>(
           N, K, K, 2, (const c64 *)H, N, h_stride, 0, (const c128 *)A_inv, K, ai_stride,
           (c64 *)W, K, w_stride, parts, tm, tn);
@@ -542,8 +737,9 @@ extern "C" int lrz_precode_rate(int dtype, int64_t B, int K, int N, const void *
     cgemm_kernel<double, double, double, 16><<<g2, GEMM_THREADS, 0, s>>>(
         K, K, K, 0, (const c128 *)G_true, K, int64_t(K) * K, 0, (const c128 *)A_inv, K,
         ai_stride, (c128 *)Gc, K, int64_t(K) * K, nullptr, tn, tn);
+    if (int rc = lrz_launch_status("coupling cgemm")) return rc;
     sinr_kernel<double><<<unsigned(B), 256, 0, s>>>(
-        K, (const c128 *)Gc, int64_t(K) * K, nullptr, parts, tm * tn, P_t, scale, noise,
+        K, (const c128 *)Gc, int64_t(K) * K, nullptr, parts, nparts, P_t, scale, noise,
         noise_div, rates, sinr, sum_rate, info, (const c128 *)A_inv, ai_stride, alpha);
     return lrz_launch_status("lrz_precode_rate");
   }

@@ -125,8 +125,9 @@ def herm_inverse(A: torch.Tensor, cond_limit: float = 1e14, mask: torch.Tensor |
     if info is None:
         info = torch.zeros(lead if lead else (1,), dtype=torch.int32, device=A.device)
     lib = N.lib_for(A.device)
+    ws = workspace(A.device, lib.lrz_workspace_bytes(N.WS_INVERSE, N.C128, B, K, 0, 0), "inv")
     N.check(lib.lrz_herm_inverse(B, K, A.data_ptr(), K * K, out.data_ptr(), K * K,
-                                 info.data_ptr(), float(cond_limit), N.ptr(mask), None,
+                                 info.data_ptr(), float(cond_limit), N.ptr(mask), ws.data_ptr(),
                                  N.stream_ptr(A.device)), "lrz_herm_inverse")
     _count(1)
     return out, info
