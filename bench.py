@@ -379,6 +379,14 @@ def run_b200(args):
     for name, a, b in prof:
         stage_ms[name] = stage_ms.get(name, 0.0) + a.elapsed_time(b)
     stage_ms = {k: v / args.steps for k, v in stage_ms.items()}
+    if world > 1:
+        # one gather of the per-trial results, merged by trial index
+        from paper_2512_16543_b200.dist import gather_results
+        merged = gather_results({"rates": last.rates.cpu().numpy(),
+                                 "k_est": last.k_est.cpu().numpy(),
+                                 "method": last.method.cpu().numpy()},
+                                trials, world * B, device=dev)
+        assert merged["rates"].shape == (world * B, T)
     method = last.method.cpu().numpy()
     k_est = last.k_est.cpu().numpy()
     iters = last.iters.cpu().numpy()

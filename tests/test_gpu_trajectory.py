@@ -125,3 +125,34 @@ def test_C2_runner_variants_match_reference(cuda, delta, via_gram):
                          keep_A_inv=True)
     for b in (0, 1):
         _compare(res, b, g, f"t{b}_e900_", 24, 1e-10, 1e-10)
+
+
+@pytest.mark.parametrize("name,B,T,dtype,etas", [
+    ("C3", 2, 10, "c64", (0.999, 0.9)),
+    ("C4", 2, 6, "c64", (0.999, 0.9)),
+    ("C5", 1, 4, "c64", (0.999, 0.9)),
+    ("C5", 1, 3, "c128", (0.999,)),
+])
+def test_larger_configs_vs_oracle(cuda, name, B, T, dtype, etas):
+    """C3-C5 shapes (K = 64 / 128 / 256, N = 1024 / 4096) at reduced B and T,
+    every method replayed by the oracle on the identical inputs."""
+    spec = S.CONFIGS[name].with_(B=B, T=T, dtype=dtype)
+    H = S.channels(spec)
+    tol = 1e-10 if dtype == "c128" else 1e-4
+    for eta in (None,) + etas:
+        res = _run(spec, H, eta, list(range(B)))
+        for b in range(B):
+            cfg = None if eta is None else port.Cfg(eta, spec.k_init, spec.p, spec.i_max)
+            sk = None if eta is None else np.random.default_rng(
+                S.stream_seed(spec.seed, S.method_label(eta), b))
+            ref = sweep.sweep_trial(H[b], spec.alpha, S.noise_vector(spec), 1.0, cfg, sk,
+                                    keep_state=True)
+            tie = ref.margin < 1e-6 if dtype == "c64" else ref.margin < 1e-9
+            assert ((res.k_est[b] == ref.k_est) | tie).all(), (name, eta, res.k_est[b], ref.k_est)
+            if not (res.k_est[b] == ref.k_est).all():
+                continue
+            assert np.array_equal(res.method[b], ref.method), (name, eta)
+            assert np.array_equal(res.consumed[b], ref.consumed), (name, eta)
+            err = max(rel(res.A_inv[b, t], ref.A_inv[t]) for t in range(T))
+            assert err < tol, (name, eta, err)
+            assert np.max(np.abs(res.rates[b] / ref.rates - 1)) < tol, (name, eta)
