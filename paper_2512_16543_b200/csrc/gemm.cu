@@ -9,6 +9,7 @@
 
 #include "common.cuh"
 
+
 namespace lrz {
 
 constexpr int TM = 32;        // output tile edge
