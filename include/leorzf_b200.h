@@ -169,12 +169,25 @@ int lrz_sinr_rate(int dtype, int64_t batch, int K, const void *G, int64_t sG,
                   const double *scale, const double *noise, int64_t noise_div, double *rates,
                   double *sinr, double *sum_rate, void *stream);
 
+/* Device sketch streams, bit-exact with numpy's Generator(PCG64).standard_normal
+ * (the reference's Omega source, lowrank.py:284-286).  For each of B streams
+ * with PCG64 state/inc (uint64 lo, hi pairs, as numpy's bit_generator.state
+ * reports them) positioned `raw0[b]` raw draws in, writes the next L
+ * normals to out[b][0..L) and the raw offset (relative to raw0) at which
+ * each normal starts to startpos[b][0..L) (nullable).  status[b] != 0 if
+ * the window could not be produced.  Workspace: lrz_workspace_bytes(
+ * LRZ_WS_RNG, 0, B, 0, L, 0). */
+int lrz_rng_normals(int64_t B, int64_t L, const uint64_t *state, const uint64_t *inc,
+                    const int64_t *raw0, double *out, int32_t *startpos, int32_t *status,
+                    void *workspace, void *stream);
+
 /* Workspace sizing for the calls that take one. */
 #define LRZ_WS_INVERSE 0
 #define LRZ_WS_ARSVD 1
 #define LRZ_WS_WOODBURY 2
 #define LRZ_WS_CHAIN 3
 #define LRZ_WS_PRECODE 4
+#define LRZ_WS_RNG 5
 size_t lrz_workspace_bytes(int op, int dtype, int64_t B, int K, int N, int d_max);
 
 /* Speculative sketch-cursor resolution for the batched runner: one thread

@@ -19,7 +19,7 @@ LIB_PATH = PKG / "_lib" / "libleorzf_b200.so"
 HEADER = PKG.parent / "include" / "leorzf_b200.h"
 
 C64, C128 = 0, 1
-WS_INVERSE, WS_ARSVD, WS_WOODBURY, WS_CHAIN, WS_PRECODE = 0, 1, 2, 3, 4
+WS_INVERSE, WS_ARSVD, WS_WOODBURY, WS_CHAIN, WS_PRECODE, WS_RNG = 0, 1, 2, 3, 4, 5
 
 P = C.c_void_p
 I32, I64, F64, SZ = C.c_int32, C.c_int64, C.c_double, C.c_size_t
@@ -51,6 +51,7 @@ _SIGS = {
     "lrz_fro2": (C.c_int, [C.c_int, I64, I64, P, I64, P, P]),
     "lrz_sinr_rate": (C.c_int, [C.c_int, I64, C.c_int, P, I64, P, P, I64, P, P, P, P]),
     "lrz_plan": (C.c_int, [I64, C.c_int, P, P, P, P]),
+    "lrz_rng_normals": (C.c_int, [I64, I64, P, P, P, P, P, P, P, P]),
     "lrz_workspace_bytes": (SZ, [C.c_int, C.c_int, I64, C.c_int, C.c_int, C.c_int]),
     "lrz_spec_verify": (C.c_int, [I64, C.c_int, C.c_int, C.POINTER(ArsvdCfg), P, P, P, P, P, P,
                                   P, P, P]),

@@ -44,7 +44,14 @@ def _stale() -> bool:
     return any(p.stat().st_mtime > t for p in deps)
 
 
+GEN = CSRC / "_gen" / "ziggurat_tables.h"
+
+
 def build(force: bool = False, verbose: bool = True) -> Path:
+    if not GEN.exists():
+        # numpy's ziggurat tables, read from the installed numpy (rng/tables.py)
+        from .rng import tables
+        tables.write_header(GEN)
     if not force and not _stale():
         return LIB
     OUT_DIR.mkdir(exist_ok=True)

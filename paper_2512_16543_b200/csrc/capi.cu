@@ -25,6 +25,7 @@ int lrz_launch_status(const char *what) {
 size_t lrz_arsvd_ws_total(int64_t B, int K, int D);
 size_t lrz_precode_ws(int dtype, int64_t B, int K, int N);
 size_t lrz_wb_ws(int64_t B, int K, int D);
+size_t lrz_rng_ws(int64_t B, int64_t L);
 
 extern "C" int lrz_version(void) { return 1; }
 
@@ -56,6 +57,8 @@ extern "C" size_t lrz_workspace_bytes(int op, int dtype, int64_t B, int K, int N
       return lrz_wb_ws(B, K, d_max);
     case LRZ_WS_PRECODE:
       return lrz_precode_ws(dtype, B, K, N);
+    case LRZ_WS_RNG:
+      return lrz_rng_ws(B, N);
     default:
       return 0;
   }

@@ -112,3 +112,68 @@ class GeneratorBudget:
         self.rng.bit_generator.state = self._state
         if consumed:
             self.rng.standard_normal(int(consumed))
+
+
+def _split_u128(x: int) -> tuple[int, int]:
+    return x & 0xFFFFFFFFFFFFFFFF, x >> 64
+
+
+class DeviceOmegaStreams:
+    """The same per-trial sketch streams as ``OmegaStreams``, generated on the
+    GPU (``lrz_rng_normals``: PCG64 + numpy's ziggurat) from each Generator's
+    PCG64 state, so neither host RNG time nor the Omega upload appears in the
+    step.  ``window(L)`` -> device tensor [B, L]; ``advance(consumed)`` moves
+    each stream past exactly the normals a device pass consumed (device
+    tensor or array)."""
+
+    def __init__(self, generators, device):
+        import torch
+        from . import _native as Nn, ops
+        self._torch, self._N, self._ops = torch, Nn, ops
+        self.device = torch.device(device)
+        st, inc = [], []
+        for g in generators:
+            s = g.bit_generator.state
+            if s.get("bit_generator") != "PCG64":
+                raise TypeError("device streams reproduce PCG64 Generators only")
+            st.extend(_split_u128(int(s["state"]["state"])))
+            inc.extend(_split_u128(int(s["state"]["inc"])))
+        as_u64 = lambda v: torch.tensor(np.array(v, dtype=np.uint64).view(np.int64),
+                                        dtype=torch.int64, device=self.device)
+        self.B = len(st) // 2
+        self.state = as_u64(st).reshape(self.B, 2)
+        self.inc = as_u64(inc).reshape(self.B, 2)
+        self.raw = torch.zeros(self.B, dtype=torch.int64, device=self.device)
+        self._startpos = None
+        self.consumed_total = torch.zeros(self.B, dtype=torch.int64, device=self.device)
+
+    @classmethod
+    def for_method(cls, master_seed: int, eta: float, trials, device) -> "DeviceOmegaStreams":
+        label = method_label(eta)
+        return cls((np.random.default_rng(stream_seed(master_seed, label, t)) for t in trials),
+                   device)
+
+    def window(self, n: int, out=None):
+        torch = self._torch
+        L = int(n) + 1  # one extra so the position after the last normal is known
+        lib = self._N.lib_for(self.device)
+        full = torch.empty(self.B, L, dtype=torch.float64, device=self.device)
+        self._startpos = torch.empty(self.B, L, dtype=torch.int32, device=self.device)
+        status = torch.zeros(self.B, dtype=torch.int32, device=self.device)
+        ws = self._ops.workspace(self.device, lib.lrz_workspace_bytes(self._N.WS_RNG, 0, self.B,
+                                                                        0, L, 0), "rng")
+        self._N.check(lib.lrz_rng_normals(self.B, L, self.state.data_ptr(), self.inc.data_ptr(),
+                                          self.raw.data_ptr(), full.data_ptr(),
+                                          self._startpos.data_ptr(), status.data_ptr(),
+                                          ws.data_ptr(), self._N.stream_ptr(self.device)),
+                      "lrz_rng_normals")
+        self._status = status
+        self._ops._count(3)
+        return full[:, :n] if out is None else out.copy_(full[:, :n])
+
+    def advance(self, consumed) -> None:
+        torch = self._torch
+        c = torch.as_tensor(consumed, dtype=torch.int64, device=self.device).reshape(self.B)
+        pos = torch.gather(self._startpos, 1, c.reshape(-1, 1)).reshape(-1).to(torch.int64)
+        self.raw += pos
+        self.consumed_total += c

@@ -140,7 +140,8 @@ def arsvd(dA: torch.Tensor, omega: torch.Tensor, cursor: torch.Tensor, eta: floa
     """K2+K3 over a flat batch of items.  dA [B,K,K] c128; omega [R,L] f64;
     cursor [B] int64; omega_row [B] int32 (row of omega per item, default = item)."""
     _chk(dA, "dA")
-    _chk(omega, "omega")
+    if not omega.is_cuda or omega.dim() != 2 or omega.stride(1) != 1:
+        raise ValueError("omega must be a [R, L] CUDA tensor with contiguous rows")
     B = dA.shape[0]
     K = dA.shape[-1]
     D = d_max_for(K, k_init, p, i_max)
@@ -159,7 +160,7 @@ def arsvd(dA: torch.Tensor, omega: torch.Tensor, cursor: torch.Tensor, eta: floa
     lib = N.lib_for(dev)
     nbytes = lib.lrz_workspace_bytes(N.WS_ARSVD, N.C128, B, K, 0, D)
     ws = workspace(dev, nbytes, "arsvd")
-    N.check(lib.lrz_arsvd(B, K, dA.data_ptr(), K * K, omega.data_ptr(), omega.shape[-1],
+    N.check(lib.lrz_arsvd(B, K, dA.data_ptr(), K * K, omega.data_ptr(), omega.stride(0),
                           N.ptr(omega_row), cursor.data_ptr(), C.byref(cfg), out["U"].data_ptr(),
                           out["V"].data_ptr(), out["S"].data_ptr(), out["k_est"].data_ptr(),
                           out["iters"].data_ptr(), out["fallback"].data_ptr(),

@@ -280,7 +280,8 @@ def run_trajectory(H, noise, cfg: TrajectoryConfig, streams: OmegaStreams | None
                    chunk: int | None = None, keep_A_inv: bool = False,
                    device=None) -> TrajectoryResult:
     """Run B trials x T steps.  H: numpy or torch [B, T, K, N]; noise [K] or
-    [B, K]; streams: per-trial sketch streams (required for WB)."""
+    [B, K]; streams: per-trial sketch streams (required for WB): host
+    ``OmegaStreams`` or GPU-generated ``DeviceOmegaStreams`` (same normals)."""
     dev = torch.device(device) if device is not None else (
         H.device if isinstance(H, torch.Tensor) and H.is_cuda else torch.device("cuda", 0))
     if isinstance(H, np.ndarray):
@@ -303,11 +304,14 @@ def run_trajectory(H, noise, cfg: TrajectoryConfig, streams: OmegaStreams | None
         om = None
         if cfg.eta is not None:
             L = (t1 - t0) * runner.normals_per_step_max()
-            om = torch.from_numpy(streams.window(L)).to(dev)
+            om = streams.window(L)
+            if isinstance(om, np.ndarray):  # host streams (OmegaStreams); device streams stay put
+                om = torch.from_numpy(om).to(dev)
         r = runner.run_chunk(Hc, noise_d, om, keep_A_inv=keep_A_inv)
         if cfg.eta is not None:
             used = r.consumed.cpu().numpy()
-            streams.advance(used)
+            streams.advance(r.consumed if isinstance(om, torch.Tensor) and
+                            not isinstance(streams, OmegaStreams) else used)
             cons_total += used
         passes.append(r.spec_passes)
         outs.append(r)

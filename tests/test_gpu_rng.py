@@ -1,0 +1,55 @@
+"""Device sketch streams vs numpy's Generator(PCG64).standard_normal."""
+
+import numpy as np
+import pytest
+import torch
+
+from paper_2512_16543_b200 import scenario as S
+from paper_2512_16543_b200.omega import DeviceOmegaStreams, OmegaStreams
+
+pytestmark = pytest.mark.gpu
+
+
+def test_device_normals_match_numpy(cuda):
+    trials = [0, 1, 5, 63]
+    dev = DeviceOmegaStreams.for_method(0, 0.999, trials, cuda)
+    host = OmegaStreams.for_method(0, 0.999, trials)
+    for L, used in [(50000, [3200, 0, 12345, 49999]), (70000, [7, 7, 7, 7]), (1000, [1000] * 4)]:
+        d = dev.window(L).cpu().numpy()
+        h = host.window(L)
+        assert int(dev._status.sum().item()) == 0
+        same = (d == h)
+        # bit-exact except ziggurat tail values, which go through log1p (ulp-level)
+        assert same.mean() > 0.999, same.mean()
+        ulp = np.abs(d - h) / np.maximum(np.abs(h), 1e-300)
+        assert ulp.max() < 1e-14
+        dev.advance(used)
+        host.advance(used)
+    assert np.array_equal(dev.consumed_total.cpu().numpy(), host.consumed_total)
+
+
+def test_device_streams_drive_the_runner(cuda):
+    """A C2-sample trajectory with device sketches equals the reference golden."""
+    from conftest import load_golden
+    from paper_2512_16543_b200 import TrajectoryConfig, TrajectoryRunner
+    g = load_golden("traj_C2s")
+    spec = S.C2
+    H = torch.from_numpy(S.channels(spec, trials=[0, 1], t1=24)).to(cuda)
+    cfg = TrajectoryConfig(alpha=spec.alpha, eta=0.9, k_init=spec.k_init, p=spec.p,
+                           i_max=spec.i_max)
+    rn = TrajectoryRunner(2, spec.K, spec.N, torch.complex128, cfg, cuda)
+    st = DeviceOmegaStreams.for_method(0, 0.9, [0, 1], cuda)
+    noise = torch.full((2, spec.K), spec.noise_var, dtype=torch.float64, device=cuda)
+    ks, rates = [], []
+    for t0 in (0, 10):
+        t1 = 10 if t0 == 0 else 24
+        om = st.window((t1 - t0) * rn.normals_per_step_max())
+        r = rn.run_chunk(H[:, t0:t1].contiguous(), noise, om)
+        st.advance(r.consumed)
+        ks.append(r.k_est.cpu().numpy())
+        rates.append(r.rates.cpu().numpy())
+    k = np.concatenate(ks, 1)
+    rt = np.concatenate(rates, 1)
+    for b in (0, 1):
+        assert np.array_equal(k[b], g[f"t{b}_e900_k_est"])
+        assert np.allclose(rt[b], g[f"t{b}_e900_rates"], rtol=1e-10)
