@@ -302,7 +302,7 @@ def run_b200(args):
     import torch.distributed as dist
 
     from paper_2512_16543_b200 import ops, scenario as S
-    from paper_2512_16543_b200.omega import OmegaStreams
+    from paper_2512_16543_b200.omega import DeviceOmegaStreams
     from paper_2512_16543_b200.trajectory import TrajectoryConfig, TrajectoryRunner
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -339,14 +339,23 @@ def run_b200(args):
                               i_max=spec.i_max)
     cfg_full = TrajectoryConfig(alpha=spec.alpha, eta=None)
     L = T * TrajectoryRunner(B, K, Nn, tdt, cfg_wb, dev).normals_per_step_max()
-    om_pin = torch.from_numpy(OmegaStreams.for_method(spec.seed, eta, trials).window(L)).pin_memory()
-    om_dev = om_pin.to(dev)
+    # sketch streams: the harness's per-(method, trial) PCG64 Generators
+    # (harness.py:88-92), reproduced on the device; each step regenerates its
+    # window from the stream start so every timed step does identical work
+    streams = DeviceOmegaStreams.for_method(spec.seed, eta, trials, dev)
     stream = torch.cuda.current_stream(dev)
 
-    def one(cfg, prof=None, Hd=H_dev, od=om_dev):
-        rn = TrajectoryRunner(B, K, Nn, tdt, cfg, dev)
+    def one(cfg, prof=None, Hd=H_dev, st=streams, sl=slice(None)):
+        nb = Hd.shape[0]
+        rn = TrajectoryRunner(nb, K, Nn, tdt, cfg, dev)
         rn.prof = prof
-        return rn.run_chunk(Hd, noise, od if cfg.eta is not None else None)
+        om = None
+        if cfg.eta is not None:
+            st.raw.zero_()
+            e0 = rn._ev()
+            om = st.window(L)
+            rn._stage("omega_rng", e0)
+        return rn.run_chunk(Hd, noise[sl], om)
 
     def timed(cfg, steps, prof=None):
         barrier()
@@ -422,34 +431,63 @@ def run_b200(args):
         else:
             all_stages[k] = {"ms": v}
 
-    # ---- e2e: host (pinned) inputs -> device -> results back, every step
+    # ---- e2e: host (pinned) channels -> device -> results back, every step.
+    # Trials are split into groups; group g+1's H2D (copy stream) overlaps group
+    # g's compute (compute stream).  Omega is generated on the device.
     e2e = None
     if not args.no_e2e:
-        H_d2 = torch.empty_like(H_dev)
-        om_d2 = torch.empty_like(om_dev)
+        ng = 4 if B % 4 == 0 else 1
+        bs = B // ng
+        gstreams = [DeviceOmegaStreams.for_method(spec.seed, eta, trials[g * bs:(g + 1) * bs], dev)
+                    for g in range(ng)]
+        bufs = [torch.empty((bs,) + tuple(H_dev.shape[1:]), dtype=H_dev.dtype, device=dev)
+                for _ in range(2)]
+        copy_s = torch.cuda.Stream(dev)
+        outs_pin = {}
         n_e2e = max(2, min(args.steps, 3))
+
+        def e2e_step():
+            freed = [torch.cuda.Event(), torch.cuda.Event()]
+            copied = []
+            for g in range(ng):
+                with torch.cuda.stream(copy_s):
+                    if g >= 2:
+                        copy_s.wait_event(freed[g % 2])
+                    bufs[g % 2].copy_(H_pin[g * bs:(g + 1) * bs], non_blocking=True)
+                    ev = torch.cuda.Event()
+                    ev.record(copy_s)
+                    copied.append(ev)
+                stream.wait_event(copied[g])
+                r = one(cfg_wb, None, bufs[g % 2], gstreams[g], slice(g * bs, (g + 1) * bs))
+                freed[g % 2] = torch.cuda.Event()
+                freed[g % 2].record(stream)
+                for name in ("rates", "per_ut", "method", "k_est"):
+                    t = getattr(r, name)
+                    key = (name, g)
+                    if key not in outs_pin:
+                        outs_pin[key] = torch.empty(t.shape, dtype=t.dtype).pin_memory()
+                    outs_pin[key].copy_(t, non_blocking=True)
+
+        e2e_step()
         barrier()
         torch.cuda.synchronize(dev)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
-        d2h = 0
         for _ in range(n_e2e):
-            H_d2.copy_(H_pin, non_blocking=True)
-            om_d2.copy_(om_pin, non_blocking=True)
-            r = one(cfg_wb, None, H_d2, om_d2)
-            outs = [r.rates.cpu(), r.per_ut.cpu(), r.method.cpu(), r.k_est.cpu()]
-            d2h = sum(o.numel() * o.element_size() for o in outs)
+            e2e_step()
         e1.record(stream)
         torch.cuda.synchronize(dev)
         barrier()
         ms_e2e = max_over_ranks(e0.elapsed_time(e1)) / n_e2e
+        d2h = sum(t.numel() * t.element_size() for t in outs_pin.values())
         e2e = {"value": world * updates / (ms_e2e / 1e3), "unit": "updates/s",
-               "h2d_bytes_per_step": H_pin.numel() * H_pin.element_size()
-               + om_pin.numel() * om_pin.element_size(),
+               "h2d_bytes_per_step": H_pin.numel() * H_pin.element_size(),
                "d2h_bytes_per_step": d2h, "ms_per_step": ms_e2e,
-               "path": "TrajectoryRunner.run_chunk (public batched API over the C ABI) with "
-                       "pinned host H and Omega copied in and rates/method/k_est copied out"}
-        del H_d2, om_d2
+               "path": "TrajectoryRunner.run_chunk (public batched API over the C ABI): pinned "
+                       f"host H copied in per step in {ng} trial groups overlapped with compute; "
+                       "Omega generated on the device from the harness's PCG64 streams; "
+                       "rates/per-UT rates/method/k_est copied out"}
+        del bufs
 
     # ---- c64 side measurement (same workload, complex64 inputs)
     extra = None
@@ -459,7 +497,11 @@ def run_b200(args):
 
         def one64(cfg):
             rn = TrajectoryRunner(B, K, Nn, torch.complex64, cfg, dev)
-            return rn.run_chunk(H64, noise, om_dev if cfg.eta is not None else None)
+            om = None
+            if cfg.eta is not None:
+                streams.raw.zero_()
+                om = streams.window(L)
+            return rn.run_chunk(H64, noise, om)
 
         for cfg in (cfg_wb, cfg_full):
             one64(cfg)
@@ -511,6 +553,9 @@ def run_b200(args):
             "e2e": e2e,
             "gpu_launches": launches,
             "spec_passes": last.spec_passes,
+            "omega": "generated on the device each step (PCG64 + numpy ziggurat, the "
+                     "harness's per-(method, trial) streams; bit-exact except ulp-level "
+                     "log1p tail values)",
             "method_counts": {"full": int((method == 0).sum()), "woodbury": wb_steps,
                               "none": int((method == 2).sum())},
             "clocks": clk.summary(),
