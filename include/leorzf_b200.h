@@ -181,6 +181,15 @@ int lrz_rng_normals(int64_t B, int64_t L, const uint64_t *state, const uint64_t 
                     const int64_t *raw0, double *out, int32_t *startpos, int32_t *status,
                     void *workspace, void *stream);
 
+/* On-device synthetic channels (scenario.py, SURVEY 8(f) "next" #1): H for
+ * steps [t0, t0 + T) of B trials, [B][T][K][N] of `dtype`.  params: [B][6][K]
+ * doubles (theta0, psi, phi, beta, kappa, drift per user); scatter: [B] rows
+ * of 2 K N standard normals (real block then imaginary block, the trial's
+ * channel stream), row stride scatter_stride.  N = n_side^2. */
+int lrz_channels(int dtype, int64_t B, int t0, int T, int K, int N, int n_side,
+                 const double *params, const double *scatter, int64_t scatter_stride, void *H,
+                 void *stream);
+
 /* Workspace sizing for the calls that take one. */
 #define LRZ_WS_INVERSE 0
 #define LRZ_WS_ARSVD 1

@@ -52,6 +52,8 @@ _SIGS = {
     "lrz_sinr_rate": (C.c_int, [C.c_int, I64, C.c_int, P, I64, P, P, I64, P, P, P, P]),
     "lrz_plan": (C.c_int, [I64, C.c_int, P, P, P, P]),
     "lrz_rng_normals": (C.c_int, [I64, I64, P, P, P, P, P, P, P, P]),
+    "lrz_channels": (C.c_int, [C.c_int, I64, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, P, P,
+                               I64, P, P]),
     "lrz_workspace_bytes": (SZ, [C.c_int, C.c_int, I64, C.c_int, C.c_int, C.c_int]),
     "lrz_spec_verify": (C.c_int, [I64, C.c_int, C.c_int, C.POINTER(ArsvdCfg), P, P, P, P, P, P,
                                   P, P, P]),

@@ -133,12 +133,13 @@ class TrialDraw:
     scatter: np.ndarray | None = field(default=None, repr=False)  # (K, N)
 
 
-def draw_trial(spec: ScenarioSpec, trial: int) -> TrialDraw:
+def draw_trial(spec: ScenarioSpec, trial: int, scatter: bool = True) -> TrialDraw:
     """Draw one trial's user parameters from its channel stream.
 
     Draw order (fixed, part of the fixture contract): cos(theta0),
     psi, phi, beta_dB, kappa_dB, drift, then the scatter S (real block,
-    then imaginary block, K x N row-major)."""
+    then imaginary block, K x N row-major).  scatter=False stops before S
+    (the device synthesis draws S from the same stream on the GPU)."""
     K, N = spec.K, spec.N
     rng = np.random.default_rng(stream_seed(spec.seed, CHANNEL_STREAM, trial))
     cos_lo = math.cos(math.radians(spec.cone_deg))
@@ -149,7 +150,8 @@ def draw_trial(spec: ScenarioSpec, trial: int) -> TrialDraw:
     kappa = 10.0 ** (rng.uniform(spec.kappa_db[0], spec.kappa_db[1], K) / 10.0)
     drift = np.radians(rng.uniform(spec.drift_deg[0], spec.drift_deg[1], K))
     d = TrialDraw(theta0, psi, phi, beta, kappa, drift, rng)
-    d.scatter = _cn(rng, K, N)
+    if scatter:
+        d.scatter = _cn(rng, K, N)
     return d
 
 
@@ -200,3 +202,42 @@ def channels(spec: ScenarioSpec, trials=None, t0: int = 0, t1: int | None = None
 
 def noise_vector(spec: ScenarioSpec) -> np.ndarray:
     return np.full(spec.K, spec.noise_var)
+
+
+class DeviceChannels:
+    """The same channels as ``channels(spec, trials)``, synthesised on the GPU
+    (``lrz_channels``): per-trial angles and gains are drawn on the host (6 K
+    numbers), the scatter S from the trial's channel stream by the device RNG,
+    and H_t for any step range is formed on the device -- no channel tensor
+    crosses PCIe and C3/C4-sized passes can be streamed chunk by chunk."""
+
+    def __init__(self, spec: ScenarioSpec, trials, device):
+        import torch
+        from . import _native as Nn
+        from .omega import DeviceOmegaStreams
+        if spec.redraw_scatter:
+            raise NotImplementedError("device synthesis holds the scatter per trial")
+        self.spec, self.trials = spec, list(trials)
+        self.device = torch.device(device)
+        self._torch, self._N = torch, Nn
+        draws = [draw_trial(spec, t, scatter=False) for t in self.trials]
+        par = np.stack([np.stack([d.theta0, d.psi, d.phi, d.beta, d.kappa, d.drift])
+                        for d in draws])                                  # [B, 6, K]
+        self.params = torch.from_numpy(np.ascontiguousarray(par)).to(self.device)
+        st = DeviceOmegaStreams([d.rng for d in draws], self.device)
+        self.scatter = st.window(2 * spec.K * spec.N)                    # [B, 2KN] (strided rows)
+        if int(st._status.sum().item()):
+            raise RuntimeError("device RNG could not produce the scatter window")
+
+    def generate(self, t0: int, t1: int, out=None):
+        torch = self._torch
+        s = self.spec
+        dt = torch.complex64 if s.dtype == "c64" else torch.complex128
+        B, T = len(self.trials), t1 - t0
+        H = out if out is not None else torch.empty(B, T, s.K, s.N, dtype=dt, device=self.device)
+        lib = self._N.lib_for(self.device)
+        self._N.check(lib.lrz_channels(0 if dt == torch.complex64 else 1, B, t0, T, s.K, s.N,
+                                       s.n_side, self.params.data_ptr(), self.scatter.data_ptr(),
+                                       self.scatter.stride(0), H.data_ptr(),
+                                       self._N.stream_ptr(self.device)), "lrz_channels")
+        return H

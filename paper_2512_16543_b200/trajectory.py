@@ -336,3 +336,53 @@ def run_trajectory(H, noise, cfg: TrajectoryConfig, streams: OmegaStreams | None
         method=method, k_est=k_est, iters=iters,
         cost=step_costs(method, k_est, sk_mask, K), consumed=cons, spec_passes=passes,
         A_inv=(torch.cat([o.A_inv for o in outs], 1).cpu().numpy() if keep_A_inv else None))
+
+
+def run_campaign_device(spec, eta, trials, device=None, chunk: int | None = None,
+                        keep: bool = True) -> TrajectoryResult:
+    """A whole synthetic pass for the given trials with everything on the
+    GPU: channels synthesised per time chunk (``scenario.DeviceChannels``),
+    sketches from the device RNG (``DeviceOmegaStreams``, the harness's
+    per-(method, trial) streams), then the runner.  Only the per-step results
+    come back to the host.  eta None = conventional method."""
+    from . import scenario as S
+    from .omega import DeviceOmegaStreams
+    dev = torch.device(device) if device is not None else torch.device("cuda", 0)
+    trials = list(trials)
+    B, T, K, Nn = len(trials), spec.T, spec.K, spec.N
+    chunk = T if chunk is None else chunk
+    tdt = torch.complex64 if spec.dtype == "c64" else torch.complex128
+    cfg = TrajectoryConfig(alpha=spec.alpha, eta=eta, k_init=spec.k_init, p=spec.p,
+                           i_max=spec.i_max)
+    chans = S.DeviceChannels(spec, trials, dev)
+    streams = None if eta is None else DeviceOmegaStreams.for_method(spec.seed, eta, trials, dev)
+    noise = torch.full((B, K), spec.noise_var, dtype=torch.float64, device=dev)
+    runner = TrajectoryRunner(B, K, Nn, tdt, cfg, dev)
+    outs, passes = [], []
+    for t0 in range(0, T, chunk):
+        t1 = min(T, t0 + chunk)
+        H = chans.generate(t0, t1)
+        om = None if eta is None else streams.window((t1 - t0) * runner.normals_per_step_max())
+        r = runner.run_chunk(H, noise, om)
+        if eta is not None:
+            streams.advance(r.consumed)
+        passes.append(r.spec_passes)
+        if keep:
+            outs.append({k: getattr(r, k).cpu() for k in ("rates", "per_ut", "method", "k_est",
+                                                             "iters", "info")})
+        del H
+    if not keep:
+        return None
+    cat = {k: torch.cat([o[k] for o in outs], 1).numpy() for k in outs[0]}
+    if np.any(cat["info"] == 1):
+        b, t = np.argwhere(cat["info"] == 1)[0]
+        raise SingularMatrixError(f"trial {trials[b]} step {t}: condition estimate exceeds 1e14")
+    tg = np.arange(T)
+    sk_mask = (np.broadcast_to((tg > 0) & ~((cfg.n_reset > 0) & (tg % max(cfg.n_reset, 1) == 0)),
+                               (B, T)) if eta is not None else np.zeros((B, T), bool))
+    cons = (consumed_by(cat["iters"], K, cfg.k_init, cfg.p, cfg.i_max) if eta is not None
+            else np.zeros((B, T), np.int64))
+    return TrajectoryResult(rates=cat["rates"], per_ut=cat["per_ut"], method=cat["method"],
+                            k_est=cat["k_est"], iters=cat["iters"],
+                            cost=step_costs(cat["method"], cat["k_est"], sk_mask, K),
+                            consumed=cons, spec_passes=passes)

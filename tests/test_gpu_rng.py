@@ -53,3 +53,45 @@ def test_device_streams_drive_the_runner(cuda):
     for b in (0, 1):
         assert np.array_equal(k[b], g[f"t{b}_e900_k_est"])
         assert np.allclose(rt[b], g[f"t{b}_e900_rates"], rtol=1e-10)
+
+
+@pytest.mark.parametrize("name,dtype", [("C1", "c128"), ("C2", "c128"), ("C3", "c64")])
+def test_device_channels_match_host(cuda, name, dtype):
+    spec = S.CONFIGS[name].with_(dtype=dtype, B=3, T=7)
+    dc = S.DeviceChannels(spec, [0, 1, 2], cuda)
+    Hd = dc.generate(2, 7).cpu().numpy()
+    Hh = S.channels(spec, trials=[0, 1, 2], t0=2, t1=7)
+    err = np.abs(Hd - Hh).max() / np.abs(Hh).max()
+    assert err < (1e-13 if dtype == "c128" else 1e-6), err
+
+
+def test_device_channels_drive_golden_trajectory(cuda):
+    from conftest import load_golden
+    from paper_2512_16543_b200 import TrajectoryConfig, run_trajectory
+    g = load_golden("traj_C2s")
+    spec = S.C2.with_(B=2, T=24)
+    H = S.DeviceChannels(spec, [0, 1], cuda).generate(0, 24)
+    cfg = TrajectoryConfig(alpha=spec.alpha, eta=0.9, k_init=spec.k_init, p=spec.p,
+                           i_max=spec.i_max)
+    res = run_trajectory(H, S.noise_vector(spec), cfg,
+                         DeviceOmegaStreams.for_method(0, 0.9, [0, 1], cuda))
+    for b in (0, 1):
+        assert np.array_equal(res.k_est[b], g[f"t{b}_e900_k_est"])
+        assert np.allclose(res.rates[b], g[f"t{b}_e900_rates"], rtol=1e-10)
+
+
+def test_campaign_device_chunked_matches_host_path(cuda):
+    """Everything-on-device campaign (synthesised channels, device sketches,
+    time chunks) equals the host-input runner on the same trials."""
+    from paper_2512_16543_b200 import TrajectoryConfig, run_trajectory
+    from paper_2512_16543_b200.trajectory import run_campaign_device
+    spec = S.C2.with_(B=3, T=30)
+    dev_res = run_campaign_device(spec, 0.9, [0, 1, 2], cuda, chunk=11)
+    H = S.channels(spec, trials=[0, 1, 2])
+    cfg = TrajectoryConfig(alpha=spec.alpha, eta=0.9, k_init=spec.k_init, p=spec.p,
+                           i_max=spec.i_max)
+    host_res = run_trajectory(H, S.noise_vector(spec), cfg,
+                              OmegaStreams.for_method(0, 0.9, [0, 1, 2]))
+    assert np.array_equal(dev_res.k_est, host_res.k_est)
+    assert np.array_equal(dev_res.method, host_res.method)
+    assert np.allclose(dev_res.rates, host_res.rates, rtol=1e-10)
