@@ -262,18 +262,15 @@ class TrajectoryRunner:
 def step_costs(method: np.ndarray, k_est: np.ndarray, is_sketch: np.ndarray, K: int) -> np.ndarray:
     """Cost units per step as the harness records them (harness.py:233,239):
     resets cost K^3; dispatcher full = K^3 + sketch; woodbury; none."""
-    out = np.empty(method.shape, dtype=float)
-    for idx in np.ndindex(method.shape):
-        m, k, sk = int(method[idx]), int(k_est[idx]), bool(is_sketch[idx])
-        if not sk:
-            out[idx] = cost_full(K)
-        elif m == 0:
-            out[idx] = cost_full(K) + sketch_cost(K, k)
-        elif m == 1:
-            out[idx] = cost_wb_arsvd(K, k)
-        else:
-            out[idx] = cost_wb_arsvd(K, 0)
-    return out
+    m = np.asarray(method)
+    k = np.asarray(k_est).astype(float)
+    sk = np.asarray(is_sketch, dtype=bool)
+    Kf = float(K)
+    full = cost_full(K)
+    sketch = Kf ** 2 * k + k ** 2 * Kf                        # sketch_cost(K, k)
+    wb = Kf ** 2 + Kf ** 2 * k + k ** 3 + k ** 2 * Kf         # cost_wb_arsvd(K, k)
+    out = np.where(m == 0, full + sketch, np.where(m == 1, wb, cost_wb_arsvd(K, 0)))
+    return np.where(sk, out, full).astype(float)
 
 
 def run_trajectory(H, noise, cfg: TrajectoryConfig, streams: OmegaStreams | None = None,
