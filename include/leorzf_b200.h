@@ -190,6 +190,61 @@ int lrz_channels(int dtype, int64_t B, int t0, int T, int K, int N, int n_side,
                  const double *params, const double *scatter, int64_t scatter_stride, void *H,
                  void *stream);
 
+/* ---- hybrid (analog beams + digital RZF) LEO pass, SURVEY 8(f) "next" #3/#4 ---- */
+
+/* Scenario constants of one LEO pass (reference config.py:27-60, channel.py:24-29). */
+typedef struct {
+  int K, n_x, n_y, N_RF;
+  int beam_hold;        /* snapshots the analog beams are held for (config.py:62) */
+  int nlos_block;       /* snapshots an NLOS draw is held for (config.py:61) */
+  double wavelength;    /* c / carrier_Hz */
+  double spacing_m;     /* spacing_wavelengths * wavelength */
+  double orbit_radius;  /* R_earth + altitude_m */
+  double orbit_rate;    /* sqrt(GM / R^3) */
+  double pass_s, dt;    /* pass length, 1 / update_rate_Hz */
+  double min_elev_rad;  /* elevation mask */
+  double atm_loss_dB;
+} lrz_leo_cfg;
+
+/* One snapshot per (trial, step) for steps [t0, t0 + T) of B trials
+ * (channel.py:352-384 + harness.py:221-226): pass geometry at t*dt, the
+ * conjugated unit-gain manifold rows H~, Rician H = w_los g H~ + w_nlos
+ * (g/sqrt(N)) S, the DFT beam powers |fft2(H~)|^2 (ortho), the greedy beam
+ * choice (channel.py:202-233; beams re-selected every beam_hold steps), and
+ *   H_eff = H~ F_RF  (K x N_RF),   H_rf = H F_RF  (K x N_RF),   cols (N_RF),
+ * F_RF = codebook columns `cols` of kron(DFT(n_x), DFT(n_y)).
+ * ut: [B][K][5] doubles (ECEF x, y, z, gain dBi, Rician K linear).
+ * dft: the two unitary DFT factors, n_x^2 then n_y^2 complex128.
+ * nlos: [B] rows (stride nlos_stride) of standard normals starting at NLOS
+ * block floor(t0 / nlos_block) (each block: K*N real then K*N imaginary).
+ * H_full / H_tilde (nullable): [B][T][K][N] complex128 for parity tests.
+ * info[b][t] = LRZ_INFO_BELOW_MASK if a UT is under the elevation mask. */
+#define LRZ_INFO_BELOW_MASK 5        /* BelowMinElevationError  channel.py:280-284 */
+int lrz_leo_snapshot(const lrz_leo_cfg *cfg, int64_t B, int t0, int T, const double *ut,
+                     const void *dft, const double *nlos, int64_t nlos_stride, void *H_eff,
+                     void *H_rf, int32_t *cols, int32_t *info, void *H_full, void *H_tilde,
+                     void *stream);
+
+/* Hybrid precoder + rate per item (precoding.py:37-80 with F_RF = DFT codebook
+ * columns `cols`): F_raw = H_eff^H A^-1, scale = sqrt(P_t)/||F_RF F_raw||_F,
+ * G = H_rf (scale F_raw), SINR / log2(1 + SINR).  All complex128; items are
+ * contiguous [B][K][N_RF] / [B][K][K] / [B][N_RF]; F_BB nullable [B][N_RF][K];
+ * noise row = item / noise_div. */
+int lrz_hybrid_precode_rate(int64_t B, int K, int N_RF, int n_x, int n_y, const void *H_eff,
+                            const void *A_inv, const void *H_rf, const int32_t *cols,
+                            const void *dft, double P_t, const double *noise, int64_t noise_div,
+                            void *F_BB, double *scale, double *rates, double *sum_rate,
+                            int32_t *info, void *stream);
+
+/* Per-trial campaign aggregates over steps [t_base, t_base + T) of B trials,
+ * ACCUMULATED into stats[b][6] = (total cost units, k_sum, k_count, n_full,
+ * n_woodbury, n_none) with the harness's accounting (harness.py:227-251):
+ * reset steps (t == 0, t % n_reset == 0, or conventional) cost K^3;
+ * otherwise the dispatcher's cost (lowrank.py:101-118, 345-373). */
+int lrz_campaign_reduce(int64_t B, int T, int t_base, int K, int n_reset, int conventional,
+                        const uint8_t *method, const int32_t *k_est, double *stats,
+                        void *stream);
+
 /* Workspace sizing for the calls that take one. */
 #define LRZ_WS_INVERSE 0
 #define LRZ_WS_ARSVD 1

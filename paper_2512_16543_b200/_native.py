@@ -30,6 +30,14 @@ class ArsvdCfg(C.Structure):
                 ("i_max", C.c_int), ("d_max", C.c_int)]
 
 
+class LeoCfg(C.Structure):
+    _fields_ = [("K", C.c_int), ("n_x", C.c_int), ("n_y", C.c_int), ("N_RF", C.c_int),
+                ("beam_hold", C.c_int), ("nlos_block", C.c_int), ("wavelength", C.c_double),
+                ("spacing_m", C.c_double), ("orbit_radius", C.c_double),
+                ("orbit_rate", C.c_double), ("pass_s", C.c_double), ("dt", C.c_double),
+                ("min_elev_rad", C.c_double), ("atm_loss_dB", C.c_double)]
+
+
 _SIGS = {
     "lrz_version": (C.c_int, []),
     "lrz_last_error": (C.c_char_p, []),
@@ -54,6 +62,12 @@ _SIGS = {
     "lrz_rng_normals": (C.c_int, [I64, I64, P, P, P, P, P, P, P, P]),
     "lrz_channels": (C.c_int, [C.c_int, I64, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, P, P,
                                I64, P, P]),
+    "lrz_leo_snapshot": (C.c_int, [C.POINTER(LeoCfg), I64, C.c_int, C.c_int, P, P, P, I64, P,
+                                   P, P, P, P, P, P]),
+    "lrz_hybrid_precode_rate": (C.c_int, [I64, C.c_int, C.c_int, C.c_int, C.c_int, P, P, P, P,
+                                          P, F64, P, I64, P, P, P, P, P, P]),
+    "lrz_campaign_reduce": (C.c_int, [I64, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, P, P,
+                                      P, P]),
     "lrz_workspace_bytes": (SZ, [C.c_int, C.c_int, I64, C.c_int, C.c_int, C.c_int]),
     "lrz_spec_verify": (C.c_int, [I64, C.c_int, C.c_int, C.POINTER(ArsvdCfg), P, P, P, P, P, P,
                                   P, P, P]),

@@ -46,6 +46,10 @@ class UnsupportedGeometryError(SimulationError):
     """Array geometry outside what an operation supports (errors.py:41)."""
 
 
+class BelowMinElevationError(SimulationError):
+    """A served user terminal is below the elevation mask (errors.py:45)."""
+
+
 class ZeroPrecoderError(SimulationError):
     """Precoder has zero Frobenius norm (errors.py:49)."""
 

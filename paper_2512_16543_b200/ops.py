@@ -324,3 +324,73 @@ def spec_verify(is_sketch, iters_pred, iters_act, cursor, cursor0, first_unverif
                                 active.data_ptr(), pending.data_ptr(), N.stream_ptr(dev)),
             "lrz_spec_verify")
     _count(1)
+
+
+# -- hybrid LEO pass (leo.cu) ------------------------------------------------------------
+
+def leo_snapshot(cfg, B: int, t0: int, T: int, ut: torch.Tensor, dft: torch.Tensor,
+                 nlos: torch.Tensor, want_channels: bool = False):
+    """Snapshots of steps [t0, t0+T) for B trials.  cfg: _native.LeoCfg; ut
+    [B,K,5] f64; dft: c128 [nx*nx + ny*ny]; nlos [B, L] f64 (row stride free)
+    starting at NLOS block t0 // nlos_block.  Returns dict(H_eff, H_rf
+    [B,T,K,N_RF] c128, cols [B,T,N_RF] int32, info [B,T] int32, and H,
+    H_tilde [B,T,K,N] when want_channels)."""
+    dev = ut.device
+    K, R, Nn = cfg.K, cfg.N_RF, cfg.n_x * cfg.n_y
+    if nlos.stride(-1) != 1:
+        raise ValueError("nlos rows must be contiguous")
+    c128 = torch.complex128
+    out = dict(H_eff=torch.empty(B, T, K, R, dtype=c128, device=dev),
+               H_rf=torch.empty(B, T, K, R, dtype=c128, device=dev),
+               cols=torch.empty(B, T, R, dtype=torch.int32, device=dev),
+               info=torch.zeros(B, T, dtype=torch.int32, device=dev))
+    if want_channels:
+        out["H"] = torch.empty(B, T, K, Nn, dtype=c128, device=dev)
+        out["H_tilde"] = torch.empty(B, T, K, Nn, dtype=c128, device=dev)
+    lib = N.lib_for(dev)
+    N.check(lib.lrz_leo_snapshot(cfg, B, t0, T, ut.data_ptr(), dft.data_ptr(), nlos.data_ptr(),
+                                 nlos.stride(0), out["H_eff"].data_ptr(), out["H_rf"].data_ptr(),
+                                 out["cols"].data_ptr(), out["info"].data_ptr(),
+                                 N.ptr(out.get("H")), N.ptr(out.get("H_tilde")),
+                                 N.stream_ptr(dev)), "lrz_leo_snapshot")
+    _count(1)
+    return out
+
+
+def hybrid_precode_rate(H_eff: torch.Tensor, A_inv: torch.Tensor, H_rf: torch.Tensor,
+                        cols: torch.Tensor, n_x: int, n_y: int, dft: torch.Tensor, P_t: float,
+                        noise: torch.Tensor, noise_div: int, want_F: bool = False):
+    """Flat batch: H_eff / H_rf [B,K,R] c128, A_inv [B,K,K] c128, cols [B,R]
+    int32.  Returns dict(F_BB [B,R,K] or None, scale, rates [B,K], sum [B], info)."""
+    for t, nm in ((H_eff, "H_eff"), (A_inv, "A_inv"), (H_rf, "H_rf"), (cols, "cols")):
+        _chk(t, nm)
+    B, K, R = H_eff.shape
+    dev = H_eff.device
+    F = torch.empty(B, R, K, dtype=torch.complex128, device=dev) if want_F else None
+    scale = torch.empty(B, dtype=torch.float64, device=dev)
+    rates = torch.empty(B, K, dtype=torch.float64, device=dev)
+    total = torch.empty(B, dtype=torch.float64, device=dev)
+    info = torch.zeros(B, dtype=torch.int32, device=dev)
+    lib = N.lib_for(dev)
+    N.check(lib.lrz_hybrid_precode_rate(B, K, R, n_x, n_y, H_eff.data_ptr(), A_inv.data_ptr(),
+                                        H_rf.data_ptr(), cols.data_ptr(), dft.data_ptr(),
+                                        float(P_t), noise.data_ptr(), int(noise_div), N.ptr(F),
+                                        scale.data_ptr(), rates.data_ptr(), total.data_ptr(),
+                                        info.data_ptr(), N.stream_ptr(dev)),
+            "lrz_hybrid_precode_rate")
+    _count(1)
+    return dict(F_BB=F, scale=scale, rates=rates, sum=total, info=info)
+
+
+def campaign_reduce(method: torch.Tensor, k_est: torch.Tensor, t_base: int, K: int,
+                    n_reset: int, conventional: bool, stats: torch.Tensor) -> torch.Tensor:
+    """Accumulate per-trial (cost, k_sum, k_count, n_full, n_woodbury, n_none)
+    of a [B,T] chunk into stats [B,6] f64."""
+    B, T = method.shape
+    lib = N.lib_for(method.device)
+    N.check(lib.lrz_campaign_reduce(B, T, int(t_base), K, int(n_reset), int(bool(conventional)),
+                                    _chk(method, "method").data_ptr(),
+                                    _chk(k_est, "k_est").data_ptr(), stats.data_ptr(),
+                                    N.stream_ptr(method.device)), "lrz_campaign_reduce")
+    _count(1)
+    return stats

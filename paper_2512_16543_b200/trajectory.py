@@ -131,10 +131,16 @@ class TrajectoryRunner:
 
     # -- one chunk -------------------------------------------------------------
     def run_chunk(self, H: torch.Tensor, noise: torch.Tensor, omega: torch.Tensor | None = None,
-                  keep_A_inv: bool = False, keep_W: bool = False) -> ChunkResult:
+                  keep_A_inv: bool = False, keep_W: bool = False, hybrid: dict | None = None
+                  ) -> ChunkResult:
         """H [B, T, K, N] (device, self.dtype); noise [B, K] float64 (device);
         omega [B, L] float64 (device; row b = trial b's next unconsumed normals,
-        L >= T * normals_per_step_max())."""
+        L >= T * normals_per_step_max()).
+
+        hybrid (analog beams, reference precoding.py:37-80 with F_RF != I): H is
+        the effective channel H_eff = H~ F_RF and the dict carries H_rf = H F_RF
+        [B,T,K,N_RF], cols [B,T,N_RF] (DFT codebook indices), n_x, n_y and dft
+        (the two DFT factors) for the hybrid precoder / rate."""
         c = self.cfg
         B, T, K, Nn = H.shape
         assert (B, K, Nn) == (self.B, self.K, self.N) and H.dtype == self.dtype
@@ -238,12 +244,21 @@ class TrajectoryRunner:
                   k_est, method, info)
         self._stage("chain", e0)
         # 7. precoder and rate
-        W = torch.empty(BT, Nn, K, dtype=self.dtype, device=dev) if keep_W else None
+        W = None
         e0 = self._ev()
-        pr = ops.precode_rate(Hf, A_inv_seq.reshape(BT, K, K), c.P_t, noise, T, W=W,
-                              want_sinr=False,
-                              G_true=G.reshape(BT, K, K) if c.rate_via_gram else None,
-                              alpha=c.alpha)
+        if hybrid is not None:
+            pr = ops.hybrid_precode_rate(Hf, A_inv_seq.reshape(BT, K, K),
+                                         hybrid["H_rf"].reshape(BT, K, Nn),
+                                         hybrid["cols"].reshape(BT, Nn), hybrid["n_x"],
+                                         hybrid["n_y"], hybrid["dft"], c.P_t, noise, T,
+                                         want_F=keep_W)
+            W = pr["F_BB"]
+        else:
+            W = torch.empty(BT, Nn, K, dtype=self.dtype, device=dev) if keep_W else None
+            pr = ops.precode_rate(Hf, A_inv_seq.reshape(BT, K, K), c.P_t, noise, T, W=W,
+                                  want_sinr=False,
+                                  G_true=G.reshape(BT, K, K) if c.rate_via_gram else None,
+                                  alpha=c.alpha)
         self._stage("precode_rate", e0)
         # state for the next chunk
         self.A_inv = A_inv_seq[:, -1].clone()
@@ -254,7 +269,7 @@ class TrajectoryRunner:
         return ChunkResult(rates=pr["sum"].reshape(B, T), per_ut=pr["rates"].reshape(B, T, K),
                            method=method, k_est=k_est, iters=iters, info=info,
                            A_inv=A_inv_seq if keep_A_inv else None,
-                           W=W.reshape(B, T, Nn, K) if keep_W else None,
+                           W=W.reshape(B, T, *W.shape[1:]) if keep_W else None,
                            scale=pr["scale"].reshape(B, T), consumed=consumed,
                            spec_passes=passes)
 
