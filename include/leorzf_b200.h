@@ -98,6 +98,10 @@ typedef struct {
   double eta;
   int k_init, p, i_max;
   int d_max;               /* >= min(k_init * 2^(i_max-1) + p, K) */
+  const double *eta_row;   /* nullable device array: eta per omega row (several
+                              methods batched as rows of one call); overrides eta */
+  int64_t omega_len;       /* > 0: normals per omega row; a call that would read
+                              past it stops with iters = -1 (0 = unchecked) */
 } lrz_arsvd_cfg;
 
 int lrz_arsvd(int64_t B, int K, const void *dA, int64_t a_stride, const double *omega,
@@ -253,6 +257,21 @@ int lrz_campaign_reduce(int64_t B, int T, int t_base, int K, int n_reset, int co
 #define LRZ_WS_PRECODE 4
 #define LRZ_WS_RNG 5
 size_t lrz_workspace_bytes(int op, int dtype, int64_t B, int K, int N, int d_max);
+
+/* In-order arSVD of the unverified suffix of each trial (the sequential
+ * fallback of the speculative runner): items are [B][T] row-major (dA
+ * contiguous K x K per item, factor outputs as lrz_arsvd with B*T items),
+ * one CTA per trial b walks the sketch steps t >= first_unverified[b]
+ * (is_sketch[b][t] != 0) starting at cursor[b][first_unverified[b]] and
+ * advancing by each call's consumption; writes cursor[b][t] and
+ * iters_pred[b][t] = iters[b][t] of every step it visits.  Omega row of
+ * trial b = omega + b * omega_stride.  Workspace as lrz_arsvd for B*T items. */
+int lrz_arsvd_seq(int64_t B, int T, int K, const void *dA, const double *omega,
+                  int64_t omega_stride, const lrz_arsvd_cfg *cfg, const uint8_t *is_sketch,
+                  const int32_t *first_unverified, int64_t *cursor, int32_t *iters_pred,
+                  void *U, void *V, double *S, int32_t *k_est, int32_t *iters,
+                  int32_t *fallback, int64_t *consumed, int want_factor, void *workspace,
+                  void *stream);
 
 /* Speculative sketch-cursor resolution for the batched runner: one thread
  * per trial walks its T steps, accepts every step whose observed iteration

@@ -27,7 +27,8 @@ I32, I64, F64, SZ = C.c_int32, C.c_int64, C.c_double, C.c_size_t
 
 class ArsvdCfg(C.Structure):
     _fields_ = [("eta", C.c_double), ("k_init", C.c_int), ("p", C.c_int),
-                ("i_max", C.c_int), ("d_max", C.c_int)]
+                ("i_max", C.c_int), ("d_max", C.c_int), ("eta_row", C.c_void_p),
+                ("omega_len", C.c_int64)]
 
 
 class LeoCfg(C.Structure):
@@ -48,6 +49,8 @@ _SIGS = {
     "lrz_herm_inverse": (C.c_int, [I64, C.c_int, P, I64, P, I64, P, F64, P, P, P]),
     "lrz_arsvd": (C.c_int, [I64, C.c_int, P, I64, P, I64, P, P, C.POINTER(ArsvdCfg), P, P, P,
                             P, P, P, P, P, C.c_int, C.c_int, P, P]),
+    "lrz_arsvd_seq": (C.c_int, [I64, C.c_int, C.c_int, P, P, I64, C.POINTER(ArsvdCfg), P, P, P,
+                                P, P, P, P, P, P, P, P, C.c_int, P, P]),
     "lrz_woodbury": (C.c_int, [I64, C.c_int, C.c_int, P, P, I64, P, P, P, P, P, P, P, P, P]),
     "lrz_chain": (C.c_int, [I64, C.c_int, C.c_int, C.c_int, P, P, P, P, P, P, P, P, P, P, P, P,
                             P]),

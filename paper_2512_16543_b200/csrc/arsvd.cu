@@ -30,8 +30,11 @@ struct ArsvdArgs {
   const double *omega;
   int64_t os;
   const int32_t *orow;
+  int64_t orow_div;  // orow == NULL: omega row of item = item / orow_div
   const int64_t *cursor;
   double eta;
+  const double *eta_row;  // nullable: energy fraction per omega row (overrides eta)
+  int64_t omega_len;      // > 0: normals available per omega row (guard)
   int k_init, p, i_max, D;
   int want;  // 1: always produce U/S/V; 0: only when 2 k_est <= K (Woodbury candidate)
   const int32_t *start_it;  // nullable: iteration to resume at (warp front end), < 0 = skip
@@ -191,11 +194,9 @@ LRZ_DEV bool gram_certificate(const c128 *M, int K, int d, double trC, c128 *Cw,
   return isfinite(F) && F * trC <= 1e9;
 }
 
-__global__ void __launch_bounds__(ARSVD_THREADS) arsvd_kernel(ArsvdArgs g) {
-  const int64_t item = blockIdx.x;
-  if (g.mask && !g.mask[item]) return;
-  const int it0 = g.start_it ? g.start_it[item] : 0;
-  if (it0 < 0) return;
+// One arsvd call (item) by the whole CTA, sketch stream read from `cur`,
+// resuming at iteration it0.  Returns the normals consumed (block-uniform).
+LRZ_DEV int64_t arsvd_item(const ArsvdArgs &g, const int64_t item, int64_t cur, const int it0) {
   const int K = g.K, D = g.D;
   const int tid = threadIdx.x, NT = blockDim.x, lane = tid & 31, wid = tid >> 5, NW = NT >> 5;
 
@@ -209,8 +210,8 @@ __global__ void __launch_bounds__(ARSVD_THREADS) arsvd_kernel(ArsvdArgs g) {
   __shared__ int s_r;
 
   const c128 *dA = g.dA + item * g.as;
-  const double *om = g.omega + (g.orow ? int64_t(g.orow[item]) : item) * g.os;
-  int64_t cur = g.cursor ? g.cursor[item] : 0;
+  const int64_t orw = g.orow ? int64_t(g.orow[item]) : item / g.orow_div;
+  const double *om = g.omega + orw * g.os;
   const int64_t cur0 = cur;
   c128 *Q = g.ws + item * (int64_t(2) * D * K + int64_t(D) * D);  // [D][K]
   c128 *M = Q + int64_t(D) * K;                                    // [D][K]
@@ -230,9 +231,9 @@ __global__ void __launch_bounds__(ARSVD_THREADS) arsvd_kernel(ArsvdArgs g) {
       g.fallback[item] = 0;
       g.consumed[item] = 0;
     }
-    return;
+    return 0;
   }
-  const double target = g.eta * energy;
+  const double target = (g.eta_row ? g.eta_row[orw] : g.eta) * energy;
   const double SQH = 0.7071067811865476;  // np.sqrt(0.5)
   int k0 = g.k_init, d = 0, it = 0, r = -1;
   bool have_sv = false, hit_found = false;
@@ -243,6 +244,16 @@ __global__ void __launch_bounds__(ARSVD_THREADS) arsvd_kernel(ArsvdArgs g) {
 
   for (it = it0; it < g.i_max; ++it) {
     d = min(k0 + g.p, K);
+    if (g.omega_len > 0 && cur + int64_t(2) * K * d > g.omega_len) {
+      // sketch window too short for this call: report, never read past it
+      if (tid == 0) {
+        g.k_est[item] = 0;
+        g.iters[item] = -1;
+        g.fallback[item] = 0;
+        g.consumed[item] = 0;
+      }
+      return 0;
+    }
     const double *zre = om + cur;
     const double *zim = zre + int64_t(K) * d;
     cur += int64_t(2) * K * d;
@@ -437,6 +448,37 @@ __global__ void __launch_bounds__(ARSVD_THREADS) arsvd_kernel(ArsvdArgs g) {
     g.fallback[item] = fb ? 1 : 0;
     g.consumed[item] = cur - cur0;
   }
+  return cur - cur0;
+}
+
+__global__ void __launch_bounds__(ARSVD_THREADS) arsvd_kernel(ArsvdArgs g) {
+  const int64_t item = blockIdx.x;
+  if (g.mask && !g.mask[item]) return;
+  const int it0 = g.start_it ? g.start_it[item] : 0;
+  if (it0 < 0) return;
+  arsvd_item(g, item, g.cursor ? g.cursor[item] : 0, it0);
+}
+
+// In-order resolution of the unverified suffix of every trial: one CTA per
+// trial walks its sketch steps t >= first[b] and feeds each call the cursor
+// the previous one ended at -- the reference's sequential use of one
+// Generator per (method, trial) (harness.py:211,236-237), with no speculation.
+__global__ void __launch_bounds__(ARSVD_THREADS)
+arsvd_seq_kernel(ArsvdArgs g, int T, const uint8_t *__restrict__ is_sketch,
+                 const int32_t *__restrict__ first, int64_t *__restrict__ cursor,
+                 int32_t *__restrict__ iters_pred) {
+  const int64_t b = blockIdx.x;
+  int t = first[b];
+  if (t >= T) return;
+  int64_t cur = cursor[b * T + t];
+  for (; t < T; ++t) {
+    const int64_t bt = b * T + t;
+    if (threadIdx.x == 0) cursor[bt] = cur;
+    if (!is_sketch[bt]) continue;
+    cur += arsvd_item(g, bt, cur, 0);
+    if (threadIdx.x == 0) iters_pred[bt] = g.iters[bt];
+    __syncthreads();
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -518,7 +560,8 @@ __global__ void __launch_bounds__(128) arsvd_screen_kernel(ArsvdArgs g, int64_t 
     }
     return;
   }
-  const double target = g.eta * energy;
+  const int64_t orw = g.orow ? int64_t(g.orow[item]) : item / g.orow_div;
+  const double target = (g.eta_row ? g.eta_row[orw] : g.eta) * energy;
   int k0 = g.k_init, o = 0;
   int64_t used = 0;
   for (int it = 0; it < g.i_max; ++it) {
@@ -736,8 +779,11 @@ extern "C" int lrz_arsvd(int64_t B, int K, const void *dA, int64_t a_stride,
   g.omega = omega;
   g.os = omega_stride;
   g.orow = omega_row;
+  g.orow_div = 1;
   g.cursor = cursor;
   g.eta = cfg->eta;
+  g.eta_row = cfg->eta_row;
+  g.omega_len = cfg->omega_len;
   g.k_init = cfg->k_init;
   g.p = cfg->p;
   g.i_max = cfg->i_max;
@@ -762,7 +808,17 @@ extern "C" int lrz_arsvd(int64_t B, int K, const void *dA, int64_t a_stride,
       kk *= 2;
     }
   }
-  if (hermitian && want_factor == 0 && g.D <= SCR_DMAX && Dtot <= 4 * g.D) {
+  // the front end reads every iteration's block: only when the window holds them
+  const bool whole = cfg->omega_len <= 0 ||
+                     [&] {
+                       long long kk = cfg->k_init, need = 0;
+                       for (int i = 0; i < cfg->i_max; ++i) {
+                         need += 2LL * K * std::min<long long>(kk + cfg->p, K);
+                         kk *= 2;
+                       }
+                       return need <= cfg->omega_len;
+                     }();
+  if (hermitian && want_factor == 0 && g.D <= SCR_DMAX && Dtot <= 4 * g.D && whole) {
     // screening front end (see arsvd_screen_kernel); workspace layout after the
     // CTA kernel's part: resume[B] int32 | Om/X [B][K][Dtot] | Y [B][K][Dtot] | W
     char *wp = (char *)workspace + lrz_arsvd_ws(B, K, cfg->d_max);
@@ -793,4 +849,54 @@ extern "C" int lrz_arsvd(int64_t B, int K, const void *dA, int64_t a_stride,
   }
   arsvd_kernel<<<unsigned(B), ARSVD_THREADS, 0, st>>>(g);
   return lrz_launch_status("lrz_arsvd");
+}
+
+extern "C" int lrz_arsvd_seq(int64_t B, int T, int K, const void *dA, const double *omega,
+                             int64_t omega_stride, const lrz_arsvd_cfg *cfg,
+                             const uint8_t *is_sketch, const int32_t *first_unverified,
+                             int64_t *cursor, int32_t *iters_pred, void *U, void *V, double *S,
+                             int32_t *k_est, int32_t *iters, int32_t *fallback, int64_t *consumed,
+                             int want_factor, void *workspace, void *stream) {
+  if (B < 0 || T < 1 || K < 1 || !dA || !omega || !cfg || !is_sketch || !first_unverified ||
+      !cursor || !iters_pred || !U || !V || !S || !k_est || !iters || !fallback || !consumed ||
+      !workspace) {
+    lrz_set_error("lrz_arsvd_seq: bad arguments");
+    return LRZ_EINVAL;
+  }
+  if (!(cfg->eta > 0.0 && cfg->eta <= 1.0) || cfg->k_init < 1 || cfg->p < 0 || cfg->i_max < 1 ||
+      cfg->d_max < 1 || cfg->d_max > ARSVD_DMAX) {
+    lrz_set_error("lrz_arsvd_seq: bad ArSvdConfig");
+    return LRZ_EINVAL;
+  }
+  if (B == 0) return LRZ_OK;
+  ArsvdArgs g;
+  g.K = K;
+  g.dA = (const c128 *)dA;
+  g.as = int64_t(K) * K;
+  g.omega = omega;
+  g.os = omega_stride;
+  g.orow = nullptr;
+  g.orow_div = T;
+  g.cursor = nullptr;
+  g.eta = cfg->eta;
+  g.eta_row = cfg->eta_row;
+  g.omega_len = cfg->omega_len;
+  g.k_init = cfg->k_init;
+  g.p = cfg->p;
+  g.i_max = cfg->i_max;
+  g.D = cfg->d_max;
+  g.want = want_factor;
+  g.start_it = nullptr;
+  g.U = (c128 *)U;
+  g.V = (c128 *)V;
+  g.S = S;
+  g.k_est = k_est;
+  g.iters = iters;
+  g.fallback = fallback;
+  g.consumed = consumed;
+  g.mask = nullptr;
+  g.ws = (c128 *)workspace;
+  arsvd_seq_kernel<<<unsigned(B), ARSVD_THREADS, 0, (cudaStream_t)stream>>>(
+      g, T, is_sketch, first_unverified, cursor, iters_pred);
+  return lrz_launch_status("lrz_arsvd_seq");
 }

@@ -166,7 +166,7 @@ __global__ void spec_verify_kernel(int64_t B, int T, int K, ConsumedTab consumed
       ++t;
       continue;
     }
-    const int pa = iters_act[bt];
+    const int pa = max(iters_act[bt], 0);  // -1 = window overflow, reported by the host
     if (pa == iters_pred[bt]) {
       ++t;
       continue;
@@ -182,7 +182,7 @@ __global__ void spec_verify_kernel(int64_t B, int T, int K, ConsumedTab consumed
   int64_t c = cursor0[b];
   for (int s = 0; s < T; ++s) {
     const int64_t bt = base + s;
-    if (iters_act && s >= t && is_sketch[bt]) iters_pred[bt] = iters_act[bt];
+    if (iters_act && s >= t && is_sketch[bt]) iters_pred[bt] = max(iters_act[bt], 0);
     cursor[bt] = c;
     active[bt] = (s >= t && is_sketch[bt]) ? 1 : 0;
     if (is_sketch[bt]) c += consumed_tab.v[iters_pred[bt]];

@@ -312,11 +312,12 @@ def _check_info(cfg, trials, t0, snap_info, run_infos):
         a = inf.cpu().numpy()
         if np.any(a == 1):
             b, t = np.argwhere(a == 1)[0]
-            raise SingularMatrixError(f"trial {trials[b]} step {t0 + t}: condition estimate "
-                                      "exceeds 1e14")
+            raise SingularMatrixError(f"trial {trials[b % len(trials)]} step {t0 + t}: "
+                                      "condition estimate exceeds 1e14")
         if np.any(a == 3):
             b, t = np.argwhere(a == 3)[0]
-            raise ZeroPrecoderError(f"trial {trials[b]} step {t0 + t}: zero precoder norm")
+            raise ZeroPrecoderError(f"trial {trials[b % len(trials)]} step {t0 + t}: zero "
+                                    "precoder norm")
 
 
 def ops_info_below() -> int:
@@ -325,53 +326,87 @@ def ops_info_below() -> int:
 
 def _simulate(cfg, specs, trials, seed, device, chunk, sketch_labels=None, keep_cols=False):
     """Run every (label, eta) of ``specs`` over ``trials`` with a shared
-    channel.  Returns label -> dict of host arrays [B, T] (rates, method,
-    k_est) and stats [B, 6]."""
+    channel.  The WB-arSVD methods run as ONE batched runner whose rows are
+    (method, trial) pairs with a per-row eta, so their in-order arSVD tails
+    overlap on the GPU.  Returns label -> dict of host arrays [B, T] (rates,
+    method, k_est) and stats [B, 6]."""
     dev = torch.device(device) if device is not None else torch.device("cuda", 0)
     B, T, K, R = len(trials), cfg.n_snapshots, cfg.K, cfg.N_RF
     chunk = T if chunk is None else max(1, int(chunk))
     ps = DevicePass(cfg, trials, seed, dev)
-    noise = torch.full((B, K), cfg.noise_variance_W, dtype=torch.float64, device=dev)
-    runs = []
-    for label, eta in specs:
-        tc = TrajectoryConfig(alpha=cfg.resolved_alpha, P_t=cfg.P_t_W, eta=eta,
+    groups = []
+    conv = [(lab, eta) for lab, eta in specs if eta is None]
+    wb = [(lab, eta) for lab, eta in specs if eta is not None]
+    for members in (conv, wb):
+        if not members:
+            continue
+        m = len(members)
+        is_wb = members[0][1] is not None
+        etas = [eta for _, eta in members for _ in trials] if is_wb else None
+        tc = TrajectoryConfig(alpha=cfg.resolved_alpha, P_t=cfg.P_t_W, eta=etas,
                               k_init=cfg.k_init, p=cfg.p, i_max=cfg.i_max, n_reset=cfg.n_reset,
                               rate_via_gram=False, delta="formula")
-        runner = TrajectoryRunner(B, K, R, torch.complex128, tc, dev)
-        sl = (sketch_labels or {}).get(label, label)
-        streams = None if eta is None else DeviceOmegaStreams(
-            [np.random.default_rng(stream_seed(seed, sl, t)) for t in trials], dev)
-        runs.append(dict(label=label, eta=eta, runner=runner, streams=streams,
-                         stats=torch.zeros(B, 6, dtype=torch.float64, device=dev),
-                         rates=[], method=[], k_est=[]))
+        runner = TrajectoryRunner(m * B, K, R, torch.complex128, tc, dev)
+        streams = None
+        if is_wb:
+            gens = []
+            for lab, _ in members:
+                sl = (sketch_labels or {}).get(lab, lab)
+                gens += [np.random.default_rng(stream_seed(seed, sl, t)) for t in trials]
+            streams = DeviceOmegaStreams(gens, dev)
+        groups.append(dict(labels=[lab for lab, _ in members], m=m, wb=is_wb, runner=runner,
+                           streams=streams,
+                           stats=torch.zeros(m * B, 6, dtype=torch.float64, device=dev),
+                           noise=torch.full((m * B, K), cfg.noise_variance_W,
+                                            dtype=torch.float64, device=dev),
+                           rates=[], method=[], k_est=[]))
     cols = []
+    rep = lambda x, m: x if m == 1 else x.repeat(m, *([1] * (x.dim() - 1)))
+    main = torch.cuda.current_stream(dev)
+    # the conventional group is launched first on a side stream so that its
+    # batched inversions overlap the WB group's in-order arSVD on the main stream
+    side = torch.cuda.Stream(dev)
+    for gr in groups:
+        gr["stream"] = side if (not gr["wb"] and len(groups) > 1) else main
     for t0 in range(0, T, chunk):
         t1 = min(T, t0 + chunk)
         snap = ps.generate(t0, t1)
-        hyb = dict(H_rf=snap["H_rf"], cols=snap["cols"], n_x=cfg.n_x, n_y=cfg.n_y, dft=ps.dft)
         infos = []
-        for r in runs:
-            om = None
-            if r["eta"] is not None:
-                om = r["streams"].window((t1 - t0) * r["runner"].normals_per_step_max())
-            res = r["runner"].run_chunk(snap["H_eff"], noise, om, hybrid=hyb)
-            if r["eta"] is not None:
-                r["streams"].advance(res.consumed)
-            ops.campaign_reduce(res.method, res.k_est, t0, K, cfg.n_reset, r["eta"] is None,
-                                r["stats"])
-            r["rates"].append(res.rates)
-            r["method"].append(res.method)
-            r["k_est"].append(res.k_est)
+        for gr in groups:
+            m, st = gr["m"], gr["stream"]
+            if st is not main:
+                st.wait_stream(main)
+            with torch.cuda.stream(st):
+                hyb = dict(H_rf=rep(snap["H_rf"], m), cols=rep(snap["cols"], m), n_x=cfg.n_x,
+                           n_y=cfg.n_y, dft=ps.dft)
+                H_in = rep(snap["H_eff"], m)
+                if st is not main:
+                    for x in (snap["H_rf"], snap["cols"], snap["H_eff"]):
+                        x.record_stream(st)
+                om = None
+                if gr["wb"]:
+                    om = gr["streams"].window((t1 - t0) * gr["runner"].normals_per_step_max())
+                res = gr["runner"].run_chunk(H_in, gr["noise"], om, hybrid=hyb)
+                if gr["wb"]:
+                    gr["streams"].advance(res.consumed)
+                ops.campaign_reduce(res.method, res.k_est, t0, K, cfg.n_reset, not gr["wb"],
+                                    gr["stats"])
+            gr["rates"].append(res.rates)
+            gr["method"].append(res.method)
+            gr["k_est"].append(res.k_est)
             infos.append(res.info)
+        main.wait_stream(side)
         _check_info(cfg, trials, t0, snap["info"], infos)
         if keep_cols:
             cols.append(snap["cols"].cpu())
     out = {}
-    for r in runs:
-        out[r["label"]] = dict(rates=torch.cat(r["rates"], 1).cpu().numpy(),
-                               method=torch.cat(r["method"], 1).cpu().numpy(),
-                               k_est=torch.cat(r["k_est"], 1).cpu().numpy(),
-                               stats=r["stats"].cpu().numpy())
+    for gr in groups:
+        full = dict(rates=torch.cat(gr["rates"], 1).cpu().numpy(),
+                    method=torch.cat(gr["method"], 1).cpu().numpy(),
+                    k_est=torch.cat(gr["k_est"], 1).cpu().numpy(),
+                    stats=gr["stats"].cpu().numpy())
+        for i, lab in enumerate(gr["labels"]):
+            out[lab] = {k: v[i * B:(i + 1) * B] for k, v in full.items()}
     if keep_cols:
         out["_cols"] = torch.cat(cols, 1).numpy()
     return out

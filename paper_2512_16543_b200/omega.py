@@ -38,6 +38,27 @@ def normals_per_call_max(K: int, k_init: int, p: int, i_max: int) -> int:
     return sum(2 * K * d for d in sketch_widths(K, k_init, p, i_max))
 
 
+def effective_i_max(K: int, k_init: int, p: int, i_max: int, eta_max: float) -> int:
+    """Iterations an arsvd call can actually run.  Once the sketch width
+    reaches K the basis Q is a full unitary (Householder QR), so B = Q^H dA
+    keeps all of ||dA||_F^2 and the energy rule (lowrank.py:290-301) is met
+    for any eta below 1 - 1e-9: the loop never goes past that iteration."""
+    if eta_max > 1.0 - 1e-9:
+        return i_max
+    k0 = k_init
+    for i in range(i_max):
+        if min(k0 + p, K) == K:
+            return i + 1
+        k0 *= 2
+    return i_max
+
+
+def normals_per_call_bound(K: int, k_init: int, p: int, i_max: int, eta_max: float) -> int:
+    """Upper bound on normals one call consumes at energy fractions <= eta_max."""
+    i_eff = effective_i_max(K, k_init, p, i_max, eta_max)
+    return sum(2 * K * d for d in sketch_widths(K, k_init, p, i_eff))
+
+
 def consumed_by(iters: np.ndarray, K: int, k_init: int, p: int, i_max: int) -> np.ndarray:
     """Normals consumed by a call that ran ``iters`` iterations (0 = none)."""
     cum = np.concatenate([[0], np.cumsum([2 * K * d for d in

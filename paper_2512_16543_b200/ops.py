@@ -28,7 +28,9 @@ def _count(n: int = 1) -> None:
 
 def workspace(device, nbytes: int, slot: str = "main") -> torch.Tensor:
     """Grow-only per-(device, slot) scratch buffer."""
-    key = (device.index if device.index is not None else 0, slot)
+    # per stream: runners on different streams must not share scratch
+    key = (device.index if device.index is not None else 0,
+           torch.cuda.current_stream(device).cuda_stream, slot)
     buf = _WS.get(key)
     if buf is None or buf.numel() < nbytes:
         buf = torch.empty(max(int(nbytes), 256), dtype=torch.uint8, device=device)
@@ -133,7 +135,18 @@ def herm_inverse(A: torch.Tensor, cond_limit: float = 1e14, mask: torch.Tensor |
     return out, info
 
 
-def arsvd(dA: torch.Tensor, omega: torch.Tensor, cursor: torch.Tensor, eta: float, k_init: int,
+def _arsvd_cfg(eta, k_init: int, p: int, i_max: int, D: int, omega_len: int = 0):
+    """ArsvdCfg for a scalar eta, or per omega row (a float64 CUDA tensor);
+    omega_len > 0 bounds the normals a call may read per omega row."""
+    if isinstance(eta, torch.Tensor):
+        if not eta.is_cuda or eta.dtype != torch.float64 or not eta.is_contiguous():
+            raise ValueError("per-row eta must be a contiguous float64 CUDA tensor")
+        return N.ArsvdCfg(1.0, int(k_init), int(p), int(i_max), int(D), eta.data_ptr(),
+                          int(omega_len))
+    return N.ArsvdCfg(float(eta), int(k_init), int(p), int(i_max), int(D), None, int(omega_len))
+
+
+def arsvd(dA: torch.Tensor, omega: torch.Tensor, cursor: torch.Tensor, eta, k_init: int,
           p: int, i_max: int, omega_row: torch.Tensor | None = None,
           mask: torch.Tensor | None = None, out: dict | None = None,
           want_factor: bool = True, hermitian: bool = False) -> dict:
@@ -156,7 +169,7 @@ def arsvd(dA: torch.Tensor, omega: torch.Tensor, cursor: torch.Tensor, eta: floa
             fallback=torch.zeros(B, dtype=torch.int32, device=dev),
             consumed=torch.zeros(B, dtype=torch.int64, device=dev),
         )
-    cfg = N.ArsvdCfg(float(eta), int(k_init), int(p), int(i_max), int(D))
+    cfg = _arsvd_cfg(eta, k_init, p, i_max, D, omega.shape[1])
     lib = N.lib_for(dev)
     nbytes = lib.lrz_workspace_bytes(N.WS_ARSVD, N.C128, B, K, 0, D)
     ws = workspace(dev, nbytes, "arsvd")
@@ -168,6 +181,36 @@ def arsvd(dA: torch.Tensor, omega: torch.Tensor, cursor: torch.Tensor, eta: floa
                           int(hermitian), ws.data_ptr(), N.stream_ptr(dev)), "lrz_arsvd")
     _count(1)
     out["D"] = D
+    return out
+
+
+def arsvd_seq(dA: torch.Tensor, omega: torch.Tensor, is_sketch: torch.Tensor,
+              first_unverified: torch.Tensor, cursor: torch.Tensor, iters_pred: torch.Tensor,
+              eta, k_init: int, p: int, i_max: int, out: dict,
+              want_factor: bool = False) -> dict:
+    """In-order arSVD of each trial's unverified suffix.  dA [B,T,K,K] c128
+    contiguous; omega [B,L] (contiguous rows); is_sketch [B,T] u8;
+    first_unverified [B] i32; cursor [B,T] i64 and iters_pred [B,T] i32 (in/out);
+    out: the flat [B*T] result dict of ``arsvd``."""
+    _chk(dA, "dA")
+    if not omega.is_cuda or omega.dim() != 2 or omega.stride(1) != 1:
+        raise ValueError("omega must be a [B, L] CUDA tensor with contiguous rows")
+    B, T, K = dA.shape[0], dA.shape[1], dA.shape[-1]
+    D = d_max_for(K, k_init, p, i_max)
+    dev = dA.device
+    cfg = _arsvd_cfg(eta, k_init, p, i_max, D, omega.shape[1])
+    lib = N.lib_for(dev)
+    ws = workspace(dev, lib.lrz_workspace_bytes(N.WS_ARSVD, N.C128, B * T, K, 0, D), "arsvd")
+    N.check(lib.lrz_arsvd_seq(B, T, K, dA.data_ptr(), omega.data_ptr(), omega.stride(0),
+                              C.byref(cfg), _chk(is_sketch, "is_sketch").data_ptr(),
+                              _chk(first_unverified, "first_unverified").data_ptr(),
+                              _chk(cursor, "cursor").data_ptr(),
+                              _chk(iters_pred, "iters_pred").data_ptr(), out["U"].data_ptr(),
+                              out["V"].data_ptr(), out["S"].data_ptr(), out["k_est"].data_ptr(),
+                              out["iters"].data_ptr(), out["fallback"].data_ptr(),
+                              out["consumed"].data_ptr(), int(want_factor), ws.data_ptr(),
+                              N.stream_ptr(dev)), "lrz_arsvd_seq")
+    _count(1)
     return out
 
 
@@ -315,8 +358,7 @@ def spec_verify(is_sketch, iters_pred, iters_act, cursor, cursor0, first_unverif
                 pending, K, eta, k_init, p, i_max):
     B, T = is_sketch.shape
     dev = is_sketch.device
-    cfg = N.ArsvdCfg(float(eta), int(k_init), int(p), int(i_max),
-                     d_max_for(K, k_init, p, i_max))
+    cfg = _arsvd_cfg(eta, k_init, p, i_max, d_max_for(K, k_init, p, i_max))
     lib = N.lib_for(dev)
     N.check(lib.lrz_spec_verify(B, T, K, C.byref(cfg), is_sketch.data_ptr(),
                                 iters_pred.data_ptr(), N.ptr(iters_act), cursor.data_ptr(),

@@ -35,7 +35,7 @@ import torch
 from . import ops
 from .errors import SingularMatrixError
 from .lowrank import cost_full, cost_wb_arsvd, sketch_cost
-from .omega import OmegaStreams, consumed_by, normals_per_call_max
+from .omega import OmegaStreams, consumed_by, effective_i_max, normals_per_call_bound
 
 
 @dataclass
@@ -44,13 +44,15 @@ class TrajectoryConfig:
 
     alpha: float
     P_t: float = 1.0
-    eta: float | None = None
+    eta: float | None = None     # or a sequence: one eta per trial
     k_init: int = 2
     p: int = 5
     i_max: int = 3
     n_reset: int = 1200          # config.py:59
     maintain_A: bool = True      # keep A = A + U S V^H like GramState.A (lowrank.py:220)
-    max_spec_passes: int = 64
+    # speculative (batched over all steps) arSVD passes before the remaining
+    # unverified suffixes are resolved in order (lrz_arsvd_seq)
+    spec_passes: int = 2
     # H W for the rate from the Gram: (G - alpha I) A^-1 (exact with F_RF = I)
     rate_via_gram: bool = True
     # Gram correction: "diff" = G_t - G_{t-1} from the Grams already formed (complex128:
@@ -100,7 +102,16 @@ class TrajectoryRunner:
         self.A_inv = torch.zeros(B, K, K, dtype=torch.complex128, device=self.device)
         self.A = torch.zeros(B, K, K, dtype=torch.complex128, device=self.device)
         self.D = ops.d_max_for(K, cfg.k_init, cfg.p, cfg.i_max)
+        # eta: None (conventional), a float, or one value per trial (several WB
+        # methods batched as trials of one runner)
+        self._eta = cfg.eta
+        if cfg.eta is not None and np.ndim(cfg.eta) == 1:
+            e = np.asarray(cfg.eta, dtype=np.float64)
+            if e.shape != (B,) or not np.all((e > 0) & (e <= 1)):
+                raise ValueError("per-trial eta must have one value in (0, 1] per trial")
+            self._eta = torch.from_numpy(e).to(self.device)
         self.prof = None          # list of (stage, start_event, end_event) when profiling
+        self._in_order = False    # set once a chunk needed the in-order arSVD
 
     def _ev(self):
         if self.prof is None:
@@ -114,9 +125,14 @@ class TrajectoryRunner:
             self.prof.append((name, e0, self._ev()))
 
     # -- helpers -------------------------------------------------------------
+    def _eta_max(self) -> float:
+        return float(np.max(np.asarray(self.cfg.eta, dtype=np.float64)))
+
     def normals_per_step_max(self) -> int:
+        """Window normals one step may need (see omega.effective_i_max)."""
         c = self.cfg
-        return 0 if c.eta is None else normals_per_call_max(self.K, c.k_init, c.p, c.i_max)
+        return 0 if c.eta is None else normals_per_call_bound(self.K, c.k_init, c.p, c.i_max,
+                                                              self._eta_max())
 
     def _is_sketch(self, T: int) -> torch.Tensor:
         c = self.cfg
@@ -182,14 +198,15 @@ class TrajectoryRunner:
             self._stage("gram_delta", e0)
             # 3. speculative arSVD
             assert omega is not None and omega.shape[0] == B
-            iters_pred = torch.full((B, T), c.i_max, dtype=torch.int32, device=dev)
+            i_eff = effective_i_max(K, c.k_init, c.p, c.i_max, self._eta_max())
+            iters_pred = torch.full((B, T), i_eff, dtype=torch.int32, device=dev)
             cursor = torch.zeros(B, T, dtype=torch.int64, device=dev)
             cursor0 = torch.zeros(B, dtype=torch.int64, device=dev)
             first = torch.zeros(B, dtype=torch.int32, device=dev)
             active = torch.zeros(B, T, dtype=torch.uint8, device=dev)
             pending = torch.zeros(1, dtype=torch.int32, device=dev)
             ops.spec_verify(is_sketch, iters_pred, None, cursor, cursor0, first, active, pending,
-                            K, c.eta, c.k_init, c.p, c.i_max)
+                            K, self._eta, c.k_init, c.p, c.i_max)
             row = torch.arange(B, dtype=torch.int32, device=dev).repeat_interleave(T)
             res = dict(
                 U=torch.empty(BT, D, K, dtype=torch.complex128, device=dev),
@@ -201,24 +218,35 @@ class TrajectoryRunner:
                 consumed=torch.zeros(BT, dtype=torch.int64, device=dev),
             )
             pinned = torch.zeros(1, dtype=torch.int32).pin_memory()
+            n_spec = 0 if self._in_order else c.spec_passes
             while True:
                 e0 = self._ev()
-                ops.arsvd(dAf, omega, cursor.reshape(BT), c.eta, c.k_init, c.p, c.i_max,
-                          omega_row=row, mask=active.reshape(BT), out=res, want_factor=False,
-                          hermitian=True)
+                if passes < n_spec:
+                    ops.arsvd(dAf, omega, cursor.reshape(BT), self._eta, c.k_init, c.p, c.i_max,
+                              omega_row=row, mask=active.reshape(BT), out=res,
+                              want_factor=False, hermitian=True)
+                else:
+                    # iteration counts keep changing with the sketch: resolve the rest
+                    # of every trial in order (one CTA per trial, exact cursors)
+                    ops.arsvd_seq(dA, omega, is_sketch, first, cursor, iters_pred, self._eta,
+                                  c.k_init, c.p, c.i_max, res)
                 self._stage("arsvd", e0)
                 passes += 1
                 pending.zero_()
                 e0 = self._ev()
                 ops.spec_verify(is_sketch, iters_pred, res["iters"], cursor, cursor0, first,
-                                active, pending, K, c.eta, c.k_init, c.p, c.i_max)
+                                active, pending, K, self._eta, c.k_init, c.p, c.i_max)
                 self._stage("verify", e0)
                 pinned.copy_(pending, non_blocking=True)
                 torch.cuda.current_stream(dev).synchronize()
                 if int(pinned[0]) == 0:
                     break
-                if passes >= c.max_spec_passes + T:
-                    raise RuntimeError("speculative arSVD did not converge")
+                if passes > n_spec:
+                    raise RuntimeError("in-order arSVD left unverified steps")
+            if passes > n_spec:
+                self._in_order = True   # iteration counts track the sketch: skip speculation
+            if int((res["iters"] < 0).sum().item()):
+                raise RuntimeError("sketch window shorter than an arsvd call needed")
             iters.copy_(iters_pred * is_sketch.to(torch.int32))
             U, V, S = res["U"], res["V"], res["S"]
             last = cursor[:, -1] + res["consumed"].reshape(B, T)[:, -1] * is_sketch[:, -1]
