@@ -130,6 +130,69 @@ def _cpu_trial(job):
     return spec.T, time.perf_counter() - t0
 
 
+def _leo_cpu_job(job):
+    """One LEO pass prefix of every method (oracle port of harness._sweep_trial
+    with the reference's hybrid beams), timed inside the worker."""
+    cfg_kw, trial, steps = job
+    from oracle import leo as OL
+    from paper_2512_16543_b200.leo import ScenarioConfig
+    cfg = ScenarioConfig(**cfg_kw)
+    etas = sorted(set(cfg.eta_list), reverse=True)
+    specs = [(OL.label_of(None), None)] + [(OL.label_of(e), e) for e in etas]
+    t0 = time.perf_counter()
+    OL.sweep_trial(cfg, specs, trial, cfg.seed, steps=steps)
+    return steps * len(specs), time.perf_counter() - t0
+
+
+def leo_side(args, dev, world, max_over_ranks):
+    """The reference's own default campaign (leorzf ScenarioConfig defaults: 50
+    LEO passes x 2400 snapshots x 4 methods, hybrid DFT beams) through the
+    run_campaign drop-in, timed on the device (max over ranks)."""
+    import dataclasses
+    import multiprocessing as mp
+    import torch
+    from paper_2512_16543_b200 import leo as L
+    cfg = L.ScenarioConfig().validate()
+    L.run_campaign(cfg.with_(mc_runs=2 * world, pass_s=10.0), device=dev)     # warm-up
+    torch.cuda.synchronize(dev)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    res = L.run_campaign(cfg, device=dev)
+    e1.record()
+    torch.cuda.synchronize(dev)
+    ms = max_over_ranks(e0.elapsed_time(e1))
+    n_methods = len(res.labels)
+    upd = cfg.mc_runs * cfg.n_snapshots * n_methods
+    out = {"value": upd / (ms / 1e3), "unit": "updates/s", "ms": ms,
+           "workload": f"leorzf default ScenarioConfig campaign: {cfg.mc_runs} passes x "
+                       f"{cfg.n_snapshots} snapshots x {n_methods} methods (K = N_RF = 16, 16x16 "
+                       "UPA, DFT beams), channels + beams + precoders + rates + reduction on "
+                       "the device",
+           "table": [[r.method_label, r.savings_pct, r.degradation_pct] for r in res.table.rows]}
+    if world == 1 and not args.no_cpu:
+        cores = _cores()
+        kw = dataclasses.asdict(cfg)
+        steps = 120
+        saved = {k: os.environ.get(k) for k in _BLAS_ENV}
+        for k in _BLAS_ENV:
+            os.environ[k] = "1"
+        try:
+            with mp.get_context("spawn").Pool(cores, initializer=_cpu_init) as pool:
+                pool.map(_leo_cpu_job, [(kw, 0, 2)] * cores)
+                r = pool.map(_leo_cpu_job, [(kw, t, steps) for t in range(cores)], chunksize=1)
+        finally:
+            for k, v in saved.items():
+                if v is None:
+                    os.environ.pop(k, None)
+                else:
+                    os.environ[k] = v
+        out["cpu_baseline"] = {"value": sum(u for u, _ in r) / max(sec for _, sec in r),
+                               "unit": "updates/s", "cores": cores, "kind": "port",
+                               "sample": f"{cores} passes x first {steps} snapshots x "
+                                         f"{n_methods} methods, one pass per worker"}
+    return out
+
+
 def _cores():
     try:
         return len(os.sched_getaffinity(0))
@@ -518,6 +581,11 @@ def run_b200(args):
         extra = {"c64_wb_updates_per_s": res64["wb"], "c64_full_updates_per_s": res64["full"]}
         del H64
 
+    # ---- the reference's own LEO campaign (hybrid beams), SURVEY 8(f) #3/#4
+    leo = None
+    if not args.no_extra:
+        leo = leo_side(args, dev, world, max_over_ranks)
+
     # ---- CPU baseline (rank 0, N = 1 only)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
@@ -562,6 +630,8 @@ def run_b200(args):
         }
         if extra:
             line["c64"] = extra
+        if leo:
+            line["leo_campaign"] = leo
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
