@@ -24,6 +24,27 @@ LRZ_DEV void tri_tile(int t, int &I, int &J) {
   J = t - i * (i + 1) / 2;
 }
 
+template <typename T>
+LRZ_DEV void cp_async16(void *smem, const void *gmem, bool pred) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  if (sizeof(cplx<T>) == 16) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(sa), "l"(gmem),
+                 "r"(pred ? 16 : 0));
+  } else {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(sa), "l"(gmem),
+                 "r"(pred ? 8 : 0));
+  }
+}
+template <typename T>
+LRZ_DEV void cp_async_el(void *smem, const void *gmem, bool pred) {
+  cp_async16<T>(smem, gmem, pred);
+}
+LRZ_DEV void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+LRZ_DEV void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
 // ---------------------------------------------------------------------------
 // K1: A = H H^H (Hermitian, lower tiles computed, mirrored) + alpha I
 // ---------------------------------------------------------------------------
@@ -75,6 +96,96 @@ __global__ void __launch_bounds__(GEMM_THREADS)
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
       const int col = J * TM + tx + 8 * j;
+      if (row < K && col < K && row >= col) {
+        c128 v = ccast<double>(acc[i][j]);
+        if (row == col) {
+          v.im = 0.0;  // 0.5 (A + A^H) has an exactly real diagonal (lowrank.py:161)
+          v.re += alpha;
+          a[int64_t(row) * K + col] = v;
+        } else {
+          a[int64_t(row) * K + col] = v;
+          a[int64_t(col) * K + row] = cconj(v);
+        }
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K1 for K <= 32: only the lower triangle is formed.  The 32 x 32 output is
+// cut into 4 x 4 register tiles; the 36 lower tiles of an item go to 36
+// threads, G32_IPB items share a CTA (288 threads), and the items' H rows
+// stream through shared memory in G32_BK-wide slabs with cp.async double
+// buffering.  Per k a thread does 8 shared loads for 16 complex FMAs.
+// ---------------------------------------------------------------------------
+constexpr int G32_IPB = 8;
+constexpr int G32_BK = 8;
+constexpr int G32_THREADS = 36 * G32_IPB;
+
+
+template <typename T>
+__global__ void __launch_bounds__(G32_THREADS, 2)
+    gram32_kernel(int64_t B, int K, int N, const cplx<T> *__restrict__ H, int64_t hs,
+                  double alpha, c128 *__restrict__ A, int64_t as) {
+  extern __shared__ __align__(16) char g32_smem[];
+  cplx<T> *S = (cplx<T> *)g32_smem;   // [3][G32_IPB][G32_BK][32]
+  const int tid = threadIdx.x;
+  const int li = tid / 36, tile = tid % 36;
+  int I, J;
+  tri_tile(tile, I, J);
+  const int64_t item0 = int64_t(blockIdx.x) * G32_IPB;
+  const int nslab = (N + G32_BK - 1) / G32_BK;
+  auto issue = [&](int slab, int buf) {
+    // G32_IPB items x 32 rows x G32_BK columns; consecutive threads walk n
+    for (int e = tid; e < G32_IPB * 32 * G32_BK; e += G32_THREADS) {
+      const int kk = e % G32_BK, r = (e / G32_BK) & 31, it = e / (G32_BK * 32);
+      const int n = slab * G32_BK + kk;
+      const int64_t item = item0 + it;
+      const bool ok = item < B && r < K && n < N;
+      // row r = 4 I + i lives at column i * 8 + I: a warp's 4-row tile loads hit
+      // 8 consecutive elements (one shared-memory wavefront per item)
+      cp_async_el<T>(S + ((buf * G32_IPB + it) * G32_BK + kk) * 32 + (r & 3) * 8 + (r >> 2),
+                     H + (ok ? item * hs + int64_t(r) * N + n : 0), ok);
+    }
+    cp_async_commit();
+  };
+  cplx<T> acc[4][4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j] = czero<T>();
+  // 3-stage ring, one barrier per slab: after the barrier of slab sl every
+  // thread is done with slab sl-1, whose buffer then receives slab sl+2
+  issue(0, 0);
+  if (nslab > 1) issue(1, 1); else cp_async_commit();
+  for (int sl = 0; sl < nslab; ++sl) {
+    cp_async_wait<1>();
+    __syncthreads();
+    if (sl + 2 < nslab) issue(sl + 2, (sl + 2) % 3); else cp_async_commit();
+    const cplx<T> *sb = S + ((sl % 3) * G32_IPB + li) * G32_BK * 32;
+#pragma unroll
+    for (int kk = 0; kk < G32_BK; ++kk) {
+      cplx<T> a[4], b[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        a[i] = sb[kk * 32 + i * 8 + I];
+        b[i] = sb[kk * 32 + i * 8 + J];
+      }
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) cfma_cb(acc[i][j], a[i], b[j]);
+    }
+  }
+  const int64_t item = item0 + li;
+  if (item >= B) return;
+  c128 *a = A + item * as;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int row = 4 * I + i;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int col = 4 * J + j;
       if (row < K && col < K && row >= col) {
         c128 v = ccast<double>(acc[i][j]);
         if (row == col) {
@@ -427,22 +538,6 @@ constexpr int PW_KC = 8;      // k rows per slab
 constexpr int PW_ROWS = 128;  // antenna rows per block pass
 constexpr int PW_THREADS = 256;
 
-template <typename T>
-LRZ_DEV void cp_async16(void *smem, const void *gmem, bool pred) {
-  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
-  if (sizeof(cplx<T>) == 16) {
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(sa), "l"(gmem),
-                 "r"(pred ? 16 : 0));
-  } else {
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(sa), "l"(gmem),
-                 "r"(pred ? 8 : 0));
-  }
-}
-LRZ_DEV void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
-template <int N>
-LRZ_DEV void cp_async_wait() {
-  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
-}
 
 template <typename T>
 __global__ void __launch_bounds__(PW_THREADS, 2)
@@ -556,9 +651,26 @@ extern "C" int lrz_gram(int dtype, int64_t B, int K, int N, const void *H, int64
     return LRZ_EINVAL;
   }
   if (B == 0) return LRZ_OK;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (K <= 32) {
+    const unsigned nb = unsigned((B + G32_IPB - 1) / G32_IPB);
+    if (dtype == LRZ_C64) {
+      const size_t sm = size_t(3) * G32_IPB * G32_BK * 32 * sizeof(c64);
+      cudaFuncSetAttribute(gram32_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           int(sm));
+      gram32_kernel<float><<<nb, G32_THREADS, sm, s>>>(B, K, N, (const c64 *)H, h_stride, alpha,
+                                                       (c128 *)A, a_stride);
+    } else {
+      const size_t sm = size_t(3) * G32_IPB * G32_BK * 32 * sizeof(c128);
+      cudaFuncSetAttribute(gram32_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           int(sm));
+      gram32_kernel<double><<<nb, G32_THREADS, sm, s>>>(B, K, N, (const c128 *)H, h_stride,
+                                                        alpha, (c128 *)A, a_stride);
+    }
+    return lrz_launch_status("lrz_gram");
+  }
   const int nt = ntiles(K), ntl = nt * (nt + 1) / 2;
   const dim3 grid(unsigned(B * ntl));
-  cudaStream_t s = (cudaStream_t)stream;
   if (dtype == LRZ_C64)
     gram_kernel<float, 32><<<grid, GEMM_THREADS, 0, s>>>(K, N, (const c64 *)H, h_stride, alpha,
                                                          (c128 *)A, a_stride, ntl);
