@@ -531,6 +531,79 @@ __global__ void omega_gather_kernel(int64_t n_items, int K, int i_max, int k_ini
   }
 }
 
+// X row k = W row k L^-H (forward substitution, d = DD columns in registers);
+// returns ||x||^2 and stores the row (stride 1) to xo.
+template <int DD>
+LRZ_DEV double scr_xrow(const c128 *__restrict__ wr, const c128 *L, int LD, c128 *xo) {
+  c128 x[DD];
+  double loc = 0.0;
+#pragma unroll
+  for (int j = 0; j < DD; ++j) {
+    c128 acc = wr[j];
+#pragma unroll
+    for (int m = 0; m < j; ++m) {
+      const c128 lj = L[j * LD + m];  // x_j -= x_m conj(L_jm)
+      acc.re -= x[m].re * lj.re + x[m].im * lj.im;
+      acc.im -= x[m].im * lj.re - x[m].re * lj.im;
+    }
+    x[j] = cscale(acc, 1.0 / L[j * LD + j].re);
+    loc += cabs2(x[j]);
+    xo[j] = x[j];
+  }
+  return loc;
+}
+
+// ||column t of L^-1||^2 for a DD x DD lower-triangular L.
+template <int DD>
+LRZ_DEV double scr_linv_col(const c128 *L, int LD, int t) {
+  c128 x[DD];
+  double f = 0.0;
+#pragma unroll
+  for (int i = 0; i < DD; ++i) {
+    if (i < t) {
+      x[i] = czero<double>();
+      continue;
+    }
+    c128 acc = mk<double>(i == t ? 1.0 : 0.0, 0.0);
+#pragma unroll
+    for (int k = 0; k < i; ++k) {
+      const c128 lk = L[i * LD + k];
+      acc.re -= lk.re * x[k].re - lk.im * x[k].im;
+      acc.im -= lk.re * x[k].im + lk.im * x[k].re;
+    }
+    x[i] = cscale(acc, 1.0 / L[i * LD + i].re);
+    f += cabs2(x[i]);
+  }
+  return f;
+}
+
+#define SCR_CASES(F)                                                                  \
+  F(1) F(2) F(3) F(4) F(5) F(6) F(7) F(8) F(9) F(10) F(11) F(12) F(13) F(14) F(15) F(16) \
+  F(17) F(18) F(19) F(20) F(21) F(22) F(23) F(24) F(25) F(26) F(27) F(28) F(29) F(30)   \
+  F(31) F(32)
+
+LRZ_DEV double scr_xrow_d(int d, const c128 *wr, const c128 *L, int LD, c128 *xo) {
+  switch (d) {
+#define SCR_X(n) \
+  case n:        \
+    return scr_xrow<n>(wr, L, LD, xo);
+    SCR_CASES(SCR_X)
+#undef SCR_X
+  }
+  return 0.0;
+}
+
+LRZ_DEV double scr_linv_col_d(int d, const c128 *L, int LD, int t) {
+  switch (d) {
+#define SCR_L(n) \
+  case n:        \
+    return scr_linv_col<n>(L, LD, t);
+    SCR_CASES(SCR_L)
+#undef SCR_L
+  }
+  return 0.0;
+}
+
 __global__ void __launch_bounds__(128) arsvd_screen_kernel(ArsvdArgs g, int64_t B, int Dtot,
                                                            const c128 *__restrict__ Yall,
                                                            const c128 *__restrict__ Wall,
@@ -619,25 +692,8 @@ __global__ void __launch_bounds__(128) arsvd_screen_kernel(ArsvdArgs g, int64_t 
     }
     // X = W_i L^-H row by row (lane = row), ||X||_F^2
     double loc = 0.0;
-    for (int k = lane; k < K; k += 32) {
-      c128 x[SCR_DMAX];
-#pragma unroll
-      for (int j = 0; j < SCR_DMAX; ++j) {
-        if (j < d) {
-          c128 acc = W[int64_t(k) * Dtot + o + j];
-#pragma unroll
-          for (int m = 0; m < SCR_DMAX; ++m)
-            if (m < j) {
-              const c128 lj = L[j * LD + m];  // x_j -= x_m conj(L_jm)
-              acc.re -= x[m].re * lj.re + x[m].im * lj.im;
-              acc.im -= x[m].im * lj.re - x[m].re * lj.im;
-            }
-          x[j] = cscale(acc, 1.0 / L[j * LD + j].re);
-          loc += cabs2(x[j]);
-          X[int64_t(k) * SCR_DMAX + j] = x[j];
-        }
-      }
-    }
+    for (int k = lane; k < K; k += 32)
+      loc += scr_xrow_d(d, W + int64_t(k) * Dtot + o, L, LD, X + int64_t(k) * SCR_DMAX);
     const double mf = warp_sum(loc);
     __syncwarp();
     if (mf < target * (1.0 - tol)) {  // no prefix of the spectrum reaches the target
@@ -689,24 +745,7 @@ __global__ void __launch_bounds__(128) arsvd_screen_kernel(ArsvdArgs g, int64_t 
           // ||L^-1||_F^2, column t per lane (forward substitution, kept in X's rows 0..d-1
           // is not possible: use registers)
           double f = 0.0;
-          for (int t = lane; t < d; t += 32) {
-            c128 x[SCR_DMAX];
-#pragma unroll
-            for (int i = 0; i < SCR_DMAX; ++i) {
-              if (i < d) {
-                c128 acc = mk<double>(i == t ? 1.0 : 0.0, 0.0);
-#pragma unroll
-                for (int k = 0; k < SCR_DMAX; ++k)
-                  if (k < i) {
-                    const c128 lk = L[i * LD + k];
-                    acc.re -= lk.re * x[k].re - lk.im * x[k].im;
-                    acc.im -= lk.re * x[k].im + lk.im * x[k].re;
-                  }
-                x[i] = (i < t) ? czero<double>() : cscale(acc, 1.0 / L[i * LD + i].re);
-                f += cabs2(x[i]);
-              }
-            }
-          }
+          for (int t = lane; t < d; t += 32) f += scr_linv_col_d(d, L, LD, t);
           const double F = warp_sum(f);
           if (isfinite(F) && F * mf <= 1e6) {
             if (lane == 0) {
