@@ -177,13 +177,21 @@ int lrz_sinr_rate(int dtype, int64_t batch, int K, const void *G, int64_t sG,
  * (the reference's Omega source, lowrank.py:284-286).  For each of B streams
  * with PCG64 state/inc (uint64 lo, hi pairs, as numpy's bit_generator.state
  * reports them) positioned `raw0[b]` raw draws in, writes the next L
- * normals to out[b][0..L) and the raw offset (relative to raw0) at which
- * each normal starts to startpos[b][0..L) (nullable).  status[b] != 0 if
- * the window could not be produced.  Workspace: lrz_workspace_bytes(
- * LRZ_WS_RNG, 0, B, 0, L, 0). */
+ * normals to out[b][0..L).  startpos must be NULL (positions are recovered
+ * on demand by lrz_rng_locate).  status[b] != 0 if the window could not be
+ * produced.  Workspace: lrz_workspace_bytes(LRZ_WS_RNG, 0, B, 0, L, 0); it
+ * keeps the window's segment tables for lrz_rng_locate. */
 int lrz_rng_normals(int64_t B, int64_t L, const uint64_t *state, const uint64_t *inc,
                     const int64_t *raw0, double *out, int32_t *startpos, int32_t *status,
                     void *workspace, void *stream);
+
+/* After lrz_rng_normals(B, L, state, inc, raw0, ..., workspace): raw draws
+ * taken by the first consumed[b] normals of the window (consumed[b] <= L),
+ * i.e. the amount to add to raw0[b] to skip exactly those normals.  Same
+ * B, L, state, inc, raw0 and workspace as the window call. */
+int lrz_rng_locate(int64_t B, int64_t L, const uint64_t *state, const uint64_t *inc,
+                   const int64_t *raw0, const int64_t *consumed, int64_t *raw_advance,
+                   void *workspace, void *stream);
 
 /* On-device synthetic channels (scenario.py, SURVEY 8(f) "next" #1): H for
  * steps [t0, t0 + T) of B trials, [B][T][K][N] of `dtype`.  params: [B][6][K]

@@ -63,6 +63,7 @@ _SIGS = {
     "lrz_sinr_rate": (C.c_int, [C.c_int, I64, C.c_int, P, I64, P, P, I64, P, P, P, P]),
     "lrz_plan": (C.c_int, [I64, C.c_int, P, P, P, P]),
     "lrz_rng_normals": (C.c_int, [I64, I64, P, P, P, P, P, P, P, P]),
+    "lrz_rng_locate": (C.c_int, [I64, I64, P, P, P, P, P, P, P]),
     "lrz_channels": (C.c_int, [C.c_int, I64, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, P, P,
                                I64, P, P]),
     "lrz_leo_snapshot": (C.c_int, [C.POINTER(LeoCfg), I64, C.c_int, C.c_int, P, P, P, I64, P,

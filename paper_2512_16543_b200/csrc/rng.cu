@@ -10,14 +10,17 @@
 // A normal consumes one raw draw 99.3 % of the time and more on the rejection
 // and tail paths, so normal n's raw position is data dependent.  Three passes:
 //   A  one thread per 256-draw segment: step PCG, record per raw position the
-//      draws a normal starting there consumes (c_j) and its value;
-//      summarise the segment for a normal starting at its first draw;
-//   B  one thread per trial: walk the segment summaries (re-walking a
-//      segment only when a multi-draw normal straddles its start) to get each
+//      draws a normal starting there consumes (c_j); follow the walk that
+//      starts at the segment's first draw ("walk 0") and store its normals
+//      compacted by rank, with their positions; summarise the walks entering
+//      at offsets 0..7 (almost every walk merges into walk 0 within a draw);
+//   B  one thread per trial: chain the segment summaries to get each
 //      segment's entry offset and the index of its first normal;
-//   C  one thread per segment: emit the normals at their stream indices and
-//      their raw start positions (used to advance the stream by exactly the
-//      normals a chunk consumed).
+//   C  one thread per segment: copy walk 0's normals from the entry's rank on
+//      to the output (independent loads); positions off walk 0 (rare) are
+//      recomputed from the PCG state.
+// lrz_rng_locate turns "normals consumed" into the raw draw offset afterwards,
+// so no per-normal position array is written.
 
 #include "common.cuh"
 #include "_gen/ziggurat_tables.h"
@@ -105,8 +108,10 @@ struct RngArgs {
   const uint64_t *st;    // [B][2] lo, hi of the PCG state at raw position 0 of the stream
   const uint64_t *inc;   // [B][2]
   const int64_t *raw0;   // [B] raw position where the window starts
-  uint8_t *cons;         // [B][nseg * SEG] draws consumed by a normal starting here
-  double *val;           // [B][nseg * SEG]
+  uint8_t *cons;         // [B][SEG][nseg] draws consumed by a normal starting here
+  double *vals0;         // [B][SEG][nseg] walk-0 normals by rank
+  uint8_t *pos0;         // [B][SEG][nseg] walk-0 positions by rank
+  uint32_t *vis;         // [B][nseg][SEG/32] walk-0 position bitmap
   int32_t *seg_cnt0;     // [B][nseg][RNG_NE] normals in the segment for entry offset e
   int32_t *seg_exit0;    // [B][nseg][RNG_NE] overhang into the next segment for entry e
   int32_t *seg_entry;    // [B][nseg] true entry offset
@@ -144,7 +149,7 @@ __global__ void __launch_bounds__(RNG_A_THREADS) rng_pass_a(RngArgs a) {
   const u128 inc = load_u128(a.inc + 2 * b);
   u128 st = pcg_advance(load_u128(a.st + 2 * b), inc,
                         uint64_t(a.raw0[b]) + uint64_t(s) * RNG_SEG);
-  int over = 0;
+  int over = 0, next0 = 0, cnt0 = 0;
   for (int j = 0; j < RNG_SEG; ++j) {
     const uint64_t r = pcg_next(st, inc);  // raw draw j; st now before draw j + 1
     int used;
@@ -152,21 +157,26 @@ __global__ void __launch_bounds__(RNG_A_THREADS) rng_pass_a(RngArgs a) {
     if (used > RNG_MAXC) over = 1;
     const uint8_t cu = uint8_t(used > 255 ? 255 : used);
     c[j] = cu;
-    const int64_t q = pos_index(a, b, j, s);
-    a.cons[q] = cu;
-    a.val[q] = x;
+    a.cons[pos_index(a, b, j, s)] = cu;
+    if (j == next0) {  // walk 0 emits a normal here
+      a.vals0[pos_index(a, b, cnt0, s)] = x;
+      a.pos0[pos_index(a, b, cnt0, s)] = uint8_t(j);
+      ++cnt0;
+      next0 = j + cu;
+    }
   }
-  // walk(0) with a visited mask, then entries 1..RNG_NE-1 merge into it
+  // walk(0) visited mask, then entries 1..RNG_NE-1 merge into it
   uint32_t vis[RNG_SEG / 32];
 #pragma unroll
   for (int i = 0; i < RNG_SEG / 32; ++i) vis[i] = 0;
-  int pos = 0, cnt0 = 0;
+  int pos = 0;
   while (pos < RNG_SEG) {
     vis[pos >> 5] |= 1u << (pos & 31);
-    ++cnt0;
     pos += c[pos];
   }
   const int exit0 = pos - RNG_SEG;
+#pragma unroll
+  for (int i = 0; i < RNG_SEG / 32; ++i) a.vis[tid * (RNG_SEG / 32) + i] = vis[i];
   int32_t *oc = a.seg_cnt0 + tid * RNG_NE, *oe = a.seg_exit0 + tid * RNG_NE;
   oc[0] = cnt0;
   oe[0] = over ? (1 << 20) : exit0;
@@ -246,7 +256,35 @@ __global__ void __launch_bounds__(256) rng_pass_b(RngArgs a) {
   if (threadIdx.x == 0) a.status[b] = (s_bad || s_base < a.L) ? 1 : 0;
 }
 
-__global__ void rng_pass_c(RngArgs a) {
+constexpr int RNG_C_THREADS = 128;
+
+// rank of position p in walk 0 (number of walk-0 positions before p)
+LRZ_DEV int walk0_rank(const uint32_t *vis, int p) {
+  int r = 0;
+  for (int i = 0; i < (p >> 5); ++i) r += __popc(vis[i]);
+  return r + __popc(vis[p >> 5] & ((1u << (p & 31)) - 1u));
+}
+
+// the normal starting at raw position `pos` of segment s (off walk 0: rare)
+LRZ_DEV double normal_at(const RngArgs &a, int64_t b, int s, int pos, const ZigTables &tb) {
+  const u128 inc = load_u128(a.inc + 2 * b);
+  u128 st = pcg_advance(load_u128(a.st + 2 * b), inc,
+                        uint64_t(a.raw0[b]) + uint64_t(s) * RNG_SEG + uint64_t(pos));
+  const uint64_t r = pcg_next(st, inc);
+  int used;
+  return zig_from(r, st, inc, tb, used);
+}
+
+__global__ void __launch_bounds__(RNG_C_THREADS) rng_pass_c(RngArgs a) {
+  __shared__ double s_wi[256], s_fi[256];
+  __shared__ uint64_t s_ki[256];
+  for (int i = threadIdx.x; i < 256; i += blockDim.x) {
+    s_wi[i] = zig_wi_double[i];
+    s_fi[i] = zig_fi_double[i];
+    s_ki[i] = zig_ki_double[i];
+  }
+  __syncthreads();
+  const ZigTables tb{s_wi, s_fi, s_ki};
   const int64_t tid = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
   if (tid >= a.B * a.nseg) return;
   const int64_t b = tid / a.nseg;
@@ -254,24 +292,115 @@ __global__ void rng_pass_c(RngArgs a) {
   int pos = a.seg_entry[tid];
   int64_t n = a.seg_base[tid];
   double *o = a.out + b * a.L;
-  int32_t *sp = a.startpos ? a.startpos + b * a.L : nullptr;
-  while (pos < RNG_SEG && n < a.L) {
-    const int64_t q = pos_index(a, b, pos, s);
-    o[n] = a.val[q];
-    if (sp) sp[n] = int32_t(int64_t(s) * RNG_SEG + pos);
-    ++n;
-    pos += a.cons[q];
+  uint32_t vis[RNG_SEG / 32];
+#pragma unroll
+  for (int i = 0; i < RNG_SEG / 32; ++i) vis[i] = a.vis[tid * (RNG_SEG / 32) + i];
+  // off walk 0: step the entry's own walk until it joins walk 0
+  while (pos < RNG_SEG && n < a.L && !((vis[pos >> 5] >> (pos & 31)) & 1u)) {
+    o[n++] = normal_at(a, b, s, pos, tb);
+    pos += a.cons[pos_index(a, b, pos, s)];
   }
+  if (pos >= RNG_SEG || n >= a.L) return;
+  // on walk 0 from rank r0: every later walk-0 normal of the segment, in order
+  const int r0 = walk0_rank(vis, pos);
+  int cnt0 = 0;
+#pragma unroll
+  for (int i = 0; i < RNG_SEG / 32; ++i) cnt0 += __popc(vis[i]);
+  const int m = int(min(int64_t(cnt0 - r0), a.L - n));
+  constexpr int V = 8;
+  for (int k0 = 0; k0 < m; k0 += V) {
+    double v[V];
+#pragma unroll
+    for (int k = 0; k < V; ++k)
+      if (k0 + k < m) v[k] = a.vals0[pos_index(a, b, r0 + k0 + k, s)];
+#pragma unroll
+    for (int k = 0; k < V; ++k)
+      if (k0 + k < m) o[n + k0 + k] = v[k];
+  }
+}
+
+// raw draws consumed by the first consumed[b] normals of the last window
+__global__ void rng_locate_kernel(RngArgs a, const int64_t *__restrict__ consumed,
+                                  int64_t *__restrict__ raw_adv) {
+  const int64_t b = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (b >= a.B) return;
+  const int64_t c = consumed[b];
+  // last segment whose first normal index is <= c
+  int lo = 0, hi = a.nseg - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (a.seg_base[b * a.nseg + mid] <= c) lo = mid; else hi = mid - 1;
+  }
+  const int s = lo;
+  const int64_t id = b * a.nseg + s;
+  int pos = a.seg_entry[id];
+  int64_t n = a.seg_base[id];
+  const uint32_t *vis = a.vis + id * (RNG_SEG / 32);
+  while (n < c && pos < RNG_SEG) {
+    if ((vis[pos >> 5] >> (pos & 31)) & 1u) {  // on walk 0: jump by rank
+      const int r = walk0_rank(vis, pos) + int(c - n);
+      int cnt0 = 0;
+      for (int i = 0; i < RNG_SEG / 32; ++i) cnt0 += __popc(vis[i]);
+      if (r < cnt0) {
+        pos = a.pos0[pos_index(a, b, r, s)];
+        n = c;
+      } else {  // past the segment's last normal: its exit
+        n += cnt0 - walk0_rank(vis, pos);
+        pos = RNG_SEG;
+        int p = 0;
+        while (p < RNG_SEG) p += a.cons[pos_index(a, b, p, s)];
+        pos = p;
+      }
+      break;
+    }
+    pos += a.cons[pos_index(a, b, pos, s)];
+    ++n;
+  }
+  raw_adv[b] = int64_t(s) * RNG_SEG + pos;
 }
 
 }  // namespace lrz
 
 using namespace lrz;
 
+static int64_t rng_nseg(int64_t L) { return (L + L / 32 + 2048 + RNG_SEG - 1) / RNG_SEG; }
+
 size_t lrz_rng_ws(int64_t B, int64_t L) {
-  const int64_t nseg = (L + L / 32 + 2048 + RNG_SEG - 1) / RNG_SEG;
-  const int64_t n = B * nseg;
-  return size_t(n) * RNG_SEG * (1 + 8) + size_t(n) * (2 * 4 * RNG_NE + 4 + 8) + 256;
+  const int64_t n = B * rng_nseg(L);
+  return size_t(n) * RNG_SEG * (8 + 1 + 1) + size_t(n) * (RNG_SEG / 8) +
+         size_t(n) * (2 * 4 * RNG_NE + 4 + 8) + 256;
+}
+
+static RngArgs rng_args(int64_t B, int64_t L, const uint64_t *state, const uint64_t *inc,
+                        const int64_t *raw0, void *workspace) {
+  RngArgs a;
+  a.B = B;
+  a.L = L;
+  a.nseg = int(rng_nseg(L));
+  a.st = state;
+  a.inc = inc;
+  a.raw0 = raw0;
+  const int64_t n = B * a.nseg;
+  char *w = (char *)workspace;
+  a.vals0 = (double *)w;
+  w += size_t(n) * RNG_SEG * 8;
+  a.seg_base = (int64_t *)w;
+  w += size_t(n) * 8;
+  a.seg_cnt0 = (int32_t *)w;
+  w += size_t(n) * 4 * RNG_NE;
+  a.seg_exit0 = (int32_t *)w;
+  w += size_t(n) * 4 * RNG_NE;
+  a.seg_entry = (int32_t *)w;
+  w += size_t(n) * 4;
+  a.vis = (uint32_t *)w;
+  w += size_t(n) * (RNG_SEG / 8);
+  a.cons = (uint8_t *)w;
+  w += size_t(n) * RNG_SEG;
+  a.pos0 = (uint8_t *)w;
+  a.out = nullptr;
+  a.startpos = nullptr;
+  a.status = nullptr;
+  return a;
 }
 
 extern "C" int lrz_rng_normals(int64_t B, int64_t L, const uint64_t *state, const uint64_t *inc,
@@ -282,33 +411,32 @@ extern "C" int lrz_rng_normals(int64_t B, int64_t L, const uint64_t *state, cons
     lrz_set_error("lrz_rng_normals: bad arguments");
     return LRZ_EINVAL;
   }
+  if (startpos) {
+    lrz_set_error("lrz_rng_normals: per-normal positions are not produced; use lrz_rng_locate");
+    return LRZ_EINVAL;
+  }
   if (B == 0) return LRZ_OK;
-  RngArgs a;
-  a.B = B;
-  a.L = L;
-  a.nseg = int((L + L / 32 + 2048 + RNG_SEG - 1) / RNG_SEG);
-  a.st = state;
-  a.inc = inc;
-  a.raw0 = raw0;
-  const int64_t n = B * a.nseg;
-  char *w = (char *)workspace;
-  a.val = (double *)w;
-  w += size_t(n) * RNG_SEG * 8;
-  a.seg_base = (int64_t *)w;
-  w += size_t(n) * 8;
-  a.seg_cnt0 = (int32_t *)w;
-  w += size_t(n) * 4 * RNG_NE;
-  a.seg_exit0 = (int32_t *)w;
-  w += size_t(n) * 4 * RNG_NE;
-  a.seg_entry = (int32_t *)w;
-  w += size_t(n) * 4;
-  a.cons = (uint8_t *)w;
+  RngArgs a = rng_args(B, L, state, inc, raw0, workspace);
   a.out = out;
-  a.startpos = startpos;
   a.status = status;
+  const int64_t n = B * a.nseg;
   cudaStream_t s = (cudaStream_t)stream;
   rng_pass_a<<<unsigned((n + RNG_A_THREADS - 1) / RNG_A_THREADS), RNG_A_THREADS, 0, s>>>(a);
   rng_pass_b<<<unsigned(B), 256, 0, s>>>(a);
-  rng_pass_c<<<unsigned((n + 127) / 128), 128, 0, s>>>(a);
+  rng_pass_c<<<unsigned((n + RNG_C_THREADS - 1) / RNG_C_THREADS), RNG_C_THREADS, 0, s>>>(a);
   return lrz_launch_status("lrz_rng_normals");
+}
+
+extern "C" int lrz_rng_locate(int64_t B, int64_t L, const uint64_t *state, const uint64_t *inc,
+                              const int64_t *raw0, const int64_t *consumed, int64_t *raw_advance,
+                              void *workspace, void *stream) {
+  if (B < 0 || L < 1 || !consumed || !raw_advance || !workspace) {
+    lrz_set_error("lrz_rng_locate: bad arguments");
+    return LRZ_EINVAL;
+  }
+  if (B == 0) return LRZ_OK;
+  RngArgs a = rng_args(B, L, state, inc, raw0, workspace);
+  rng_locate_kernel<<<unsigned((B + 127) / 128), 128, 0, (cudaStream_t)stream>>>(a, consumed,
+                                                                               raw_advance);
+  return lrz_launch_status("lrz_rng_locate");
 }

@@ -165,8 +165,9 @@ class DeviceOmegaStreams:
         self.state = as_u64(st).reshape(self.B, 2)
         self.inc = as_u64(inc).reshape(self.B, 2)
         self.raw = torch.zeros(self.B, dtype=torch.int64, device=self.device)
-        self._startpos = None
         self.consumed_total = torch.zeros(self.B, dtype=torch.int64, device=self.device)
+        self._L = None
+        self._ws = None        # this stream set's own RNG workspace (window tables)
 
     @classmethod
     def for_method(cls, master_seed: int, eta: float, trials, device) -> "DeviceOmegaStreams":
@@ -176,25 +177,34 @@ class DeviceOmegaStreams:
 
     def window(self, n: int, out=None):
         torch = self._torch
-        L = int(n) + 1  # one extra so the position after the last normal is known
+        L = int(n)
         lib = self._N.lib_for(self.device)
         full = torch.empty(self.B, L, dtype=torch.float64, device=self.device)
-        self._startpos = torch.empty(self.B, L, dtype=torch.int32, device=self.device)
         status = torch.zeros(self.B, dtype=torch.int32, device=self.device)
-        ws = self._ops.workspace(self.device, lib.lrz_workspace_bytes(self._N.WS_RNG, 0, self.B,
-                                                                        0, L, 0), "rng")
+        nbytes = int(lib.lrz_workspace_bytes(self._N.WS_RNG, 0, self.B, 0, L, 0))
+        if self._ws is None or self._ws.numel() < nbytes:
+            self._ws = torch.empty(nbytes, dtype=torch.uint8, device=self.device)
         self._N.check(lib.lrz_rng_normals(self.B, L, self.state.data_ptr(), self.inc.data_ptr(),
-                                          self.raw.data_ptr(), full.data_ptr(),
-                                          self._startpos.data_ptr(), status.data_ptr(),
-                                          ws.data_ptr(), self._N.stream_ptr(self.device)),
+                                          self.raw.data_ptr(), full.data_ptr(), None,
+                                          status.data_ptr(), self._ws.data_ptr(),
+                                          self._N.stream_ptr(self.device)),
                       "lrz_rng_normals")
         self._status = status
+        self._L = L
         self._ops._count(3)
-        return full[:, :n] if out is None else out.copy_(full[:, :n])
+        return full if out is None else out.copy_(full)
 
     def advance(self, consumed) -> None:
+        """Skip exactly the first consumed[b] normals of the last window."""
         torch = self._torch
         c = torch.as_tensor(consumed, dtype=torch.int64, device=self.device).reshape(self.B)
-        pos = torch.gather(self._startpos, 1, c.reshape(-1, 1)).reshape(-1).to(torch.int64)
-        self.raw += pos
+        c = c.contiguous()
+        adv = torch.empty(self.B, dtype=torch.int64, device=self.device)
+        lib = self._N.lib_for(self.device)
+        self._N.check(lib.lrz_rng_locate(self.B, self._L, self.state.data_ptr(),
+                                         self.inc.data_ptr(), self.raw.data_ptr(), c.data_ptr(),
+                                         adv.data_ptr(), self._ws.data_ptr(),
+                                         self._N.stream_ptr(self.device)), "lrz_rng_locate")
+        self._ops._count(1)
+        self.raw += adv
         self.consumed_total += c
