@@ -604,7 +604,7 @@ LRZ_DEV double scr_linv_col_d(int d, const c128 *L, int LD, int t) {
   return 0.0;
 }
 
-__global__ void __launch_bounds__(128) arsvd_screen_kernel(ArsvdArgs g, int64_t B, int Dtot,
+__global__ void __launch_bounds__(128, 4) arsvd_screen_kernel(ArsvdArgs g, int64_t B, int Dtot,
                                                            const c128 *__restrict__ Yall,
                                                            const c128 *__restrict__ Wall,
                                                            c128 *__restrict__ Xs,
