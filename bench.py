@@ -408,6 +408,8 @@ def run_b200(args):
     streams = DeviceOmegaStreams.for_method(spec.seed, eta, trials, dev)
     stream = torch.cuda.current_stream(dev)
 
+    rng_stream = torch.cuda.Stream(dev)
+
     def one(cfg, prof=None, Hd=H_dev, st=streams, sl=slice(None)):
         nb = Hd.shape[0]
         rn = TrajectoryRunner(nb, K, Nn, tdt, cfg, dev)
@@ -415,10 +417,13 @@ def run_b200(args):
         om = None
         if cfg.eta is not None:
             st.raw.zero_()
-            e0 = rn._ev()
-            om = st.window(L)
-            rn._stage("omega_rng", e0)
-        return rn.run_chunk(Hd, noise[sl], om)
+            if prof is not None:   # stage profile: serialised so the RNG's own time is seen
+                e0 = rn._ev()
+                om = st.window(L)
+                rn._stage("omega_rng", e0)
+            else:                  # the step: Omega generated on a side stream under the Gram
+                om = st.window(L, stream=rng_stream)
+        return rn.run_chunk(Hd, noise[sl], om, omega_ready=st.ready)
 
     def timed(cfg, steps, prof=None):
         barrier()

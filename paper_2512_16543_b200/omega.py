@@ -168,6 +168,7 @@ class DeviceOmegaStreams:
         self.consumed_total = torch.zeros(self.B, dtype=torch.int64, device=self.device)
         self._L = None
         self._ws = None        # this stream set's own RNG workspace (window tables)
+        self.ready = None      # event of the last window generated on a side stream
 
     @classmethod
     def for_method(cls, master_seed: int, eta: float, trials, device) -> "DeviceOmegaStreams":
@@ -175,8 +176,23 @@ class DeviceOmegaStreams:
         return cls((np.random.default_rng(stream_seed(master_seed, label, t)) for t in trials),
                    device)
 
-    def window(self, n: int, out=None):
+    def window(self, n: int, out=None, stream=None):
+        """(B, n) device tensor of each trial's next n normals.  With `stream`
+        the generation runs there (after the current stream's pending work)
+        and ``self.ready`` is an event the consumer waits on -- the RNG is
+        integer work and overlaps the FP64 Gram stage."""
         torch = self._torch
+        if stream is not None:
+            cur = torch.cuda.current_stream(self.device)
+            stream.wait_stream(cur)
+            with torch.cuda.stream(stream):
+                w = self.window(n, out)
+                self.ready = torch.cuda.Event()
+                self.ready.record(stream)
+            w.record_stream(cur)
+            self._ws.record_stream(cur)
+            return w
+        self.ready = None
         L = int(n)
         lib = self._N.lib_for(self.device)
         full = torch.empty(self.B, L, dtype=torch.float64, device=self.device)

@@ -89,6 +89,9 @@ class TrajectoryResult:
     A_inv: np.ndarray | None = None
 
 
+_MASKS: dict = {}   # dispatcher-step masks by (B, reset pattern, device)
+
+
 class TrajectoryRunner:
     """Stateful runner over consecutive time chunks of B trials."""
 
@@ -134,7 +137,9 @@ class TrajectoryRunner:
         return 0 if c.eta is None else normals_per_call_bound(self.K, c.k_init, c.p, c.i_max,
                                                               self._eta_max())
 
-    def _is_sketch(self, T: int) -> torch.Tensor:
+    def _is_sketch(self, T: int):
+        """(device [B, T] uint8 mask of dispatcher steps, host count per trial);
+        built on the host from the step indices -- no device round trip."""
         c = self.cfg
         tg = np.arange(self.t, self.t + T)
         reset = (tg == 0) | ((c.n_reset > 0) & (tg % max(c.n_reset, 1) == 0))
@@ -142,13 +147,71 @@ class TrajectoryRunner:
             reset[0] = True
         if c.eta is None:
             reset[:] = True
-        row = torch.from_numpy((~reset).astype(np.uint8))
-        return row.to(self.device).reshape(1, T).expand(self.B, T).contiguous()
+        key = (self.B, reset.tobytes(), self.device)
+        dev_mask = _MASKS.get(key)
+        if dev_mask is None:
+            row = torch.from_numpy((~reset).astype(np.uint8))
+            dev_mask = row.to(self.device).reshape(1, T).expand(self.B, T).contiguous()
+            if len(_MASKS) > 64:
+                _MASKS.clear()
+            _MASKS[key] = dev_mask
+        return dev_mask, int((~reset).sum())
+
+    def _tail(self, G, Hf, noise, is_sketch, iters_pred, cursor, res, k_est, plan, hybrid,
+              keep_W):
+        """Stages 4-7 of a chunk (dispatcher, batched full inversions, Woodbury
+        chain, precoder + rate) from the arSVD results."""
+        c = self.cfg
+        B, T, K = G.shape[0], G.shape[1], self.K
+        BT, Nn, dev = B * T, Hf.shape[-1], self.device
+        iters = torch.zeros(B, T, dtype=torch.int32, device=dev)
+        consumed = torch.zeros(B, dtype=torch.int64, device=dev)
+        if res is not None:
+            iters.copy_(iters_pred * is_sketch.to(torch.int32))
+            U, V, S = res["U"], res["V"], res["S"]
+            consumed = cursor[:, -1] + res["consumed"].reshape(B, T)[:, -1] * is_sketch[:, -1]
+            # 4. dispatcher
+            ops.plan(is_sketch, k_est, K, out=plan)
+        else:
+            U = torch.zeros(BT, 1, K, dtype=torch.complex128, device=dev)
+            V = torch.zeros_like(U)
+            S = torch.ones(BT, 1, dtype=torch.float64, device=dev)
+        # 5. full inversions (plan == 0) batched
+        A_inv_seq = torch.empty(B, T, K, K, dtype=torch.complex128, device=dev)
+        info = torch.zeros(B, T, dtype=torch.int32, device=dev)
+        full_mask = (plan == 0).to(torch.uint8)
+        e0 = self._ev()
+        ops.herm_inverse(G.reshape(BT, K, K), 1e14, mask=full_mask.reshape(BT),
+                         out=A_inv_seq.reshape(BT, K, K), info=info.reshape(BT))
+        self._stage("inverse", e0)
+        # 6. sequential Woodbury recurrence per trial
+        method = torch.zeros(B, T, dtype=torch.uint8, device=dev)
+        e0 = self._ev()
+        ops.chain(plan, G, self.A_inv, A_inv_seq, self.A if c.maintain_A else None, U, V, S,
+                  k_est, method, info)
+        self._stage("chain", e0)
+        # 7. precoder and rate
+        e0 = self._ev()
+        if hybrid is not None:
+            pr = ops.hybrid_precode_rate(Hf, A_inv_seq.reshape(BT, K, K),
+                                         hybrid["H_rf"].reshape(BT, K, Nn),
+                                         hybrid["cols"].reshape(BT, Nn), hybrid["n_x"],
+                                         hybrid["n_y"], hybrid["dft"], c.P_t, noise, T,
+                                         want_F=keep_W)
+            W = pr["F_BB"]
+        else:
+            W = torch.empty(BT, Nn, K, dtype=self.dtype, device=dev) if keep_W else None
+            pr = ops.precode_rate(Hf, A_inv_seq.reshape(BT, K, K), c.P_t, noise, T, W=W,
+                                  want_sinr=False,
+                                  G_true=G.reshape(BT, K, K) if c.rate_via_gram else None,
+                                  alpha=c.alpha)
+        self._stage("precode_rate", e0)
+        return A_inv_seq, method, info, pr, W, iters, consumed
 
     # -- one chunk -------------------------------------------------------------
     def run_chunk(self, H: torch.Tensor, noise: torch.Tensor, omega: torch.Tensor | None = None,
-                  keep_A_inv: bool = False, keep_W: bool = False, hybrid: dict | None = None
-                  ) -> ChunkResult:
+                  keep_A_inv: bool = False, keep_W: bool = False, hybrid: dict | None = None,
+                  omega_ready=None) -> ChunkResult:
         """H [B, T, K, N] (device, self.dtype); noise [B, K] float64 (device);
         omega [B, L] float64 (device; row b = trial b's next unconsumed normals,
         L >= T * normals_per_step_max()).
@@ -156,15 +219,15 @@ class TrajectoryRunner:
         hybrid (analog beams, reference precoding.py:37-80 with F_RF != I): H is
         the effective channel H_eff = H~ F_RF and the dict carries H_rf = H F_RF
         [B,T,K,N_RF], cols [B,T,N_RF] (DFT codebook indices), n_x, n_y and dft
-        (the two DFT factors) for the hybrid precoder / rate."""
+        (the two DFT factors) for the hybrid precoder / rate.  omega_ready: CUDA
+        event the sketch window was produced under (another stream)."""
         c = self.cfg
         B, T, K, Nn = H.shape
         assert (B, K, Nn) == (self.B, self.K, self.N) and H.dtype == self.dtype
         dev = self.device
         BT = B * T
         Hf = H.reshape(BT, K, Nn)
-        is_sketch = self._is_sketch(T)
-        n_sketch = int(is_sketch[0].sum().item()) if T else 0
+        is_sketch, n_sketch = self._is_sketch(T)
 
         # 1. true Grams of every step
         e0 = self._ev()
@@ -172,10 +235,7 @@ class TrajectoryRunner:
         self._stage("gram", e0)
         plan = torch.zeros(B, T, dtype=torch.uint8, device=dev)
         k_est = torch.zeros(B, T, dtype=torch.int32, device=dev)
-        iters = torch.zeros(B, T, dtype=torch.int32, device=dev)
-        consumed = torch.zeros(B, dtype=torch.int64, device=dev)
         D = self.D
-        U = V = S = None
         passes = 0
         if n_sketch:
             # 2. Gram corrections between consecutive channels (dH = H_t - H_{t-1})
@@ -198,6 +258,8 @@ class TrajectoryRunner:
             self._stage("gram_delta", e0)
             # 3. speculative arSVD
             assert omega is not None and omega.shape[0] == B
+            if omega_ready is not None:
+                torch.cuda.current_stream(dev).wait_event(omega_ready)
             i_eff = effective_i_max(K, c.k_init, c.p, c.i_max, self._eta_max())
             iters_pred = torch.full((B, T), i_eff, dtype=torch.int32, device=dev)
             cursor = torch.zeros(B, T, dtype=torch.int64, device=dev)
@@ -217,9 +279,9 @@ class TrajectoryRunner:
                 fallback=torch.zeros(BT, dtype=torch.int32, device=dev),
                 consumed=torch.zeros(BT, dtype=torch.int64, device=dev),
             )
-            pinned = torch.zeros(1, dtype=torch.int32).pin_memory()
             n_spec = 0 if self._in_order else c.spec_passes
-            while True:
+
+            def one_pass():
                 e0 = self._ev()
                 if passes < n_spec:
                     ops.arsvd(dAf, omega, cursor.reshape(BT), self._eta, c.k_init, c.p, c.i_max,
@@ -231,63 +293,50 @@ class TrajectoryRunner:
                     ops.arsvd_seq(dA, omega, is_sketch, first, cursor, iters_pred, self._eta,
                                   c.k_init, c.p, c.i_max, res)
                 self._stage("arsvd", e0)
-                passes += 1
                 pending.zero_()
                 e0 = self._ev()
                 ops.spec_verify(is_sketch, iters_pred, res["iters"], cursor, cursor0, first,
                                 active, pending, K, self._eta, c.k_init, c.p, c.i_max)
                 self._stage("verify", e0)
-                pinned.copy_(pending, non_blocking=True)
-                torch.cuda.current_stream(dev).synchronize()
-                if int(pinned[0]) == 0:
-                    break
-                if passes > n_spec:
-                    raise RuntimeError("in-order arSVD left unverified steps")
+                # pending trials, and calls that found their sketch window too short
+                torch.stack([pending[0], (res["iters"] < 0).sum().to(torch.int32)],
+                            out=flags)
+
+            flags = torch.zeros(2, dtype=torch.int32, device=dev)
+            pinned = torch.zeros(2, dtype=torch.int32).pin_memory()
+            A_state0 = self.A.clone() if c.maintain_A else None
+            one_pass()
+            passes = 1
+            # optimistic: the rest of the chunk is queued behind the first pass and
+            # only then is the verifier's answer read back (one sync per chunk)
+            pinned.copy_(flags, non_blocking=True)
+            tail = self._tail(G, Hf, noise, is_sketch, iters_pred, cursor, res, k_est, plan,
+                              hybrid, keep_W)
+            torch.cuda.current_stream(dev).synchronize()
+            if int(pinned[1]):
+                raise RuntimeError("sketch window shorter than an arsvd call needed")
+            if int(pinned[0]):
+                while True:
+                    one_pass()
+                    passes += 1
+                    pinned.copy_(flags, non_blocking=True)
+                    torch.cuda.current_stream(dev).synchronize()
+                    if int(pinned[1]):
+                        raise RuntimeError("sketch window shorter than an arsvd call needed")
+                    if int(pinned[0]) == 0:
+                        break
+                    if passes > n_spec:
+                        raise RuntimeError("in-order arSVD left unverified steps")
+                if A_state0 is not None:
+                    self.A.copy_(A_state0)
+                tail = self._tail(G, Hf, noise, is_sketch, iters_pred, cursor, res, k_est, plan,
+                                  hybrid, keep_W)
             if passes > n_spec:
                 self._in_order = True   # iteration counts track the sketch: skip speculation
-            if int((res["iters"] < 0).sum().item()):
-                raise RuntimeError("sketch window shorter than an arsvd call needed")
-            iters.copy_(iters_pred * is_sketch.to(torch.int32))
-            U, V, S = res["U"], res["V"], res["S"]
-            last = cursor[:, -1] + res["consumed"].reshape(B, T)[:, -1] * is_sketch[:, -1]
-            consumed = last
-            # 4. dispatcher
-            ops.plan(is_sketch, k_est, K, out=plan)
-        # 5. full inversions (plan == 0) batched
-        A_inv_seq = torch.empty(B, T, K, K, dtype=torch.complex128, device=dev)
-        info = torch.zeros(B, T, dtype=torch.int32, device=dev)
-        full_mask = (plan == 0).to(torch.uint8)
-        e0 = self._ev()
-        ops.herm_inverse(G.reshape(BT, K, K), 1e14, mask=full_mask.reshape(BT),
-                         out=A_inv_seq.reshape(BT, K, K), info=info.reshape(BT))
-        self._stage("inverse", e0)
-        # 6. sequential Woodbury recurrence per trial
-        method = torch.zeros(B, T, dtype=torch.uint8, device=dev)
-        if U is None:
-            U = torch.zeros(BT, 1, K, dtype=torch.complex128, device=dev)
-            V = torch.zeros_like(U)
-            S = torch.ones(BT, 1, dtype=torch.float64, device=dev)
-        e0 = self._ev()
-        ops.chain(plan, G, self.A_inv, A_inv_seq, self.A if c.maintain_A else None, U, V, S,
-                  k_est, method, info)
-        self._stage("chain", e0)
-        # 7. precoder and rate
-        W = None
-        e0 = self._ev()
-        if hybrid is not None:
-            pr = ops.hybrid_precode_rate(Hf, A_inv_seq.reshape(BT, K, K),
-                                         hybrid["H_rf"].reshape(BT, K, Nn),
-                                         hybrid["cols"].reshape(BT, Nn), hybrid["n_x"],
-                                         hybrid["n_y"], hybrid["dft"], c.P_t, noise, T,
-                                         want_F=keep_W)
-            W = pr["F_BB"]
         else:
-            W = torch.empty(BT, Nn, K, dtype=self.dtype, device=dev) if keep_W else None
-            pr = ops.precode_rate(Hf, A_inv_seq.reshape(BT, K, K), c.P_t, noise, T, W=W,
-                                  want_sinr=False,
-                                  G_true=G.reshape(BT, K, K) if c.rate_via_gram else None,
-                                  alpha=c.alpha)
-        self._stage("precode_rate", e0)
+            tail = self._tail(G, Hf, noise, is_sketch, None, None, None, k_est, plan, hybrid,
+                              keep_W)
+        A_inv_seq, method, info, pr, W, iters, consumed = tail
         # state for the next chunk
         self.A_inv = A_inv_seq[:, -1].clone()
         self.H_prev = H[:, -1].contiguous().clone()
