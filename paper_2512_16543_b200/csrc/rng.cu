@@ -32,7 +32,6 @@ constexpr int RNG_SEG = 256;
 constexpr int RNG_MAXC = 64;  // a normal consuming more draws aborts the window (never seen)
 constexpr int RNG_NE = 8;     // entry offsets summarised per segment by pass A
 constexpr int RNG_A_THREADS = 128;
-constexpr int RNG_B_CHUNK = 512;  // segments per shared-memory chunk in pass B
 LRZ_DEV u128 pcg_mult() {
   return (u128(0x2360ED051FC65DA4ull) << 64) | u128(0x4385DF649FCCF645ull);
 }
@@ -150,6 +149,9 @@ __global__ void __launch_bounds__(RNG_A_THREADS) rng_pass_a(RngArgs a) {
   u128 st = pcg_advance(load_u128(a.st + 2 * b), inc,
                         uint64_t(a.raw0[b]) + uint64_t(s) * RNG_SEG);
   int over = 0, next0 = 0, cnt0 = 0;
+  const int64_t col = pos_index(a, b, 0, s), stride = a.nseg;  // [b][j][s]: j advances by nseg
+  uint8_t *pc = a.cons + col, *pp = a.pos0 + col;
+  double *pv = a.vals0 + col;
   for (int j = 0; j < RNG_SEG; ++j) {
     const uint64_t r = pcg_next(st, inc);  // raw draw j; st now before draw j + 1
     int used;
@@ -157,10 +159,10 @@ __global__ void __launch_bounds__(RNG_A_THREADS) rng_pass_a(RngArgs a) {
     if (used > RNG_MAXC) over = 1;
     const uint8_t cu = uint8_t(used > 255 ? 255 : used);
     c[j] = cu;
-    a.cons[pos_index(a, b, j, s)] = cu;
+    pc[int64_t(j) * stride] = cu;
     if (j == next0) {  // walk 0 emits a normal here
-      a.vals0[pos_index(a, b, cnt0, s)] = x;
-      a.pos0[pos_index(a, b, cnt0, s)] = uint8_t(j);
+      pv[int64_t(cnt0) * stride] = x;
+      pp[int64_t(cnt0) * stride] = uint8_t(j);
       ++cnt0;
       next0 = j + cu;
     }
@@ -199,61 +201,140 @@ __global__ void __launch_bounds__(RNG_A_THREADS) rng_pass_a(RngArgs a) {
   }
 }
 
-// one CTA per trial: segment summaries staged in shared memory, thread 0 walks
-__global__ void __launch_bounds__(256) rng_pass_b(RngArgs a) {
-  __shared__ int32_t s_cnt[RNG_B_CHUNK * RNG_NE], s_exit[RNG_B_CHUNK * RNG_NE];
-  __shared__ int s_entry;
-  __shared__ long long s_base;
-  __shared__ int s_bad;
-  const int64_t b = blockIdx.x;
-  if (threadIdx.x == 0) {
-    s_entry = 0;
-    s_base = 0;
-    s_bad = 0;
+// Pass B: segment s maps an entry offset e < RNG_NE to (exit offset, normals
+// emitted) -- pass A's summaries.  These maps compose associatively, so a CTA
+// per trial scans them in parallel (per-thread runs of segments, then a
+// Hillis-Steele scan of the run maps).  An exit >= RNG_NE (a normal
+// overhanging the next segment by >= RNG_NE draws, ~1e-6 per segment) or an
+// overlong normal sends the trial through the sequential walk instead.
+constexpr int RNG_B_THREADS = 512;
+constexpr uint8_t RNG_BIG = 255;
+
+struct SegMap {
+  uint8_t ex[RNG_NE];
+  int32_t cn[RNG_NE];
+};
+
+LRZ_DEV SegMap map_identity() {
+  SegMap m;
+#pragma unroll
+  for (int e = 0; e < RNG_NE; ++e) {
+    m.ex[e] = uint8_t(e);
+    m.cn[e] = 0;
   }
-  for (int s0 = 0; s0 < a.nseg; s0 += RNG_B_CHUNK) {
-    const int ns = min(RNG_B_CHUNK, a.nseg - s0);
-    __syncthreads();
-    for (int i = threadIdx.x; i < ns * RNG_NE; i += blockDim.x) {
-      const int64_t g = (b * a.nseg + s0) * RNG_NE + i;
-      s_cnt[i] = a.seg_cnt0[g];
-      s_exit[i] = a.seg_exit0[g];
+  return m;
+}
+
+// g after f
+LRZ_DEV SegMap map_then(const SegMap &f, const SegMap &g) {
+  SegMap m;
+#pragma unroll
+  for (int e = 0; e < RNG_NE; ++e) {
+    const uint8_t x = f.ex[e];
+    if (x == RNG_BIG) {
+      m.ex[e] = RNG_BIG;
+      m.cn[e] = 0;
+    } else {
+      m.ex[e] = g.ex[x];
+      m.cn[e] = f.cn[e] + g.cn[x];
     }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      int entry = s_entry, bad = s_bad;
-      long long base = s_base;
-      for (int i = 0; i < ns; ++i) {
-        const int s = s0 + i;
-        const int64_t id = b * a.nseg + s;
-        a.seg_entry[id] = entry;
-        a.seg_base[id] = base;
-        if (entry < RNG_NE) {
-          const int ex = s_exit[i * RNG_NE + entry];
-          if (ex >= (1 << 20)) bad = 1;
-          base += s_cnt[i * RNG_NE + entry];
-          entry = ex >= (1 << 20) ? 0 : ex;
-        } else if (entry >= RNG_SEG) {
-          entry -= RNG_SEG;
-        } else {  // rare: re-walk from global memory
-          int pos = entry, cnt = 0;
-          while (pos < RNG_SEG) {
-            const int cp = a.cons[pos_index(a, b, pos, s)];
-            if (cp >= 255) bad = 1;
-            ++cnt;
-            pos += cp;
-          }
-          base += cnt;
-          entry = pos - RNG_SEG;
-        }
+  }
+  return m;
+}
+
+LRZ_DEV SegMap seg_map(const RngArgs &a, int64_t id) {
+  SegMap m;
+#pragma unroll
+  for (int e = 0; e < RNG_NE; ++e) {
+    const int ex = a.seg_exit0[id * RNG_NE + e];
+    m.ex[e] = (ex >= 0 && ex < RNG_NE) ? uint8_t(ex) : RNG_BIG;
+    m.cn[e] = a.seg_cnt0[id * RNG_NE + e];
+  }
+  return m;
+}
+
+// the original sequential walk (fallback)
+LRZ_DEV void pass_b_serial(const RngArgs &a, int64_t b) {
+  int entry = 0, bad = 0;
+  long long base = 0;
+  for (int s = 0; s < a.nseg; ++s) {
+    const int64_t id = b * a.nseg + s;
+    a.seg_entry[id] = entry;
+    a.seg_base[id] = base;
+    if (entry < RNG_NE) {
+      const int ex = a.seg_exit0[id * RNG_NE + entry];
+      if (ex >= (1 << 20)) bad = 1;
+      base += a.seg_cnt0[id * RNG_NE + entry];
+      entry = ex >= (1 << 20) ? 0 : ex;
+    } else if (entry >= RNG_SEG) {
+      entry -= RNG_SEG;
+    } else {  // re-walk from the draw counts
+      int pos = entry, cnt = 0;
+      while (pos < RNG_SEG) {
+        const int cp = a.cons[pos_index(a, b, pos, s)];
+        if (cp >= 255) bad = 1;
+        ++cnt;
+        pos += cp;
       }
-      s_entry = entry;
-      s_base = base;
-      s_bad = bad;
+      base += cnt;
+      entry = pos - RNG_SEG;
+    }
+  }
+  a.status[b] = (bad || base < a.L) ? 1 : 0;
+}
+
+__global__ void __launch_bounds__(RNG_B_THREADS) rng_pass_b(RngArgs a) {
+  __shared__ SegMap s_map[RNG_B_THREADS];
+  __shared__ int s_fallback;
+  const int64_t b = blockIdx.x;
+  const int t = threadIdx.x;
+  const int per = (a.nseg + RNG_B_THREADS - 1) / RNG_B_THREADS;
+  const int s0 = min(a.nseg, t * per), s1 = min(a.nseg, s0 + per);
+  if (t == 0) s_fallback = 0;
+  SegMap run = map_identity();
+  for (int s = s0; s < s1; ++s) run = map_then(run, seg_map(a, b * a.nseg + s));
+  s_map[t] = run;
+  __syncthreads();
+  // inclusive Hillis-Steele scan: s_map[t] = run_0 then ... then run_t
+  for (int off = 1; off < RNG_B_THREADS; off <<= 1) {
+    SegMap left;
+    const bool has = t >= off;
+    if (has) left = s_map[t - off];
+    __syncthreads();
+    if (has) s_map[t] = map_then(left, s_map[t]);
+    __syncthreads();
+  }
+  // entry state at this thread's first segment: the scan up to the previous run
+  int entry = 0;
+  long long base = 0;
+  if (t > 0) {
+    const SegMap &p = s_map[t - 1];
+    if (p.ex[0] == RNG_BIG) {
+      s_fallback = 1;
+    } else {
+      entry = p.ex[0];
+      base = p.cn[0];
+    }
+  }
+  for (int s = s0; s < s1; ++s) {
+    const int64_t id = b * a.nseg + s;
+    a.seg_entry[id] = entry;
+    a.seg_base[id] = base;
+    const int ex = a.seg_exit0[id * RNG_NE + entry];
+    base += a.seg_cnt0[id * RNG_NE + entry];
+    if (ex < 0 || ex >= RNG_NE) {  // includes the overlong-normal marker
+      if (s + 1 < a.nseg || ex >= (1 << 20)) s_fallback = 1;
+      entry = 0;
+    } else {
+      entry = ex;
     }
   }
   __syncthreads();
-  if (threadIdx.x == 0) a.status[b] = (s_bad || s_base < a.L) ? 1 : 0;
+  if (s_fallback) {
+    if (t == 0) pass_b_serial(a, b);
+    return;
+  }
+  if (t == RNG_B_THREADS - 1) a.status[b] = (base < a.L) ? 1 : 0;
 }
 
 constexpr int RNG_C_THREADS = 128;
@@ -422,7 +503,7 @@ extern "C" int lrz_rng_normals(int64_t B, int64_t L, const uint64_t *state, cons
   const int64_t n = B * a.nseg;
   cudaStream_t s = (cudaStream_t)stream;
   rng_pass_a<<<unsigned((n + RNG_A_THREADS - 1) / RNG_A_THREADS), RNG_A_THREADS, 0, s>>>(a);
-  rng_pass_b<<<unsigned(B), 256, 0, s>>>(a);
+  rng_pass_b<<<unsigned(B), RNG_B_THREADS, 0, s>>>(a);
   rng_pass_c<<<unsigned((n + RNG_C_THREADS - 1) / RNG_C_THREADS), RNG_C_THREADS, 0, s>>>(a);
   return lrz_launch_status("lrz_rng_normals");
 }
