@@ -359,6 +359,10 @@ LRZ_DEV double normal_at(const RngArgs &a, int64_t b, int s, int pos, const ZigT
 __global__ void __launch_bounds__(RNG_C_THREADS) rng_pass_c(RngArgs a) {
   __shared__ double s_wi[256], s_fi[256];
   __shared__ uint64_t s_ki[256];
+  __shared__ double s_v[RNG_C_THREADS][33];
+  __shared__ int s_m[RNG_C_THREADS];
+  __shared__ int64_t s_n[RNG_C_THREADS];
+  __shared__ double *s_o[RNG_C_THREADS];
   for (int i = threadIdx.x; i < 256; i += blockDim.x) {
     s_wi[i] = zig_wi_double[i];
     s_fi[i] = zig_fi_double[i];
@@ -366,11 +370,12 @@ __global__ void __launch_bounds__(RNG_C_THREADS) rng_pass_c(RngArgs a) {
   }
   __syncthreads();
   const ZigTables tb{s_wi, s_fi, s_ki};
-  const int64_t tid = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
-  if (tid >= a.B * a.nseg) return;
+  const int64_t tid0 = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  const bool live = tid0 < a.B * a.nseg;
+  const int64_t tid = live ? tid0 : 0;
   const int64_t b = tid / a.nseg;
   const int s = int(tid - b * a.nseg);
-  int pos = a.seg_entry[tid];
+  int pos = live ? a.seg_entry[tid] : RNG_SEG;
   int64_t n = a.seg_base[tid];
   double *o = a.out + b * a.L;
   uint32_t vis[RNG_SEG / 32];
@@ -381,22 +386,38 @@ __global__ void __launch_bounds__(RNG_C_THREADS) rng_pass_c(RngArgs a) {
     o[n++] = normal_at(a, b, s, pos, tb);
     pos += a.cons[pos_index(a, b, pos, s)];
   }
-  if (pos >= RNG_SEG || n >= a.L) return;
-  // on walk 0 from rank r0: every later walk-0 normal of the segment, in order
-  const int r0 = walk0_rank(vis, pos);
-  int cnt0 = 0;
+  // on walk 0 from rank r0: every later walk-0 normal of the segment, in order;
+  // copied through shared memory in 32-normal chunks so that each warp writes
+  // one segment's 32 consecutive outputs per store (coalesced)
+  int r0 = 0, m = 0;
+  if (pos < RNG_SEG && n < a.L) {
+    r0 = walk0_rank(vis, pos);
+    int cnt0 = 0;
 #pragma unroll
-  for (int i = 0; i < RNG_SEG / 32; ++i) cnt0 += __popc(vis[i]);
-  const int m = int(min(int64_t(cnt0 - r0), a.L - n));
-  constexpr int V = 8;
-  for (int k0 = 0; k0 < m; k0 += V) {
-    double v[V];
-#pragma unroll
-    for (int k = 0; k < V; ++k)
-      if (k0 + k < m) v[k] = a.vals0[pos_index(a, b, r0 + k0 + k, s)];
-#pragma unroll
-    for (int k = 0; k < V; ++k)
-      if (k0 + k < m) o[n + k0 + k] = v[k];
+    for (int i = 0; i < RNG_SEG / 32; ++i) cnt0 += __popc(vis[i]);
+    m = int(min(int64_t(cnt0 - r0), a.L - n));
+  }
+  s_m[threadIdx.x] = m;
+  s_n[threadIdx.x] = n;
+  s_o[threadIdx.x] = o;
+  int mmax = m;
+  mmax = max(mmax, __shfl_xor_sync(0xffffffffu, mmax, 16));
+  mmax = max(mmax, __shfl_xor_sync(0xffffffffu, mmax, 8));
+  mmax = max(mmax, __shfl_xor_sync(0xffffffffu, mmax, 4));
+  mmax = max(mmax, __shfl_xor_sync(0xffffffffu, mmax, 2));
+  mmax = max(mmax, __shfl_xor_sync(0xffffffffu, mmax, 1));
+  const int lane = threadIdx.x & 31, wb = threadIdx.x & ~31;
+  const double *src = a.vals0 + pos_index(a, b, r0, s);
+  for (int k0 = 0; k0 < mmax; k0 += 32) {   // warp-uniform bound (shfl max)
+#pragma unroll 8
+    for (int kk = 0; kk < 32; ++kk)
+      if (k0 + kk < m) s_v[threadIdx.x][kk] = src[int64_t(k0 + kk) * a.nseg];
+    __syncwarp();
+    for (int u = 0; u < 32; ++u) {            // the warp writes thread u's chunk
+      const int mu = s_m[wb + u];
+      if (k0 + lane < mu) s_o[wb + u][s_n[wb + u] + k0 + lane] = s_v[wb + u][lane];
+    }
+    __syncwarp();
   }
 }
 
