@@ -189,8 +189,9 @@ class DeviceOmegaStreams:
                 w = self.window(n, out)
                 self.ready = torch.cuda.Event()
                 self.ready.record(stream)
-            w.record_stream(cur)
-            self._ws.record_stream(cur)
+            if not torch.cuda.is_current_stream_capturing():
+                w.record_stream(cur)
+                self._ws.record_stream(cur)
             return w
         self.ready = None
         L = int(n)

@@ -74,6 +74,7 @@ class ChunkResult:
     scale: torch.Tensor          # [B, T] power normalisation
     consumed: torch.Tensor       # [B] normals consumed in this chunk
     spec_passes: int = 0
+    flags: torch.Tensor | None = None   # sync=False: [unverified trials, short windows]
 
 
 @dataclass
@@ -90,6 +91,13 @@ class TrajectoryResult:
 
 
 _MASKS: dict = {}   # dispatcher-step masks by (B, reset pattern, device)
+_PINNED: list = []  # one pinned int32[2] readback buffer (page-locking per call is slow)
+
+
+def _pinned_flags() -> torch.Tensor:
+    if not _PINNED:
+        _PINNED.append(torch.zeros(2, dtype=torch.int32).pin_memory())
+    return _PINNED[0]
 
 
 class TrajectoryRunner:
@@ -211,7 +219,7 @@ class TrajectoryRunner:
     # -- one chunk -------------------------------------------------------------
     def run_chunk(self, H: torch.Tensor, noise: torch.Tensor, omega: torch.Tensor | None = None,
                   keep_A_inv: bool = False, keep_W: bool = False, hybrid: dict | None = None,
-                  omega_ready=None) -> ChunkResult:
+                  omega_ready=None, sync: bool = True) -> ChunkResult:
         """H [B, T, K, N] (device, self.dtype); noise [B, K] float64 (device);
         omega [B, L] float64 (device; row b = trial b's next unconsumed normals,
         L >= T * normals_per_step_max()).
@@ -220,7 +228,12 @@ class TrajectoryRunner:
         the effective channel H_eff = H~ F_RF and the dict carries H_rf = H F_RF
         [B,T,K,N_RF], cols [B,T,N_RF] (DFT codebook indices), n_x, n_y and dft
         (the two DFT factors) for the hybrid precoder / rate.  omega_ready: CUDA
-        event the sketch window was produced under (another stream)."""
+        event the sketch window was produced under (another stream).
+
+        sync=False: no host round trip at all (CUDA-graph capture): the chunk is
+        computed optimistically from the first arSVD pass and ``result.flags``
+        (device int32[2]: unverified trials, short sketch windows) must be
+        checked by the caller -- nonzero means re-run the chunk with sync=True."""
         c = self.cfg
         B, T, K, Nn = H.shape
         assert (B, K, Nn) == (self.B, self.K, self.N) and H.dtype == self.dtype
@@ -237,6 +250,7 @@ class TrajectoryRunner:
         k_est = torch.zeros(B, T, dtype=torch.int32, device=dev)
         D = self.D
         passes = 0
+        chunk_flags = None
         if n_sketch:
             # 2. Gram corrections between consecutive channels (dH = H_t - H_{t-1})
             dA = torch.empty(B, T, K, K, dtype=torch.complex128, device=dev)
@@ -303,36 +317,38 @@ class TrajectoryRunner:
                             out=flags)
 
             flags = torch.zeros(2, dtype=torch.int32, device=dev)
-            pinned = torch.zeros(2, dtype=torch.int32).pin_memory()
-            A_state0 = self.A.clone() if c.maintain_A else None
+            A_state0 = self.A.clone() if (c.maintain_A and sync) else None
             one_pass()
             passes = 1
             # optimistic: the rest of the chunk is queued behind the first pass and
             # only then is the verifier's answer read back (one sync per chunk)
-            pinned.copy_(flags, non_blocking=True)
             tail = self._tail(G, Hf, noise, is_sketch, iters_pred, cursor, res, k_est, plan,
                               hybrid, keep_W)
-            torch.cuda.current_stream(dev).synchronize()
-            if int(pinned[1]):
-                raise RuntimeError("sketch window shorter than an arsvd call needed")
-            if int(pinned[0]):
-                while True:
-                    one_pass()
-                    passes += 1
-                    pinned.copy_(flags, non_blocking=True)
-                    torch.cuda.current_stream(dev).synchronize()
-                    if int(pinned[1]):
-                        raise RuntimeError("sketch window shorter than an arsvd call needed")
-                    if int(pinned[0]) == 0:
-                        break
-                    if passes > n_spec:
-                        raise RuntimeError("in-order arSVD left unverified steps")
-                if A_state0 is not None:
-                    self.A.copy_(A_state0)
-                tail = self._tail(G, Hf, noise, is_sketch, iters_pred, cursor, res, k_est, plan,
-                                  hybrid, keep_W)
-            if passes > n_spec:
-                self._in_order = True   # iteration counts track the sketch: skip speculation
+            chunk_flags = flags
+            if sync:
+                pinned = _pinned_flags()
+                pinned.copy_(flags, non_blocking=True)
+                torch.cuda.current_stream(dev).synchronize()
+                if int(pinned[1]):
+                    raise RuntimeError("sketch window shorter than an arsvd call needed")
+                if int(pinned[0]):
+                    while True:
+                        one_pass()
+                        passes += 1
+                        pinned.copy_(flags, non_blocking=True)
+                        torch.cuda.current_stream(dev).synchronize()
+                        if int(pinned[1]):
+                            raise RuntimeError("sketch window shorter than an arsvd call needed")
+                        if int(pinned[0]) == 0:
+                            break
+                        if passes > n_spec:
+                            raise RuntimeError("in-order arSVD left unverified steps")
+                    if A_state0 is not None:
+                        self.A.copy_(A_state0)
+                    tail = self._tail(G, Hf, noise, is_sketch, iters_pred, cursor, res, k_est,
+                                      plan, hybrid, keep_W)
+                if passes > n_spec:
+                    self._in_order = True   # iteration counts track the sketch: skip speculation
         else:
             tail = self._tail(G, Hf, noise, is_sketch, None, None, None, k_est, plan, hybrid,
                               keep_W)
@@ -348,7 +364,7 @@ class TrajectoryRunner:
                            A_inv=A_inv_seq if keep_A_inv else None,
                            W=W.reshape(B, T, *W.shape[1:]) if keep_W else None,
                            scale=pr["scale"].reshape(B, T), consumed=consumed,
-                           spec_passes=passes)
+                           spec_passes=passes, flags=None if sync else chunk_flags)
 
 
 def step_costs(method: np.ndarray, k_est: np.ndarray, is_sketch: np.ndarray, K: int) -> np.ndarray:
