@@ -536,11 +536,11 @@ __global__ void __launch_bounds__(256)
 // ---------------------------------------------------------------------------
 constexpr int PW_KC = 8;      // k rows per slab
 constexpr int PW_ROWS = 128;  // antenna rows per block pass
-constexpr int PW_THREADS = 256;
+constexpr int PW_THREADS = 128;
 
 
 template <typename T>
-__global__ void __launch_bounds__(PW_THREADS, 2)
+__global__ void __launch_bounds__(PW_THREADS, 3)
     precoder_w32_kernel(int K, int N, const cplx<T> *__restrict__ H, int64_t hs,
                         const c128 *__restrict__ Ainv, int64_t ais, cplx<T> *__restrict__ W,
                         int64_t wst, double *__restrict__ norm2) {
@@ -548,7 +548,7 @@ __global__ void __launch_bounds__(PW_THREADS, 2)
   cplx<T> *As = (cplx<T> *)pw2_smem;               // [32][32]
   cplx<T> *Hs = As + 32 * 32;                      // [2][PW_KC][PW_ROWS]
   __shared__ double red[16];
-  const int tid = threadIdx.x, cg = tid & 3, rg = tid >> 2;
+  const int tid = threadIdx.x, cg = tid & 3, rg = tid >> 2;   // rows rg + 32 r, r < 4
   const int64_t item = blockIdx.x;
   const c128 *ai = Ainv + item * ais;
   for (int e = tid; e < 32 * 32; e += PW_THREADS) {
@@ -560,9 +560,9 @@ __global__ void __launch_bounds__(PW_THREADS, 2)
   double nrm = 0.0;
   const int nslab = (K + PW_KC - 1) / PW_KC;
   for (int n0 = 0; n0 < N; n0 += PW_ROWS) {
-    cplx<T> acc[2][8];
+    cplx<T> acc[4][8];
 #pragma unroll
-    for (int r = 0; r < 2; ++r)
+    for (int r = 0; r < 4; ++r)
 #pragma unroll
       for (int c = 0; c < 8; ++c) acc[r][c] = czero<T>();
     auto issue = [&](int slab, int buf) {
@@ -590,20 +590,22 @@ __global__ void __launch_bounds__(PW_THREADS, 2)
 #pragma unroll
       for (int kk = 0; kk < PW_KC; ++kk) {
         const int k = sl * PW_KC + kk;
-        const cplx<T> a0 = hb[kk * PW_ROWS + rg], a1 = hb[kk * PW_ROWS + rg + 64];
+        cplx<T> a[4];
+#pragma unroll
+        for (int r = 0; r < 4; ++r) a[r] = hb[kk * PW_ROWS + rg + 32 * r];
         const cplx<T> *br = As + k * 32 + cg;
 #pragma unroll
         for (int c = 0; c < 8; ++c) {
           const cplx<T> b = br[4 * c];
-          cfma_ca(acc[0][c], a0, b);
-          cfma_ca(acc[1][c], a1, b);
+#pragma unroll
+          for (int r = 0; r < 4; ++r) cfma_ca(acc[r][c], a[r], b);
         }
       }
       __syncthreads();
     }
 #pragma unroll
-    for (int r = 0; r < 2; ++r) {
-      const int n = n0 + rg + 64 * r;
+    for (int r = 0; r < 4; ++r) {
+      const int n = n0 + rg + 32 * r;
       if (n < N) {
 #pragma unroll
         for (int c = 0; c < 8; ++c) {
