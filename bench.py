@@ -643,6 +643,11 @@ def run_b200(args):
     # ---- the reference's own LEO campaign (hybrid beams), SURVEY 8(f) #3/#4
     leo = None
     if not args.no_extra:
+        # the campaign allocates its own multi-GB chunk buffers: hand back the
+        # graph pools and cached blocks of the C2 measurements first
+        graphs.clear()
+        torch.cuda.synchronize(dev)
+        torch.cuda.empty_cache()
         leo = leo_side(args, dev, world, max_over_ranks)
 
     # ---- CPU baseline (rank 0, N = 1 only)

@@ -169,6 +169,7 @@ class DeviceOmegaStreams:
         self._L = None
         self._ws = None        # this stream set's own RNG workspace (window tables)
         self.ready = None      # event of the last window generated on a side stream
+        self._out = None       # reused window buffer
 
     @classmethod
     def for_method(cls, master_seed: int, eta: float, trials, device) -> "DeviceOmegaStreams":
@@ -177,7 +178,8 @@ class DeviceOmegaStreams:
                    device)
 
     def window(self, n: int, out=None, stream=None):
-        """(B, n) device tensor of each trial's next n normals.  With `stream`
+        """(B, n) device tensor of each trial's next n normals (a view of a
+        buffer the next window() call overwrites).  With `stream`
         the generation runs there (after the current stream's pending work)
         and ``self.ready`` is an event the consumer waits on -- the RNG is
         integer work and overlaps the FP64 Gram stage."""
@@ -196,7 +198,12 @@ class DeviceOmegaStreams:
         self.ready = None
         L = int(n)
         lib = self._N.lib_for(self.device)
-        full = torch.empty(self.B, L, dtype=torch.float64, device=self.device)
+        # one output buffer per stream set, reused by every window (the previous
+        # window is dead once the next is requested: callers consume a window
+        # within its chunk); avoids a multi-hundred-MB allocation per chunk
+        if self._out is None or self._out.numel() < self.B * L:
+            self._out = torch.empty(self.B * L, dtype=torch.float64, device=self.device)
+        full = self._out[:self.B * L].view(self.B, L)
         status = torch.zeros(self.B, dtype=torch.int32, device=self.device)
         nbytes = int(lib.lrz_workspace_bytes(self._N.WS_RNG, 0, self.B, 0, L, 0))
         if self._ws is None or self._ws.numel() < nbytes:
