@@ -72,5 +72,45 @@ def report(path):
                     print(f"  raw {name:60s} {vals[i]} {units[i]}")
 
 
+def traffic(path, out=None):
+    """Per-kernel launches, mean duration and mean DRAM bytes per launch from an
+    ncu --csv log with gpu__time_duration.sum, dram__bytes_read.sum and
+    dram__bytes_write.sum; optionally written as JSON (read by bench.py)."""
+    import json
+    rows = list(csv.reader(open(path)))
+    hi = [i for i, r in enumerate(rows) if "Kernel Name" in r][0]
+    h, data = rows[hi], rows[hi + 1:]
+    ki, ii = h.index("Kernel Name"), h.index("ID")
+    mi, vi, ui = h.index("Metric Name"), h.index("Metric Value"), h.index("Metric Unit")
+    per = {}
+    for r in data:
+        if len(r) <= vi:
+            continue
+        key = (r[ii], r[ki].split("(")[0])
+        d = per.setdefault(key, {})
+        v = float(r[vi].replace(",", ""))
+        unit = r[ui]
+        if r[mi] == "gpu__time_duration.sum":
+            v *= {"ns": 1e-6, "nsecond": 1e-6, "us": 1e-3, "usecond": 1e-3, "ms": 1.0,
+                  "msecond": 1.0}.get(unit, 1e-6)
+        else:
+            v *= {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(unit, 1.0)
+        d[r[mi]] = v
+    agg = {}
+    for (_, name), d in per.items():
+        a = agg.setdefault(name, {"launches": 0, "ms": 0.0, "dram_bytes": 0.0})
+        a["launches"] += 1
+        a["ms"] += d.get("gpu__time_duration.sum", 0.0)
+        a["dram_bytes"] += d.get("dram__bytes_read.sum", 0.0) + d.get("dram__bytes_write.sum", 0.0)
+    res = {k: {"launches": v["launches"], "ms_per_launch": v["ms"] / v["launches"],
+               "dram_bytes_per_launch": v["dram_bytes"] / v["launches"]} for k, v in agg.items()}
+    for k, v in sorted(res.items(), key=lambda x: -x[1]["ms_per_launch"] * x[1]["launches"]):
+        print(f"{v['launches']:6d} {v['ms_per_launch']:9.4f} ms {v['dram_bytes_per_launch'] / 1e6:10.1f} MB  {k[:80]}")
+    if out:
+        with open(out, "w") as f:
+            json.dump(res, f, indent=1)
+
+
 if __name__ == "__main__":
-    {"launches": launches, "report": report}[sys.argv[1]](sys.argv[2])
+    fn = {"launches": launches, "report": report, "traffic": traffic}[sys.argv[1]]
+    fn(*sys.argv[2:])
