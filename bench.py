@@ -362,6 +362,34 @@ def stage_model(spec, T, B, k_mean, iters_hist, wb_steps):
     return m
 
 
+# kernels (name fragment, launches per WB step) behind each bench stage
+STAGE_KERNELS = {
+    "arsvd": [("omega_gather_kernel", 1), ("cgemm_kernel", 2), ("arsvd_screen_kernel", 1),
+              ("arsvd_kernel", 1)],
+    "gram": [("gram32_kernel", 1)],
+    "precode_rate": [("precoder_w32_kernel", 1), ("sinr_kernel", 1)],
+    "inverse": [("herm_inverse_warp_kernel", 1), ("herm_inverse_kernel", 1)],
+    "omega_rng": [("rng_pass_a", 1), ("rng_pass_b", 1), ("rng_pass_c", 1)],
+}
+
+
+def stage_traffic(stage, spec):
+    """DRAM bytes per step of a stage (sum over its kernels, per launch x launches)
+    from the committed ncu capture of the same command (profiles/, C2 c128 only)."""
+    path = ROOT / "profiles" / "r01_traffic_C2_c128.json"
+    if spec.name != "C2" or spec.dtype != "c128" or not path.exists() or stage not in STAGE_KERNELS:
+        return None
+    tab = json.loads(path.read_text())
+    tot = 0.0
+    for frag, n in STAGE_KERNELS[stage]:
+        hits = [v for k, v in tab.items() if k.split("<")[0].endswith(frag)]
+        if not hits:
+            return None
+        tot += hits[0]["dram_bytes_per_launch"] * n
+    return {"bytes_per_step": tot, "source": f"ncu dram__bytes_read.sum + dram__bytes_write.sum, "
+                                               f"{path.relative_to(ROOT)}"}
+
+
 def run_b200(args):
     import torch
     import torch.distributed as dist
@@ -534,7 +562,10 @@ def run_b200(args):
     roof["frac"] = roof["achieved"] / roof["peak"]
     roof["kernel"] = dom
     roof["launches_per_step"] = launches_dom
-    roof["traffic"] = None
+    tr = stage_traffic(dom, spec)
+    roof["traffic"] = tr["bytes_per_step"] if tr else None
+    roof["traffic_note"] = (tr["source"] + "; per step of the stage, like 'algorithmic' (the "
+                            "algorithmic bytes are the compulsory dA + Omega reads)") if tr else None
     roof["algorithmic"] = {"flops_per_step": flops, "bytes_per_step": byts}
     all_stages = {}
     for k, v in stage_ms.items():
