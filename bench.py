@@ -364,7 +364,7 @@ def stage_model(spec, T, B, k_mean, iters_hist, wb_steps):
 
 # kernels (name fragment, launches per WB step) behind each bench stage
 STAGE_KERNELS = {
-    "arsvd": [("omega_gather_kernel", 1), ("cgemm_kernel", 2), ("arsvd_screen_kernel", 1),
+    "arsvd": [("sketch_cgemm_kernel", 1), ("cgemm_kernel", 1), ("arsvd_screen_kernel", 1),
               ("arsvd_kernel", 1)],
     "gram": [("gram32_kernel", 1)],
     "precode_rate": [("precoder_w32_kernel", 1), ("sinr_kernel", 1)],

@@ -16,6 +16,11 @@
 
 #include "common.cuh"
 
+int lrz_sketch_gemm(int64_t B, int K, int Dtot, const void *dA, int64_t a_stride,
+                    const double *omega, int64_t omega_stride, const int32_t *omega_row,
+                    int64_t orow_div, const int64_t *cursor, int k_init, int p,
+                    const uint8_t *mask, void *Y, void *stream);
+
 namespace lrz {
 
 constexpr int ARSVD_THREADS = 256;
@@ -501,35 +506,6 @@ arsvd_seq_kernel(ArsvdArgs g, int T, const uint8_t *__restrict__ is_sketch,
 // ---------------------------------------------------------------------------
 constexpr int SCR_DMAX = 32;
 
-__global__ void omega_gather_kernel(int64_t n_items, int K, int i_max, int k_init, int p,
-                                    int Dtot, const double *__restrict__ omega, int64_t os,
-                                    const int32_t *__restrict__ orow,
-                                    const int64_t *__restrict__ cursor,
-                                    const uint8_t *__restrict__ mask, c128 *__restrict__ Om) {
-  const int64_t per = int64_t(K) * Dtot;
-  const int64_t total = n_items * per;
-  const double SQH = 0.7071067811865476;
-  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < total;
-       e += int64_t(gridDim.x) * blockDim.x) {
-    const int64_t item = e / per;
-    if (mask && !mask[item]) continue;
-    const int rem = int(e - item * per);
-    const int m = rem / Dtot, col = rem - m * Dtot;
-    // locate the iteration block holding this column
-    int o = 0, k0 = k_init;
-    int64_t c = cursor ? cursor[item] : 0;
-    int d = min(k0 + p, K);
-    while (col >= o + d) {
-      o += d;
-      c += int64_t(2) * K * d;
-      k0 *= 2;
-      d = min(k0 + p, K);
-    }
-    const int j = col - o;
-    const double *z = omega + (orow ? int64_t(orow[item]) : item) * os + c;
-    Om[e] = mk<double>(SQH * z[m * d + j], SQH * z[int64_t(K) * d + m * d + j]);
-  }
-}
 
 // X row k = W row k L^-H (forward substitution, d = DD columns in registers);
 // returns ||x||^2 and stores the row (stride 1) to xo.
@@ -548,7 +524,7 @@ LRZ_DEV double scr_xrow(const c128 *__restrict__ wr, const c128 *L, int LD, c128
     }
     x[j] = cscale(acc, 1.0 / L[j * LD + j].re);
     loc += cabs2(x[j]);
-    xo[j] = x[j];
+    if (xo) xo[j] = x[j];
   }
   return loc;
 }
@@ -693,7 +669,9 @@ __global__ void __launch_bounds__(128, 4) arsvd_screen_kernel(ArsvdArgs g, int64
     // X = W_i L^-H row by row (lane = row), ||X||_F^2
     double loc = 0.0;
     for (int k = lane; k < K; k += 32)
-      loc += scr_xrow_d(d, W + int64_t(k) * Dtot + o, L, LD, X + int64_t(k) * SCR_DMAX);
+      // X itself is only needed by the iteration-cap tail's certificate
+      loc += scr_xrow_d(d, W + int64_t(k) * Dtot + o, L, LD,
+                        last ? X + int64_t(k) * SCR_DMAX : nullptr);
     const double mf = warp_sum(loc);
     __syncwarp();
     if (mf < target * (1.0 - tol)) {  // no prefix of the spectrum reaches the target
@@ -867,12 +845,8 @@ extern "C" int lrz_arsvd(int64_t B, int K, const void *dA, int64_t a_stride,
     c128 *Om = (c128 *)wp;
     c128 *Ya = (c128 *)(wp + blk);
     c128 *Wa = (c128 *)(wp + 2 * blk);
-    const int64_t tot = B * int64_t(K) * Dtot;
-    omega_gather_kernel<<<unsigned(std::min<int64_t>((tot + 255) / 256, 148 * 64)), 256, 0, st>>>(
-        B, K, cfg->i_max, cfg->k_init, cfg->p, Dtot, omega, omega_stride, omega_row, cursor,
-        item_mask, Om);
-    int rc = lrz_cgemm(LRZ_C128, B, K, Dtot, K, 0, dA, K, a_stride, 0, Om, Dtot,
-                       int64_t(K) * Dtot, Ya, Dtot, int64_t(K) * Dtot, stream);
+    int rc = lrz_sketch_gemm(B, K, Dtot, dA, a_stride, omega, omega_stride, omega_row, 1, cursor,
+                             cfg->k_init, cfg->p, item_mask, Ya, stream);
     if (rc) return rc;
     rc = lrz_cgemm(LRZ_C128, B, K, Dtot, K, 0, dA, K, a_stride, 0, Ya, Dtot, int64_t(K) * Dtot,
                    Wa, Dtot, int64_t(K) * Dtot, stream);

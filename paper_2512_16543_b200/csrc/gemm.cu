@@ -527,6 +527,100 @@ __global__ void __launch_bounds__(256)
 
 
 // ---------------------------------------------------------------------------
+// Y = dA [Omega_0 ... Omega_{i_max-1}] for the arSVD front end, with the
+// sketch operand read straight from the normal window (block i: real K x d_i
+// then imaginary K x d_i at cursor + sum_{i'<i} 2 K d_i', scaled by sqrt(1/2),
+// lowrank.py:284-286) -- no materialised complex Omega.  Same tiling as
+// cgemm_kernel (32 x 32 output tiles, A row-major).
+// ---------------------------------------------------------------------------
+struct SketchOperand {
+  const double *omega;
+  int64_t os;
+  const int32_t *orow;
+  int64_t orow_div;
+  const int64_t *cursor;
+  int k_init, p;
+};
+
+__global__ void __launch_bounds__(GEMM_THREADS)
+    sketch_cgemm_kernel(int K, int Dtot, const c128 *__restrict__ A, int64_t sA, SketchOperand so,
+                        const uint8_t *__restrict__ mask, c128 *__restrict__ C, int tiles_n) {
+  constexpr int BK = 16;
+  __shared__ c128 As[BK][TM + 1];
+  __shared__ c128 Bs[BK][TM + 1];
+  __shared__ int s_off[TM], s_d[TM], s_j[TM];
+  const int tiles_m = (K + TM - 1) / TM, ntile = tiles_m * tiles_n;
+  const int64_t item = blockIdx.x / ntile;
+  if (mask && !mask[item]) return;
+  const int tile = int(blockIdx.x % ntile);
+  const int I = tile / tiles_n, J = tile % tiles_n;
+  const c128 *a = A + item * sA;
+  const int64_t row = so.orow ? int64_t(so.orow[item]) : item / so.orow_div;
+  const double *z = so.omega + row * so.os + (so.cursor ? so.cursor[item] : 0);
+  const int tid = threadIdx.x, tx = tid & 7, ty = tid >> 3;
+  // column -> (block offset in the stream, block width d, column j in block)
+  for (int n = tid; n < TM; n += GEMM_THREADS) {
+    const int gn = J * TM + n;
+    int o = 0, k0 = so.k_init, d = min(k0 + so.p, K);
+    int off = 0;
+    while (gn >= o + d && gn < Dtot) {
+      o += d;
+      off += 2 * K * d;
+      k0 *= 2;
+      d = min(k0 + so.p, K);
+    }
+    s_off[n] = off;
+    s_d[n] = d;
+    s_j[n] = gn - o;
+  }
+  __syncthreads();
+  const double SQH = 0.7071067811865476;
+  c128 acc[2][4];
+#pragma unroll
+  for (int i = 0; i < 2; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j] = czero<double>();
+  for (int k0 = 0; k0 < K; k0 += BK) {
+    for (int e = tid; e < TM * BK; e += GEMM_THREADS) {
+      const int m = e / BK, k = e % BK, gm = I * TM + m, gk = k0 + k;
+      As[k][m] = (gm < K && gk < K) ? a[int64_t(gm) * K + gk] : czero<double>();
+    }
+    for (int e = tid; e < TM * BK; e += GEMM_THREADS) {
+      const int k = e / TM, n = e % TM, gn = J * TM + n, gk = k0 + k;
+      c128 v = czero<double>();
+      if (gn < Dtot && gk < K) {
+        const int d = s_d[n];
+        const double *zb = z + s_off[n] + int64_t(gk) * d + s_j[n];
+        v = mk<double>(SQH * zb[0], SQH * zb[int64_t(K) * d]);
+      }
+      Bs[k][n] = v;
+    }
+    __syncthreads();
+#pragma unroll 4
+    for (int k = 0; k < BK; ++k) {
+      const c128 a0 = As[k][ty], a1 = As[k][ty + 16];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const c128 bj = Bs[k][tx + 8 * j];
+        cfma(acc[0][j], a0, bj);
+        cfma(acc[1][j], a1, bj);
+      }
+    }
+    __syncthreads();
+  }
+  c128 *c = C + item * int64_t(K) * Dtot;
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    const int r = I * TM + ty + 16 * i;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int col = J * TM + tx + 8 * j;
+      if (r < K && col < Dtot) c[int64_t(r) * Dtot + col] = acc[i][j];
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
 // K6 precoder W = H^H A^-1, one item per CTA, K <= 32, 256 threads (2 CTAs/SM).
 // Thread (rg, cg): rows {rg, rg + 64} of each 128-row block, columns
 // {cg + 4 c : c < 8}; H streamed through shared memory in 8-row k-slabs
@@ -702,6 +796,18 @@ extern "C" int lrz_gram_delta(int dtype, int64_t B, int K, int N, const void *P,
         K, N, (const c128 *)P, p_stride, (const c128 *)Q, q_stride, mode, (c128 *)dA,
         a_stride, ntl);
   return lrz_launch_status("lrz_gram_delta");
+}
+
+// Y = dA Omega_all with Omega read from the normal window (lrz_arsvd's front end)
+int lrz_sketch_gemm(int64_t B, int K, int Dtot, const void *dA, int64_t a_stride,
+                    const double *omega, int64_t omega_stride, const int32_t *omega_row,
+                    int64_t orow_div, const int64_t *cursor, int k_init, int p,
+                    const uint8_t *mask, void *Y, void *stream) {
+  const int tn = (Dtot + TM - 1) / TM, tm = (K + TM - 1) / TM;
+  SketchOperand so{omega, omega_stride, omega_row, orow_div, cursor, k_init, p};
+  sketch_cgemm_kernel<<<unsigned(B * tm * tn), GEMM_THREADS, 0, (cudaStream_t)stream>>>(
+      K, Dtot, (const c128 *)dA, a_stride, so, mask, (c128 *)Y, tn);
+  return lrz_launch_status("sketch_cgemm_kernel");
 }
 
 extern "C" int lrz_cgemm(int dtype, int64_t batch, int M, int N, int Kd, int opA,
