@@ -1,0 +1,116 @@
+"""Runner execution modes against the eager, verified path: CUDA-graph capture
+(run_chunk(sync=False)), the in-order arSVD fallback (lrz_arsvd_seq), several
+WB methods batched with a per-row eta, and lrz_rng_locate."""
+
+import numpy as np
+import pytest
+import torch
+
+from conftest import load_golden
+from paper_2512_16543_b200 import TrajectoryConfig, TrajectoryRunner, scenario as S
+from paper_2512_16543_b200.omega import DeviceOmegaStreams, OmegaStreams
+
+pytestmark = pytest.mark.gpu
+
+
+def _setup(cuda, spec, eta, trials):
+    H = torch.from_numpy(S.channels(spec, trials=trials)).to(cuda)
+    noise = torch.full((len(trials), spec.K), spec.noise_var, dtype=torch.float64, device=cuda)
+    cfg = TrajectoryConfig(alpha=spec.alpha, eta=eta, k_init=spec.k_init, p=spec.p,
+                           i_max=spec.i_max)
+    return H, noise, cfg
+
+
+def test_graph_replay_equals_eager(cuda):
+    spec = S.C2.with_(B=8, T=40)
+    trials = list(range(8))
+    H, noise, cfg = _setup(cuda, spec, spec.eta, trials)
+    st = DeviceOmegaStreams.for_method(spec.seed, spec.eta, trials, cuda)
+    side = torch.cuda.Stream(cuda)
+
+    def step(sync):
+        rn = TrajectoryRunner(8, spec.K, spec.N, torch.complex128, cfg, cuda)
+        st.raw.zero_()
+        L = spec.T * rn.normals_per_step_max()
+        om = st.window(L, stream=side)
+        return rn.run_chunk(H, noise, om, omega_ready=st.ready, sync=sync)
+
+    ref = step(True)
+    for _ in range(2):
+        step(False)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        out = step(False)
+    for _ in range(3):
+        g.replay()
+    torch.cuda.synchronize()
+    assert int(out.flags.abs().sum()) == 0
+    assert torch.equal(out.method, ref.method)
+    assert torch.equal(out.k_est, ref.k_est)
+    assert torch.equal(out.rates, ref.rates)
+
+
+def test_in_order_arsvd_equals_speculative(cuda):
+    """spec_passes = 0 (in-order from the first step) and the default policy give
+    the same trajectory, and both match the reference golden at eta = 0.9."""
+    g = load_golden("traj_C2s")
+    spec = S.C2
+    H = torch.from_numpy(S.channels(spec, trials=[0, 1], t1=24)).to(cuda)
+    noise = torch.full((2, spec.K), spec.noise_var, dtype=torch.float64, device=cuda)
+    outs = []
+    for sp in (0, 2):
+        cfg = TrajectoryConfig(alpha=spec.alpha, eta=0.9, k_init=spec.k_init, p=spec.p,
+                               i_max=spec.i_max, spec_passes=sp)
+        rn = TrajectoryRunner(2, spec.K, spec.N, torch.complex128, cfg, cuda)
+        st = OmegaStreams.for_method(0, 0.9, [0, 1])
+        om = torch.from_numpy(st.window(24 * rn.normals_per_step_max())).to(cuda)
+        outs.append(rn.run_chunk(H, noise, om))
+    a, b = outs
+    assert torch.equal(a.k_est, b.k_est) and torch.equal(a.method, b.method)
+    assert torch.equal(a.consumed, b.consumed)
+    for t in (0, 1):
+        assert np.array_equal(a.k_est[t].cpu().numpy(), g[f"t{t}_e900_k_est"])
+        np.testing.assert_allclose(a.rates[t].cpu().numpy(), g[f"t{t}_e900_rates"], rtol=1e-10)
+
+
+def test_per_row_eta_equals_separate_runners(cuda):
+    spec = S.C2.with_(B=3, T=30)
+    trials = [0, 1, 2]
+    H, noise, _ = _setup(cuda, spec, None, trials)
+    etas = (0.9, 0.8)
+    sep = []
+    for eta in etas:
+        cfg = TrajectoryConfig(alpha=spec.alpha, eta=eta, k_init=spec.k_init, p=spec.p,
+                               i_max=spec.i_max)
+        rn = TrajectoryRunner(3, spec.K, spec.N, torch.complex128, cfg, cuda)
+        st = DeviceOmegaStreams.for_method(spec.seed, eta, trials, cuda)
+        sep.append(rn.run_chunk(H, noise, st.window(spec.T * rn.normals_per_step_max())))
+    cfg = TrajectoryConfig(alpha=spec.alpha, eta=[e for e in etas for _ in trials],
+                           k_init=spec.k_init, p=spec.p, i_max=spec.i_max)
+    rn = TrajectoryRunner(6, spec.K, spec.N, torch.complex128, cfg, cuda)
+    gens = [np.random.default_rng(S.stream_seed(spec.seed, S.method_label(e), t))
+            for e in etas for t in trials]
+    st = DeviceOmegaStreams(gens, cuda)
+    both = rn.run_chunk(H.repeat(2, 1, 1, 1), noise.repeat(2, 1),
+                        st.window(spec.T * rn.normals_per_step_max()))
+    for i in range(2):
+        assert torch.equal(both.k_est[3 * i:3 * i + 3], sep[i].k_est)
+        assert torch.equal(both.method[3 * i:3 * i + 3], sep[i].method)
+        assert torch.equal(both.rates[3 * i:3 * i + 3], sep[i].rates)
+
+
+def test_rng_locate_matches_host_stream(cuda):
+    """Advancing by the located raw offsets lands each stream exactly where
+    numpy's Generator is after drawing the same number of normals."""
+    trials = [0, 3, 7]
+    dev = DeviceOmegaStreams.for_method(0, 0.9, trials, cuda)
+    host = OmegaStreams.for_method(0, 0.9, trials)
+    for L, used in [(4000, [0, 1, 3999]), (30000, [12345, 29999, 7]), (5000, [5000, 2500, 1])]:
+        d = dev.window(L).cpu().numpy()
+        h = host.window(L)
+        assert (d == h).mean() > 0.999
+        dev.advance(used)
+        host.advance(used)
+    d = dev.window(1000).cpu().numpy()
+    assert (d == host.window(1000)).mean() > 0.999
