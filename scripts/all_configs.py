@@ -3,7 +3,8 @@ reference algorithm on the host cores.
 
 GPU: the everything-on-device campaign (channels synthesised per time chunk,
 device sketch streams, batched runner), full trial count and T of each
-config, timed with CUDA events after one warm-up chunk.  CPU: the oracle port
+config, timed with CUDA events after one untimed warm-up pass of the same
+config (the time includes the host-side parameter draws of every trial).  CPU: the oracle port
 on all cores (one trial per worker, BLAS 1 thread) on a bounded sample of
 trials x steps of the same config.
 
@@ -46,9 +47,8 @@ RUNS = [
 
 
 def gpu_rate(spec, eta, chunk, dev):
-    # warm-up on a short pass, then the full config
-    run_campaign_device(spec.with_(T=min(spec.T, chunk)), eta, range(min(spec.B, 8)), dev,
-                        chunk=chunk, keep=False)
+    # warm-up: one full pass (allocations, library first calls), then the timed pass
+    run_campaign_device(spec, eta, range(spec.B), dev, chunk=chunk, keep=True)
     torch.cuda.synchronize(dev)
     t0 = time.perf_counter()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
