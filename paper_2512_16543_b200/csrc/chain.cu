@@ -1,6 +1,8 @@
 // K5 batched Hermitian inverse, K4 Woodbury update, the per-trial chain of
 // the batched runner, and the speculative sketch-cursor verifier.
 
+#include <cooperative_groups.h>
+
 #include "linalg.cuh"
 
 namespace lrz {
@@ -61,6 +63,137 @@ __global__ void __launch_bounds__(INV_THREADS)
   const InvScratch sc = carve_inv(smem, K, &M, K, K <= INV_SMEM_KMAX);
   const int st = cta_herm_inverse(A + item * as, Ainv + item * ais, K, M, limit, sc);
   if (threadIdx.x == 0 && info) info[item] = st;
+}
+
+// ---------------------------------------------------------------------------
+// K5 for 64 < K <= 256: the K x K complex128 matrix (256 KB at K = 128, 1 MB at
+// K = 256) does not fit one SM's shared memory, so a thread-block cluster of
+// CS CTAs holds it in distributed shared memory, R = ceil(K / CS) rows each.
+// In-place Gauss-Jordan without pivoting (the HPD fast path of
+// cta_gauss_jordan): at step k the owner of row k scales it and writes it into
+// every cluster member's row buffer over DSMEM; one cluster barrier per step
+// (row buffers are double-buffered).  Items that are not positive definite or
+// whose ||A||_F ||A^-1||_F bound exceeds the limit are flagged in `redo` for
+// the single-CTA kernel (pivoted path / power-iteration condition estimate).
+// ---------------------------------------------------------------------------
+constexpr int CINV_THREADS = 512;
+
+__global__ void __launch_bounds__(CINV_THREADS)
+    herm_inverse_cluster_kernel(int K, int CS, const c128 *__restrict__ A, int64_t as,
+                                c128 *__restrict__ Ainv, int64_t ais, int32_t *__restrict__ info,
+                                double limit, const uint8_t *__restrict__ mask,
+                                uint8_t *__restrict__ redo) {
+  namespace cg = cooperative_groups;
+  cg::cluster_group cl = cg::this_cluster();
+  extern __shared__ __align__(16) char cs_smem[];
+  const int R = (K + CS - 1) / CS;
+  c128 *Mloc = (c128 *)cs_smem;             // [R][K] this CTA's rows
+  c128 *rowbuf = Mloc + R * K;              // [2][K] scaled pivot rows (written remotely)
+  c128 *colbuf = rowbuf + 2 * K;            // [R] column k of own rows
+  __shared__ double red[CINV_THREADS / 32];
+  __shared__ double s_fa[8], s_fi[8];
+  __shared__ int s_bad;
+  const int rank = int(cl.block_rank());
+  const int64_t item = blockIdx.x / CS;
+  const bool active = !(mask && !mask[item]);
+  const int tid = threadIdx.x, NT = blockDim.x;
+  const int r0 = rank * R, nr = max(0, min(R, K - r0));
+  const int tpc = max(1, NT / K);   // threads per column in the update
+  const c128 *a = A + item * as;
+  double loc = 0.0;
+  if (active)
+    for (int e = tid; e < nr * K; e += NT) {
+      const c128 v = a[int64_t(r0) * K + e];
+      Mloc[e] = v;
+      loc += cabs2(v);
+    }
+  const double fa_part = block_sum(loc, red);
+  if (tid == 0) s_bad = 0;
+  cl.sync();
+  if (!active) {   // every member must still take part in the cluster barriers
+    for (int k = 0; k < K; ++k) {
+      asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
+      asm volatile("barrier.cluster.wait.aligned;" ::: "memory");
+    }
+    cl.sync();
+    if (rank == 0 && tid == 0) redo[item] = 0;
+    return;
+  }
+  for (int k = 0; k < K; ++k) {
+    const int owner = k / R;
+    c128 *rb = rowbuf + (k & 1) * K;
+    if (rank == owner) {
+      const int lk = k - r0;
+      const c128 piv = Mloc[lk * K + k];
+      const bool ok = piv.re > 0.0 && isfinite(piv.re) && isfinite(piv.im);
+      const c128 pinv = ok ? cinv(piv) : mk<double>(0.0, 0.0);
+      for (int j = tid; j < K; j += NT) {
+        const c128 v = (j == k) ? pinv : cmul(Mloc[lk * K + j], pinv);
+        for (int q = 0; q < CS; ++q) *cl.map_shared_rank(rb + j, q) = v;
+      }
+      if (tid == 0 && !ok)
+        for (int q = 0; q < CS; ++q) *cl.map_shared_rank(&s_bad, q) = 1;
+    }
+    for (int i = tid; i < nr; i += NT) colbuf[i] = Mloc[i * K + k];
+    // cluster barrier: only the owner's remote row-buffer stores need ordering
+    if (rank == owner) asm volatile("fence.acq_rel.cluster;" ::: "memory");
+    asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
+    asm volatile("barrier.cluster.wait.aligned;" ::: "memory");
+    if (s_bad) continue;   // uniform across the cluster (set before the barrier)
+    const c128 pinv = rb[k];
+    // thread -> column j (tpc threads per column, interleaved rows): no index
+    // division in the loop, r_j in registers, c_i broadcast from shared memory
+    if (tid < tpc * K) {
+      const int j = tid % K, i0 = tid / K;
+      const c128 r = rb[j];
+      const int lk = k - r0;
+      if (j == k) {
+        for (int i = i0; i < nr; i += tpc)
+          Mloc[i * K + j] = (i == lk) ? pinv
+                                      : cmul(mk<double>(-colbuf[i].re, -colbuf[i].im), pinv);
+      } else {
+        for (int i = i0; i < nr; i += tpc) {
+          c128 &m = Mloc[i * K + j];
+          if (i == lk) {
+            m = r;
+          } else {
+            const c128 c = colbuf[i];
+            m.re = fma(-c.re, r.re, m.re);
+            m.re = fma(c.im, r.im, m.re);
+            m.im = fma(-c.re, r.im, m.im);
+            m.im = fma(-c.im, r.re, m.im);
+          }
+        }
+      }
+    }
+    __syncthreads();
+  }
+  // ||A||_F^2 and ||A^-1||_F^2 summed over the cluster
+  double li = 0.0;
+  for (int e = tid; e < nr * K; e += NT) li += cabs2(Mloc[e]);
+  const double fi_part = block_sum(li, red);
+  // gather the partial sums at rank 0 through DSMEM
+  if (tid == 0) {
+    *cl.map_shared_rank(&s_fa[rank], 0) = fa_part;
+    *cl.map_shared_rank(&s_fi[rank], 0) = fi_part;
+  }
+  cl.sync();
+  bool flag = s_bad != 0;
+  if (rank == 0 && tid == 0) {
+    double fa = 0.0, fi = 0.0;
+    for (int q = 0; q < CS; ++q) {
+      fa += s_fa[q];
+      fi += s_fi[q];
+    }
+    const double fb = sqrt(fa) * sqrt(fi);
+    const bool good = !flag && isfinite(fb) && fb <= limit;
+    redo[item] = good ? 0 : 1;
+    if (good && info) info[item] = LRZ_INFO_OK;
+  }
+  if (!flag) {
+    c128 *o = Ainv + item * ais;
+    for (int e = tid; e < nr * K; e += NT) o[int64_t(r0) * K + e] = Mloc[e];
+  }
 }
 
 // Batched Woodbury (single step per item).
@@ -343,6 +476,34 @@ extern "C" int lrz_herm_inverse(int64_t B, int K, const void *A, int64_t a_strid
     herm_inverse_warp_kernel<<<unsigned((B + 3) / 4), 128, 0, st>>>(
         B, K, (const c128 *)A, a_stride, (c128 *)A_inv, ai_stride, info, cond_limit, item_mask,
         redo);
+    mask = redo;
+  } else if (K > INV_SMEM_KMAX && K <= 256 && workspace) {
+    // cluster path: the matrix spread over CS CTAs' shared memory
+    uint8_t *redo = (uint8_t *)workspace;
+    const int CS = K <= 128 ? 2 : 8;
+    const int R = (K + CS - 1) / CS;
+    const size_t csm = (size_t(R) * K + 2 * size_t(K) + R) * sizeof(c128);
+    if (cudaFuncSetAttribute(herm_inverse_cluster_kernel,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, int(csm)) != cudaSuccess) {
+      lrz_set_error("lrz_herm_inverse: cannot reserve %zu bytes of shared memory", csm);
+      return LRZ_ELAUNCH;
+    }
+    cudaLaunchConfig_t lc = {};
+    lc.gridDim = dim3(unsigned(B * CS));
+    lc.blockDim = dim3(CINV_THREADS);
+    lc.dynamicSmemBytes = csm;
+    lc.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = CS;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    lc.attrs = at;
+    lc.numAttrs = 1;
+    if (cudaLaunchKernelEx(&lc, herm_inverse_cluster_kernel, K, CS, (const c128 *)A, a_stride,
+                           (c128 *)A_inv, ai_stride, info, cond_limit, item_mask, redo) !=
+        cudaSuccess)
+      return lrz_launch_status("herm_inverse_cluster_kernel");
     mask = redo;
   }
   herm_inverse_kernel<<<unsigned(B), INV_THREADS, sm, st>>>(

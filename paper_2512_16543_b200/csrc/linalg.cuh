@@ -71,19 +71,25 @@ LRZ_DEV int cta_gauss_jordan(c128 *M, int K, int ld, bool pivot, c128 *colbuf, c
       rowbuf[i] = cmul(M[int64_t(k) * ld + i], pinv);
     }
     __syncthreads();
-    for (int e = tid; e < K * K; e += NT) {
-      const int i = e / K, j = e - i * K;
-      c128 &m = M[int64_t(i) * ld + j];
-      if (i == k) {
-        m = (j == k) ? pinv : rowbuf[j];
-      } else if (j == k) {
-        m = cmul(mk<double>(-colbuf[i].re, -colbuf[i].im), pinv);
-      } else {
-        const c128 c = colbuf[i], r = rowbuf[j];
-        m.re = fma(-c.re, r.re, m.re);
-        m.re = fma(c.im, r.im, m.re);
-        m.im = fma(-c.re, r.im, m.im);
-        m.im = fma(-c.im, r.re, m.im);
+    // thread -> column j (tpc threads per column, interleaved rows): the
+    // pivot-row factor stays in a register, column factors are broadcasts
+    const int tpc = max(1, NT / K);
+    for (int jt = tid; jt < K * tpc; jt += NT) {
+      const int j = jt % K, i0 = jt / K;
+      const c128 r = rowbuf[j];
+      for (int i = i0; i < K; i += tpc) {
+        c128 &m = M[int64_t(i) * ld + j];
+        if (i == k) {
+          m = (j == k) ? pinv : r;
+        } else if (j == k) {
+          m = cmul(mk<double>(-colbuf[i].re, -colbuf[i].im), pinv);
+        } else {
+          const c128 c = colbuf[i];
+          m.re = fma(-c.re, r.re, m.re);
+          m.re = fma(c.im, r.im, m.re);
+          m.im = fma(-c.re, r.im, m.im);
+          m.im = fma(-c.im, r.re, m.im);
+        }
       }
     }
     __syncthreads();
