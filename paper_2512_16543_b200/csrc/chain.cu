@@ -77,9 +77,49 @@ __global__ void __launch_bounds__(INV_THREADS)
 // the single-CTA kernel (pivoted path / power-iteration condition estimate).
 // ---------------------------------------------------------------------------
 constexpr int CINV_THREADS = 512;
+constexpr int CINV_BMAX = 16;
 
+// In-place inverse of the bb x bb HPD block D (row stride ld) by one warp:
+// Gauss-Jordan without pivoting, lane i owns row i.  False on a non-positive
+// or non-finite pivot.
+LRZ_DEV bool warp_small_gj(c128 *D, int bb, int ld) {
+  const int lane = threadIdx.x & 31;
+  for (int k = 0; k < bb; ++k) {
+    const c128 piv = D[k * ld + k];
+    if (!(piv.re > 0.0 && isfinite(piv.re) && isfinite(piv.im))) return false;
+    const c128 pinv = cinv(piv);
+    c128 c = czero<double>();
+    if (lane < bb) c = D[lane * ld + k];
+    __syncwarp();
+    if (lane < bb) {
+      for (int j = 0; j < bb; ++j) {
+        const c128 r = (j == k) ? mk<double>(1.0, 0.0) : D[k * ld + j];
+        const c128 rs = cmul(r, pinv);       // scaled pivot-row entry (row k of the result)
+        c128 &m = D[lane * ld + j];
+        if (lane == k) {
+          m = (j == k) ? pinv : rs;
+        } else if (j == k) {
+          m = cmul(mk<double>(-c.re, -c.im), pinv);
+        } else {
+          m.re = fma(-c.re, rs.re, m.re);
+          m.re = fma(c.im, rs.im, m.re);
+          m.im = fma(-c.re, rs.im, m.im);
+          m.im = fma(-c.im, rs.re, m.im);
+        }
+      }
+    }
+    __syncwarp();
+  }
+  return true;
+}
+
+// Blocked in-place Gauss-Jordan over the cluster: for each pivot block p of
+// bb rows (owned by one CTA) the owner inverts D = M_pp, forms the new pivot
+// block rows P = [D^-1 M_pq | D^-1] and pushes them to every member over
+// DSMEM; after one cluster barrier every CTA applies the rank-bb update
+// M_iq -= M_ip P_q, M_ip = -M_ip D^-1 to its own rows.  K / bb barriers.
 __global__ void __launch_bounds__(CINV_THREADS)
-    herm_inverse_cluster_kernel(int K, int CS, const c128 *__restrict__ A, int64_t as,
+    herm_inverse_cluster_kernel(int K, int CS, int bsz, const c128 *__restrict__ A, int64_t as,
                                 c128 *__restrict__ Ainv, int64_t ais, int32_t *__restrict__ info,
                                 double limit, const uint8_t *__restrict__ mask,
                                 uint8_t *__restrict__ redo) {
@@ -88,8 +128,9 @@ __global__ void __launch_bounds__(CINV_THREADS)
   extern __shared__ __align__(16) char cs_smem[];
   const int R = (K + CS - 1) / CS;
   c128 *Mloc = (c128 *)cs_smem;             // [R][K] this CTA's rows
-  c128 *rowbuf = Mloc + R * K;              // [2][K] scaled pivot rows (written remotely)
-  c128 *colbuf = rowbuf + 2 * K;            // [R] column k of own rows
+  c128 *Pbuf = Mloc + R * K;                // [2][bsz][K] pivot block rows (written remotely)
+  c128 *Cs = Pbuf + 2 * bsz * K;            // [R][bsz] saved M_ip of own rows
+  c128 *Dm = Cs + R * bsz;                  // [bsz][bsz + 1] owner's pivot block
   __shared__ double red[CINV_THREADS / 32];
   __shared__ double s_fa[8], s_fi[8];
   __shared__ int s_bad;
@@ -98,7 +139,7 @@ __global__ void __launch_bounds__(CINV_THREADS)
   const bool active = !(mask && !mask[item]);
   const int tid = threadIdx.x, NT = blockDim.x;
   const int r0 = rank * R, nr = max(0, min(R, K - r0));
-  const int tpc = max(1, NT / K);   // threads per column in the update
+  const int nblk = (K + bsz - 1) / bsz;
   const c128 *a = A + item * as;
   double loc = 0.0;
   if (active)
@@ -111,7 +152,7 @@ __global__ void __launch_bounds__(CINV_THREADS)
   if (tid == 0) s_bad = 0;
   cl.sync();
   if (!active) {   // every member must still take part in the cluster barriers
-    for (int k = 0; k < K; ++k) {
+    for (int n = 0; n < nblk; ++n) {
       asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
       asm volatile("barrier.cluster.wait.aligned;" ::: "memory");
     }
@@ -119,51 +160,67 @@ __global__ void __launch_bounds__(CINV_THREADS)
     if (rank == 0 && tid == 0) redo[item] = 0;
     return;
   }
-  for (int k = 0; k < K; ++k) {
-    const int owner = k / R;
-    c128 *rb = rowbuf + (k & 1) * K;
+  const int LDD = bsz + 1;
+  for (int n = 0; n < nblk; ++n) {
+    const int k0 = n * bsz, bb = min(bsz, K - k0);
+    const int owner = k0 / R, lk0 = k0 - owner * R;
+    c128 *P = Pbuf + (n & 1) * bsz * K;
     if (rank == owner) {
-      const int lk = k - r0;
-      const c128 piv = Mloc[lk * K + k];
-      const bool ok = piv.re > 0.0 && isfinite(piv.re) && isfinite(piv.im);
-      const c128 pinv = ok ? cinv(piv) : mk<double>(0.0, 0.0);
-      for (int j = tid; j < K; j += NT) {
-        const c128 v = (j == k) ? pinv : cmul(Mloc[lk * K + j], pinv);
-        for (int q = 0; q < CS; ++q) *cl.map_shared_rank(rb + j, q) = v;
+      // D = M_pp, inverted by warp 0
+      for (int e = tid; e < bb * bb; e += NT) Dm[(e / bb) * LDD + e % bb] = Mloc[(lk0 + e / bb) * K + k0 + e % bb];
+      __syncthreads();
+      if (tid < 32) {
+        const bool ok = warp_small_gj(Dm, bb, LDD);
+        if (tid == 0 && !ok)
+          for (int q = 0; q < CS; ++q) *cl.map_shared_rank(&s_bad, q) = 1;
       }
-      if (tid == 0 && !ok)
-        for (int q = 0; q < CS; ++q) *cl.map_shared_rank(&s_bad, q) = 1;
+      __syncthreads();
+      // P[t][j] = (D^-1 M_p)[t][j] for j outside the block, D^-1[t][j - k0] inside
+      for (int e = tid; e < bb * K; e += NT) {
+        const int t = e / K, j = e - t * K;
+        c128 v;
+        if (j >= k0 && j < k0 + bb) {
+          v = Dm[t * LDD + (j - k0)];
+        } else {
+          v = czero<double>();
+          for (int u = 0; u < bb; ++u) cfma(v, Dm[t * LDD + u], Mloc[(lk0 + u) * K + j]);
+        }
+        for (int q = 0; q < CS; ++q) *cl.map_shared_rank(P + e, q) = v;
+      }
+      asm volatile("fence.acq_rel.cluster;" ::: "memory");
     }
-    for (int i = tid; i < nr; i += NT) colbuf[i] = Mloc[i * K + k];
-    // cluster barrier: only the owner's remote row-buffer stores need ordering
-    if (rank == owner) asm volatile("fence.acq_rel.cluster;" ::: "memory");
+    // own rows' M_ip, saved before the update overwrites them
+    for (int e = tid; e < nr * bb; e += NT) Cs[(e / bb) * bsz + e % bb] = Mloc[(e / bb) * K + k0 + e % bb];
     asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
     asm volatile("barrier.cluster.wait.aligned;" ::: "memory");
     if (s_bad) continue;   // uniform across the cluster (set before the barrier)
-    const c128 pinv = rb[k];
-    // thread -> column j (tpc threads per column, interleaved rows): no index
-    // division in the loop, r_j in registers, c_i broadcast from shared memory
+    // rank-bb update: thread -> column j (tpc threads per column), P_j in registers
+    const int tpc = max(1, NT / K);
     if (tid < tpc * K) {
       const int j = tid % K, i0 = tid / K;
-      const c128 r = rb[j];
-      const int lk = k - r0;
-      if (j == k) {
-        for (int i = i0; i < nr; i += tpc)
-          Mloc[i * K + j] = (i == lk) ? pinv
-                                      : cmul(mk<double>(-colbuf[i].re, -colbuf[i].im), pinv);
-      } else {
-        for (int i = i0; i < nr; i += tpc) {
-          c128 &m = Mloc[i * K + j];
-          if (i == lk) {
-            m = r;
-          } else {
-            const c128 c = colbuf[i];
-            m.re = fma(-c.re, r.re, m.re);
-            m.re = fma(c.im, r.im, m.re);
-            m.im = fma(-c.re, r.im, m.im);
-            m.im = fma(-c.im, r.re, m.im);
+      const bool inblk = (j >= k0 && j < k0 + bb);
+      c128 pc[CINV_BMAX];
+#pragma unroll
+      for (int t = 0; t < CINV_BMAX; ++t) pc[t] = (t < bb) ? P[t * K + j] : czero<double>();
+      for (int i = i0; i < nr; i += tpc) {
+        c128 &m = Mloc[i * K + j];
+        if (rank == owner && i >= lk0 && i < lk0 + bb) {
+          m = pc[i - lk0];   // pivot block rows: P itself
+          continue;
+        }
+        c128 acc = inblk ? czero<double>() : m;
+        const c128 *ci = Cs + i * bsz;
+#pragma unroll
+        for (int t = 0; t < CINV_BMAX; ++t) {
+          if (t < bb) {
+            const c128 c = ci[t];
+            acc.re = fma(-c.re, pc[t].re, acc.re);
+            acc.re = fma(c.im, pc[t].im, acc.re);
+            acc.im = fma(-c.re, pc[t].im, acc.im);
+            acc.im = fma(-c.im, pc[t].re, acc.im);
           }
         }
+        m = acc;
       }
     }
     __syncthreads();
@@ -482,7 +539,11 @@ extern "C" int lrz_herm_inverse(int64_t B, int K, const void *A, int64_t a_strid
     uint8_t *redo = (uint8_t *)workspace;
     const int CS = K <= 128 ? 2 : 8;
     const int R = (K + CS - 1) / CS;
-    const size_t csm = (size_t(R) * K + 2 * size_t(K) + R) * sizeof(c128);
+    // pivot blocks must not straddle two members' rows: bsz divides R
+    int bsz = K <= 128 ? 16 : 8;
+    while (R % bsz) bsz >>= 1;
+    const size_t csm = (size_t(R) * K + 2 * size_t(bsz) * K + size_t(R) * bsz +
+                        size_t(bsz) * (bsz + 1)) * sizeof(c128);
     if (cudaFuncSetAttribute(herm_inverse_cluster_kernel,
                              cudaFuncAttributeMaxDynamicSharedMemorySize, int(csm)) != cudaSuccess) {
       lrz_set_error("lrz_herm_inverse: cannot reserve %zu bytes of shared memory", csm);
@@ -500,7 +561,7 @@ extern "C" int lrz_herm_inverse(int64_t B, int K, const void *A, int64_t a_strid
     at[0].val.clusterDim.z = 1;
     lc.attrs = at;
     lc.numAttrs = 1;
-    if (cudaLaunchKernelEx(&lc, herm_inverse_cluster_kernel, K, CS, (const c128 *)A, a_stride,
+    if (cudaLaunchKernelEx(&lc, herm_inverse_cluster_kernel, K, CS, bsz, (const c128 *)A, a_stride,
                            (c128 *)A_inv, ai_stride, info, cond_limit, item_mask, redo) !=
         cudaSuccess)
       return lrz_launch_status("herm_inverse_cluster_kernel");
