@@ -343,9 +343,12 @@ def _simulate(cfg, specs, trials, seed, device, chunk, sketch_labels=None, keep_
         m = len(members)
         is_wb = members[0][1] is not None
         etas = [eta for _, eta in members for _ in trials] if is_wb else None
+        # with oversampling p <= 2 the iteration count follows the sketch draw itself,
+        # so speculative sketch cursors rarely survive: resolve in order from the start
         tc = TrajectoryConfig(alpha=cfg.resolved_alpha, P_t=cfg.P_t_W, eta=etas,
                               k_init=cfg.k_init, p=cfg.p, i_max=cfg.i_max, n_reset=cfg.n_reset,
-                              rate_via_gram=False, delta="formula")
+                              rate_via_gram=False, delta="formula",
+                              spec_passes=0 if cfg.p <= 2 else 2)
         runner = TrajectoryRunner(m * B, K, R, torch.complex128, tc, dev)
         streams = None
         if is_wb:
@@ -368,9 +371,26 @@ def _simulate(cfg, specs, trials, seed, device, chunk, sketch_labels=None, keep_
     side = torch.cuda.Stream(dev)
     for gr in groups:
         gr["stream"] = side if (not gr["wb"] and len(groups) > 1) else main
-    for t0 in range(0, T, chunk):
+    # snapshots are generated one chunk ahead on their own stream, so chunk c+1's
+    # channels, beams and NLOS draws overlap chunk c's in-order arSVD
+    snap_stream = torch.cuda.Stream(dev)
+    starts = list(range(0, T, chunk))
+
+    def prefetch(t0):
+        snap_stream.wait_stream(main)
+        with torch.cuda.stream(snap_stream):
+            sn = ps.generate(t0, min(T, t0 + chunk))
+            ev = torch.cuda.Event()
+            ev.record(snap_stream)
+        return sn, ev
+
+    nxt = prefetch(starts[0])
+    for ci, t0 in enumerate(starts):
         t1 = min(T, t0 + chunk)
-        snap = ps.generate(t0, t1)
+        snap, ev = nxt
+        main.wait_event(ev)
+        if ci + 1 < len(starts):
+            nxt = prefetch(starts[ci + 1])
         infos = []
         for gr in groups:
             m, st = gr["m"], gr["stream"]
