@@ -368,12 +368,12 @@ def _simulate(cfg, specs, trials, seed, device, chunk, sketch_labels=None, keep_
     main = torch.cuda.current_stream(dev)
     # the conventional group is launched first on a side stream so that its
     # batched inversions overlap the WB group's in-order arSVD on the main stream
-    side = torch.cuda.Stream(dev)
+    side = _aux_stream(dev, "side")
     for gr in groups:
         gr["stream"] = side if (not gr["wb"] and len(groups) > 1) else main
     # snapshots are generated one chunk ahead on their own stream, so chunk c+1's
     # channels, beams and NLOS draws overlap chunk c's in-order arSVD
-    snap_stream = torch.cuda.Stream(dev)
+    snap_stream = _aux_stream(dev, "snap")
     starts = list(range(0, T, chunk))
 
     def prefetch(t0):
@@ -430,6 +430,18 @@ def _simulate(cfg, specs, trials, seed, device, chunk, sketch_labels=None, keep_
     if keep_cols:
         out["_cols"] = torch.cat(cols, 1).numpy()
     return out
+
+
+_STREAMS: dict = {}
+
+
+def _aux_stream(dev, name: str):
+    """One long-lived side stream per (device, role): the ops workspace cache is
+    keyed by stream, so fresh streams per call would grow it without bound."""
+    key = (dev.index if dev.index is not None else 0, name)
+    if key not in _STREAMS:
+        _STREAMS[key] = torch.cuda.Stream(dev)
+    return _STREAMS[key]
 
 
 def _dist_world():
