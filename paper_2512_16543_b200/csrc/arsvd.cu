@@ -553,10 +553,43 @@ LRZ_DEV double scr_linv_col(const c128 *L, int LD, int t) {
   return f;
 }
 
+// widths up to 24 are unrolled with x in registers; wider sketches take the
+// generic loop below (x through the row's scratch), which keeps the kernel's
+// register budget -- and so its occupancy -- set by the common widths
 #define SCR_CASES(F)                                                                  \
   F(1) F(2) F(3) F(4) F(5) F(6) F(7) F(8) F(9) F(10) F(11) F(12) F(13) F(14) F(15) F(16) \
-  F(17) F(18) F(19) F(20) F(21) F(22) F(23) F(24) F(25) F(26) F(27) F(28) F(29) F(30)   \
-  F(31) F(32)
+  F(17) F(18) F(19) F(20) F(21) F(22) F(23) F(24)
+
+LRZ_DEV double scr_xrow_generic(int d, const c128 *wr, const c128 *L, int LD, c128 *xo) {
+  double loc = 0.0;
+  for (int j = 0; j < d; ++j) {
+    c128 acc = wr[j];
+    for (int m = 0; m < j; ++m) {
+      const c128 x = xo[m], lj = L[j * LD + m];
+      acc.re -= x.re * lj.re + x.im * lj.im;
+      acc.im -= x.im * lj.re - x.re * lj.im;
+    }
+    const c128 xj = cscale(acc, 1.0 / L[j * LD + j].re);
+    xo[j] = xj;
+    loc += cabs2(xj);
+  }
+  return loc;
+}
+
+LRZ_DEV double scr_linv_col_generic(int d, const c128 *L, int LD, int t, c128 *x) {
+  double f = 0.0;
+  for (int i = t; i < d; ++i) {
+    c128 acc = mk<double>(i == t ? 1.0 : 0.0, 0.0);
+    for (int k = t; k < i; ++k) {
+      const c128 lk = L[i * LD + k];
+      acc.re -= lk.re * x[k].re - lk.im * x[k].im;
+      acc.im -= lk.re * x[k].im + lk.im * x[k].re;
+    }
+    x[i] = cscale(acc, 1.0 / L[i * LD + i].re);
+    f += cabs2(x[i]);
+  }
+  return f;
+}
 
 LRZ_DEV double scr_xrow_d(int d, const c128 *wr, const c128 *L, int LD, c128 *xo) {
   switch (d) {
@@ -566,10 +599,10 @@ LRZ_DEV double scr_xrow_d(int d, const c128 *wr, const c128 *L, int LD, c128 *xo
     SCR_CASES(SCR_X)
 #undef SCR_X
   }
-  return 0.0;
+  return scr_xrow_generic(d, wr, L, LD, xo);
 }
 
-LRZ_DEV double scr_linv_col_d(int d, const c128 *L, int LD, int t) {
+LRZ_DEV double scr_linv_col_d(int d, const c128 *L, int LD, int t, c128 *scratch) {
   switch (d) {
 #define SCR_L(n) \
   case n:        \
@@ -577,7 +610,7 @@ LRZ_DEV double scr_linv_col_d(int d, const c128 *L, int LD, int t) {
     SCR_CASES(SCR_L)
 #undef SCR_L
   }
-  return 0.0;
+  return scr_linv_col_generic(d, L, LD, t, scratch);
 }
 
 __global__ void __launch_bounds__(128, 4) arsvd_screen_kernel(ArsvdArgs g, int64_t B, int Dtot,
@@ -671,7 +704,7 @@ __global__ void __launch_bounds__(128, 4) arsvd_screen_kernel(ArsvdArgs g, int64
     for (int k = lane; k < K; k += 32)
       // X itself is only needed by the iteration-cap tail's certificate
       loc += scr_xrow_d(d, W + int64_t(k) * Dtot + o, L, LD,
-                        last ? X + int64_t(k) * SCR_DMAX : nullptr);
+                        (last || d > 24) ? X + int64_t(k) * SCR_DMAX : nullptr);
     const double mf = warp_sum(loc);
     __syncwarp();
     if (mf < target * (1.0 - tol)) {  // no prefix of the spectrum reaches the target
@@ -723,7 +756,9 @@ __global__ void __launch_bounds__(128, 4) arsvd_screen_kernel(ArsvdArgs g, int64
           // ||L^-1||_F^2, column t per lane (forward substitution, kept in X's rows 0..d-1
           // is not possible: use registers)
           double f = 0.0;
-          for (int t = lane; t < d; t += 32) f += scr_linv_col_d(d, L, LD, t);
+          // (X is consumed by the Gram above: its rows serve as the generic path's scratch)
+          for (int t = lane; t < d; t += 32)
+            f += scr_linv_col_d(d, L, LD, t, X + int64_t(t) * SCR_DMAX);
           const double F = warp_sum(f);
           if (isfinite(F) && F * mf <= 1e6) {
             if (lane == 0) {
