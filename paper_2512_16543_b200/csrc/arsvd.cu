@@ -19,7 +19,7 @@
 int lrz_sketch_gemm(int64_t B, int K, int Dtot, const void *dA, int64_t a_stride,
                     const double *omega, int64_t omega_stride, const int32_t *omega_row,
                     int64_t orow_div, const int64_t *cursor, int k_init, int p,
-                    const uint8_t *mask, void *Y, void *stream);
+                    const uint8_t *mask, void *Y, void *W, void *stream);
 
 namespace lrz {
 
@@ -880,12 +880,15 @@ extern "C" int lrz_arsvd(int64_t B, int K, const void *dA, int64_t a_stride,
     c128 *Om = (c128 *)wp;
     c128 *Ya = (c128 *)(wp + blk);
     c128 *Wa = (c128 *)(wp + 2 * blk);
+    // Y = dA Omega_all; for K <= 32 the same kernel also forms W = dA Y per tile
     int rc = lrz_sketch_gemm(B, K, Dtot, dA, a_stride, omega, omega_stride, omega_row, 1, cursor,
-                             cfg->k_init, cfg->p, item_mask, Ya, stream);
+                             cfg->k_init, cfg->p, item_mask, Ya, K <= 32 ? Wa : nullptr, stream);
     if (rc) return rc;
-    rc = lrz_cgemm(LRZ_C128, B, K, Dtot, K, 0, dA, K, a_stride, 0, Ya, Dtot, int64_t(K) * Dtot,
-                   Wa, Dtot, int64_t(K) * Dtot, stream);
-    if (rc) return rc;
+    if (K > 32) {
+      rc = lrz_cgemm(LRZ_C128, B, K, Dtot, K, 0, dA, K, a_stride, 0, Ya, Dtot, int64_t(K) * Dtot,
+                     Wa, Dtot, int64_t(K) * Dtot, stream);
+      if (rc) return rc;
+    }
     const size_t sm = 4 * size_t(g.D) * (g.D + 1) * sizeof(c128);
     if (cudaFuncSetAttribute(arsvd_screen_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              int(sm)) != cudaSuccess) {

@@ -544,7 +544,11 @@ struct SketchOperand {
 
 __global__ void __launch_bounds__(GEMM_THREADS)
     sketch_cgemm_kernel(int K, int Dtot, const c128 *__restrict__ A, int64_t sA, SketchOperand so,
-                        const uint8_t *__restrict__ mask, c128 *__restrict__ C, int tiles_n) {
+                        const uint8_t *__restrict__ mask, c128 *__restrict__ C, int tiles_n,
+                        c128 *__restrict__ W) {
+  // W != nullptr (K <= 32): also W = dA Y for this tile's columns, with dA and
+  // the Y tile kept in shared memory (dynamic: [32][33] each)
+  extern __shared__ __align__(16) char sk_smem[];
   constexpr int BK = 16;
   __shared__ c128 As[BK][TM + 1];
   __shared__ c128 Bs[BK][TM + 1];
@@ -616,6 +620,42 @@ __global__ void __launch_bounds__(GEMM_THREADS)
     for (int j = 0; j < 4; ++j) {
       const int col = J * TM + tx + 8 * j;
       if (r < K && col < Dtot) c[int64_t(r) * Dtot + col] = acc[i][j];
+    }
+  }
+  if (W == nullptr) return;
+  c128(*Af)[TM + 1] = (c128(*)[TM + 1])sk_smem;                 // dA, [32][33]
+  c128(*Ys)[TM + 1] = (c128(*)[TM + 1])(sk_smem + TM * (TM + 1) * sizeof(c128));
+  for (int e = tid; e < TM * TM; e += GEMM_THREADS) {
+    const int r = e / TM, m = e % TM;
+    Af[r][m] = (r < K && m < K) ? a[int64_t(r) * K + m] : czero<double>();
+  }
+#pragma unroll
+  for (int i = 0; i < 2; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) Ys[ty + 16 * i][tx + 8 * j] = acc[i][j];
+  __syncthreads();
+  c128 wv[2][4];
+#pragma unroll
+  for (int i = 0; i < 2; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) wv[i][j] = czero<double>();
+  for (int m = 0; m < K; ++m) {
+    const c128 a0 = Af[ty][m], a1 = Af[ty + 16][m];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const c128 y = Ys[m][tx + 8 * j];
+      cfma(wv[0][j], a0, y);
+      cfma(wv[1][j], a1, y);
+    }
+  }
+  c128 *w = W + item * int64_t(K) * Dtot;
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    const int r = ty + 16 * i;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int col = J * TM + tx + 8 * j;
+      if (r < K && col < Dtot) w[int64_t(r) * Dtot + col] = wv[i][j];
     }
   }
 }
@@ -802,11 +842,16 @@ extern "C" int lrz_gram_delta(int dtype, int64_t B, int K, int N, const void *P,
 int lrz_sketch_gemm(int64_t B, int K, int Dtot, const void *dA, int64_t a_stride,
                     const double *omega, int64_t omega_stride, const int32_t *omega_row,
                     int64_t orow_div, const int64_t *cursor, int k_init, int p,
-                    const uint8_t *mask, void *Y, void *stream) {
+                    const uint8_t *mask, void *Y, void *W, void *stream) {
   const int tn = (Dtot + TM - 1) / TM, tm = (K + TM - 1) / TM;
   SketchOperand so{omega, omega_stride, omega_row, orow_div, cursor, k_init, p};
-  sketch_cgemm_kernel<<<unsigned(B * tm * tn), GEMM_THREADS, 0, (cudaStream_t)stream>>>(
-      K, Dtot, (const c128 *)dA, a_stride, so, mask, (c128 *)Y, tn);
+  const bool fuse = W != nullptr && K <= TM;
+  const size_t sm = fuse ? 2 * size_t(TM) * (TM + 1) * sizeof(c128) : 0;
+  if (fuse)
+    cudaFuncSetAttribute(sketch_cgemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
+  sketch_cgemm_kernel<<<unsigned(B * tm * tn), GEMM_THREADS, sm, (cudaStream_t)stream>>>(
+      K, Dtot, (const c128 *)dA, a_stride, so, mask, (c128 *)Y, tn,
+      fuse ? (c128 *)W : nullptr);
   return lrz_launch_status("sketch_cgemm_kernel");
 }
 
