@@ -131,7 +131,8 @@ def herm_inverse(A: torch.Tensor, cond_limit: float = 1e14, mask: torch.Tensor |
     N.check(lib.lrz_herm_inverse(B, K, A.data_ptr(), K * K, out.data_ptr(), K * K,
                                  info.data_ptr(), float(cond_limit), N.ptr(mask), ws.data_ptr(),
                                  N.stream_ptr(A.device)), "lrz_herm_inverse")
-    _count(1)
+    # warp (K <= 32) or cluster (64 < K <= 256) fast path + the CTA kernel for flagged items
+    _count(2 if (K <= 32 or 64 < K <= 256) else 1)
     return out, info
 
 
@@ -179,7 +180,9 @@ def arsvd(dA: torch.Tensor, omega: torch.Tensor, cursor: torch.Tensor, eta, k_in
                           out["iters"].data_ptr(), out["fallback"].data_ptr(),
                           out["consumed"].data_ptr(), N.ptr(mask), int(want_factor),
                           int(hermitian), ws.data_ptr(), N.stream_ptr(dev)), "lrz_arsvd")
-    _count(1)
+    # screening front end (sketch GEMM [+ W GEMM for K > 32] + screen) + the exact kernel
+    front = hermitian and not want_factor and D <= 32
+    _count((3 if K <= 32 else 4) if front else 1)
     out["D"] = D
     return out
 
