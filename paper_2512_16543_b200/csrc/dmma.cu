@@ -1,0 +1,314 @@
+// complex128 kernels on the FP64 tensor pipe (DMMA, mma.sync m8n8k4 f64) for
+// K <= 32: the Gram G = H H^H + alpha I (K1, lowrank.py:147-164) and the fused
+// fully digital precoder + coupling + SINR/rate (K6, precoding.py:37-80).
+//
+// One complex MAC block is four real DMMAs on the (re, im) halves of the same
+// fragments.  m8n8k4 f64 fragments (PTX ISA): lane L = 4 g + t holds
+//   A[g][t] (one double), B[t][g] (one double), C[g][2t + e] (two doubles).
+// A DMMA is 256 FMAs per warp instruction against 32 for a DFMA, so these
+// kernels are bound by the FP64 pipe (and HBM for the precoder's H in / W
+// out), not by instruction issue -- the SIMT versions (gemm.cu) issue one
+// shared-memory load per two DFMAs and stall at 43-59 % of the pipe.
+
+#include "common.cuh"
+
+namespace lrz {
+
+LRZ_DEV void dmma(double (&c)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(c[0]), "+d"(c[1])
+               : "d"(a), "d"(b));
+}
+
+LRZ_DEV c128 ldg_c128(const c128 *p) {
+  const double2 v = __ldg(reinterpret_cast<const double2 *>(p));
+  return mk<double>(v.x, v.y);
+}
+
+// ---------------------------------------------------------------------------
+// K1: G = H H^H + alpha I, one item per warp, RB = ceil(K / 8) row blocks.
+// Lane (g, t) holds H[8 rb + g][n0 + 4 s + t] (s < 4: one 16-column chunk);
+// the same register is the A fragment of row block rb and the B fragment of
+// column block rb (B[k][j] = H[8 jb + j][k] up to the conjugate), so the
+// RB (RB + 1) / 2 lower 8 x 8 tiles need no shared memory at all:
+//   Re G += Hr Hr^T + Hi Hi^T,   Im G += Hi Hr^T - Hr Hi^T.
+// Lower tiles are written and mirrored (exactly Hermitian, real diagonal
+// + alpha: the reference's 0.5 (A + A^H) + alpha I, lowrank.py:160-162).
+// ---------------------------------------------------------------------------
+constexpr int GD_WARPS = 4;
+
+template <int RB>
+__global__ void __launch_bounds__(32 * GD_WARPS, 3)
+    gram_dmma_kernel(int64_t B, int K, int N, const c128 *__restrict__ H, int64_t hs,
+                     double alpha, c128 *__restrict__ A, int64_t as) {
+  constexpr int NT = RB * (RB + 1) / 2;
+  const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+  const int64_t item = int64_t(blockIdx.x) * GD_WARPS + (threadIdx.x >> 5);
+  if (item >= B) return;
+  const c128 *h = H + item * hs;
+  double cr[NT][2], ci[NT][2];
+#pragma unroll
+  for (int i = 0; i < NT; ++i) cr[i][0] = cr[i][1] = ci[i][0] = ci[i][1] = 0.0;
+  bool rok[RB];
+  const c128 *hrow[RB];
+#pragma unroll
+  for (int rb = 0; rb < RB; ++rb) {
+    rok[rb] = 8 * rb + g < K;
+    hrow[rb] = h + int64_t(rok[rb] ? 8 * rb + g : 0) * N;
+  }
+  const bool full = (N % 16) == 0;
+  for (int n0 = 0; n0 < N; n0 += 16) {
+    c128 v[RB][4];
+#pragma unroll
+    for (int rb = 0; rb < RB; ++rb)
+#pragma unroll
+      for (int s = 0; s < 4; ++s) {
+        const int n = n0 + 4 * s + t;
+        v[rb][s] = (rok[rb] && (full || n < N)) ? ldg_c128(hrow[rb] + n) : czero<double>();
+      }
+#pragma unroll
+    for (int s = 0; s < 4; ++s) {
+#pragma unroll
+      for (int ib = 0; ib < RB; ++ib) {
+        const double ar = v[ib][s].re, ai = v[ib][s].im, nar = -ar;
+#pragma unroll
+        for (int jb = 0; jb <= ib; ++jb) {
+          const int x = ib * (ib + 1) / 2 + jb;
+          const double br = v[jb][s].re, bi = v[jb][s].im;
+          dmma(cr[x], ar, br);
+          dmma(cr[x], ai, bi);
+          dmma(ci[x], ai, br);
+          dmma(ci[x], nar, bi);
+        }
+      }
+    }
+  }
+  c128 *a = A + item * as;
+#pragma unroll
+  for (int ib = 0; ib < RB; ++ib)
+#pragma unroll
+    for (int jb = 0; jb <= ib; ++jb) {
+      const int x = ib * (ib + 1) / 2 + jb;
+      const int row = 8 * ib + g;
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int col = 8 * jb + 2 * t + e;
+        if (row < K && col < K && col <= row) {
+          c128 z = mk<double>(cr[x][e], ci[x][e]);
+          if (row == col) {
+            z.im = 0.0;
+            z.re += alpha;
+            a[int64_t(row) * K + col] = z;
+          } else {
+            a[int64_t(row) * K + col] = z;
+            a[int64_t(col) * K + row] = cconj(z);
+          }
+        }
+      }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// K6 fused, K <= 32, one item per CTA of 4 warps:
+//   W = H^H A^-1 (N x K, unscaled, precoding.py:47), ||W||_F^2,
+//   C = G A^-1 - alpha A^-1 = H W for F_RF = I, s = sqrt(P_t)/||W||,
+//   SINR_n = |s C_nn|^2 / (sum_{i != n} |s C_ni|^2 + noise_n), rates, sum.
+// A^-1 is staged once in shared memory as separate re / im planes with a row
+// stride of 36 doubles (the B-fragment loads A^-1[4c + t][8kb + g] are then
+// bank-conflict free).  Warp w computes 16-row slabs n0 = 16 (w + 4 j) of W:
+// lane (g, t) loads conj(H)[4c + t][n0 + 8 nb + g] straight from global
+// memory as the A fragment (a warp load touches 4 rows x 128 contiguous
+// bytes), 2 x 4 complex 8 x 8 accumulator tiles per slab, written as
+// 32-byte row segments.
+// ---------------------------------------------------------------------------
+constexpr int PD_WARPS = 4;
+constexpr int PD_LD = 36;
+
+__global__ void __launch_bounds__(32 * PD_WARPS, 3)
+    precode_dmma32_kernel(int K, int N, const c128 *__restrict__ H, int64_t hs,
+                          const c128 *__restrict__ Ainv, int64_t ais,
+                          const c128 *__restrict__ Gt, int64_t gs, double alpha, double P_t,
+                          const double *__restrict__ noise, int64_t noise_div,
+                          c128 *__restrict__ W, int64_t wst, double *__restrict__ scale_out,
+                          double *__restrict__ rates, double *__restrict__ sinr,
+                          double *__restrict__ sum_rate, int32_t *__restrict__ info) {
+  __shared__ __align__(16) double Sr[32 * PD_LD], Si[32 * PD_LD];
+  __shared__ double red[PD_WARPS], red2[PD_WARPS];
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5, g = lane >> 2, t = lane & 3;
+  const int64_t item = blockIdx.x;
+  const c128 *ai = Ainv + item * ais;
+  for (int e = tid; e < 32 * 32; e += 32 * PD_WARPS) {
+    const int i = e >> 5, k = e & 31;
+    const c128 v = (i < K && k < K) ? ai[i * K + k] : czero<double>();
+    Sr[i * PD_LD + k] = v.re;
+    Si[i * PD_LD + k] = v.im;
+  }
+  __syncthreads();
+  const c128 *h = H + item * hs;
+  c128 *wo = W + item * wst;
+  double nrm = 0.0;
+  const int nslab = (N + 15) / 16;
+  for (int sl = w; sl < nslab; sl += PD_WARPS) {
+    const int n0 = 16 * sl;
+    c128 hv[8][2];
+#pragma unroll
+    for (int c = 0; c < 8; ++c)
+#pragma unroll
+      for (int nb = 0; nb < 2; ++nb) {
+        const int i = 4 * c + t, n = n0 + 8 * nb + g;
+        hv[c][nb] = (i < K && n < N) ? ldg_c128(h + int64_t(i) * N + n) : czero<double>();
+      }
+    double acr[2][4][2], aci[2][4][2];
+#pragma unroll
+    for (int nb = 0; nb < 2; ++nb)
+#pragma unroll
+      for (int kb = 0; kb < 4; ++kb) acr[nb][kb][0] = acr[nb][kb][1] = aci[nb][kb][0] =
+          aci[nb][kb][1] = 0.0;
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+#pragma unroll
+      for (int kb = 0; kb < 4; ++kb) {
+        const double br = Sr[(4 * c + t) * PD_LD + 8 * kb + g];
+        const double bi = Si[(4 * c + t) * PD_LD + 8 * kb + g];
+#pragma unroll
+        for (int nb = 0; nb < 2; ++nb) {
+          const double hr = hv[c][nb].re, hi = hv[c][nb].im;
+          // conj(h) b = (hr br + hi bi) + i (hr bi - hi br)
+          dmma(acr[nb][kb], hr, br);
+          dmma(acr[nb][kb], hi, bi);
+          dmma(aci[nb][kb], hr, bi);
+          dmma(aci[nb][kb], -hi, br);
+        }
+      }
+    }
+#pragma unroll
+    for (int nb = 0; nb < 2; ++nb) {
+      const int n = n0 + 8 * nb + g;
+      if (n < N) {
+#pragma unroll
+        for (int kb = 0; kb < 4; ++kb) {
+          const int k = 8 * kb + 2 * t;
+          if (k + 1 < K) {
+            double4 o;
+            o.x = acr[nb][kb][0];
+            o.y = aci[nb][kb][0];
+            o.z = acr[nb][kb][1];
+            o.w = aci[nb][kb][1];
+            double2 *dst = reinterpret_cast<double2 *>(wo + int64_t(n) * K + k);
+            dst[0] = make_double2(o.x, o.y);
+            dst[1] = make_double2(o.z, o.w);
+            nrm += o.x * o.x + o.y * o.y + o.z * o.z + o.w * o.w;
+          } else if (k < K) {
+            wo[int64_t(n) * K + k] = mk<double>(acr[nb][kb][0], aci[nb][kb][0]);
+            nrm += acr[nb][kb][0] * acr[nb][kb][0] + aci[nb][kb][0] * aci[nb][kb][0];
+          }
+        }
+      }
+    }
+  }
+  // coupling C = G A^-1 for row block w (rows 8 w + g)
+  const int row = 8 * w + g;
+  double ccr[4][2], cci[4][2];
+#pragma unroll
+  for (int kb = 0; kb < 4; ++kb) ccr[kb][0] = ccr[kb][1] = cci[kb][0] = cci[kb][1] = 0.0;
+  if (8 * w < K) {
+    const c128 *gr = Gt + item * gs + int64_t(row < K ? row : 0) * K;
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      const int i = 4 * c + t;
+      const c128 a = (row < K && i < K) ? ldg_c128(gr + i) : czero<double>();
+#pragma unroll
+      for (int kb = 0; kb < 4; ++kb) {
+        const double br = Sr[(4 * c + t) * PD_LD + 8 * kb + g];
+        const double bi = Si[(4 * c + t) * PD_LD + 8 * kb + g];
+        // a b = (ar br - ai bi) + i (ar bi + ai br)
+        dmma(ccr[kb], a.re, br);
+        dmma(ccr[kb], -a.im, bi);
+        dmma(cci[kb], a.re, bi);
+        dmma(cci[kb], a.im, br);
+      }
+    }
+  }
+  // ||W||_F^2 in a fixed order: lanes, then warps 0..3
+  nrm = warp_sum(nrm);
+  if (lane == 0) red[w] = nrm;
+  __syncthreads();
+  double n2 = 0.0;
+#pragma unroll
+  for (int i = 0; i < PD_WARPS; ++i) n2 += red[i];
+  const double nw = sqrt(n2);
+  const bool bad = !(nw > 0.0);
+  const double s = bad ? 0.0 : sqrt(P_t) / nw;
+  double r = 0.0;
+  if (8 * w < K) {
+    double tot = 0.0, sig = 0.0;
+#pragma unroll
+    for (int kb = 0; kb < 4; ++kb)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int col = 8 * kb + 2 * t + e;
+        if (row < K && col < K) {
+          // H W = (G_true - alpha I) A^-1 = G_true A^-1 - alpha A^-1
+          c128 gv = mk<double>(ccr[kb][e], cci[kb][e]);
+          gv.re -= alpha * Sr[row * PD_LD + col];
+          gv.im -= alpha * Si[row * PD_LD + col];
+          const double p = cabs2(cscale(gv, s));
+          tot += p;
+          if (col == row) sig = p;
+        }
+      }
+    tot += __shfl_xor_sync(0xffffffffu, tot, 1);
+    tot += __shfl_xor_sync(0xffffffffu, tot, 2);
+    sig += __shfl_xor_sync(0xffffffffu, sig, 1);
+    sig += __shfl_xor_sync(0xffffffffu, sig, 2);
+    if (row < K && t == 0) {
+      const double q = sig / ((tot - sig) + noise[(item / noise_div) * K + row]);
+      r = log2(1.0 + q);
+      if (rates) rates[item * K + row] = r;
+      if (sinr) sinr[item * K + row] = q;
+    }
+  }
+  r = warp_sum(r);
+  if (lane == 0) red2[w] = r;
+  __syncthreads();
+  if (tid == 0) {
+    double tsum = 0.0;
+#pragma unroll
+    for (int i = 0; i < PD_WARPS; ++i) tsum += red2[i];
+    if (sum_rate) sum_rate[item] = tsum;
+    if (scale_out) scale_out[item] = s;
+    if (info) info[item] = bad ? LRZ_INFO_ZERO_PRECODER : LRZ_INFO_OK;
+  }
+}
+
+}  // namespace lrz
+
+using namespace lrz;
+
+// Launchers used by lrz_gram / lrz_precode_rate (gemm.cu) for complex128, K <= 32.
+int lrz_gram_dmma(int64_t B, int K, int N, const void *H, int64_t hs, double alpha, void *A,
+                  int64_t as, cudaStream_t s) {
+  const unsigned nb = unsigned((B + GD_WARPS - 1) / GD_WARPS);
+  const int rb = (K + 7) / 8;
+  const c128 *h = (const c128 *)H;
+  c128 *a = (c128 *)A;
+  switch (rb) {
+    case 1: gram_dmma_kernel<1><<<nb, 32 * GD_WARPS, 0, s>>>(B, K, N, h, hs, alpha, a, as); break;
+    case 2: gram_dmma_kernel<2><<<nb, 32 * GD_WARPS, 0, s>>>(B, K, N, h, hs, alpha, a, as); break;
+    case 3: gram_dmma_kernel<3><<<nb, 32 * GD_WARPS, 0, s>>>(B, K, N, h, hs, alpha, a, as); break;
+    default: gram_dmma_kernel<4><<<nb, 32 * GD_WARPS, 0, s>>>(B, K, N, h, hs, alpha, a, as); break;
+  }
+  return lrz_launch_status("gram_dmma_kernel");
+}
+
+int lrz_precode_dmma32(int64_t B, int K, int N, const void *H, int64_t hs, const void *A_inv,
+                       int64_t ais, const void *G_true, double alpha, double P_t,
+                       const double *noise, int64_t noise_div, void *W, int64_t wst,
+                       double *scale, double *rates, double *sinr, double *sum_rate,
+                       int32_t *info, cudaStream_t s) {
+  precode_dmma32_kernel<<<unsigned(B), 32 * PD_WARPS, 0, s>>>(
+      K, N, (const c128 *)H, hs, (const c128 *)A_inv, ais, (const c128 *)G_true,
+      int64_t(K) * K, alpha, P_t, noise, noise_div, (c128 *)W, wst, scale, rates, sinr, sum_rate,
+      info);
+  return lrz_launch_status("precode_dmma32_kernel");
+}

@@ -7,6 +7,8 @@
 // inputs and fp64 FMA for complex128 inputs; one CTA per (item, tile) so a
 // B*T batch of small matrices fills all 148 SMs.
 
+#include <stdlib.h>
+
 #include "common.cuh"
 
 
@@ -780,6 +782,23 @@ extern "C" int lrz_axpby(int dtype, int64_t n, double a, const void *X, double b
 
 static int ntiles(int K) { return (K + TM - 1) / TM; }
 
+// complex128 DMMA kernels for K <= 32 (dmma.cu); LRZ_SIMT_FP64=1 selects the
+// SIMT DFMA kernels instead (A/B measurements)
+int lrz_gram_dmma(int64_t B, int K, int N, const void *H, int64_t hs, double alpha, void *A,
+                  int64_t as, cudaStream_t s);
+int lrz_precode_dmma32(int64_t B, int K, int N, const void *H, int64_t hs, const void *A_inv,
+                       int64_t ais, const void *G_true, double alpha, double P_t,
+                       const double *noise, int64_t noise_div, void *W, int64_t wst,
+                       double *scale, double *rates, double *sinr, double *sum_rate,
+                       int32_t *info, cudaStream_t s);
+static bool use_dmma() {
+  static const int v = [] {
+    const char *e = getenv("LRZ_SIMT_FP64");
+    return (e && e[0] == '1') ? 0 : 1;
+  }();
+  return v != 0;
+}
+
 extern "C" int lrz_gram(int dtype, int64_t B, int K, int N, const void *H, int64_t h_stride,
                         double alpha, void *A, int64_t a_stride, void *stream) {
   if (B < 0 || K < 1 || N < 1 || !H || !A) {
@@ -788,6 +807,8 @@ extern "C" int lrz_gram(int dtype, int64_t B, int K, int N, const void *H, int64
   }
   if (B == 0) return LRZ_OK;
   cudaStream_t s = (cudaStream_t)stream;
+  if (K <= 32 && dtype == LRZ_C128 && use_dmma())
+    return lrz_gram_dmma(B, K, N, H, h_stride, alpha, A, a_stride, s);
   if (K <= 32) {
     const unsigned nb = unsigned((B + G32_IPB - 1) / G32_IPB);
     if (dtype == LRZ_C64) {
@@ -956,6 +977,10 @@ extern "C" int lrz_precode_rate(int dtype, int64_t B, int K, int N, const void *
   if (G_true) {
     // W = H^H A^-1 (norm partials in the epilogue), coupling from the Gram:
     // H W = (G - alpha I) A^-1, K^3 instead of K^2 N work (F_RF = I)
+    if (K <= 32 && dtype == LRZ_C128 && use_dmma())
+      return lrz_precode_dmma32(B, K, N, H, h_stride, A_inv, ai_stride, G_true, alpha, P_t,
+                                noise, noise_div, W, w_stride, scale, rates, sinr, sum_rate,
+                                info, s);
     int nparts = tm * tn;
     if (K <= 32) {
       const size_t es = dtype == LRZ_C64 ? 8 : 16;

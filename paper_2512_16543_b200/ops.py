@@ -8,6 +8,8 @@ and the batched trajectory runner (trajectory.py) are built on these.
 
 from __future__ import annotations
 
+import os
+
 import ctypes as C
 import math
 
@@ -273,7 +275,10 @@ def precode_rate(H: torch.Tensor, A_inv: torch.Tensor, P_t: float, noise: torch.
                                  scale.data_ptr(), rates.data_ptr(), N.ptr(sinr),
                                  total.data_ptr(), info.data_ptr(), ws.data_ptr(),
                                  N.stream_ptr(dev)), "lrz_precode_rate")
-    _count(3)
+    # complex128, K <= 32 with the Gram shortcut: one fused DMMA kernel (dmma.cu)
+    fused = (G_true is not None and K <= 32 and H.dtype == torch.complex128
+             and os.environ.get("LRZ_SIMT_FP64") != "1")
+    _count(1 if fused else 3)
     return dict(W=W, scale=scale, rates=rates, sinr=sinr, sum=total, info=info)
 
 
