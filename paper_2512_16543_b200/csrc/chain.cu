@@ -397,12 +397,22 @@ __global__ void plan_kernel(int64_t n, int K, const uint8_t *is_sketch, const in
 
 
 // K5 fast path for K <= 32: one warp per matrix, lane i holds row i in
-// registers (padded to 32 x 32 with the identity), Gauss-Jordan without
-// pivoting; the pivot row is broadcast with shuffles, no shared memory and
-// no block barriers.  Items that are not positive definite or whose
-// ||A||_F ||A^-1||_F bound exceeds the limit are flagged in `redo` for the
-// CTA kernel (pivoted path / power-iteration condition estimate).
-__global__ void __launch_bounds__(128)
+// registers (KP = 16 or 32 columns; rows >= K are identity rows), Gauss-Jordan
+// without pivoting.  The register row is rotated by one slot per pivot step
+// (slot s holds column (s + k) mod KP at step k), so the pivot column is
+// always slot 0 and every register index is static inside a rolled loop
+// (no per-element selects, a small instruction footprint).  Hermitian
+// structure gives the pivot row for free: after pivots 0..k-1 the working
+// matrix is [[A_SS^-1, A_SS^-1 A_SU], [-A_US A_SS^-1, Schur]], so
+// M[k][j] = conj(M[j][k]) for j > k and -conj(M[j][k]) for j < k -- every lane
+// publishes its own entry of the pivot row (one shared store per lane).
+// The matrix is read column-wise (conj(A[j][i]): coalesced, the Hermitian
+// matrix of the lower triangle) and A^-1 is written the same way.  Items that
+// are not positive definite or whose ||A||_F ||A^-1||_F bound exceeds the
+// limit are flagged in `redo` for the CTA kernel (pivoted path /
+// power-iteration condition estimate).
+template <int KP>
+__global__ void __launch_bounds__(128, KP > 16 ? 3 : 4)
     herm_inverse_warp_kernel(int64_t B, int K, const c128 *__restrict__ A, int64_t as,
                              c128 *__restrict__ Ainv, int64_t ais, int32_t *__restrict__ info,
                              double limit, const uint8_t *__restrict__ mask,
@@ -412,69 +422,73 @@ __global__ void __launch_bounds__(128)
   if (item >= B) return;
   if (mask && !mask[item]) return;
   const c128 *a = A + item * as;
-  c128 m[32];
+  c128 m[KP];
   double fa = 0.0;
 #pragma unroll
-  for (int j = 0; j < 32; ++j) {
+  for (int j = 0; j < KP; ++j) {
     if (lane < K && j < K) {
-      m[j] = a[lane * K + j];
-      fa += cabs2(m[j]);
+      c128 v = cconj(a[j * K + lane]);
+      if (j == lane) v.im = 0.0;
+      m[j] = v;
+      fa += cabs2(v);
     } else {
       m[j] = mk<double>(lane == j ? 1.0 : 0.0, 0.0);
     }
   }
   fa = warp_sum(fa);
-  __shared__ c128 prow[4][32];
+  __shared__ c128 prow[4][KP];
   c128 *pr_s = prow[threadIdx.x >> 5];
   bool ok = true;
 #pragma unroll 1
   for (int k = 0; k < K; ++k) {
-    c128 ci = m[0];  // M[lane][k], selected without dynamic register indexing
-#pragma unroll
-    for (int j = 1; j < 32; ++j)
-      if (j == k) ci = m[j];
-    const double pr = __shfl_sync(0xffffffffu, ci.re, k);
-    const double pi = __shfl_sync(0xffffffffu, ci.im, k);
+    const c128 ck = m[0];  // M[lane][k]
+    const double pr = __shfl_sync(0xffffffffu, ck.re, k);
+    const double pi = __shfl_sync(0xffffffffu, ck.im, k);
     if (!(pr > 0.0) || !isfinite(pr) || !isfinite(pi)) {  // warp-uniform
       ok = false;
       break;
     }
     const c128 pinv = cinv(mk<double>(pr, pi));
-    if (lane == k) {  // scaled pivot row through shared memory (broadcast reads)
-#pragma unroll
-      for (int j = 0; j < 32; ++j) pr_s[j] = cmul(m[j], pinv);
-    }
+    // this lane's entry of the scaled pivot row, M[k][lane] / p
+    const c128 mk_l = (lane == k) ? mk<double>(pr, pi)
+                                  : (lane > k ? cconj(ck) : mk<double>(-ck.re, ck.im));
+    if (lane < KP) pr_s[lane] = cmul(mk_l, pinv);
     __syncwarp();
-    // uniform update row_i -= c_i r with c_k = p - 1 (so row k becomes r);
-    // column k is then set to -c_i / p (i != k) and 1 / p (i = k)
-    const c128 c = (lane == k) ? mk<double>(ci.re - 1.0, ci.im) : ci;
-    const c128 colv = (lane == k) ? pinv : cmul(mk<double>(-ci.re, -ci.im), pinv);
+    // row_i -= c_i r with c_k = p - 1 (so row k becomes r); column k is then
+    // -c_i / p (i != k) and 1 / p (i = k), stored in the last slot
+    const c128 c = (lane == k) ? mk<double>(ck.re - 1.0, ck.im) : ck;
+    const c128 colv = (lane == k) ? pinv : cmul(mk<double>(-ck.re, -ck.im), pinv);
 #pragma unroll
-    for (int j = 0; j < 32; ++j) {
-      const c128 r = pr_s[j];
-      c128 u = m[j];
+    for (int j = 0; j < KP - 1; ++j) {
+      const c128 r = pr_s[(j + 1 + k) & (KP - 1)];
+      c128 u = m[j + 1];
       u.re = fma(-c.re, r.re, u.re);
       u.re = fma(c.im, r.im, u.re);
       u.im = fma(-c.re, r.im, u.im);
       u.im = fma(-c.im, r.re, u.im);
-      m[j] = (j == k) ? colv : u;
+      m[j] = u;
     }
+    m[KP - 1] = colv;
     __syncwarp();
   }
   double fi = 0.0;
 #pragma unroll
-  for (int j = 0; j < 32; ++j)
-    if (lane < K && j < K) fi += cabs2(m[j]);
+  for (int j = 0; j < KP; ++j) fi += cabs2(m[j]);
+  if (lane >= K) fi = 0.0;
+  // padded columns of real rows are exactly zero, identity rows are excluded
   fi = warp_sum(fi);
   const bool good = ok && isfinite(fi) && sqrt(fa) * sqrt(fi) <= limit;
   if (!good) {
     if (lane == 0) redo[item] = 1;
     return;
   }
+  // slot j holds column (j + K) mod KP; A^-1[c][lane] = conj(M[lane][c])
   c128 *o = Ainv + item * ais;
 #pragma unroll
-  for (int j = 0; j < 32; ++j)
-    if (lane < K && j < K) o[lane * K + j] = m[j];
+  for (int j = 0; j < KP; ++j) {
+    const int col = (j + K) & (KP - 1);
+    if (lane < K && col < K) o[col * K + lane] = cconj(m[j]);
+  }
   if (lane == 0) {
     redo[item] = 0;
     if (info) info[item] = LRZ_INFO_OK;
@@ -530,9 +544,14 @@ extern "C" int lrz_herm_inverse(int64_t B, int K, const void *A, int64_t a_strid
   if (K <= 32 && workspace) {
     // warp-per-matrix fast path; the CTA kernel re-does only flagged items
     uint8_t *redo = (uint8_t *)workspace;
-    herm_inverse_warp_kernel<<<unsigned((B + 3) / 4), 128, 0, st>>>(
-        B, K, (const c128 *)A, a_stride, (c128 *)A_inv, ai_stride, info, cond_limit, item_mask,
-        redo);
+    if (K <= 16)
+      herm_inverse_warp_kernel<16><<<unsigned((B + 3) / 4), 128, 0, st>>>(
+          B, K, (const c128 *)A, a_stride, (c128 *)A_inv, ai_stride, info, cond_limit,
+          item_mask, redo);
+    else
+      herm_inverse_warp_kernel<32><<<unsigned((B + 3) / 4), 128, 0, st>>>(
+          B, K, (const c128 *)A, a_stride, (c128 *)A_inv, ai_stride, info, cond_limit,
+          item_mask, redo);
     mask = redo;
   } else if (K > INV_SMEM_KMAX && K <= 256 && workspace) {
     // cluster path: the matrix spread over CS CTAs' shared memory
