@@ -10,20 +10,9 @@
 // out), not by instruction issue -- the SIMT versions (gemm.cu) issue one
 // shared-memory load per two DFMAs and stall at 43-59 % of the pipe.
 
-#include "common.cuh"
+#include "dmma.cuh"
 
 namespace lrz {
-
-LRZ_DEV void dmma(double (&c)[2], double a, double b) {
-  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
-               : "+d"(c[0]), "+d"(c[1])
-               : "d"(a), "d"(b));
-}
-
-LRZ_DEV c128 ldg_c128(const c128 *p) {
-  const double2 v = __ldg(reinterpret_cast<const double2 *>(p));
-  return mk<double>(v.x, v.y);
-}
 
 // ---------------------------------------------------------------------------
 // K1: G = H H^H + alpha I, one item per warp, RB = ceil(K / 8) row blocks.
@@ -37,20 +26,20 @@ LRZ_DEV c128 ldg_c128(const c128 *p) {
 // ---------------------------------------------------------------------------
 constexpr int GD_WARPS = 4;
 
-template <int RB>
+template <int RB, typename T>
 __global__ void __launch_bounds__(32 * GD_WARPS, 3)
-    gram_dmma_kernel(int64_t B, int K, int N, const c128 *__restrict__ H, int64_t hs,
+    gram_dmma_kernel(int64_t B, int K, int N, const cplx<T> *__restrict__ H, int64_t hs,
                      double alpha, c128 *__restrict__ A, int64_t as) {
   constexpr int NT = RB * (RB + 1) / 2;
   const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
   const int64_t item = int64_t(blockIdx.x) * GD_WARPS + (threadIdx.x >> 5);
   if (item >= B) return;
-  const c128 *h = H + item * hs;
+  const cplx<T> *h = H + item * hs;
   double cr[NT][2], ci[NT][2];
 #pragma unroll
   for (int i = 0; i < NT; ++i) cr[i][0] = cr[i][1] = ci[i][0] = ci[i][1] = 0.0;
   bool rok[RB];
-  const c128 *hrow[RB];
+  const cplx<T> *hrow[RB];
 #pragma unroll
   for (int rb = 0; rb < RB; ++rb) {
     rok[rb] = 8 * rb + g < K;
@@ -64,7 +53,7 @@ __global__ void __launch_bounds__(32 * GD_WARPS, 3)
 #pragma unroll
       for (int s = 0; s < 4; ++s) {
         const int n = n0 + 4 * s + t;
-        v[rb][s] = (rok[rb] && (full || n < N)) ? ldg_c128(hrow[rb] + n) : czero<double>();
+        v[rb][s] = (rok[rb] && (full || n < N)) ? ldg_c(hrow[rb] + n) : czero<double>();
       }
 #pragma unroll
     for (int s = 0; s < 4; ++s) {
@@ -124,12 +113,13 @@ __global__ void __launch_bounds__(32 * GD_WARPS, 3)
 constexpr int PD_WARPS = 4;
 constexpr int PD_LD = 36;
 
+template <typename T>
 __global__ void __launch_bounds__(32 * PD_WARPS, 3)
-    precode_dmma32_kernel(int K, int N, const c128 *__restrict__ H, int64_t hs,
+    precode_dmma32_kernel(int K, int N, const cplx<T> *__restrict__ H, int64_t hs,
                           const c128 *__restrict__ Ainv, int64_t ais,
                           const c128 *__restrict__ Gt, int64_t gs, double alpha, double P_t,
                           const double *__restrict__ noise, int64_t noise_div,
-                          c128 *__restrict__ W, int64_t wst, double *__restrict__ scale_out,
+                          cplx<T> *__restrict__ W, int64_t wst, double *__restrict__ scale_out,
                           double *__restrict__ rates, double *__restrict__ sinr,
                           double *__restrict__ sum_rate, int32_t *__restrict__ info) {
   __shared__ __align__(16) double Sr[32 * PD_LD], Si[32 * PD_LD];
@@ -144,8 +134,8 @@ __global__ void __launch_bounds__(32 * PD_WARPS, 3)
     Si[i * PD_LD + k] = v.im;
   }
   __syncthreads();
-  const c128 *h = H + item * hs;
-  c128 *wo = W + item * wst;
+  const cplx<T> *h = H + item * hs;
+  cplx<T> *wo = W + item * wst;
   double nrm = 0.0;
   const int nslab = (N + 15) / 16;
   for (int sl = w; sl < nslab; sl += PD_WARPS) {
@@ -156,7 +146,7 @@ __global__ void __launch_bounds__(32 * PD_WARPS, 3)
 #pragma unroll
       for (int nb = 0; nb < 2; ++nb) {
         const int i = 4 * c + t, n = n0 + 8 * nb + g;
-        hv[c][nb] = (i < K && n < N) ? ldg_c128(h + int64_t(i) * N + n) : czero<double>();
+        hv[c][nb] = (i < K && n < N) ? ldg_c(h + int64_t(i) * N + n) : czero<double>();
       }
     double acr[2][4][2], aci[2][4][2];
 #pragma unroll
@@ -188,20 +178,14 @@ __global__ void __launch_bounds__(32 * PD_WARPS, 3)
 #pragma unroll
         for (int kb = 0; kb < 4; ++kb) {
           const int k = 8 * kb + 2 * t;
-          if (k + 1 < K) {
-            double4 o;
-            o.x = acr[nb][kb][0];
-            o.y = aci[nb][kb][0];
-            o.z = acr[nb][kb][1];
-            o.w = aci[nb][kb][1];
-            double2 *dst = reinterpret_cast<double2 *>(wo + int64_t(n) * K + k);
-            dst[0] = make_double2(o.x, o.y);
-            dst[1] = make_double2(o.z, o.w);
-            nrm += o.x * o.x + o.y * o.y + o.z * o.z + o.w * o.w;
-          } else if (k < K) {
-            wo[int64_t(n) * K + k] = mk<double>(acr[nb][kb][0], aci[nb][kb][0]);
-            nrm += acr[nb][kb][0] * acr[nb][kb][0] + aci[nb][kb][0] * aci[nb][kb][0];
-          }
+          // W in the input precision; ||W||^2 of the stored values (precoding.py:47-48)
+#pragma unroll
+          for (int e = 0; e < 2; ++e)
+            if (k + e < K) {
+              const cplx<T> o = mk<T>(T(acr[nb][kb][e]), T(aci[nb][kb][e]));
+              wo[int64_t(n) * K + k + e] = o;
+              nrm += double(o.re) * double(o.re) + double(o.im) * double(o.im);
+            }
         }
       }
     }
@@ -216,7 +200,7 @@ __global__ void __launch_bounds__(32 * PD_WARPS, 3)
 #pragma unroll
     for (int c = 0; c < 8; ++c) {
       const int i = 4 * c + t;
-      const c128 a = (row < K && i < K) ? ldg_c128(gr + i) : czero<double>();
+      const c128 a = (row < K && i < K) ? ldg_c(gr + i) : czero<double>();
 #pragma unroll
       for (int kb = 0; kb < 4; ++kb) {
         const double br = Sr[(4 * c + t) * PD_LD + 8 * kb + g];
@@ -285,30 +269,45 @@ __global__ void __launch_bounds__(32 * PD_WARPS, 3)
 
 using namespace lrz;
 
-// Launchers used by lrz_gram / lrz_precode_rate (gemm.cu) for complex128, K <= 32.
-int lrz_gram_dmma(int64_t B, int K, int N, const void *H, int64_t hs, double alpha, void *A,
-                  int64_t as, cudaStream_t s) {
+// Launchers used by lrz_gram / lrz_precode_rate (gemm.cu), K <= 32.  complex64
+// inputs are widened to double on load: the N-sized products run on the FP64
+// tensor pipe for both dtypes (the reference promotes c64 H against the
+// complex128 state), and only W is stored back in complex64.
+template <typename T>
+static void gram_dmma_launch(int64_t B, int K, int N, const cplx<T> *h, int64_t hs, double alpha,
+                             c128 *a, int64_t as, cudaStream_t s) {
   const unsigned nb = unsigned((B + GD_WARPS - 1) / GD_WARPS);
-  const int rb = (K + 7) / 8;
-  const c128 *h = (const c128 *)H;
-  c128 *a = (c128 *)A;
-  switch (rb) {
-    case 1: gram_dmma_kernel<1><<<nb, 32 * GD_WARPS, 0, s>>>(B, K, N, h, hs, alpha, a, as); break;
-    case 2: gram_dmma_kernel<2><<<nb, 32 * GD_WARPS, 0, s>>>(B, K, N, h, hs, alpha, a, as); break;
-    case 3: gram_dmma_kernel<3><<<nb, 32 * GD_WARPS, 0, s>>>(B, K, N, h, hs, alpha, a, as); break;
-    default: gram_dmma_kernel<4><<<nb, 32 * GD_WARPS, 0, s>>>(B, K, N, h, hs, alpha, a, as); break;
+  switch ((K + 7) / 8) {
+    case 1: gram_dmma_kernel<1, T><<<nb, 32 * GD_WARPS, 0, s>>>(B, K, N, h, hs, alpha, a, as); break;
+    case 2: gram_dmma_kernel<2, T><<<nb, 32 * GD_WARPS, 0, s>>>(B, K, N, h, hs, alpha, a, as); break;
+    case 3: gram_dmma_kernel<3, T><<<nb, 32 * GD_WARPS, 0, s>>>(B, K, N, h, hs, alpha, a, as); break;
+    default: gram_dmma_kernel<4, T><<<nb, 32 * GD_WARPS, 0, s>>>(B, K, N, h, hs, alpha, a, as); break;
   }
+}
+
+int lrz_gram_dmma(int dtype, int64_t B, int K, int N, const void *H, int64_t hs, double alpha,
+                  void *A, int64_t as, cudaStream_t s) {
+  if (dtype == LRZ_C64)
+    gram_dmma_launch<float>(B, K, N, (const c64 *)H, hs, alpha, (c128 *)A, as, s);
+  else
+    gram_dmma_launch<double>(B, K, N, (const c128 *)H, hs, alpha, (c128 *)A, as, s);
   return lrz_launch_status("gram_dmma_kernel");
 }
 
-int lrz_precode_dmma32(int64_t B, int K, int N, const void *H, int64_t hs, const void *A_inv,
-                       int64_t ais, const void *G_true, double alpha, double P_t,
-                       const double *noise, int64_t noise_div, void *W, int64_t wst,
+int lrz_precode_dmma32(int dtype, int64_t B, int K, int N, const void *H, int64_t hs,
+                       const void *A_inv, int64_t ais, const void *G_true, double alpha,
+                       double P_t, const double *noise, int64_t noise_div, void *W, int64_t wst,
                        double *scale, double *rates, double *sinr, double *sum_rate,
                        int32_t *info, cudaStream_t s) {
-  precode_dmma32_kernel<<<unsigned(B), 32 * PD_WARPS, 0, s>>>(
-      K, N, (const c128 *)H, hs, (const c128 *)A_inv, ais, (const c128 *)G_true,
-      int64_t(K) * K, alpha, P_t, noise, noise_div, (c128 *)W, wst, scale, rates, sinr, sum_rate,
-      info);
+  if (dtype == LRZ_C64)
+    precode_dmma32_kernel<float><<<unsigned(B), 32 * PD_WARPS, 0, s>>>(
+        K, N, (const c64 *)H, hs, (const c128 *)A_inv, ais, (const c128 *)G_true,
+        int64_t(K) * K, alpha, P_t, noise, noise_div, (c64 *)W, wst, scale, rates, sinr,
+        sum_rate, info);
+  else
+    precode_dmma32_kernel<double><<<unsigned(B), 32 * PD_WARPS, 0, s>>>(
+        K, N, (const c128 *)H, hs, (const c128 *)A_inv, ais, (const c128 *)G_true,
+        int64_t(K) * K, alpha, P_t, noise, noise_div, (c128 *)W, wst, scale, rates, sinr,
+        sum_rate, info);
   return lrz_launch_status("precode_dmma32_kernel");
 }

@@ -782,11 +782,11 @@ extern "C" int lrz_axpby(int dtype, int64_t n, double a, const void *X, double b
 
 static int ntiles(int K) { return (K + TM - 1) / TM; }
 
-// complex128 DMMA kernels for K <= 32 (dmma.cu); LRZ_SIMT_FP64=1 selects the
-// SIMT DFMA kernels instead (A/B measurements)
-int lrz_gram_dmma(int64_t B, int K, int N, const void *H, int64_t hs, double alpha, void *A,
-                  int64_t as, cudaStream_t s);
-int lrz_precode_dmma32(int64_t B, int K, int N, const void *H, int64_t hs, const void *A_inv,
+// DMMA kernels for K <= 32 (dmma.cu, both dtypes); LRZ_SIMT_FP64=1 selects the
+// SIMT kernels instead (A/B measurements)
+int lrz_gram_dmma(int dtype, int64_t B, int K, int N, const void *H, int64_t hs, double alpha,
+                  void *A, int64_t as, cudaStream_t s);
+int lrz_precode_dmma32(int dtype, int64_t B, int K, int N, const void *H, int64_t hs, const void *A_inv,
                        int64_t ais, const void *G_true, double alpha, double P_t,
                        const double *noise, int64_t noise_div, void *W, int64_t wst,
                        double *scale, double *rates, double *sinr, double *sum_rate,
@@ -807,8 +807,8 @@ extern "C" int lrz_gram(int dtype, int64_t B, int K, int N, const void *H, int64
   }
   if (B == 0) return LRZ_OK;
   cudaStream_t s = (cudaStream_t)stream;
-  if (K <= 32 && dtype == LRZ_C128 && use_dmma())
-    return lrz_gram_dmma(B, K, N, H, h_stride, alpha, A, a_stride, s);
+  if (K <= 32 && use_dmma())
+    return lrz_gram_dmma(dtype, B, K, N, H, h_stride, alpha, A, a_stride, s);
   if (K <= 32) {
     const unsigned nb = unsigned((B + G32_IPB - 1) / G32_IPB);
     if (dtype == LRZ_C64) {
@@ -977,8 +977,8 @@ extern "C" int lrz_precode_rate(int dtype, int64_t B, int K, int N, const void *
   if (G_true) {
     // W = H^H A^-1 (norm partials in the epilogue), coupling from the Gram:
     // H W = (G - alpha I) A^-1, K^3 instead of K^2 N work (F_RF = I)
-    if (K <= 32 && dtype == LRZ_C128 && use_dmma())
-      return lrz_precode_dmma32(B, K, N, H, h_stride, A_inv, ai_stride, G_true, alpha, P_t,
+    if (K <= 32 && use_dmma())
+      return lrz_precode_dmma32(dtype, B, K, N, H, h_stride, A_inv, ai_stride, G_true, alpha, P_t,
                                 noise, noise_div, W, w_stride, scale, rates, sinr, sum_rate,
                                 info, s);
     int nparts = tm * tn;

@@ -24,6 +24,12 @@ _WS: dict = {}
 LAUNCHES = [0]
 
 
+def dmma_active() -> bool:
+    """The K <= 32 Gram / precoder kernels run on the FP64 tensor pipe (both
+    dtypes) unless LRZ_SIMT_FP64=1 selects the SIMT kernels (A/B runs)."""
+    return os.environ.get("LRZ_SIMT_FP64") != "1"
+
+
 def _count(n: int = 1) -> None:
     LAUNCHES[0] += n
 
@@ -276,8 +282,7 @@ def precode_rate(H: torch.Tensor, A_inv: torch.Tensor, P_t: float, noise: torch.
                                  total.data_ptr(), info.data_ptr(), ws.data_ptr(),
                                  N.stream_ptr(dev)), "lrz_precode_rate")
     # complex128, K <= 32 with the Gram shortcut: one fused DMMA kernel (dmma.cu)
-    fused = (G_true is not None and K <= 32 and H.dtype == torch.complex128
-             and os.environ.get("LRZ_SIMT_FP64") != "1")
+    fused = G_true is not None and K <= 32 and dmma_active()
     _count(1 if fused else 3)
     return dict(W=W, scale=scale, rates=rates, sinr=sinr, sum=total, info=info)
 

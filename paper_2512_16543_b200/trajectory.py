@@ -57,7 +57,8 @@ class TrajectoryConfig:
     rate_via_gram: bool = True
     # Gram correction: "diff" = G_t - G_{t-1} from the Grams already formed (complex128:
     # cancellation error ~1e-14 relative); "formula" = the gram_delta products; "auto" =
-    # diff for complex128, formula for complex64
+    # diff when the Grams are fp64-accumulated (complex128, or K <= 32 on the FP64
+    # tensor pipe), formula otherwise (complex64 FP32 Grams)
     delta: str = "auto"
 
 
@@ -256,7 +257,11 @@ class TrajectoryRunner:
             dA = torch.empty(B, T, K, K, dtype=torch.complex128, device=dev)
             dAf = dA.reshape(BT, K, K)
             e0 = self._ev()
-            use_diff = c.delta == "diff" or (c.delta == "auto" and self.dtype == torch.complex128)
+            # "auto": difference the complex128 Grams whenever they are accumulated in
+            # fp64 -- complex128 inputs, or K <= 32 where complex64 H is widened to
+            # fp64 on the tensor pipe (gram_dmma_kernel)
+            fp64_gram = self.dtype == torch.complex128 or (K <= 32 and ops.dmma_active())
+            use_diff = c.delta == "diff" or (c.delta == "auto" and fp64_gram)
             if use_diff:
                 Gf = G.reshape(BT, K, K)
                 if T > 1:

@@ -11,13 +11,14 @@ import torch
 sys.path.insert(0, ".")
 from paper_2512_16543_b200 import ops, scenario as S  # noqa: E402
 
-spec = S.C2.with_(dtype="c128")
+dt = sys.argv[1] if len(sys.argv) > 1 else "c128"
+spec = S.C2.with_(dtype=dt)
 dev = torch.device("cuda", 0)
 H = torch.from_numpy(S.channels(spec)).to(dev)
 B, T, K, N = H.shape
 Hf = H.reshape(B * T, K, N)
 BT = B * T
-mode = "SIMT" if os.environ.get("LRZ_SIMT_FP64") == "1" else "DMMA"
+mode = ("SIMT" if os.environ.get("LRZ_SIMT_FP64") == "1" else "DMMA") + " " + dt
 
 
 def timeit(name, fn, n=10):
@@ -35,7 +36,8 @@ def timeit(name, fn, n=10):
 
 
 G = ops.gram(Hf, spec.alpha)
-Gref = Hf @ Hf.conj().transpose(-1, -2)
+Hd = Hf.to(torch.complex128)
+Gref = Hd @ Hd.conj().transpose(-1, -2)
 Gref = 0.5 * (Gref + Gref.conj().transpose(-1, -2))
 Gref = Gref + spec.alpha * torch.eye(K, dtype=Gref.dtype, device=dev)
 eg = ((G - Gref).abs().pow(2).sum((-1, -2)).sqrt() / Gref.abs().pow(2).sum((-1, -2)).sqrt()).max()
@@ -43,12 +45,12 @@ herm = (G - G.conj().transpose(-1, -2)).abs().max()
 print(f"{mode} gram max rel err vs torch {eg.item():.2e}, hermitian defect {herm.item():.1e}")
 Ainv, info = ops.herm_inverse(G)
 noise = torch.full((B, K), spec.noise_var, dtype=torch.float64, device=dev)
-W = torch.empty(BT, N, K, dtype=torch.complex128, device=dev)
+W = torch.empty(BT, N, K, dtype=Hf.dtype, device=dev)
 pr = ops.precode_rate(Hf, Ainv, 1.0, noise, T, W=W, G_true=G, alpha=spec.alpha)
-Wref = Hf.conj().transpose(-1, -2) @ Ainv
+Wref = Hd.conj().transpose(-1, -2) @ Ainv
 ew = ((W - Wref).abs().pow(2).sum((-1, -2)).sqrt() / Wref.abs().pow(2).sum((-1, -2)).sqrt()).max()
 s = 1.0 / Wref.abs().pow(2).sum((-1, -2)).sqrt()
-C = (Hf @ Wref) * s[:, None, None]
+C = (Hd @ Wref) * s[:, None, None]
 P = C.abs() ** 2
 sig = torch.diagonal(P, dim1=-2, dim2=-1)
 q = sig / (P.sum(-1) - sig + spec.noise_var)
