@@ -66,6 +66,8 @@ def report(path):
         for want in ("dram__bytes_read.sum", "dram__bytes_write.sum", "gpu__time_duration.sum",
                      "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active",
                      "sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active",
+                     "sm__pipe_tensor_subpipe_dmma_cycles_active.avg.pct_of_peak_sustained_active",
+                     "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed",
                      "smsp__inst_executed.sum", "sm__warps_active.avg.pct_of_peak_sustained_active"):
             for i, name in enumerate(hh):
                 if name == want:
