@@ -338,12 +338,9 @@ def stage_model(spec, T, B, k_mean, iters_hist, wb_steps):
     n_sk = B * (T - 1)
     m = {}
     m["gram"] = (4 * K * (K + 1) * N * BT, (K * N * c + K * K * 16) * BT)
-    if spec.dtype == "c128" or K <= 32:
-        # difference form G_t - G_{t-1} of the fp64 Grams (TrajectoryConfig.delta "auto")
-        m["gram_delta"] = (2 * K * K * n_sk, 3 * K * K * 16 * n_sk)
-    else:
-        m["gram_delta"] = ((8 * K * K * N + 4 * K * (K + 1) * N) * n_sk,
-                           (2 * K * N * c + K * K * 16) * n_sk)
+    # difference form G_t - G_{t-1} of the fp64 Grams (TrajectoryConfig.delta "auto":
+    # the DMMA Grams accumulate in fp64 for both dtypes)
+    m["gram_delta"] = (2 * K * K * n_sk, 3 * K * K * 16 * n_sk)
     widths = []
     k0 = spec.k_init
     for _ in range(spec.i_max):

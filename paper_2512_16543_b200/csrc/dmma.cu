@@ -29,12 +29,17 @@ constexpr int GD_WARPS = 4;
 template <int RB, typename T>
 __global__ void __launch_bounds__(32 * GD_WARPS, 3)
     gram_dmma_kernel(int64_t B, int K, int N, const cplx<T> *__restrict__ H, int64_t hs,
-                     double alpha, c128 *__restrict__ A, int64_t as) {
+                     double alpha, c128 *__restrict__ A, int64_t as, int nb) {
   constexpr int NT = RB * (RB + 1) / 2;
   const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
-  const int64_t item = int64_t(blockIdx.x) * GD_WARPS + (threadIdx.x >> 5);
-  if (item >= B) return;
-  const cplx<T> *h = H + item * hs;
+  const int64_t wid = int64_t(blockIdx.x) * GD_WARPS + (threadIdx.x >> 5);
+  if (wid >= B * nb) return;
+  // K > 32: warp = (item, diagonal 32-row block I) of the Gram
+  const int64_t item = wid / nb;
+  const int I = int(wid - item * nb), r0 = 32 * I;
+  const cplx<T> *h = H + item * hs + int64_t(r0) * N;
+  const int Kfull = K;
+  K = min(32, Kfull - r0);  // valid rows of this block
   double cr[NT][2], ci[NT][2];
 #pragma unroll
   for (int i = 0; i < NT; ++i) cr[i][0] = cr[i][1] = ci[i][0] = ci[i][1] = 0.0;
@@ -72,7 +77,7 @@ __global__ void __launch_bounds__(32 * GD_WARPS, 3)
       }
     }
   }
-  c128 *a = A + item * as;
+  c128 *a = A + item * as + int64_t(r0) * Kfull + r0;
 #pragma unroll
   for (int ib = 0; ib < RB; ++ib)
 #pragma unroll
@@ -87,14 +92,87 @@ __global__ void __launch_bounds__(32 * GD_WARPS, 3)
           if (row == col) {
             z.im = 0.0;
             z.re += alpha;
-            a[int64_t(row) * K + col] = z;
+            a[int64_t(row) * Kfull + col] = z;
           } else {
-            a[int64_t(row) * K + col] = z;
-            a[int64_t(col) * K + row] = cconj(z);
+            a[int64_t(row) * Kfull + col] = z;
+            a[int64_t(col) * Kfull + row] = cconj(z);
           }
         }
       }
     }
+}
+
+// K > 32: off-diagonal 32 x 32 blocks (I > J) of the Gram, one warp per
+// (item, block): 16 8 x 8 tiles, A fragments from the rows of block I, B
+// fragments from the rows of block J, 8 columns of H per step; written with
+// the mirrored upper block.
+template <typename T>
+__global__ void __launch_bounds__(32 * GD_WARPS)
+    gram_dmma_off_kernel(int64_t B, int K, int N, const cplx<T> *__restrict__ H, int64_t hs,
+                         c128 *__restrict__ A, int64_t as, int npair) {
+  const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+  const int64_t wid = int64_t(blockIdx.x) * GD_WARPS + (threadIdx.x >> 5);
+  if (wid >= B * npair) return;
+  const int64_t item = wid / npair;
+  int p = int(wid - item * npair), I = 1;
+  while (p >= I) {  // pairs (I, J), J < I, in row order
+    p -= I;
+    ++I;
+  }
+  const int J = p;
+  const cplx<T> *h = H + item * hs;
+  bool iok[4], jok[4];
+  const cplx<T> *hi[4], *hj[4];
+#pragma unroll
+  for (int b = 0; b < 4; ++b) {
+    const int ri = 32 * I + 8 * b + g, rj = 32 * J + 8 * b + g;
+    iok[b] = ri < K;
+    jok[b] = rj < K;
+    hi[b] = h + int64_t(iok[b] ? ri : 0) * N;
+    hj[b] = h + int64_t(jok[b] ? rj : 0) * N;
+  }
+  double cr[16][2], ci[16][2];
+#pragma unroll
+  for (int x = 0; x < 16; ++x) cr[x][0] = cr[x][1] = ci[x][0] = ci[x][1] = 0.0;
+  for (int n0 = 0; n0 < N; n0 += 8) {
+    c128 vi[4][2], vj[4][2];
+#pragma unroll
+    for (int b = 0; b < 4; ++b)
+#pragma unroll
+      for (int s = 0; s < 2; ++s) {
+        const int n = n0 + 4 * s + t;
+        vi[b][s] = (iok[b] && n < N) ? ldg_c(hi[b] + n) : czero<double>();
+        vj[b][s] = (jok[b] && n < N) ? ldg_c(hj[b] + n) : czero<double>();
+      }
+#pragma unroll
+    for (int s = 0; s < 2; ++s)
+#pragma unroll
+      for (int ib = 0; ib < 4; ++ib) {
+        const double ar = vi[ib][s].re, ai = vi[ib][s].im, nar = -ar;
+#pragma unroll
+        for (int jb = 0; jb < 4; ++jb) {
+          const double br = vj[jb][s].re, bi = vj[jb][s].im;
+          dmma(cr[4 * ib + jb], ar, br);
+          dmma(cr[4 * ib + jb], ai, bi);
+          dmma(ci[4 * ib + jb], ai, br);
+          dmma(ci[4 * ib + jb], nar, bi);
+        }
+      }
+  }
+  c128 *a = A + item * as;
+#pragma unroll
+  for (int ib = 0; ib < 4; ++ib)
+#pragma unroll
+    for (int jb = 0; jb < 4; ++jb)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int row = 32 * I + 8 * ib + g, col = 32 * J + 8 * jb + 2 * t + e;
+        if (row < K && col < K) {
+          const c128 z = mk<double>(cr[4 * ib + jb][e], ci[4 * ib + jb][e]);
+          a[int64_t(row) * K + col] = z;
+          a[int64_t(col) * K + row] = cconj(z);
+        }
+      }
 }
 
 // ---------------------------------------------------------------------------
@@ -276,12 +354,18 @@ using namespace lrz;
 template <typename T>
 static void gram_dmma_launch(int64_t B, int K, int N, const cplx<T> *h, int64_t hs, double alpha,
                              c128 *a, int64_t as, cudaStream_t s) {
-  const unsigned nb = unsigned((B + GD_WARPS - 1) / GD_WARPS);
-  switch ((K + 7) / 8) {
-    case 1: gram_dmma_kernel<1, T><<<nb, 32 * GD_WARPS, 0, s>>>(B, K, N, h, hs, alpha, a, as); break;
-    case 2: gram_dmma_kernel<2, T><<<nb, 32 * GD_WARPS, 0, s>>>(B, K, N, h, hs, alpha, a, as); break;
-    case 3: gram_dmma_kernel<3, T><<<nb, 32 * GD_WARPS, 0, s>>>(B, K, N, h, hs, alpha, a, as); break;
-    default: gram_dmma_kernel<4, T><<<nb, 32 * GD_WARPS, 0, s>>>(B, K, N, h, hs, alpha, a, as); break;
+  const int nb = (K + 31) / 32;
+  const unsigned nd = unsigned((B * nb + GD_WARPS - 1) / GD_WARPS);
+  switch (K > 32 ? 4 : (K + 7) / 8) {
+    case 1: gram_dmma_kernel<1, T><<<nd, 32 * GD_WARPS, 0, s>>>(B, K, N, h, hs, alpha, a, as, nb); break;
+    case 2: gram_dmma_kernel<2, T><<<nd, 32 * GD_WARPS, 0, s>>>(B, K, N, h, hs, alpha, a, as, nb); break;
+    case 3: gram_dmma_kernel<3, T><<<nd, 32 * GD_WARPS, 0, s>>>(B, K, N, h, hs, alpha, a, as, nb); break;
+    default: gram_dmma_kernel<4, T><<<nd, 32 * GD_WARPS, 0, s>>>(B, K, N, h, hs, alpha, a, as, nb); break;
+  }
+  if (nb > 1) {
+    const int np = nb * (nb - 1) / 2;
+    const unsigned no = unsigned((B * np + GD_WARPS - 1) / GD_WARPS);
+    gram_dmma_off_kernel<T><<<no, 32 * GD_WARPS, 0, s>>>(B, K, N, h, hs, a, as, np);
   }
 }
 

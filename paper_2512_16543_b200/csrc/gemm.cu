@@ -807,8 +807,7 @@ extern "C" int lrz_gram(int dtype, int64_t B, int K, int N, const void *H, int64
   }
   if (B == 0) return LRZ_OK;
   cudaStream_t s = (cudaStream_t)stream;
-  if (K <= 32 && use_dmma())
-    return lrz_gram_dmma(dtype, B, K, N, H, h_stride, alpha, A, a_stride, s);
+  if (use_dmma()) return lrz_gram_dmma(dtype, B, K, N, H, h_stride, alpha, A, a_stride, s);
   if (K <= 32) {
     const unsigned nb = unsigned((B + G32_IPB - 1) / G32_IPB);
     if (dtype == LRZ_C64) {

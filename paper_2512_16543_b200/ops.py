@@ -94,7 +94,7 @@ def gram(H: torch.Tensor, alpha: float, out: torch.Tensor | None = None) -> torc
     lib = N.lib_for(H.device)
     N.check(lib.lrz_gram(_dt(H), B, K, Nn, H.data_ptr(), K * Nn, float(alpha), A.data_ptr(),
                          K * K, N.stream_ptr(H.device)), "lrz_gram")
-    _count(1)
+    _count(2 if (K > 32 and dmma_active()) else 1)  # diagonal + off-diagonal blocks
     return A
 
 

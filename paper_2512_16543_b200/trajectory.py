@@ -57,8 +57,8 @@ class TrajectoryConfig:
     rate_via_gram: bool = True
     # Gram correction: "diff" = G_t - G_{t-1} from the Grams already formed (complex128:
     # cancellation error ~1e-14 relative); "formula" = the gram_delta products; "auto" =
-    # diff when the Grams are fp64-accumulated (complex128, or K <= 32 on the FP64
-    # tensor pipe), formula otherwise (complex64 FP32 Grams)
+    # diff when the Grams are fp64-accumulated (complex128, or complex64 on the
+    # FP64 tensor pipe), formula otherwise (complex64 FP32 Grams)
     delta: str = "auto"
 
 
@@ -258,9 +258,9 @@ class TrajectoryRunner:
             dAf = dA.reshape(BT, K, K)
             e0 = self._ev()
             # "auto": difference the complex128 Grams whenever they are accumulated in
-            # fp64 -- complex128 inputs, or K <= 32 where complex64 H is widened to
-            # fp64 on the tensor pipe (gram_dmma_kernel)
-            fp64_gram = self.dtype == torch.complex128 or (K <= 32 and ops.dmma_active())
+            # fp64 -- complex128 inputs, or complex64 H widened to fp64 on the tensor
+            # pipe (gram_dmma_kernel)
+            fp64_gram = self.dtype == torch.complex128 or ops.dmma_active()
             use_diff = c.delta == "diff" or (c.delta == "auto" and fp64_gram)
             if use_diff:
                 Gf = G.reshape(BT, K, K)
