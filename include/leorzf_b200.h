@@ -132,6 +132,16 @@ int lrz_chain(int64_t B, int T, int K, int d_max, const uint8_t *plan, const voi
               const void *V, const double *S, const int32_t *r, uint8_t *method,
               int32_t *info, void *workspace, void *stream);
 
+/* Same chain, step-parallel: the B trials advance one time step per launch
+ * group and every product of the Woodbury step is batched over the trials
+ * (2 batched GEMMs, the r x r core per trial, tiled A^-1 / A update, fallback
+ * inversions).  Same arguments, results and workspace as lrz_chain; faster
+ * when K is large and B small (one CTA per trial leaves SMs idle there). */
+int lrz_chain_steps(int64_t B, int T, int K, int d_max, const uint8_t *plan, const void *G,
+                    const void *A_inv_prev, void *A_inv_seq, void *A_state, const void *U,
+                    const void *V, const double *S, const int32_t *r, uint8_t *method,
+                    int32_t *info, void *workspace, void *stream);
+
 /* Dispatcher decision (lowrank.py:345-359) for n steps: plan = 2 (none,
  * k_est == 0), 1 (Woodbury, k_est/K <= 0.5), 0 (full); is_sketch == 0 -> 0. */
 int lrz_plan(int64_t n, int K, const uint8_t *is_sketch, const int32_t *k_est, uint8_t *plan,

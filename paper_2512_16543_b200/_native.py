@@ -54,6 +54,8 @@ _SIGS = {
     "lrz_woodbury": (C.c_int, [I64, C.c_int, C.c_int, P, P, I64, P, P, P, P, P, P, P, P, P]),
     "lrz_chain": (C.c_int, [I64, C.c_int, C.c_int, C.c_int, P, P, P, P, P, P, P, P, P, P, P, P,
                             P]),
+    "lrz_chain_steps": (C.c_int, [I64, C.c_int, C.c_int, C.c_int, P, P, P, P, P, P, P, P, P, P,
+                                  P, P, P]),
     "lrz_precode_rate": (C.c_int, [C.c_int, I64, C.c_int, C.c_int, P, I64, P, I64, F64, P, I64,
                                    P, I64, P, F64, P, P, P, P, P, P, P]),
     "lrz_cgemm": (C.c_int, [C.c_int, I64, C.c_int, C.c_int, C.c_int, C.c_int, P, I64, I64,

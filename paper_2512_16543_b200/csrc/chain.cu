@@ -333,6 +333,203 @@ __global__ void __launch_bounds__(INV_THREADS)
   }
 }
 
+
+// ---------------------------------------------------------------------------
+// Step-parallel Woodbury chain (K > 32).  chain_kernel walks each trial's
+// steps in one CTA, which leaves most of the GPU idle when B is small and
+// the K x K products are large (C5: 64 trials x K = 256).  Here the trials
+// advance together, one time step per group of launches, and every product is
+// batched over the trials (reference lowrank.py:182-227 per trial):
+//   1. AiU^T = U^T A^-1^T, VhAi = V^H A^-1        (two batched GEMMs, lrz_chain)
+//   2. wb_core_kernel  (CTA per trial): aux = diag(1/S) + V^H AiU, aux^-1 with
+//      the 1e12 condition guard, T = AiU aux^-1 (SingularAuxiliary -> fb flag)
+//   3. wb_apply_kernel (32 x 32 tiles): A^-1_t = A^-1_{t-1} - T VhAi,
+//      A += U S V^H, 'none' copies, A = G_t where the reference re-forms it
+//   4. wb_fallback_kernel (CTA per flagged trial): A^-1_t = inv(G_t)
+// Same per-step semantics as chain_kernel.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(INV_THREADS)
+    wb_core_kernel(int T, int t, int K, int D, const uint8_t *__restrict__ plan,
+                   const c128 *__restrict__ V, const double *__restrict__ S,
+                   const int32_t *__restrict__ r, c128 *__restrict__ ws, uint8_t *__restrict__ fb,
+                   uint8_t *__restrict__ method, int32_t *__restrict__ info) {
+  extern __shared__ __align__(16) char wbc_smem[];
+  const int64_t b = blockIdx.x, bt = b * T + t;
+  if (plan[bt] != 1) return;
+  const int tid = threadIdx.x, NT = blockDim.x;
+  const int rr = r[bt];
+  WbScratch sc;
+  c128 *unused;
+  sc.inv = carve_inv(wbc_smem, D, &unused, D, false);
+  carve_wb(sc, wbc_smem + InvSmem::bytes(D, D, false), ws + b * wb_ws_elems(K, D), K, D);
+  const c128 *Vb = V + bt * int64_t(D) * K;
+  const double *Sb = S + bt * D;
+  bool ok = rr >= 1 && rr <= D;
+  if (ok) {
+    // aux = diag(1/S) + V^H AiU (lowrank.py:208-211)
+    double loc = 0.0;
+    for (int e = tid; e < rr * rr; e += NT) {
+      const int i = e / rr, j = e - i * rr;
+      c128 a = czero<double>();
+      const c128 *vc = Vb + int64_t(i) * K;
+      const c128 *au = sc.AiU + int64_t(j) * K;
+      for (int k = 0; k < K; ++k) cfma_ca(a, vc[k], au[k]);
+      if (i == j) a.re = 1.0 / Sb[i] + a.re;
+      sc.aux[e] = a;
+      sc.auxinv[e] = a;
+      loc += cabs2(a);
+    }
+    const double fa = block_sum(loc, sc.inv.red);
+    // aux^-1 with the 1e12 condition guard (lowrank.py:212-217)
+    int st = cta_gauss_jordan(sc.auxinv, rr, rr, true, sc.inv.colbuf, sc.inv.rowbuf,
+                              sc.inv.perm, sc.inv.red, sc.inv.ired);
+    if (st != 0) {
+      ok = false;
+    } else {
+      const double fi = cta_fro2(sc.auxinv, rr, rr, sc.inv.red);
+      ok = cta_cond_ok(sc.aux, sc.auxinv, rr, rr, rr, fa, fi, 1e12, sc.inv.v, sc.inv.w,
+                       sc.inv.red);
+    }
+  }
+  if (ok) {
+    // T = AiU aux^-1 (K x r), zero beyond r; VhAi rows beyond r zeroed too, so the
+    // apply stage can run its inner loop over all D columns
+    for (int e = tid; e < K * D; e += NT) {
+      const int j = e / K, k = e - j * K;
+      c128 a = czero<double>();
+      if (j < rr)
+        for (int i = 0; i < rr; ++i) cfma(a, sc.AiU[int64_t(i) * K + k], sc.auxinv[i * rr + j]);
+      sc.T[int64_t(j) * K + k] = a;
+      if (j >= rr) sc.VhAi[int64_t(j) * K + k] = czero<double>();
+    }
+  }
+  if (tid == 0) {
+    fb[b] = ok ? 0 : 1;
+    if (ok) {
+      method[bt] = uint8_t(LRZ_METHOD_WOODBURY);
+      info[bt] = LRZ_INFO_OK;
+    }
+  }
+}
+
+constexpr int WBA_TILE = 32;
+
+__global__ void __launch_bounds__(256)
+    wb_apply_kernel(int T, int t, int K, int D, const uint8_t *__restrict__ plan,
+                    const c128 *__restrict__ G, const c128 *__restrict__ prev_base,
+                    int64_t prev_stride, c128 *__restrict__ Ainv_seq, c128 *__restrict__ A_state,
+                    const c128 *__restrict__ U, const c128 *__restrict__ V,
+                    const double *__restrict__ S, const c128 *__restrict__ ws,
+                    const uint8_t *__restrict__ fb, uint8_t *__restrict__ method) {
+  __shared__ c128 Ts[8][WBA_TILE + 1], Ws[8][WBA_TILE + 1];
+  const int nt = (K + WBA_TILE - 1) / WBA_TILE, ntile = nt * nt;
+  const int64_t b = blockIdx.x / ntile;
+  const int tile = int(blockIdx.x % ntile), I = tile / nt, J = tile % nt;
+  const int64_t bt = b * T + t, KK = int64_t(K) * K;
+  const int pl = plan[bt];
+  const int tid = threadIdx.x, tx = tid & 31, ty = tid >> 5;  // 8 rows x 32 cols per pass
+  const c128 *prev = prev_base + b * prev_stride;
+  c128 *out = Ainv_seq + bt * KK;
+  c128 *Ast = A_state ? A_state + b * KK : nullptr;
+  const c128 *Gt = G + bt * KK;
+  const int col = J * WBA_TILE + tx;
+  if (pl == 2) {  // 'none': A^-1 aliases the previous one (lowrank.py:345-351)
+    for (int i = ty; i < WBA_TILE; i += 8) {
+      const int row = I * WBA_TILE + i;
+      if (row < K && col < K) out[int64_t(row) * K + col] = prev[int64_t(row) * K + col];
+    }
+    if (tile == 0 && tid == 0) method[bt] = uint8_t(LRZ_METHOD_NONE);
+    return;
+  }
+  const bool wb = pl == 1 && !fb[b];
+  if (!wb) {
+    // full step (plan 0, or the SingularAuxiliary fallback): A = G_t where it is
+    // still needed -- before a Woodbury / 'none' step and at the chunk end
+    const bool needed = (pl == 1) || (t == T - 1) || plan[bt + 1] != 0;
+    if (Ast && needed)
+      for (int i = ty; i < WBA_TILE; i += 8) {
+        const int row = I * WBA_TILE + i;
+        if (row < K && col < K) Ast[int64_t(row) * K + col] = Gt[int64_t(row) * K + col];
+      }
+    if (pl == 0 && tile == 0 && tid == 0) method[bt] = uint8_t(LRZ_METHOD_FULL);
+    return;
+  }
+  const c128 *w = ws + b * wb_ws_elems(K, D);
+  const c128 *Tm = w + int64_t(K) * D, *VhAi = w + 2 * int64_t(K) * D;
+  const c128 *Ub = U + bt * int64_t(D) * K, *Vb = V + bt * int64_t(D) * K;
+  const double *Sb = S + bt * D;
+  // rows I*32 + ty + 8 q of the tile, column col: acc over the D factor columns
+  c128 acc[4], accA[4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) acc[q] = accA[q] = czero<double>();
+  for (int j0 = 0; j0 < D; j0 += 8) {
+    // stage T[j][rows] and VhAi[j][cols] for 8 factor columns
+    __syncthreads();
+    {
+      const int j = j0 + ty;
+      const int row = I * WBA_TILE + tx;
+      Ts[ty][tx] = (j < D && row < K) ? Tm[int64_t(j) * K + row] : czero<double>();
+      Ws[ty][tx] = (j < D && col < K) ? VhAi[int64_t(j) * K + col] : czero<double>();
+    }
+    __syncthreads();
+#pragma unroll
+    for (int jj = 0; jj < 8; ++jj) {
+      const c128 wv = Ws[jj][tx];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) cfma(acc[q], Ts[jj][ty + 8 * q], wv);
+    }
+    if (Ast) {
+      __syncthreads();
+      {
+        const int j = j0 + ty;
+        const int row = I * WBA_TILE + tx;
+        // U S (rows) and V (cols): A += (U S) V^H (lowrank.py:220)
+        Ts[ty][tx] = (j < D && row < K) ? cscale(Ub[int64_t(j) * K + row], Sb[j])
+                                       : czero<double>();
+        Ws[ty][tx] = (j < D && col < K) ? Vb[int64_t(j) * K + col] : czero<double>();
+      }
+      __syncthreads();
+#pragma unroll
+      for (int jj = 0; jj < 8; ++jj) {
+        const c128 vv = Ws[jj][tx];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) cfma_cb(accA[q], Ts[jj][ty + 8 * q], vv);
+      }
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const int row = I * WBA_TILE + ty + 8 * q;
+    if (row < K && col < K) {
+      const int64_t e = int64_t(row) * K + col;
+      const c128 o = prev[e];
+      out[e] = mk<double>(o.re - acc[q].re, o.im - acc[q].im);
+      if (Ast) {
+        const c128 x = Ast[e];
+        Ast[e] = mk<double>(x.re + accA[q].re, x.im + accA[q].im);
+      }
+    }
+  }
+}
+
+__global__ void __launch_bounds__(INV_THREADS)
+    wb_fallback_kernel(int T, int t, int K, const uint8_t *__restrict__ plan,
+                       const c128 *__restrict__ G, c128 *__restrict__ Ainv_seq,
+                       const uint8_t *__restrict__ fb, uint8_t *__restrict__ method,
+                       int32_t *__restrict__ info) {
+  extern __shared__ __align__(16) char wbf_smem[];
+  const int64_t b = blockIdx.x, bt = b * T + t, KK = int64_t(K) * K;
+  if (plan[bt] != 1 || !fb[b]) return;
+  c128 *M;
+  const InvScratch sc = carve_inv(wbf_smem, K, &M, K, K <= INV_SMEM_KMAX);
+  // full branch: invert the true Gram of the new channel (lowrank.py:353-367)
+  const int st = cta_herm_inverse(G + bt * KK, Ainv_seq + bt * KK, K, M, 1e14, sc);
+  if (threadIdx.x == 0) {
+    method[bt] = uint8_t(LRZ_METHOD_FULL);
+    info[bt] = st;
+  }
+}
+
 // Speculative cursor verification: one thread per trial.
 //   is_sketch[b][t]: step runs arsvd.  iters_pred: iterations assumed when the
 //   cursor of every later step was computed; iters_act: what the last pass saw.
@@ -516,7 +713,13 @@ size_t lrz_woodbury_smem(int D) { return InvSmem::bytes(D, D, false) + wb_aux_sm
 size_t lrz_chain_smem(int K, int D) {
   return InvSmem::bytes(K, D, K <= INV_SMEM_KMAX) + wb_aux_smem(D);
 }
-size_t lrz_wb_ws(int64_t B, int K, int D) { return size_t(B) * wb_ws_elems(K, D) * sizeof(c128); }
+size_t lrz_wb_ws(int64_t B, int K, int D) {
+  // + per-trial SingularAuxiliary flags of the step-parallel chain
+  return size_t(B) * wb_ws_elems(K, D) * sizeof(c128) + size_t(B);
+}
+int lrz_zgemm_internal(int64_t batch, int M, int N, int Kd, int opA, const void *A, int64_t lda,
+                       int64_t sA, int opB, const void *Bm, int64_t ldb, int64_t sB, void *C,
+                       int64_t ldc, int64_t sC, cudaStream_t s);
 
 static int set_smem(const void *fn, size_t bytes) {
   if (bytes > 32 * 1024) {  // static shared memory counts against the 48 KB default too
@@ -626,6 +829,55 @@ extern "C" int lrz_chain(int64_t B, int T, int K, int d_max, const uint8_t *plan
       (c128 *)A_state, (const c128 *)U, (const c128 *)V, S, r, method, info,
       (c128 *)workspace);
   return lrz_launch_status("lrz_chain");
+}
+
+
+extern "C" int lrz_chain_steps(int64_t B, int T, int K, int d_max, const uint8_t *plan,
+                               const void *G, const void *A_inv_prev, void *A_inv_seq,
+                               void *A_state, const void *U, const void *V, const double *S,
+                               const int32_t *r, uint8_t *method, int32_t *info, void *workspace,
+                               void *stream) {
+  if (B < 0 || T < 1 || K < 1 || d_max < 1 || d_max > 256 || !plan || !G || !A_inv_prev ||
+      !A_inv_seq || !U || !V || !S || !r || !method || !info || !workspace) {
+    lrz_set_error("lrz_chain_steps: bad arguments");
+    return LRZ_EINVAL;
+  }
+  if (B == 0) return LRZ_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  {
+    // step-parallel chain: the trials advance together, products batched over them
+    c128 *ws = (c128 *)workspace;
+    uint8_t *fb = (uint8_t *)(ws + B * wb_ws_elems(K, d_max));
+    const int64_t KK = int64_t(K) * K, E = wb_ws_elems(K, d_max);
+    const size_t smc = lrz_woodbury_smem(d_max), smf = lrz_inverse_smem(K);
+    if (set_smem((const void *)wb_core_kernel, smc) ||
+        set_smem((const void *)wb_fallback_kernel, smf))
+      return LRZ_ELAUNCH;
+    const int nt = (K + WBA_TILE - 1) / WBA_TILE;
+    for (int t = 0; t < T; ++t) {
+      const c128 *prev = t == 0 ? (const c128 *)A_inv_prev : (const c128 *)A_inv_seq + (t - 1) * KK;
+      const int64_t pst = t == 0 ? KK : int64_t(T) * KK;
+      // AiU^T = U^T (A^-1)^T  (D x K)  and  VhAi = conj(V^T) A^-1  (D x K)
+      int rc = lrz_zgemm_internal(B, d_max, K, K, 0, (const c128 *)U + t * int64_t(d_max) * K, K,
+                                  int64_t(T) * d_max * K, 1, prev, K, pst, ws, K, E, st);
+      if (!rc)
+        rc = lrz_zgemm_internal(B, d_max, K, K, 3, (const c128 *)V + t * int64_t(d_max) * K, K,
+                                int64_t(T) * d_max * K, 0, prev, K, pst,
+                                ws + 2 * int64_t(K) * d_max, K, E, st);
+      if (rc) return rc;
+      wb_core_kernel<<<unsigned(B), INV_THREADS, smc, st>>>(T, t, K, d_max, plan,
+                                                            (const c128 *)V, S, r, ws, fb,
+                                                            method, info);
+      wb_apply_kernel<<<unsigned(B * nt * nt), 256, 0, st>>>(
+          T, t, K, d_max, plan, (const c128 *)G, prev, pst, (c128 *)A_inv_seq, (c128 *)A_state,
+          (const c128 *)U, (const c128 *)V, S, ws, fb, method);
+      wb_fallback_kernel<<<unsigned(B), INV_THREADS, smf, st>>>(T, t, K, plan, (const c128 *)G,
+                                                                (c128 *)A_inv_seq, fb, method,
+                                                                info);
+      if (int rc2 = lrz_launch_status("lrz_chain (step-parallel)")) return rc2;
+    }
+    return LRZ_OK;
+  }
 }
 
 extern "C" int lrz_spec_verify(int64_t B, int T, int K, const lrz_arsvd_cfg *cfg,

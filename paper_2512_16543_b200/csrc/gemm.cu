@@ -324,7 +324,7 @@ __global__ void __launch_bounds__(GEMM_THREADS)
     for (int e = tid; e < TM * BK; e += GEMM_THREADS) {
       // A_eff[m][k]: op 0 -> A[m][k] (k contiguous); op 1/2 -> A[k][m] (m contiguous)
       int m, k;
-      if (opA == 0) {
+      if (opA == 0 || opA == 3) {  // 3: conj(A[m][k]) (internal)
         m = e / BK;
         k = e % BK;
       } else {
@@ -334,9 +334,10 @@ __global__ void __launch_bounds__(GEMM_THREADS)
       const int gm = I * TM + m, gk = k0 + k;
       cplx<T> v = czero<T>();
       if (gm < M && gk < Kd) {
-        cplx<TA> x = (opA == 0) ? a[int64_t(gm) * lda + gk] : a[int64_t(gk) * lda + gm];
+        cplx<TA> x = (opA == 0 || opA == 3) ? a[int64_t(gm) * lda + gk]
+                                            : a[int64_t(gk) * lda + gm];
         v = ccast<T>(x);
-        if (opA == 2) v.im = -v.im;
+        if (opA >= 2) v.im = -v.im;
       }
       As[k][m] = v;
     }
@@ -873,6 +874,19 @@ int lrz_sketch_gemm(int64_t B, int K, int Dtot, const void *dA, int64_t a_stride
       K, Dtot, (const c128 *)dA, a_stride, so, mask, (c128 *)Y, tn,
       fuse ? (c128 *)W : nullptr);
   return lrz_launch_status("sketch_cgemm_kernel");
+}
+
+// complex128 batched GEMM without argument checks (opA 3 = conj, no transpose);
+// used by the step-parallel Woodbury chain (chain.cu)
+int lrz_zgemm_internal(int64_t batch, int M, int N, int Kd, int opA, const void *A, int64_t lda,
+                       int64_t sA, int opB, const void *Bm, int64_t ldb, int64_t sB, void *C,
+                       int64_t ldc, int64_t sC, cudaStream_t s) {
+  if (batch == 0) return LRZ_OK;
+  const int tm = ntiles(M), tn = ntiles(N);
+  cgemm_kernel<double, double, double, 16><<<unsigned(batch * tm * tn), GEMM_THREADS, 0, s>>>(
+      M, N, Kd, opA, (const c128 *)A, lda, sA, opB, (const c128 *)Bm, ldb, sB, (c128 *)C, ldc,
+      sC, nullptr, tm, tn);
+  return lrz_launch_status("cgemm_kernel (chain)");
 }
 
 extern "C" int lrz_cgemm(int dtype, int64_t batch, int M, int N, int Kd, int opA,

@@ -244,19 +244,23 @@ def woodbury(A: torch.Tensor | None, A_inv: torch.Tensor, U: torch.Tensor, V: to
     return A_out, A_inv_out, info
 
 
-def chain(plan, G, A_inv_prev, A_inv_seq, A_state, U, V, S, r, method, info):
-    """Per-trial sequential Woodbury chain over [B, T] steps (in place)."""
+def chain(plan, G, A_inv_prev, A_inv_seq, A_state, U, V, S, r, method, info,
+          steps: bool = False):
+    """Sequential Woodbury chain over [B, T] steps (in place): one CTA per trial,
+    or with ``steps`` the step-parallel form (products batched over trials)."""
     B, T = plan.shape
     K = A_inv_seq.shape[-1]
     D = U.shape[-2]
     dev = plan.device
     lib = N.lib_for(dev)
     ws = workspace(dev, lib.lrz_workspace_bytes(N.WS_CHAIN, N.C128, B, K, 0, D), "chain")
-    N.check(lib.lrz_chain(B, T, K, D, plan.data_ptr(), G.data_ptr(), A_inv_prev.data_ptr(),
-                          A_inv_seq.data_ptr(), N.ptr(A_state), U.data_ptr(), V.data_ptr(),
-                          S.data_ptr(), r.data_ptr(), method.data_ptr(), info.data_ptr(),
-                          ws.data_ptr(), N.stream_ptr(dev)), "lrz_chain")
-    _count(1)
+    fn = lib.lrz_chain_steps if steps else lib.lrz_chain
+    N.check(fn(B, T, K, D, plan.data_ptr(), G.data_ptr(), A_inv_prev.data_ptr(),
+               A_inv_seq.data_ptr(), N.ptr(A_state), U.data_ptr(), V.data_ptr(),
+               S.data_ptr(), r.data_ptr(), method.data_ptr(), info.data_ptr(),
+               ws.data_ptr(), N.stream_ptr(dev)), "lrz_chain")
+    # step-parallel: 2 GEMMs + core + apply + fallback per step
+    _count(5 * T if steps else 1)
 
 
 def precode_rate(H: torch.Tensor, A_inv: torch.Tensor, P_t: float, noise: torch.Tensor,

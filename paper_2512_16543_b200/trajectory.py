@@ -196,8 +196,10 @@ class TrajectoryRunner:
         # 6. sequential Woodbury recurrence per trial
         method = torch.zeros(B, T, dtype=torch.uint8, device=dev)
         e0 = self._ev()
+        # large K: the step-parallel chain (products batched over trials) when there
+        # are dispatcher steps; otherwise only A-state copies remain (CTA per trial)
         ops.chain(plan, G, self.A_inv, A_inv_seq, self.A if c.maintain_A else None, U, V, S,
-                  k_est, method, info)
+                  k_est, method, info, steps=(res is not None and K > 32))
         self._stage("chain", e0)
         # 7. precoder and rate
         e0 = self._ev()
