@@ -419,8 +419,9 @@ __global__ void __launch_bounds__(256)
                     const c128 *__restrict__ G, const c128 *__restrict__ prev_base,
                     int64_t prev_stride, c128 *__restrict__ Ainv_seq, c128 *__restrict__ A_state,
                     const c128 *__restrict__ U, const c128 *__restrict__ V,
-                    const double *__restrict__ S, const c128 *__restrict__ ws,
-                    const uint8_t *__restrict__ fb, uint8_t *__restrict__ method) {
+                    const double *__restrict__ S, const int32_t *__restrict__ r,
+                    const c128 *__restrict__ ws, const uint8_t *__restrict__ fb,
+                    uint8_t *__restrict__ method) {
   __shared__ c128 Ts[8][WBA_TILE + 1], Ws[8][WBA_TILE + 1];
   const int nt = (K + WBA_TILE - 1) / WBA_TILE, ntile = nt * nt;
   const int64_t b = blockIdx.x / ntile;
@@ -458,6 +459,7 @@ __global__ void __launch_bounds__(256)
   const c128 *Tm = w + int64_t(K) * D, *VhAi = w + 2 * int64_t(K) * D;
   const c128 *Ub = U + bt * int64_t(D) * K, *Vb = V + bt * int64_t(D) * K;
   const double *Sb = S + bt * D;
+  const int rr = r[bt];  // factor columns beyond the rank do not enter A (lowrank.py:220)
   // rows I*32 + ty + 8 q of the tile, column col: acc over the D factor columns
   c128 acc[4], accA[4];
 #pragma unroll
@@ -484,8 +486,8 @@ __global__ void __launch_bounds__(256)
         const int j = j0 + ty;
         const int row = I * WBA_TILE + tx;
         // U S (rows) and V (cols): A += (U S) V^H (lowrank.py:220)
-        Ts[ty][tx] = (j < D && row < K) ? cscale(Ub[int64_t(j) * K + row], Sb[j])
-                                       : czero<double>();
+        Ts[ty][tx] = (j < rr && row < K) ? cscale(Ub[int64_t(j) * K + row], Sb[j])
+                                        : czero<double>();
         Ws[ty][tx] = (j < D && col < K) ? Vb[int64_t(j) * K + col] : czero<double>();
       }
       __syncthreads();
@@ -870,7 +872,7 @@ extern "C" int lrz_chain_steps(int64_t B, int T, int K, int d_max, const uint8_t
                                                             method, info);
       wb_apply_kernel<<<unsigned(B * nt * nt), 256, 0, st>>>(
           T, t, K, d_max, plan, (const c128 *)G, prev, pst, (c128 *)A_inv_seq, (c128 *)A_state,
-          (const c128 *)U, (const c128 *)V, S, ws, fb, method);
+          (const c128 *)U, (const c128 *)V, S, r, ws, fb, method);
       wb_fallback_kernel<<<unsigned(B), INV_THREADS, smf, st>>>(T, t, K, plan, (const c128 *)G,
                                                                 (c128 *)A_inv_seq, fb, method,
                                                                 info);

@@ -248,6 +248,11 @@ def chain(plan, G, A_inv_prev, A_inv_seq, A_state, U, V, S, r, method, info,
           steps: bool = False):
     """Sequential Woodbury chain over [B, T] steps (in place): one CTA per trial,
     or with ``steps`` the step-parallel form (products batched over trials)."""
+    for t_, n_ in ((plan, "plan"), (G, "G"), (A_inv_prev, "A_inv_prev"), (A_inv_seq, "A_inv_seq"),
+                   (U, "U"), (V, "V"), (S, "S"), (r, "r"), (method, "method"), (info, "info")):
+        _chk(t_, n_)
+    if A_state is not None:
+        _chk(A_state, "A_state")
     B, T = plan.shape
     K = A_inv_seq.shape[-1]
     D = U.shape[-2]
