@@ -14,7 +14,7 @@
 //   U = Q J                       (lowrank.py:291)
 // All in complex128 / fp64 (the reference promotes c64 input here, D8).
 
-#include "common.cuh"
+#include "dmma.cuh"
 
 int lrz_sketch_gemm(int64_t B, int K, int Dtot, const void *dA, int64_t a_stride,
                     const double *omega, int64_t omega_stride, const int32_t *omega_row,
@@ -506,6 +506,69 @@ arsvd_seq_kernel(ArsvdArgs g, int T, const uint8_t *__restrict__ is_sketch,
 // ---------------------------------------------------------------------------
 constexpr int SCR_DMAX = 32;
 
+// Lower triangle of P^H P (d x d, d <= 32) for the K x d block P (row stride
+// ld) on the FP64 tensor pipe, one warp: lane (g, t) loads P[k0 + t][8a + g],
+// which is at once the (conjugated) A fragment of row block a and the B
+// fragment of column block a, so NB (NB + 1) / 2 lower 8 x 8 tiles need no
+// shared memory; written to L (row stride LD).  Replaces K-long per-entry dot
+// products that were ~45 % of the screen's stall samples.
+template <int NB, int IB0, int IB1>
+LRZ_DEV void warp_gram_dmma_nb(const c128 *P, int64_t ld, int K, int d, c128 *L, int LD) {
+  // row blocks IB0 <= ib < IB1 (all jb <= ib); plain loads: P may have been
+  // written earlier in this kernel by other lanes (the tail's X)
+  constexpr int NT = (IB1 * (IB1 + 1) - IB0 * (IB0 + 1)) / 2;
+  const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+  double cr[NT][2], ci[NT][2];
+#pragma unroll
+  for (int x = 0; x < NT; ++x) cr[x][0] = cr[x][1] = ci[x][0] = ci[x][1] = 0.0;
+  for (int k0 = 0; k0 < K; k0 += 4) {
+    const int k = k0 + t;
+    double xr[IB1], xi[IB1];
+#pragma unroll
+    for (int a = 0; a < IB1; ++a) {
+      const int col = 8 * a + g;
+      const c128 v = (k < K && col < d) ? P[int64_t(k) * ld + col] : czero<double>();
+      xr[a] = v.re;
+      xi[a] = v.im;
+    }
+#pragma unroll
+    for (int ib = IB0; ib < IB1; ++ib)
+#pragma unroll
+      for (int jb = 0; jb <= ib; ++jb) {
+        const int x = (ib * (ib + 1) - IB0 * (IB0 + 1)) / 2 + jb;
+        // conj(p_i) p_j = (pr_i pr_j + pi_i pi_j) + i (pr_i pi_j - pi_i pr_j)
+        dmma(cr[x], xr[ib], xr[jb]);
+        dmma(cr[x], xi[ib], xi[jb]);
+        dmma(ci[x], xr[ib], xi[jb]);
+        dmma(ci[x], -xi[ib], xr[jb]);
+      }
+  }
+#pragma unroll
+  for (int ib = IB0; ib < IB1; ++ib)
+#pragma unroll
+    for (int jb = 0; jb <= ib; ++jb) {
+      const int x = (ib * (ib + 1) - IB0 * (IB0 + 1)) / 2 + jb;
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int row = 8 * ib + g, col = 8 * jb + 2 * t + e;
+        if (row < d && col <= row) L[row * LD + col] = mk<double>(cr[x][e], ci[x][e]);
+      }
+    }
+}
+
+LRZ_DEV void warp_gram_dmma(const c128 *P, int64_t ld, int K, int d, c128 *L, int LD) {
+  switch ((d + 7) / 8) {
+    case 1: warp_gram_dmma_nb<1, 0, 1>(P, ld, K, d, L, LD); break;
+    case 2: warp_gram_dmma_nb<2, 0, 2>(P, ld, K, d, L, LD); break;
+    case 3: warp_gram_dmma_nb<3, 0, 3>(P, ld, K, d, L, LD); break;
+    default:  // 10 tiles in two passes (register budget of the 4-CTA/SM screen)
+      warp_gram_dmma_nb<4, 0, 3>(P, ld, K, d, L, LD);
+      warp_gram_dmma_nb<4, 3, 4>(P, ld, K, d, L, LD);
+      break;
+  }
+}
+
+
 
 // X row k = W row k L^-H (forward substitution, d = DD columns in registers);
 // returns ||x||^2 and stores the row (stride 1) to xo.
@@ -650,17 +713,8 @@ __global__ void __launch_bounds__(128, 4) arsvd_screen_kernel(ArsvdArgs g, int64
     const int d = min(k0 + g.p, K);
     used += int64_t(2) * K * d;
     const bool last = (it == g.i_max - 1);
-    // G = Y_i^H Y_i (lower triangle)
-    const int ne = d * (d + 1) / 2;
-    for (int e = lane; e < ne; e += 32) {
-      int a = int((sqrtf(8.0f * e + 1.0f) - 1.0f) * 0.5f);
-      while ((a + 1) * (a + 2) / 2 <= e) ++a;
-      while (a * (a + 1) / 2 > e) --a;
-      const int b = e - a * (a + 1) / 2;
-      c128 s = czero<double>();
-      for (int k = 0; k < K; ++k) cfma_ca(s, Y[int64_t(k) * Dtot + o + a], Y[int64_t(k) * Dtot + o + b]);
-      L[a * LD + b] = s;
-    }
+    // G = Y_i^H Y_i (lower triangle), DMMA
+    warp_gram_dmma(Y + o, Dtot, K, d, L, LD);
     __syncwarp();
     // Cholesky G = L L^H, warp-synchronous
     bool ok = true;
@@ -715,16 +769,8 @@ __global__ void __launch_bounds__(128, 4) arsvd_screen_kernel(ArsvdArgs g, int64
       }
       if (g.want == 0 && 2 * d > K && kap2 < 1e4) {
         // tail: certify sigma_min(B)^2 = lambda_min(X^H X) >= 1e-6 tr(X^H X)
-        for (int e = lane; e < d * (d + 1) / 2; e += 32) {
-          int a = int((sqrtf(8.0f * e + 1.0f) - 1.0f) * 0.5f);
-          while ((a + 1) * (a + 2) / 2 <= e) ++a;
-          while (a * (a + 1) / 2 > e) --a;
-          const int b = e - a * (a + 1) / 2;
-          c128 s = czero<double>();
-          for (int k = 0; k < K; ++k)
-            cfma_ca(s, X[int64_t(k) * SCR_DMAX + a], X[int64_t(k) * SCR_DMAX + b]);
-          L[a * LD + b] = s;
-        }
+        __syncwarp();  // X rows were written by other lanes
+        warp_gram_dmma(X, SCR_DMAX, K, d, L, LD);
         __syncwarp();
         bool ok2 = true;
         for (int jj = 0; jj < d; ++jj) {
