@@ -9,7 +9,7 @@
 
 #include <stdlib.h>
 
-#include "common.cuh"
+#include "dmma.cuh"
 
 
 namespace lrz {
@@ -663,6 +663,103 @@ __global__ void __launch_bounds__(GEMM_THREADS)
   }
 }
 
+
+// Y = dA Omega_all and W = dA Y for K <= 32 on the FP64 tensor pipe: one CTA
+// (4 warps) per (item, 32-column tile); the Omega tile is staged from the
+// normal window (same addressing as sketch_cgemm_kernel) into re / im planes
+// with a row stride of 36 doubles (conflict-free B fragments); warp w owns rows
+// 8w..8w+7 with its dA A fragments in registers; the Y tile goes to global
+// memory and to shared memory as the B operand of W = dA Y.
+constexpr int SD_LD = 36;
+
+__global__ void __launch_bounds__(128)
+    sketch_dmma_kernel(int K, int Dtot, const c128 *__restrict__ A, int64_t sA, SketchOperand so,
+                       const uint8_t *__restrict__ mask, c128 *__restrict__ C, int tiles_n,
+                       c128 *__restrict__ W) {
+  __shared__ __align__(16) double Pr[32 * SD_LD], Pi[32 * SD_LD];
+  __shared__ int s_off[32], s_d[32], s_j[32];
+  const int64_t item = blockIdx.x / tiles_n;
+  if (mask && !mask[item]) return;
+  const int J = int(blockIdx.x % tiles_n);
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5, g = lane >> 2, t = lane & 3;
+  const c128 *a = A + item * sA;
+  const int64_t row = so.orow ? int64_t(so.orow[item]) : item / so.orow_div;
+  const double *z = so.omega + row * so.os + (so.cursor ? so.cursor[item] : 0);
+  if (tid < 32) {
+    const int gn = J * 32 + tid;
+    int o = 0, k0 = so.k_init, d = min(k0 + so.p, K), off = 0;
+    while (gn >= o + d && gn < Dtot) {
+      o += d;
+      off += 2 * K * d;
+      k0 *= 2;
+      d = min(k0 + so.p, K);
+    }
+    s_off[tid] = off;
+    s_d[tid] = d;
+    s_j[tid] = gn - o;
+  }
+  // dA fragments of this warp's rows (A[8w + g][4c + t])
+  double ar[8], ai[8];
+  {
+    const int r = 8 * w + g;
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      const int k = 4 * c + t;
+      const c128 v = (r < K && k < K) ? ldg_c(a + int64_t(r) * K + k) : czero<double>();
+      ar[c] = v.re;
+      ai[c] = v.im;
+    }
+  }
+  __syncthreads();
+  const double SQH = 0.7071067811865476;
+  for (int e = tid; e < 32 * 32; e += 128) {
+    const int k = e >> 5, n = e & 31, gn = J * 32 + n;
+    double vr = 0.0, vi = 0.0;
+    if (gn < Dtot && k < K) {
+      const int d = s_d[n];
+      const double *zb = z + s_off[n] + int64_t(k) * d + s_j[n];
+      vr = SQH * zb[0];
+      vi = SQH * zb[int64_t(K) * d];
+    }
+    Pr[k * SD_LD + n] = vr;
+    Pi[k * SD_LD + n] = vi;
+  }
+  __syncthreads();
+  for (int pass = 0; pass < (W ? 2 : 1); ++pass) {
+    double cr[4][2], ci[4][2];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) cr[j][0] = cr[j][1] = ci[j][0] = ci[j][1] = 0.0;
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      const double xr = ar[c], xi = ai[c], nxi = -ai[c];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const double br = Pr[(4 * c + t) * SD_LD + 8 * j + g];
+        const double bi = Pi[(4 * c + t) * SD_LD + 8 * j + g];
+        dmma(cr[j], xr, br);  // (xr + i xi)(br + i bi)
+        dmma(cr[j], nxi, bi);
+        dmma(ci[j], xr, bi);
+        dmma(ci[j], xi, br);
+      }
+    }
+    __syncthreads();  // every warp is done reading the B planes
+    c128 *out = (pass == 0 ? C : W) + item * int64_t(K) * Dtot;
+    const int r = 8 * w + g;
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int cl = 8 * j + 2 * t + e, col = J * 32 + cl;
+        if (r < K && col < Dtot) out[int64_t(r) * Dtot + col] = mk<double>(cr[j][e], ci[j][e]);
+        if (pass == 0) {  // Y tile -> B planes for W = dA Y (rows >= K are zero)
+          Pr[r * SD_LD + cl] = cr[j][e];
+          Pi[r * SD_LD + cl] = ci[j][e];
+        }
+      }
+    __syncthreads();
+  }
+}
+
 // ---------------------------------------------------------------------------
 // K6 precoder W = H^H A^-1, one item per CTA, K <= 32, 256 threads (2 CTAs/SM).
 // Thread (rg, cg): rows {rg, rg + 64} of each 128-row block, columns
@@ -867,6 +964,11 @@ int lrz_sketch_gemm(int64_t B, int K, int Dtot, const void *dA, int64_t a_stride
   const int tn = (Dtot + TM - 1) / TM, tm = (K + TM - 1) / TM;
   SketchOperand so{omega, omega_stride, omega_row, orow_div, cursor, k_init, p};
   const bool fuse = W != nullptr && K <= TM;
+  if (fuse && use_dmma()) {
+    sketch_dmma_kernel<<<unsigned(B * tn), 128, 0, (cudaStream_t)stream>>>(
+        K, Dtot, (const c128 *)dA, a_stride, so, mask, (c128 *)Y, tn, (c128 *)W);
+    return lrz_launch_status("sketch_dmma_kernel");
+  }
   const size_t sm = fuse ? 2 * size_t(TM) * (TM + 1) * sizeof(c128) : 0;
   if (fuse)
     cudaFuncSetAttribute(sketch_cgemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
