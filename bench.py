@@ -340,7 +340,8 @@ def stage_model(spec, T, B, k_mean, iters_hist, wb_steps):
     m["gram"] = (4 * K * (K + 1) * N * BT, (K * N * c + K * K * 16) * BT)
     # difference form G_t - G_{t-1} of the fp64 Grams (TrajectoryConfig.delta "auto":
     # the DMMA Grams accumulate in fp64 for both dtypes)
-    m["gram_delta"] = (2 * K * K * n_sk, 3 * K * K * 16 * n_sk)
+    # (each Gram is read once as G_t and once as G_{t-1}: compulsory = one read + dA out)
+    m["gram_delta"] = (2 * K * K * n_sk, 2 * K * K * 16 * n_sk)
     widths = []
     k0 = spec.k_init
     for _ in range(spec.i_max):

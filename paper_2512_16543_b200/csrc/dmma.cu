@@ -182,17 +182,23 @@ __global__ void __launch_bounds__(32 * GD_WARPS)
 //   SINR_n = |s C_nn|^2 / (sum_{i != n} |s C_ni|^2 + noise_n), rates, sum.
 // A^-1 is staged once in shared memory as separate re / im planes with a row
 // stride of 36 doubles (the B-fragment loads A^-1[4c + t][8kb + g] are then
-// bank-conflict free).  Warp w computes 16-row slabs n0 = 16 (w + 4 j) of W:
-// lane (g, t) loads conj(H)[4c + t][n0 + 8 nb + g] straight from global
-// memory as the A fragment (a warp load touches 4 rows x 128 contiguous
-// bytes), 2 x 4 complex 8 x 8 accumulator tiles per slab, written as
-// 32-byte row segments.
+// bank-conflict free).  Warp w computes 8-row slabs n0 = 8 (w + 4 j) of W:
+// lane (g, t) loads conj(H)[4c + t][n0 + g] straight from global memory as
+// the A fragment (a warp load touches 4 rows x 128 contiguous bytes), 4
+// complex 8 x 8 accumulator tiles per slab, written as 32-byte row segments.
+// One block per slab (rather than two) keeps the kernel at <= 80 registers, so
+// 6-8 CTAs per SM hide the H loads (1.16 -> 1.03 ms at C2 c128).
 // ---------------------------------------------------------------------------
 constexpr int PD_WARPS = 4;
+constexpr int PD_NB = 1;    // 8-row n-blocks per warp slab
+// CTAs per SM (register budget): one 8-row block per slab keeps the kernel at
+// <= 80 registers; complex64 (half the H bytes per fragment) fits 8 CTAs
+template <typename T>
+constexpr int pd_minb() { return sizeof(T) == 8 ? 6 : 8; }
 constexpr int PD_LD = 36;
 
 template <typename T>
-__global__ void __launch_bounds__(32 * PD_WARPS, 3)
+__global__ void __launch_bounds__(32 * PD_WARPS, pd_minb<T>())
     precode_dmma32_kernel(int K, int N, const cplx<T> *__restrict__ H, int64_t hs,
                           const c128 *__restrict__ Ainv, int64_t ais,
                           const c128 *__restrict__ Gt, int64_t gs, double alpha, double P_t,
@@ -215,20 +221,20 @@ __global__ void __launch_bounds__(32 * PD_WARPS, 3)
   const cplx<T> *h = H + item * hs;
   cplx<T> *wo = W + item * wst;
   double nrm = 0.0;
-  const int nslab = (N + 15) / 16;
+  const int nslab = (N + 8 * PD_NB - 1) / (8 * PD_NB);
   for (int sl = w; sl < nslab; sl += PD_WARPS) {
-    const int n0 = 16 * sl;
-    c128 hv[8][2];
+    const int n0 = 8 * PD_NB * sl;
+    c128 hv[8][PD_NB];
 #pragma unroll
     for (int c = 0; c < 8; ++c)
 #pragma unroll
-      for (int nb = 0; nb < 2; ++nb) {
+      for (int nb = 0; nb < PD_NB; ++nb) {
         const int i = 4 * c + t, n = n0 + 8 * nb + g;
         hv[c][nb] = (i < K && n < N) ? ldg_c(h + int64_t(i) * N + n) : czero<double>();
       }
-    double acr[2][4][2], aci[2][4][2];
+    double acr[PD_NB][4][2], aci[PD_NB][4][2];
 #pragma unroll
-    for (int nb = 0; nb < 2; ++nb)
+    for (int nb = 0; nb < PD_NB; ++nb)
 #pragma unroll
       for (int kb = 0; kb < 4; ++kb) acr[nb][kb][0] = acr[nb][kb][1] = aci[nb][kb][0] =
           aci[nb][kb][1] = 0.0;
@@ -239,7 +245,7 @@ __global__ void __launch_bounds__(32 * PD_WARPS, 3)
         const double br = Sr[(4 * c + t) * PD_LD + 8 * kb + g];
         const double bi = Si[(4 * c + t) * PD_LD + 8 * kb + g];
 #pragma unroll
-        for (int nb = 0; nb < 2; ++nb) {
+        for (int nb = 0; nb < PD_NB; ++nb) {
           const double hr = hv[c][nb].re, hi = hv[c][nb].im;
           // conj(h) b = (hr br + hi bi) + i (hr bi - hi br)
           dmma(acr[nb][kb], hr, br);
@@ -250,7 +256,7 @@ __global__ void __launch_bounds__(32 * PD_WARPS, 3)
       }
     }
 #pragma unroll
-    for (int nb = 0; nb < 2; ++nb) {
+    for (int nb = 0; nb < PD_NB; ++nb) {
       const int n = n0 + 8 * nb + g;
       if (n < N) {
 #pragma unroll
