@@ -544,39 +544,69 @@ __global__ void spec_verify_kernel(int64_t B, int T, int K, ConsumedTab consumed
                                    const int32_t *iters_act, int64_t *cursor,
                                    const int64_t *cursor0, int32_t *first_unverified,
                                    uint8_t *active, int32_t *pending) {
-  const int64_t b = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  // one warp per trial: ballots find the first mispredicted step, a warp scan
+  // rebuilds the cursors (32 steps per iteration instead of one)
+  const int lane = threadIdx.x & 31;
+  const int64_t b = blockIdx.x * int64_t(blockDim.x >> 5) + (threadIdx.x >> 5);
   if (b >= B) return;
-  int t = first_unverified[b];
   const int64_t base = b * T;
-  // accept the verified prefix (init mode, iters_act == NULL: nothing to accept)
-  while (iters_act && t < T) {
-    const int64_t bt = base + t;
-    if (!is_sketch[bt]) {
-      ++t;
-      continue;
+  int t = first_unverified[b];
+  if (iters_act) {
+    // accept the verified prefix: the first sketch step s >= t whose observed
+    // iteration count differs from the prediction is corrected and ends it
+    int hit = T;
+    for (int s0 = t; s0 < T && hit == T; s0 += 32) {
+      const int s = s0 + lane;
+      bool bad = false;
+      if (s < T && is_sketch[base + s]) {
+        const int pa = max(iters_act[base + s], 0);  // -1 = window overflow (host)
+        bad = pa != iters_pred[base + s];
+      }
+      const unsigned m = __ballot_sync(0xffffffffu, bad);
+      if (m) hit = s0 + __ffs(m) - 1;
     }
-    const int pa = max(iters_act[bt], 0);  // -1 = window overflow, reported by the host
-    if (pa == iters_pred[bt]) {
-      ++t;
-      continue;
+    if (hit < T) {
+      if (lane == 0) iters_pred[base + hit] = max(iters_act[base + hit], 0);
+      t = hit + 1;
+    } else {
+      t = T;
     }
-    iters_pred[bt] = pa;  // cursor was right -> result right; consumption differs
-    ++t;
-    break;
+    __syncwarp();
   }
   // skip trailing non-sketch steps
-  while (t < T && !is_sketch[base + t]) ++t;
-  first_unverified[b] = t;
-  // re-predict the unverified suffix from the last observation and recompute cursors
-  int64_t c = cursor0[b];
-  for (int s = 0; s < T; ++s) {
-    const int64_t bt = base + s;
-    if (iters_act && s >= t && is_sketch[bt]) iters_pred[bt] = max(iters_act[bt], 0);
-    cursor[bt] = c;
-    active[bt] = (s >= t && is_sketch[bt]) ? 1 : 0;
-    if (is_sketch[bt]) c += consumed_tab.v[iters_pred[bt]];
+  for (int s0 = t; s0 < T; s0 += 32) {
+    const int s = s0 + lane;
+    const unsigned m = __ballot_sync(0xffffffffu, s < T && is_sketch[base + s]);
+    if (m) {
+      t = s0 + __ffs(m) - 1;
+      break;
+    }
+    t = min(s0 + 32, T);
   }
-  if (t < T) atomicAdd(pending, 1);
+  if (lane == 0) first_unverified[b] = t;
+  // re-predict the unverified suffix from the last observation and recompute cursors
+  int64_t carry = cursor0[b];
+  for (int s0 = 0; s0 < T; s0 += 32) {
+    const int s = s0 + lane;
+    int64_t inc = 0;
+    if (s < T) {
+      const int64_t bt = base + s;
+      const bool sk = is_sketch[bt];
+      if (iters_act && s >= t && sk) iters_pred[bt] = max(iters_act[bt], 0);
+      active[bt] = (s >= t && sk) ? 1 : 0;
+      if (sk) inc = consumed_tab.v[iters_pred[bt]];
+    }
+    // exclusive scan of inc over the lanes
+    int64_t x = inc;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int64_t y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    if (s < T) cursor[base + s] = carry + x - inc;
+    carry += __shfl_sync(0xffffffffu, x, 31);
+  }
+  if (lane == 0 && t < T) atomicAdd(pending, 1);
 }
 
 // Dispatcher decision per step (lowrank.py:345-359): 2 = none (k_est == 0),
@@ -901,7 +931,7 @@ extern "C" int lrz_spec_verify(int64_t B, int T, int K, const lrz_arsvd_cfg *cfg
     tab.v[i + 1] = tab.v[i] + 2LL * K * d;
     k0 *= 2;
   }
-  const unsigned nb = unsigned((B + 127) / 128);
+  const unsigned nb = unsigned((B + 3) / 4);  // one warp per trial
   spec_verify_kernel<<<nb, 128, 0, (cudaStream_t)stream>>>(B, T, K, tab, is_sketch, iters_pred,
                                                            iters_act, cursor, cursor0,
                                                            first_unverified, active, pending);
