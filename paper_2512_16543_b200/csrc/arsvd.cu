@@ -682,6 +682,16 @@ __global__ void __launch_bounds__(128, 4) arsvd_screen_kernel(ArsvdArgs g, int64
                                                            c128 *__restrict__ Xs,
                                                            int32_t *__restrict__ resume) {
   extern __shared__ __align__(16) char scr_smem[];
+  // (row, col) of the e-th entry of a lower triangle in row order, for the
+  // Cholesky trailing updates (replaces a sqrt + correction loops per entry)
+  __shared__ uint16_t s_tri[SCR_DMAX * (SCR_DMAX + 1) / 2];
+  for (int e = threadIdx.x; e < SCR_DMAX * (SCR_DMAX + 1) / 2; e += blockDim.x) {
+    int a = int((sqrtf(8.0f * e + 1.0f) - 1.0f) * 0.5f);
+    while ((a + 1) * (a + 2) / 2 <= e) ++a;
+    while (a * (a + 1) / 2 > e) --a;
+    s_tri[e] = uint16_t((a << 8) | (e - a * (a + 1) / 2));
+  }
+  __syncthreads();
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int64_t item = blockIdx.x * int64_t(blockDim.x >> 5) + wib;
   if (item >= B) return;
@@ -734,10 +744,7 @@ __global__ void __launch_bounds__(128, 4) arsvd_screen_kernel(ArsvdArgs g, int64
       __syncwarp();
       const int n = d - jj - 1, nt = n * (n + 1) / 2;
       for (int e = lane; e < nt; e += 32) {
-        int a = int((sqrtf(8.0f * e + 1.0f) - 1.0f) * 0.5f);
-        while ((a + 1) * (a + 2) / 2 <= e) ++a;
-        while (a * (a + 1) / 2 > e) --a;
-        const int b = e - a * (a + 1) / 2;
+        const int a = s_tri[e] >> 8, b = s_tri[e] & 0xff;
         const int ra = jj + 1 + a, rb = jj + 1 + b;  // rb <= ra
         const c128 x = L[ra * LD + jj], y = L[rb * LD + jj];
         c128 &t = L[ra * LD + rb];
@@ -786,10 +793,7 @@ __global__ void __launch_bounds__(128, 4) arsvd_screen_kernel(ArsvdArgs g, int64
           __syncwarp();
           const int n = d - jj - 1, nt = n * (n + 1) / 2;
           for (int e = lane; e < nt; e += 32) {
-            int a = int((sqrtf(8.0f * e + 1.0f) - 1.0f) * 0.5f);
-            while ((a + 1) * (a + 2) / 2 <= e) ++a;
-            while (a * (a + 1) / 2 > e) --a;
-            const int b = e - a * (a + 1) / 2;
+            const int a = s_tri[e] >> 8, b = s_tri[e] & 0xff;
             const int ra = jj + 1 + a, rb = jj + 1 + b;
             const c128 x = L[ra * LD + jj], y = L[rb * LD + jj];
             c128 &t = L[ra * LD + rb];
