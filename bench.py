@@ -368,7 +368,7 @@ def stage_model(spec, T, B, k_mean, iters_hist, wb_steps):
 
 # kernels (name fragment, launches per WB step) behind each bench stage
 STAGE_KERNELS = {
-    "arsvd": [("sketch_cgemm_kernel", 1), ("arsvd_screen_kernel", 1), ("arsvd_kernel", 1)],
+    "arsvd": [("sketch_dmma_kernel", 1), ("arsvd_screen_kernel", 1), ("arsvd_kernel", 1)],
     "gram": [("gram_dmma_kernel", 1)],
     "precode_rate": [("precode_dmma32_kernel", 1)],
     "inverse": [("herm_inverse_warp_kernel", 1), ("herm_inverse_kernel", 1)],
