@@ -60,7 +60,9 @@ int lrz_device_check(int device);
 
 /* K1  Gram + regularisation: A[i] = 0.5 (H H^H + (H H^H)^H) + alpha I.
  *     Replaces lowrank.py:160-162 (and :365-366).  H: [B][K][N] dtype,
- *     A: [B][K][K] complex128 (always: the reference promotes via alpha I). */
+ *     A: [B][K][K] complex128 (always: the reference promotes via alpha I).
+ *     Runs on the FP64 tensor pipe (DMMA) for both dtypes, complex64 H widened
+ *     to fp64 on load; exactly Hermitian output with a real diagonal. */
 int lrz_gram(int dtype, int64_t B, int K, int N, const void *H, int64_t h_stride,
              double alpha, void *A, int64_t a_stride, void *stream);
 
@@ -154,7 +156,8 @@ int lrz_plan(int64_t n, int K, const uint8_t *is_sketch, const int32_t *k_est, u
  *     W may be NULL (then kept in workspace).  info = ZERO_PRECODER if ||W||=0.
  *     G_true (nullable, complex128 [B][K][K]) = H H^H + alpha I of the same H:
  *     then H W is formed as G_true A^-1 - alpha A^-1 in K^3
- *     instead of K^2 N work. */
+ *     instead of K^2 N work; for K <= 32 W, ||W||, the coupling and the
+ *     SINR / rate reduction are one fused DMMA kernel. */
 int lrz_precode_rate(int dtype, int64_t B, int K, int N, const void *H, int64_t h_stride,
                      const void *A_inv, int64_t ai_stride, double P_t, const double *noise,
                      int64_t noise_div, void *W, int64_t w_stride, const void *G_true,
