@@ -294,6 +294,18 @@ int lrz_arsvd_seq(int64_t B, int T, int K, const void *dA, const double *omega,
                   int32_t *fallback, int64_t *consumed, int want_factor, void *workspace,
                   void *stream);
 
+/* Cursor walk (K <= 32, sketch widths <= 24): one warp per trial walks the
+ * steps t >= first_unverified[b] in order and fixes each sketch step's cursor
+ * and iteration count from the CholeskyQR energy total alone (a step's normal
+ * consumption depends only on its hit iteration, lowrank.py:284-300), without
+ * QR / SVD.  Writes cursor[b][t] and iters_pred[b][t]; stops at a step whose
+ * total is within the rounding bound of the target.  The factors are then
+ * computed by one speculative lrz_arsvd pass at these cursors. */
+int lrz_arsvd_walk(int64_t B, int T, int K, const void *dA, const double *omega,
+                   int64_t omega_stride, const lrz_arsvd_cfg *cfg, const uint8_t *is_sketch,
+                   const int32_t *first_unverified, int64_t *cursor, int32_t *iters_pred,
+                   void *stream);
+
 /* Speculative sketch-cursor resolution for the batched runner: one thread
  * per trial walks its T steps, accepts every step whose observed iteration
  * count matches the prediction, and re-predicts the suffix after the first

@@ -51,6 +51,8 @@ _SIGS = {
                             P, P, P, P, P, C.c_int, C.c_int, P, P]),
     "lrz_arsvd_seq": (C.c_int, [I64, C.c_int, C.c_int, P, P, I64, C.POINTER(ArsvdCfg), P, P, P,
                                 P, P, P, P, P, P, P, P, C.c_int, P, P]),
+    "lrz_arsvd_walk": (C.c_int, [I64, C.c_int, C.c_int, P, P, I64, C.POINTER(ArsvdCfg), P, P, P,
+                                 P, P]),
     "lrz_woodbury": (C.c_int, [I64, C.c_int, C.c_int, P, P, I64, P, P, P, P, P, P, P, P, P]),
     "lrz_chain": (C.c_int, [I64, C.c_int, C.c_int, C.c_int, P, P, P, P, P, P, P, P, P, P, P, P,
                             P]),

@@ -830,6 +830,204 @@ __global__ void __launch_bounds__(128, 4) arsvd_screen_kernel(ArsvdArgs g, int64
   }
 }
 
+
+// ---------------------------------------------------------------------------
+// Cursor walk (K <= 32, sketch widths <= 24).  In the reference the sketch
+// stream is consumed sequentially across steps, and a step's consumption is
+// fixed by its iteration count alone: iteration i hits iff cumsum(s^2) reaches
+// eta ||dA||^2 for some prefix, i.e. iff the total ||B_i||_F^2 = ||Q_i^H dA||_F^2
+// does (lowrank.py:289-300).  That total is what the CholeskyQR screen
+// computes, so one warp per trial can walk its steps in order with only the
+// sketch GEMMs (DMMA), the sketch Gram (DMMA), a warp Cholesky and the X rows
+// -- no QR / SVD -- and fix every step's cursor and iteration count.  The
+// exact factors are then computed for all steps in one batched speculative
+// pass at the now-known cursors.  A step whose total is within the CholeskyQR
+// error bound of the target (or ill-conditioned, or past the window) stops the
+// walk there; the verifier then finds the first misprediction and the in-order
+// exact path takes over from it.
+// ---------------------------------------------------------------------------
+constexpr int WK_LD = 33;   // row stride (complex) of the K x K / K x d shared tiles
+constexpr int WK_DMAX = 24;
+
+// C (K x NB*8) = A (K x K) B (K x NB*8), all complex128 in shared memory
+// (row strides WK_LD), K <= 32 (zero padded to 32), one warp on DMMA.
+template <int NB>
+LRZ_DEV void warp_zgemm_dmma(const c128 *A, const c128 *Bm, c128 *C) {
+  const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+  double cr[4][NB][2], ci[4][NB][2];
+#pragma unroll
+  for (int rb = 0; rb < 4; ++rb)
+#pragma unroll
+    for (int cb = 0; cb < NB; ++cb) cr[rb][cb][0] = cr[rb][cb][1] = ci[rb][cb][0] = ci[rb][cb][1] = 0.0;
+#pragma unroll
+  for (int c = 0; c < 8; ++c) {
+    double br[NB], bi[NB];
+#pragma unroll
+    for (int cb = 0; cb < NB; ++cb) {
+      const c128 v = Bm[(4 * c + t) * WK_LD + 8 * cb + g];
+      br[cb] = v.re;
+      bi[cb] = v.im;
+    }
+#pragma unroll
+    for (int rb = 0; rb < 4; ++rb) {
+      const c128 a = A[(8 * rb + g) * WK_LD + 4 * c + t];
+      const double nai = -a.im;
+#pragma unroll
+      for (int cb = 0; cb < NB; ++cb) {
+        dmma(cr[rb][cb], a.re, br[cb]);  // (ar + i ai)(br + i bi)
+        dmma(cr[rb][cb], nai, bi[cb]);
+        dmma(ci[rb][cb], a.re, bi[cb]);
+        dmma(ci[rb][cb], a.im, br[cb]);
+      }
+    }
+  }
+  __syncwarp();
+#pragma unroll
+  for (int rb = 0; rb < 4; ++rb)
+#pragma unroll
+    for (int cb = 0; cb < NB; ++cb)
+#pragma unroll
+      for (int e = 0; e < 2; ++e)
+        C[(8 * rb + g) * WK_LD + 8 * cb + 2 * t + e] = mk<double>(cr[rb][cb][e], ci[rb][cb][e]);
+  __syncwarp();
+}
+
+LRZ_DEV void warp_zgemm(const c128 *A, const c128 *Bm, c128 *C, int d) {
+  switch ((d + 7) / 8) {
+    case 1: warp_zgemm_dmma<1>(A, Bm, C); break;
+    case 2: warp_zgemm_dmma<2>(A, Bm, C); break;
+    default: warp_zgemm_dmma<3>(A, Bm, C); break;
+  }
+}
+
+// Warp Cholesky of the lower triangle of L (d x d, row stride LD) in place;
+// (lmin, lmax) of the diagonal of the factor.  False on a non-positive pivot.
+LRZ_DEV bool warp_chol_tri(c128 *L, int d, int LD, const uint16_t *tri, double &lmin,
+                           double &lmax) {
+  const int lane = threadIdx.x & 31;
+  lmin = 1e300;
+  lmax = 0.0;
+  for (int jj = 0; jj < d; ++jj) {
+    const double piv = L[jj * LD + jj].re;
+    if (!(piv > 0.0)) return false;
+    const double l = sqrt(piv), il = 1.0 / l;
+    lmin = fmin(lmin, l);
+    lmax = fmax(lmax, l);
+    __syncwarp();
+    for (int a = jj + 1 + lane; a < d; a += 32) L[a * LD + jj] = cscale(L[a * LD + jj], il);
+    if (lane == 0) L[jj * LD + jj] = mk<double>(l, 0.0);
+    __syncwarp();
+    const int n = d - jj - 1, nt = n * (n + 1) / 2;
+    for (int e = lane; e < nt; e += 32) {
+      const int a = tri[e] >> 8, b = tri[e] & 0xff;
+      const int ra = jj + 1 + a, rb = jj + 1 + b;
+      const c128 x = L[ra * LD + jj], y = L[rb * LD + jj];
+      c128 &t = L[ra * LD + rb];
+      t.re -= x.re * y.re + x.im * y.im;
+      t.im -= x.im * y.re - x.re * y.im;
+    }
+    __syncwarp();
+  }
+  return true;
+}
+
+__global__ void __launch_bounds__(32)
+    arsvd_walk_kernel(ArsvdArgs g, int T, const uint8_t *__restrict__ is_sketch,
+                      const int32_t *__restrict__ first, int64_t *__restrict__ cursor,
+                      int32_t *__restrict__ iters_pred) {
+  extern __shared__ __align__(16) char wk_smem[];
+  c128 *As = (c128 *)wk_smem;            // dA          [32][WK_LD]
+  c128 *Os = As + 32 * WK_LD;            // Omega_i     [32][WK_LD]
+  c128 *Ys = Os + 32 * WK_LD;            // Y = dA Omega
+  c128 *Ws = Ys + 32 * WK_LD;            // W = dA Y
+  c128 *L = Ws + 32 * WK_LD;             // [WK_DMAX][WK_DMAX + 1]
+  __shared__ uint16_t tri[WK_DMAX * (WK_DMAX + 1) / 2];
+  const int lane = threadIdx.x & 31;
+  for (int e = lane; e < WK_DMAX * (WK_DMAX + 1) / 2; e += 32) {
+    int a = int((sqrtf(8.0f * e + 1.0f) - 1.0f) * 0.5f);
+    while ((a + 1) * (a + 2) / 2 <= e) ++a;
+    while (a * (a + 1) / 2 > e) --a;
+    tri[e] = uint16_t((a << 8) | (e - a * (a + 1) / 2));
+  }
+  __syncwarp();
+  const int64_t b = blockIdx.x;
+  const int K = g.K, LDL = WK_DMAX + 1;
+  const double SQH = 0.7071067811865476;
+  const double *om = g.omega + b * g.os;
+  const double eta = g.eta_row ? g.eta_row[b] : g.eta;
+  int t = first[b];
+  if (t >= T) return;
+  int64_t cur = cursor[b * T + t];
+  for (; t < T; ++t) {
+    const int64_t bt = b * T + t;
+    cursor[bt] = cur;
+    if (!is_sketch[bt]) continue;
+    const c128 *dA = g.dA + bt * int64_t(K) * K;
+    double e2 = 0.0;
+    for (int e = lane; e < 32 * 32; e += 32) {
+      const int r = e >> 5, c = e & 31;
+      const c128 v = (r < K && c < K) ? dA[r * K + c] : czero<double>();
+      As[r * WK_LD + c] = v;
+      e2 += cabs2(v);
+    }
+    const double energy = warp_sum(e2);
+    __syncwarp();
+    if (energy == 0.0) {  // empty factor: no sketch drawn (lowrank.py:275-276)
+      if (lane == 0) iters_pred[bt] = 0;
+      continue;
+    }
+    const double target = eta * energy;
+    int k0 = g.k_init, iters = -1;
+    int64_t used = 0;
+    bool undecided = false;
+    for (int it = 0; it < g.i_max; ++it) {
+      const int d = min(k0 + g.p, K);
+      if (g.omega_len > 0 && cur + used + int64_t(2) * K * d > g.omega_len) {
+        undecided = true;  // the exact path reports the short window
+        break;
+      }
+      const double *zre = om + cur + used, *zim = zre + int64_t(K) * d;
+      for (int e = lane; e < 32 * 24; e += 32) {
+        const int r = e / 24, c = e - r * 24;
+        Os[r * WK_LD + c] = (r < K && c < d)
+                                ? mk<double>(SQH * zre[r * d + c], SQH * zim[r * d + c])
+                                : czero<double>();
+      }
+      __syncwarp();
+      warp_zgemm(As, Os, Ys, d);   // Y = dA Omega (lowrank.py:288)
+      warp_zgemm(As, Ys, Ws, d);   // W = dA Y = (Q^H dA)^H L^H-scaled
+      warp_gram_dmma(Ys, WK_LD, K, d, L, LDL);
+      __syncwarp();
+      double lmin, lmax;
+      const bool ok = warp_chol_tri(L, d, LDL, tri, lmin, lmax);
+      const double kap2 = ok ? (lmax / lmin) * (lmax / lmin) : 1e300;
+      if (!ok || kap2 > 1e8) {
+        undecided = true;
+        break;
+      }
+      double loc = 0.0;
+      for (int k = lane; k < K; k += 32) loc += scr_xrow_d(d, Ws + k * WK_LD, L, LDL, nullptr);
+      const double mf = warp_sum(loc);
+      const double tol = 64.0 * d * EPS64 * kap2 + 1e-12;
+      used += int64_t(2) * K * d;
+      if (mf < target * (1.0 - tol)) {  // certainly no hit: next, wider sketch
+        k0 *= 2;
+        continue;
+      }
+      if (mf > target * (1.0 + tol)) {  // certainly a hit at this iteration
+        iters = it + 1;
+        break;
+      }
+      undecided = true;  // within the rounding bound of the target
+      break;
+    }
+    if (undecided) return;  // later predictions stay; the verifier finds the first miss
+    if (iters < 0) iters = g.i_max;  // iteration cap: all sketches drawn
+    if (lane == 0) iters_pred[bt] = iters;
+    cur += used;
+  }
+}
+
 }  // namespace lrz
 
 using namespace lrz;
@@ -1000,4 +1198,49 @@ extern "C" int lrz_arsvd_seq(int64_t B, int T, int K, const void *dA, const doub
   arsvd_seq_kernel<<<unsigned(B), ARSVD_THREADS, 0, (cudaStream_t)stream>>>(
       g, T, is_sketch, first_unverified, cursor, iters_pred);
   return lrz_launch_status("lrz_arsvd_seq");
+}
+
+extern "C" int lrz_arsvd_walk(int64_t B, int T, int K, const void *dA, const double *omega,
+                              int64_t omega_stride, const lrz_arsvd_cfg *cfg,
+                              const uint8_t *is_sketch, const int32_t *first_unverified,
+                              int64_t *cursor, int32_t *iters_pred, void *stream) {
+  if (B < 0 || T < 1 || K < 1 || K > 32 || !dA || !omega || !cfg || !is_sketch ||
+      !first_unverified || !cursor || !iters_pred) {
+    lrz_set_error("lrz_arsvd_walk: bad arguments (K <= 32)");
+    return LRZ_EINVAL;
+  }
+  long long kk = cfg->k_init;
+  for (int i = 0; i < cfg->i_max; ++i) {
+    if (std::min<long long>(kk + cfg->p, K) > WK_DMAX) {
+      lrz_set_error("lrz_arsvd_walk: sketch widths must be <= %d", WK_DMAX);
+      return LRZ_EINVAL;
+    }
+    kk *= 2;
+  }
+  if (B == 0) return LRZ_OK;
+  ArsvdArgs g{};
+  g.K = K;
+  g.dA = (const c128 *)dA;
+  g.as = int64_t(K) * K;
+  g.omega = omega;
+  g.os = omega_stride;
+  g.orow = nullptr;
+  g.orow_div = T;
+  g.eta = cfg->eta;
+  g.eta_row = cfg->eta_row;
+  g.omega_len = cfg->omega_len;
+  g.k_init = cfg->k_init;
+  g.p = cfg->p;
+  g.i_max = cfg->i_max;
+  g.D = cfg->d_max;
+  const size_t sm = (4 * 32 * WK_LD + WK_DMAX * (WK_DMAX + 1)) * sizeof(c128);
+  if (cudaFuncSetAttribute(arsvd_walk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           int(sm)) != cudaSuccess) {
+    lrz_set_error("lrz_arsvd_walk: cannot reserve %zu bytes of shared memory", sm);
+    return LRZ_ELAUNCH;
+  }
+  arsvd_walk_kernel<<<unsigned(B), 32, sm, (cudaStream_t)stream>>>(g, T, is_sketch,
+                                                                   first_unverified, cursor,
+                                                                   iters_pred);
+  return lrz_launch_status("lrz_arsvd_walk");
 }

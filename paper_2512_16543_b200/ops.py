@@ -225,6 +225,38 @@ def arsvd_seq(dA: torch.Tensor, omega: torch.Tensor, is_sketch: torch.Tensor,
     return out
 
 
+def arsvd_walk(dA: torch.Tensor, omega: torch.Tensor, is_sketch: torch.Tensor,
+               first_unverified: torch.Tensor, cursor: torch.Tensor, iters_pred: torch.Tensor,
+               eta, k_init: int, p: int, i_max: int) -> None:
+    """Cursor walk (K <= 32): cursors and iteration counts of each trial's steps
+    from first_unverified on, in order, from the CholeskyQR energy screen alone.
+    dA [B,T,K,K]; omega [B,L]; cursor [B,T] i64 and iters_pred [B,T] i32 (in/out)."""
+    _chk(dA, "dA")
+    B, T, K = dA.shape[0], dA.shape[1], dA.shape[-1]
+    D = d_max_for(K, k_init, p, i_max)
+    cfg = _arsvd_cfg(eta, k_init, p, i_max, D, omega.shape[1])
+    lib = N.lib_for(dA.device)
+    N.check(lib.lrz_arsvd_walk(B, T, K, dA.data_ptr(), omega.data_ptr(), omega.stride(0),
+                               C.byref(cfg), _chk(is_sketch, "is_sketch").data_ptr(),
+                               _chk(first_unverified, "first_unverified").data_ptr(),
+                               _chk(cursor, "cursor").data_ptr(),
+                               _chk(iters_pred, "iters_pred").data_ptr(),
+                               N.stream_ptr(dA.device)), "lrz_arsvd_walk")
+    _count(1)
+
+
+def walk_ok(K: int, k_init: int, p: int, i_max: int) -> bool:
+    """lrz_arsvd_walk's limits: K <= 32, every sketch width <= 24."""
+    if K > 32:
+        return False
+    k0 = k_init
+    for _ in range(i_max):
+        if min(k0 + p, K) > 24:
+            return False
+        k0 *= 2
+    return True
+
+
 def woodbury(A: torch.Tensor | None, A_inv: torch.Tensor, U: torch.Tensor, V: torch.Tensor,
              S: torch.Tensor, r: torch.Tensor):
     """K4 over a batch: returns (A_out or None, A_inv_out, info)."""

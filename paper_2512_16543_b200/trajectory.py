@@ -60,6 +60,10 @@ class TrajectoryConfig:
     # diff when the Grams are fp64-accumulated (complex128, or complex64 on the
     # FP64 tensor pipe), formula otherwise (complex64 FP32 Grams)
     delta: str = "auto"
+    # resolve the sketch cursors with the energy-screen walk (lrz_arsvd_walk, K <= 32)
+    # before the first speculative pass -- for workloads whose iteration counts
+    # follow the sketch (the LEO campaign's eta = 0.65-0.9, p = 1)
+    walk_first: bool = False
 
 
 @dataclass
@@ -124,6 +128,7 @@ class TrajectoryRunner:
             self._eta = torch.from_numpy(e).to(self.device)
         self.prof = None          # list of (stage, start_event, end_event) when profiling
         self._in_order = False    # set once a chunk needed the in-order arSVD
+        self._walk_first = False  # set once a chunk needed the cursor walk
 
     def _ev(self):
         if self.prof is None:
@@ -197,7 +202,8 @@ class TrajectoryRunner:
         method = torch.zeros(B, T, dtype=torch.uint8, device=dev)
         e0 = self._ev()
         # large K: the step-parallel chain (products batched over trials) when there
-        # are dispatcher steps; otherwise only A-state copies remain (CTA per trial)
+        # are dispatcher steps (measured slower at K = 32: launch bound); otherwise
+        # one CTA per trial
         ops.chain(plan, G, self.A_inv, A_inv_seq, self.A if c.maintain_A else None, U, V, S,
                   k_est, method, info, steps=(res is not None and K > 32))
         self._stage("chain", e0)
@@ -301,6 +307,18 @@ class TrajectoryRunner:
                 consumed=torch.zeros(BT, dtype=torch.int64, device=dev),
             )
             n_spec = 0 if self._in_order else c.spec_passes
+            # cursor walk (K <= 32): resolves every step's cursor from the energy
+            # screen alone, in order, so one more speculative pass settles the chunk
+            can_walk = sync and ops.walk_ok(K, c.k_init, c.p, c.i_max)
+
+            def walk():
+                e0 = self._ev()
+                ops.arsvd_walk(dA, omega, is_sketch, first, cursor, iters_pred, self._eta,
+                               c.k_init, c.p, c.i_max)
+                pending.zero_()
+                ops.spec_verify(is_sketch, iters_pred, None, cursor, cursor0, first, active,
+                                pending, K, self._eta, c.k_init, c.p, c.i_max)
+                self._stage("walk", e0)
 
             def one_pass():
                 e0 = self._ev()
@@ -325,6 +343,10 @@ class TrajectoryRunner:
 
             flags = torch.zeros(2, dtype=torch.int32, device=dev)
             A_state0 = self.A.clone() if (c.maintain_A and sync) else None
+            walked = False
+            if can_walk and (self._walk_first or c.walk_first):
+                walk()          # the last chunk's iteration counts followed the sketch
+                walked = True
             one_pass()
             passes = 1
             # optimistic: the rest of the chunk is queued behind the first pass and
@@ -340,6 +362,10 @@ class TrajectoryRunner:
                     raise RuntimeError("sketch window shorter than an arsvd call needed")
                 if int(pinned[0]):
                     while True:
+                        if can_walk and not walked:
+                            walk()
+                            walked = True
+                            self._walk_first = True
                         one_pass()
                         passes += 1
                         pinned.copy_(flags, non_blocking=True)
