@@ -711,27 +711,34 @@ __global__ void __launch_bounds__(128)
     }
   }
   __syncthreads();
+  // Omega tile straight from the window into the planes with cp.async (all
+  // 16 loads per thread in flight at once; zero fill outside the tile); the
+  // sqrt(1/2) of lowrank.py:284-286 is applied to dA in the first pass instead
   const double SQH = 0.7071067811865476;
   for (int e = tid; e < 32 * 32; e += 128) {
     const int k = e >> 5, n = e & 31, gn = J * 32 + n;
-    double vr = 0.0, vi = 0.0;
-    if (gn < Dtot && k < K) {
+    const bool ok = gn < Dtot && k < K;
+    const double *zb = z;
+    int64_t im_off = 0;
+    if (ok) {
       const int d = s_d[n];
-      const double *zb = z + s_off[n] + int64_t(k) * d + s_j[n];
-      vr = SQH * zb[0];
-      vi = SQH * zb[int64_t(K) * d];
+      zb = z + s_off[n] + int64_t(k) * d + s_j[n];
+      im_off = int64_t(K) * d;
     }
-    Pr[k * SD_LD + n] = vr;
-    Pi[k * SD_LD + n] = vi;
+    cp_async_el<float>(Pr + k * SD_LD + n, zb, ok);           // 8-byte copies
+    cp_async_el<float>(Pi + k * SD_LD + n, zb + im_off, ok);
   }
+  cp_async_commit();
+  cp_async_wait<0>();
   __syncthreads();
   for (int pass = 0; pass < (W ? 2 : 1); ++pass) {
     double cr[4][2], ci[4][2];
 #pragma unroll
     for (int j = 0; j < 4; ++j) cr[j][0] = cr[j][1] = ci[j][0] = ci[j][1] = 0.0;
+    const double sc = pass == 0 ? SQH : 1.0;
 #pragma unroll
     for (int c = 0; c < 8; ++c) {
-      const double xr = ar[c], xi = ai[c], nxi = -ai[c];
+      const double xr = sc * ar[c], xi = sc * ai[c], nxi = -xi;
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
         const double br = Pr[(4 * c + t) * SD_LD + 8 * j + g];
