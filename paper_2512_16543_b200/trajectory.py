@@ -61,9 +61,10 @@ class TrajectoryConfig:
     # FP64 tensor pipe), formula otherwise (complex64 FP32 Grams)
     delta: str = "auto"
     # resolve the sketch cursors with the energy-screen walk (lrz_arsvd_walk, K <= 32)
-    # before the first speculative pass -- for workloads whose iteration counts
-    # follow the sketch (the LEO campaign's eta = 0.65-0.9, p = 1)
-    walk_first: bool = False
+    # before the first speculative pass: True / False, or None = when eta < 0.99
+    # (ranks then usually hit before the iteration cap, so iteration counts follow
+    # the sketch and a first speculative pass at predicted cursors is wasted)
+    walk_first: bool | None = None
 
 
 @dataclass
@@ -309,7 +310,7 @@ class TrajectoryRunner:
             n_spec = 0 if self._in_order else c.spec_passes
             # cursor walk (K <= 32): resolves every step's cursor from the energy
             # screen alone, in order, so one more speculative pass settles the chunk
-            can_walk = sync and ops.walk_ok(K, c.k_init, c.p, c.i_max)
+            can_walk = sync and n_spec > 0 and ops.walk_ok(K, c.k_init, c.p, c.i_max)
 
             def walk():
                 e0 = self._ev()
@@ -344,7 +345,8 @@ class TrajectoryRunner:
             flags = torch.zeros(2, dtype=torch.int32, device=dev)
             A_state0 = self.A.clone() if (c.maintain_A and sync) else None
             walked = False
-            if can_walk and (self._walk_first or c.walk_first):
+            wf = c.walk_first if c.walk_first is not None else self._eta_max() < 0.99
+            if can_walk and (self._walk_first or wf):
                 walk()          # the last chunk's iteration counts followed the sketch
                 walked = True
             one_pass()
