@@ -114,3 +114,26 @@ def test_rng_locate_matches_host_stream(cuda):
         host.advance(used)
     d = dev.window(1000).cpu().numpy()
     assert (d == host.window(1000)).mean() > 0.999
+
+
+@pytest.mark.parametrize("walk_first", [True, False])
+def test_cursor_walk_equals_in_order(cuda, walk_first):
+    """The energy-screen cursor walk (lrz_arsvd_walk) followed by one speculative
+    pass gives the in-order trajectory (iteration counts, consumption, ranks,
+    methods, rates) on a Woodbury-regime C2 slice (eta = 0.9)."""
+    spec = S.C2.with_(B=6, T=40)
+    trials = list(range(6))
+    H, noise, _ = _setup(cuda, spec, None, trials)
+    outs = []
+    for sp, wf in ((0, None), (2, walk_first)):
+        cfg = TrajectoryConfig(alpha=spec.alpha, eta=0.9, k_init=spec.k_init, p=spec.p,
+                               i_max=spec.i_max, spec_passes=sp, walk_first=wf)
+        rn = TrajectoryRunner(6, spec.K, spec.N, torch.complex128, cfg, cuda)
+        st = DeviceOmegaStreams.for_method(spec.seed, 0.9, trials, cuda)
+        outs.append(rn.run_chunk(H, noise, st.window(spec.T * rn.normals_per_step_max())))
+    a, b = outs
+    assert (a.method.cpu().numpy() == 1).mean() > 0.5          # Woodbury regime
+    assert torch.equal(a.iters, b.iters) and torch.equal(a.consumed, b.consumed)
+    assert torch.equal(a.k_est, b.k_est) and torch.equal(a.method, b.method)
+    assert b.spec_passes <= 2
+    torch.testing.assert_close(a.rates, b.rates, rtol=1e-10, atol=0)
