@@ -20,42 +20,51 @@ __global__ void channel_kernel(int64_t B, int t0, int T, int K, int N, int n_sid
                                const double *__restrict__ par,   // [B][6][K]
                                const double *__restrict__ scat,  // [B][2 K N] (re block, im block)
                                int64_t scat_stride, cplx<E> *__restrict__ H) {
-  const int64_t total = B * int64_t(T) * K * N;
+  // one warp per channel row (b, t, k): the per-row terms (sin / cos of the
+  // angles, the LoS phase offset, the Rician weights, the gain) are computed
+  // once per lane and reused for the row's N / 32 antennas per lane, instead
+  // of once per entry; the arithmetic per entry is unchanged (same operations,
+  // same order), so the result is still the host generator's to the last bit
+  const int64_t rows = B * int64_t(T) * K;
+  const int lane = threadIdx.x & 31;
+  const int64_t w0 = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) >> 5;
+  const int64_t nw = (int64_t(gridDim.x) * blockDim.x) >> 5;
   const double c = (n_side - 1) / 2.0;
   const double twopi = 2.0 * 3.141592653589793;
-  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < total;
-       e += int64_t(gridDim.x) * blockDim.x) {
-    const int m = int(e % N);
-    int64_t r = e / N;
-    const int k = int(r % K);
-    r /= K;
+  for (int64_t row = w0; row < rows; row += nw) {
+    const int k = int(row % K);
+    int64_t r = row / K;
     const int t = int(r % T);
     const int64_t b = r / T;
     const double *p = par + b * 6 * K;
     const double th0 = p[k], psi = p[K + k], phi = p[2 * K + k], beta = p[3 * K + k],
                  kap = p[4 * K + k], drift = p[5 * K + k];
     // every product and sum rounded separately, in numpy's order (no FMA contraction)
-    const double x = __dmul_rn(double(m / n_side) - c, 0.5);
-    const double y = __dmul_rn(double(m % n_side) - c, 0.5);
     const double theta = __dadd_rn(th0, __dmul_rn(drift, double(t0 + t)));
     const double st = sin(theta);
     const double kx = __dmul_rn(st, cos(psi)), ky = __dmul_rn(st, sin(psi));
-    const double phase = __dmul_rn(twopi, __dadd_rn(__dmul_rn(kx, x), __dmul_rn(ky, y)));
-    double sph, cph, sp, cp;
-    sincos(phase, &sph, &cph);
+    double sp, cp;
     sincos(phi, &sp, &cp);
-    // exp(-j phase) * exp(j phi) as numpy's complex product (a c - b d, a d + b c)
-    const double lr = __dsub_rn(__dmul_rn(cph, cp), __dmul_rn(-sph, sp));
-    const double li = __dadd_rn(__dmul_rn(cph, sp), __dmul_rn(-sph, cp));
     const double al = sqrt(__ddiv_rn(kap, __dadd_rn(1.0, kap)));
     const double an = sqrt(__ddiv_rn(1.0, __dadd_rn(1.0, kap)));
-    const double *sc = scat + b * scat_stride;
-    const double sr = __dmul_rn(sc[int64_t(k) * N + m], 0.7071067811865476);
-    const double si = __dmul_rn(sc[int64_t(K) * N + int64_t(k) * N + m], 0.7071067811865476);
     const double g = sqrt(beta);
-    const double hr = __dmul_rn(g, __dadd_rn(__dmul_rn(al, lr), __dmul_rn(an, sr)));
-    const double hi = __dmul_rn(g, __dadd_rn(__dmul_rn(al, li), __dmul_rn(an, si)));
-    H[e] = mk<E>(E(hr), E(hi));
+    const double *sc = scat + b * scat_stride;
+    cplx<E> *h = H + row * N;
+    for (int m = lane; m < N; m += 32) {
+      const double x = __dmul_rn(double(m / n_side) - c, 0.5);
+      const double y = __dmul_rn(double(m % n_side) - c, 0.5);
+      const double phase = __dmul_rn(twopi, __dadd_rn(__dmul_rn(kx, x), __dmul_rn(ky, y)));
+      double sph, cph;
+      sincos(phase, &sph, &cph);
+      // exp(-j phase) * exp(j phi) as numpy's complex product (a c - b d, a d + b c)
+      const double lr = __dsub_rn(__dmul_rn(cph, cp), __dmul_rn(-sph, sp));
+      const double li = __dadd_rn(__dmul_rn(cph, sp), __dmul_rn(-sph, cp));
+      const double sr = __dmul_rn(sc[int64_t(k) * N + m], 0.7071067811865476);
+      const double si = __dmul_rn(sc[int64_t(K) * N + int64_t(k) * N + m], 0.7071067811865476);
+      const double hr = __dmul_rn(g, __dadd_rn(__dmul_rn(al, lr), __dmul_rn(an, sr)));
+      const double hi = __dmul_rn(g, __dadd_rn(__dmul_rn(al, li), __dmul_rn(an, si)));
+      h[m] = mk<E>(E(hr), E(hi));
+    }
   }
 }
 
@@ -71,8 +80,8 @@ extern "C" int lrz_channels(int dtype, int64_t B, int t0, int T, int K, int N, i
     return LRZ_EINVAL;
   }
   if (B == 0) return LRZ_OK;
-  const int64_t total = B * int64_t(T) * K * N;
-  const unsigned nb = unsigned(std::min<int64_t>((total + 255) / 256, 148 * 64));
+  const int64_t rows = B * int64_t(T) * K;  // one warp per row
+  const unsigned nb = unsigned(std::min<int64_t>((rows + 7) / 8, 148 * 64));
   cudaStream_t s = (cudaStream_t)stream;
   if (dtype == LRZ_C64)
     channel_kernel<float><<<nb, 256, 0, s>>>(B, t0, T, K, N, n_side, params, scatter,
