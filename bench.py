@@ -445,7 +445,9 @@ def run_b200(args):
     streams = DeviceOmegaStreams.for_method(spec.seed, eta, trials, dev)
     stream = torch.cuda.current_stream(dev)
 
-    rng_stream = torch.cuda.Stream(dev)
+    # LRZ_RNG_PRIO=-1 puts the sketch RNG on a high-priority stream (its CTAs are
+    # dispatched first as SM slots free up beside the Gram)
+    rng_stream = torch.cuda.Stream(dev, priority=int(os.environ.get("LRZ_RNG_PRIO", "0")))
 
     def one(cfg, prof=None, Hd=H_dev, st=streams, sl=slice(None), sync=True):
         nb = Hd.shape[0]

@@ -931,13 +931,38 @@ LRZ_DEV bool warp_chol_tri(c128 *L, int d, int LD, const uint16_t *tri, double &
   return true;
 }
 
+LRZ_DEV void wk_cp16(void *smem, const void *gmem) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem));
+}
+LRZ_DEV void wk_cp8(void *smem, const void *gmem) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(gmem));
+}
+LRZ_DEV void wk_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+LRZ_DEV void wk_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
+// dA of step bt into a zero-padded [32][WK_LD] tile (one cp.async group)
+LRZ_DEV void wk_prefetch_dA(const ArsvdArgs &g, int64_t bt, c128 *dst) {
+  const int lane = threadIdx.x & 31, K = g.K;
+  const c128 *src = g.dA + bt * int64_t(K) * K;
+  for (int e = lane; e < K * K; e += 32) {
+    const int r = e / K, c = e - r * K;
+    wk_cp16(dst + r * WK_LD + c, src + e);
+  }
+  wk_commit();
+}
+
 __global__ void __launch_bounds__(32)
     arsvd_walk_kernel(ArsvdArgs g, int T, const uint8_t *__restrict__ is_sketch,
                       const int32_t *__restrict__ first, int64_t *__restrict__ cursor,
                       int32_t *__restrict__ iters_pred) {
   extern __shared__ __align__(16) char wk_smem[];
-  c128 *As = (c128 *)wk_smem;            // dA          [32][WK_LD]
-  c128 *Os = As + 32 * WK_LD;            // Omega_i     [32][WK_LD]
+  c128 *Abuf = (c128 *)wk_smem;          // dA, two steps [2][32][WK_LD] (next step prefetched)
+  c128 *Os = Abuf + 2 * 32 * WK_LD;      // Omega_i     [32][WK_LD]
   c128 *Ys = Os + 32 * WK_LD;            // Y = dA Omega
   c128 *Ws = Ys + 32 * WK_LD;            // W = dA Y
   c128 *L = Ws + 32 * WK_LD;             // [WK_DMAX][WK_DMAX + 1]
@@ -958,20 +983,26 @@ __global__ void __launch_bounds__(32)
   int t = first[b];
   if (t >= T) return;
   int64_t cur = cursor[b * T + t];
-  for (; t < T; ++t) {
+  // the padding of both dA tiles stays zero; the valid K x K block of step t + 1
+  // is fetched with cp.async while step t runs (the walk is latency bound)
+  for (int e = lane; e < 2 * 32 * WK_LD; e += 32) Abuf[e] = czero<double>();
+  __syncwarp();
+  int cb = 0;
+  wk_prefetch_dA(g, b * T + t, Abuf);
+  for (; t < T; ++t, cb ^= 1) {
     const int64_t bt = b * T + t;
     cursor[bt] = cur;
-    if (!is_sketch[bt]) continue;
-    const c128 *dA = g.dA + bt * int64_t(K) * K;
-    double e2 = 0.0;
-    for (int e = lane; e < 32 * 32; e += 32) {
-      const int r = e >> 5, c = e & 31;
-      const c128 v = (r < K && c < K) ? dA[r * K + c] : czero<double>();
-      As[r * WK_LD + c] = v;
-      e2 += cabs2(v);
-    }
-    const double energy = warp_sum(e2);
+    if (t + 1 < T) wk_prefetch_dA(g, bt + 1, Abuf + (cb ^ 1) * 32 * WK_LD);
+    else wk_commit();
+    // this step's tile has landed (the next one may be in flight); waited for
+    // on skipped steps too, so no two copies into one tile are ever in flight
+    wk_wait<1>();
     __syncwarp();
+    if (!is_sketch[bt]) continue;
+    const c128 *As = Abuf + cb * 32 * WK_LD;
+    double e2 = 0.0;
+    for (int e = lane; e < 32 * 32; e += 32) e2 += cabs2(As[(e >> 5) * WK_LD + (e & 31)]);
+    const double energy = warp_sum(e2);
     if (energy == 0.0) {  // empty factor: no sketch drawn (lowrank.py:275-276)
       if (lane == 0) iters_pred[bt] = 0;
       continue;
@@ -987,10 +1018,21 @@ __global__ void __launch_bounds__(32)
         break;
       }
       const double *zre = om + cur + used, *zim = zre + int64_t(K) * d;
+      // the iteration's Omega block staged raw through W's tile with every
+      // copy in flight at once (W is only written by the GEMM below)
+      double *stg = (double *)Ws;
+      const int nz = K * d;
+      for (int e = lane; e < nz; e += 32) {
+        wk_cp8(stg + e, zre + e);
+        wk_cp8(stg + nz + e, zim + e);
+      }
+      wk_commit();
+      wk_wait<0>();
+      __syncwarp();
       for (int e = lane; e < 32 * 24; e += 32) {
         const int r = e / 24, c = e - r * 24;
         Os[r * WK_LD + c] = (r < K && c < d)
-                                ? mk<double>(SQH * zre[r * d + c], SQH * zim[r * d + c])
+                                ? mk<double>(SQH * stg[r * d + c], SQH * stg[nz + r * d + c])
                                 : czero<double>();
       }
       __syncwarp();
@@ -1021,11 +1063,16 @@ __global__ void __launch_bounds__(32)
       undecided = true;  // within the rounding bound of the target
       break;
     }
-    if (undecided) return;  // later predictions stay; the verifier finds the first miss
+    if (undecided) {  // later predictions stay; the verifier finds the first miss
+      wk_wait<0>();
+      return;
+    }
     if (iters < 0) iters = g.i_max;  // iteration cap: all sketches drawn
     if (lane == 0) iters_pred[bt] = iters;
     cur += used;
+    __syncwarp();  // every lane is done with this tile before it is refilled
   }
+  wk_wait<0>();
 }
 
 }  // namespace lrz
@@ -1233,7 +1280,7 @@ extern "C" int lrz_arsvd_walk(int64_t B, int T, int K, const void *dA, const dou
   g.p = cfg->p;
   g.i_max = cfg->i_max;
   g.D = cfg->d_max;
-  const size_t sm = (4 * 32 * WK_LD + WK_DMAX * (WK_DMAX + 1)) * sizeof(c128);
+  const size_t sm = (5 * 32 * WK_LD + WK_DMAX * (WK_DMAX + 1)) * sizeof(c128);
   if (cudaFuncSetAttribute(arsvd_walk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            int(sm)) != cudaSuccess) {
     lrz_set_error("lrz_arsvd_walk: cannot reserve %zu bytes of shared memory", sm);
