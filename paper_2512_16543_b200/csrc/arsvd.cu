@@ -985,7 +985,7 @@ __global__ void __launch_bounds__(32)
   int64_t cur = cursor[b * T + t];
   // the padding of both dA tiles stays zero; the valid K x K block of step t + 1
   // is fetched with cp.async while step t runs (the walk is latency bound)
-  for (int e = lane; e < 2 * 32 * WK_LD; e += 32) Abuf[e] = czero<double>();
+  for (int e = lane; e < 3 * 32 * WK_LD; e += 32) Abuf[e] = czero<double>();  // dA x 2, Omega
   __syncwarp();
   int cb = 0;
   wk_prefetch_dA(g, b * T + t, Abuf);
@@ -1018,22 +1018,28 @@ __global__ void __launch_bounds__(32)
         break;
       }
       const double *zre = om + cur + used, *zim = zre + int64_t(K) * d;
-      // the iteration's Omega block staged raw through W's tile with every
-      // copy in flight at once (W is only written by the GEMM below)
-      double *stg = (double *)Ws;
+      // Omega_i lands straight in its tile (re / im halves by 8-byte cp.async,
+      // every copy in flight at once), then each lane scales the entries it
+      // copied by sqrt(1/2) and clears the pad columns d .. 8 ceil(d / 8)
       const int nz = K * d;
+      const float inv_d = 1.0f / float(d);
       for (int e = lane; e < nz; e += 32) {
-        wk_cp8(stg + e, zre + e);
-        wk_cp8(stg + nz + e, zim + e);
+        const int r = int((float(e) + 0.5f) * inv_d), c = e - r * d;  // exact: e < 1024
+        c128 *o = Os + r * WK_LD + c;
+        wk_cp8(&o->re, zre + e);
+        wk_cp8(&o->im, zim + e);
       }
       wk_commit();
+      const int dpad = 8 * ((d + 7) / 8);
+      for (int e = lane; e < 32 * (dpad - d); e += 32) {
+        const int r = e / (dpad - d), c = d + e - r * (dpad - d);
+        Os[r * WK_LD + c] = czero<double>();
+      }
       wk_wait<0>();
-      __syncwarp();
-      for (int e = lane; e < 32 * 24; e += 32) {
-        const int r = e / 24, c = e - r * 24;
-        Os[r * WK_LD + c] = (r < K && c < d)
-                                ? mk<double>(SQH * stg[r * d + c], SQH * stg[nz + r * d + c])
-                                : czero<double>();
+      for (int e = lane; e < nz; e += 32) {
+        const int r = int((float(e) + 0.5f) * inv_d), c = e - r * d;
+        c128 &o = Os[r * WK_LD + c];
+        o = mk<double>(SQH * o.re, SQH * o.im);
       }
       __syncwarp();
       warp_zgemm(As, Os, Ys, d);   // Y = dA Omega (lowrank.py:288)

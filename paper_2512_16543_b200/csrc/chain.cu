@@ -282,6 +282,30 @@ __global__ void __launch_bounds__(INV_THREADS)
 //   plan 1 (Woodbury): A_inv_seq[t] = woodbury(A_inv_seq[t-1]); on SingularAux
 //                      fall back to inv(G_t) (lowrank.py:353-367)
 //   plan 2 (none):     A_inv_seq[t] = A_inv_seq[t-1] (lowrank.py:345-351)
+// K <= 32: the trial's A^-1 (double buffered), A, the step's U / V and the
+// Woodbury intermediates (A^-1 U, T, V^H A^-1) stay in shared memory, so the
+// serial chain pays one global-load latency per step (U / V by cp.async)
+// instead of one per dependent product; the arithmetic and its order are the
+// global-memory path's, so the results are bit-identical.
+__host__ __device__ inline bool chain_resident(int K, int D) { return K <= 32 && D <= 32; }
+__host__ __device__ inline size_t chain_base_smem(int K, int D) {
+  return (InvSmem::bytes(K, D, K <= INV_SMEM_KMAX) + wb_aux_smem(D) + 15) & ~size_t(15);
+}
+__host__ __device__ inline size_t chain_resident_smem(int K, int D) {
+  // A^-1 x 2 and U, V, A^-1 U, T, V^H A^-1 at stride K + 1; A at stride K
+  return (2 * size_t(K) * (K + 1) + size_t(K) * K + 5 * size_t(K + 1) * D) * sizeof(c128);
+}
+
+LRZ_DEV void chain_cp16(void *smem, const void *gmem) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem));
+}
+
+// Per-trial chain over T steps (harness.py:228-241 semantics):
+//   plan 0 (full):     A_inv_seq[t] already holds inv(G_t); A_state = G_t
+//   plan 1 (Woodbury): A_inv_seq[t] = woodbury(A_inv_seq[t-1]); on SingularAux
+//                      fall back to inv(G_t) (lowrank.py:353-367)
+//   plan 2 (none):     A_inv_seq[t] = A_inv_seq[t-1] (lowrank.py:345-351)
 __global__ void __launch_bounds__(INV_THREADS)
     chain_kernel(int T, int K, int D, const uint8_t *plan, const c128 *G, const c128 *Ainv_prev,
                  c128 *Ainv_seq, c128 *A_state, const c128 *U, const c128 *V, const double *S,
@@ -290,46 +314,97 @@ __global__ void __launch_bounds__(INV_THREADS)
   const int64_t b = blockIdx.x;
   const int64_t KK = int64_t(K) * K;
   const int n = K > D ? K : D;
+  const int tid = threadIdx.x, NT = blockDim.x;
   c128 *M;
   WbScratch sc;
   sc.inv = carve_inv(smem, n, &M, K, K <= INV_SMEM_KMAX);
-  c128 *w = ws + b * wb_ws_elems(K, D);
-  carve_wb(sc, smem + InvSmem::bytes(K, D, K <= INV_SMEM_KMAX), w, K, D);
+  const bool res = chain_resident(K, D);
+  c128 *sAi = nullptr, *sA = nullptr, *sU = nullptr, *sV = nullptr;
+  const int ld = K + 1;                   // resident stride (bank spread)
+  const int64_t KL = int64_t(K) * ld;     // one resident A^-1 buffer
+  if (res) {
+    sAi = (c128 *)(smem + chain_base_smem(K, D));  // [2][K][ld]
+    sA = sAi + 2 * KL;                             // [K][K]
+    sU = sA + KK;                                  // [D][ld]
+    sV = sU + int64_t(ld) * D;
+    carve_wb(sc, smem + InvSmem::bytes(K, D, K <= INV_SMEM_KMAX), sV + int64_t(ld) * D, ld, D);
+  } else {
+    carve_wb(sc, smem + InvSmem::bytes(K, D, K <= INV_SMEM_KMAX), ws + b * wb_ws_elems(K, D),
+             K, D);
+  }
   c128 *Ast = A_state ? A_state + b * KK : nullptr;
+  int cb = 0;  // resident: sAi + cb KL holds A^-1 of the previous step
+  if (res) {
+    for (int64_t e = tid; e < KK; e += NT) {
+      sAi[(e / K) * ld + e % K] = Ainv_prev[b * KK + e];
+      if (Ast) sA[e] = Ast[e];
+    }
+    __syncthreads();
+  }
+  c128 *Acur = res ? (Ast ? sA : nullptr) : Ast;  // where the A state lives
   for (int t = 0; t < T; ++t) {
     const int64_t bt = b * T + t;
     const int pl = plan[bt];
     c128 *out = Ainv_seq + bt * KK;
     const c128 *prev = (t == 0) ? Ainv_prev + b * KK : out - KK;
     int m = LRZ_METHOD_FULL, st = LRZ_INFO_OK;
+    bool reload = false;  // resident: A^-1 of this step is in `out` (global)
     if (pl == 1) {
-      st = cta_woodbury(K, r[bt], prev, out, Ast, Ast, U + bt * int64_t(D) * K,
-                        V + bt * int64_t(D) * K, S + bt * D, sc);
+      const c128 *Ub = U + bt * int64_t(D) * K, *Vb = V + bt * int64_t(D) * K;
+      if (res) {
+        const int rk = r[bt] * K;
+        for (int e = tid; e < rk; e += NT) {
+          const int o = (e / K) * ld + e % K;
+          chain_cp16(sU + o, Ub + e);
+          chain_cp16(sV + o, Vb + e);
+        }
+        asm volatile("cp.async.commit_group;\n" ::);
+        asm volatile("cp.async.wait_group 0;\n" ::);
+        __syncthreads();
+        st = cta_woodbury(K, r[bt], sAi + cb * KL, sAi + (cb ^ 1) * KL, Acur, Acur, sU, sV,
+                          S + bt * D, sc, ld);
+        if (st == LRZ_INFO_OK) {
+          cb ^= 1;
+          for (int64_t e = tid; e < KK; e += NT) out[e] = sAi[cb * KL + (e / K) * ld + e % K];
+        }
+      } else {
+        st = cta_woodbury(K, r[bt], prev, out, Ast, Ast, Ub, Vb, S + bt * D, sc);
+      }
       if (st == LRZ_INFO_OK) {
         m = LRZ_METHOD_WOODBURY;
       } else {
         // full branch: invert the true Gram of the new channel
         st = cta_herm_inverse(G + bt * KK, out, K, M, 1e14, sc.inv);
-        if (Ast)
-          for (int64_t e = threadIdx.x; e < KK; e += blockDim.x) Ast[e] = G[bt * KK + e];
+        if (Acur)
+          for (int64_t e = tid; e < KK; e += NT) Acur[e] = G[bt * KK + e];
         m = LRZ_METHOD_FULL;
+        reload = true;
       }
     } else if (pl == 2) {
-      for (int64_t e = threadIdx.x; e < KK; e += blockDim.x) out[e] = prev[e];
+      for (int64_t e = tid; e < KK; e += NT)
+        out[e] = res ? sAi[cb * KL + (e / K) * ld + e % K] : prev[e];
       m = LRZ_METHOD_NONE;
     } else {
       // A = G_t; dead if the next step is another full inversion (it overwrites
       // A); needed before a Woodbury or 'none' step and at the chunk end
       const bool needed = (t == T - 1) || plan[bt + 1] != 0;
-      if (Ast && needed)
-        for (int64_t e = threadIdx.x; e < KK; e += blockDim.x) Ast[e] = G[bt * KK + e];
+      if (Acur && needed)
+        for (int64_t e = tid; e < KK; e += NT) Acur[e] = G[bt * KK + e];
       st = info ? info[bt] : LRZ_INFO_OK;  // written by the batched inverse
+      reload = needed;
     }
     __syncthreads();
-    if (threadIdx.x == 0) {
+    if (res && reload) {  // out was written by this CTA (fallback) or the batched inverse
+      for (int64_t e = tid; e < KK; e += NT) sAi[cb * KL + (e / K) * ld + e % K] = out[e];
+      __syncthreads();
+    }
+    if (tid == 0) {
       method[bt] = uint8_t(m);
       if (info) info[bt] = st;
     }
+  }
+  if (res && Ast) {
+    for (int64_t e = tid; e < KK; e += NT) Ast[e] = sA[e];
   }
 }
 
@@ -743,7 +818,8 @@ extern "C" int lrz_plan(int64_t n, int K, const uint8_t *is_sketch, const int32_
 size_t lrz_inverse_smem(int K) { return InvSmem::bytes(K, K, K <= INV_SMEM_KMAX); }
 size_t lrz_woodbury_smem(int D) { return InvSmem::bytes(D, D, false) + wb_aux_smem(D); }
 size_t lrz_chain_smem(int K, int D) {
-  return InvSmem::bytes(K, D, K <= INV_SMEM_KMAX) + wb_aux_smem(D);
+  return chain_resident(K, D) ? chain_base_smem(K, D) + chain_resident_smem(K, D)
+                              : InvSmem::bytes(K, D, K <= INV_SMEM_KMAX) + wb_aux_smem(D);
 }
 size_t lrz_wb_ws(int64_t B, int K, int D) {
   // + per-trial SingularAuxiliary flags of the step-parallel chain

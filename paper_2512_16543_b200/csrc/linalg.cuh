@@ -222,29 +222,33 @@ struct WbScratch {
 };
 
 // One Woodbury step (lowrank.py:208-220).  Ainv_in, Ainv_out, A_in, A_out
-// row-major K x K global (Ainv_out != Ainv_in; A_out may alias A_in);
+// row-major K x K (Ainv_out != Ainv_in; A_out may alias A_in);
 // U, V column-major [j][K]; S descending.  Returns LRZ_INFO_OK or
-// LRZ_INFO_SINGULAR_AUX (nothing written).
+// LRZ_INFO_SINGULAR_AUX (nothing written).  `ld` is the row stride of
+// A^-1 and the column stride of U, V and the K-long scratch columns (K in
+// global memory; K + 1 when they sit in shared memory, which spreads the
+// K-strided accesses over the banks); A itself is K-strided.
 LRZ_DEV int cta_woodbury(int K, int r, const c128 *__restrict__ Ainv_in, c128 *Ainv_out,
                          const c128 *A_in, c128 *A_out, const c128 *__restrict__ U,
                          const c128 *__restrict__ V, const double *__restrict__ S,
-                         const WbScratch &sc) {
+                         const WbScratch &sc, int ld = 0) {
+  if (ld == 0) ld = K;
   const int tid = threadIdx.x, NT = blockDim.x;
   // 1. AiU = A^-1 U (K x r) and VhAi = V^H A^-1 (r x K)
   for (int e = tid; e < K * r; e += NT) {
     const int j = e / K, k = e - j * K;
     c128 a = czero<double>();
-    const c128 *arow = Ainv_in + int64_t(k) * K;
-    const c128 *uc = U + int64_t(j) * K;
+    const c128 *arow = Ainv_in + int64_t(k) * ld;
+    const c128 *uc = U + int64_t(j) * ld;
     for (int m = 0; m < K; ++m) cfma(a, arow[m], uc[m]);
-    sc.AiU[int64_t(j) * K + k] = a;
+    sc.AiU[int64_t(j) * ld + k] = a;
   }
   for (int e = tid; e < K * r; e += NT) {
     const int j = e / K, m = e - j * K;
     c128 a = czero<double>();
-    const c128 *vc = V + int64_t(j) * K;
-    for (int k = 0; k < K; ++k) cfma_ca(a, vc[k], Ainv_in[int64_t(k) * K + m]);
-    sc.VhAi[int64_t(j) * K + m] = a;
+    const c128 *vc = V + int64_t(j) * ld;
+    for (int k = 0; k < K; ++k) cfma_ca(a, vc[k], Ainv_in[int64_t(k) * ld + m]);
+    sc.VhAi[int64_t(j) * ld + m] = a;
   }
   __syncthreads();
   // 2. aux = diag(1/S) + V^H AiU
@@ -252,8 +256,8 @@ LRZ_DEV int cta_woodbury(int K, int r, const c128 *__restrict__ Ainv_in, c128 *A
   for (int e = tid; e < r * r; e += NT) {
     const int i = e / r, j = e - i * r;
     c128 a = czero<double>();
-    const c128 *vc = V + int64_t(i) * K;
-    const c128 *au = sc.AiU + int64_t(j) * K;
+    const c128 *vc = V + int64_t(i) * ld;
+    const c128 *au = sc.AiU + int64_t(j) * ld;
     for (int k = 0; k < K; ++k) cfma_ca(a, vc[k], au[k]);
     if (i == j) a.re = 1.0 / S[i] + a.re;
     sc.aux[e] = a;
@@ -272,21 +276,21 @@ LRZ_DEV int cta_woodbury(int K, int r, const c128 *__restrict__ Ainv_in, c128 *A
   for (int e = tid; e < K * r; e += NT) {
     const int j = e / K, k = e - j * K;
     c128 a = czero<double>();
-    for (int i = 0; i < r; ++i) cfma(a, sc.AiU[int64_t(i) * K + k], sc.auxinv[i * r + j]);
-    sc.T[int64_t(j) * K + k] = a;
+    for (int i = 0; i < r; ++i) cfma(a, sc.AiU[int64_t(i) * ld + k], sc.auxinv[i * r + j]);
+    sc.T[int64_t(j) * ld + k] = a;
   }
   __syncthreads();
   // 5. A^-1 - T VhAi ;  A + (U S) V^H
   for (int e = tid; e < K * K; e += NT) {
     const int k = e / K, m = e - k * K;
     c128 a = czero<double>();
-    for (int j = 0; j < r; ++j) cfma(a, sc.T[int64_t(j) * K + k], sc.VhAi[int64_t(j) * K + m]);
-    const c128 o = Ainv_in[e];
-    Ainv_out[e] = mk<double>(o.re - a.re, o.im - a.im);
+    for (int j = 0; j < r; ++j) cfma(a, sc.T[int64_t(j) * ld + k], sc.VhAi[int64_t(j) * ld + m]);
+    const c128 o = Ainv_in[int64_t(k) * ld + m];
+    Ainv_out[int64_t(k) * ld + m] = mk<double>(o.re - a.re, o.im - a.im);
     if (A_out) {
       c128 b = czero<double>();
       for (int j = 0; j < r; ++j)
-        cfma_cb(b, cscale(U[int64_t(j) * K + k], S[j]), V[int64_t(j) * K + m]);
+        cfma_cb(b, cscale(U[int64_t(j) * ld + k], S[j]), V[int64_t(j) * ld + m]);
       const c128 x = A_in[e];
       A_out[e] = mk<double>(x.re + b.re, x.im + b.im);
     }
