@@ -70,51 +70,69 @@ LRZ_DEV void rr_pair(int rnd, int pi, int dp, int &a, int &b) {
 
 // One-sided Jacobi (Hestenes) on the d columns of M (length K), rotations
 // accumulated in J (d x d, column-major); parallel round-robin ordering, one
-// warp per column pair.  On exit sval[j] = ||M_j|| and perm sorts them
-// descending (stable).  Block-cooperative; contains barriers.
+// 8-lane group per column pair (a warp carries four pairs, so the per-pair
+// scalar chain -- hypot, sqrt, divisions -- is issued once for four pairs and
+// the dot products reduce in three shuffle rounds).  On exit sval[j] = ||M_j||
+// and perm sorts them descending (stable).  Block-cooperative; contains barriers.
+constexpr int JG = 8;  // lanes per column pair
+
+LRZ_DEV double grp_sum(double v) {
+  v += __shfl_xor_sync(0xffffffffu, v, 4);
+  v += __shfl_xor_sync(0xffffffffu, v, 2);
+  v += __shfl_xor_sync(0xffffffffu, v, 1);
+  return v;
+}
+
 LRZ_DEV void jacobi_sv(c128 *M, c128 *J, int K, int d, double *sval, int *perm, int *s_rot) {
   const int tid = threadIdx.x, NT = blockDim.x, lane = tid & 31, wid = tid >> 5, NW = NT >> 5;
+  const int gl = lane & (JG - 1), grp = tid / JG, NG = NT / JG;
   for (int e = tid; e < d * d; e += NT) J[e] = mk<double>((e % (d + 1)) == 0 ? 1.0 : 0.0, 0.0);
   if (tid == 0) s_rot[0] = s_rot[1] = 0;
   __syncthreads();
   const int dp = d + (d & 1), npairs = dp / 2;
   for (int sweep = 0; sweep < JACOBI_MAX_SWEEPS; ++sweep) {
     for (int rnd = 0; rnd < dp - 1; ++rnd) {
-      for (int pi = wid; pi < npairs; pi += NW) {
-        int a, b;
-        rr_pair(rnd, pi, dp, a, b);
-        if (b >= d) continue;
-        c128 *ma = M + int64_t(a) * K, *mb = M + int64_t(b) * K;
+      // warp-uniform trip count: every lane reaches the group shuffles
+      for (int base = 0; base < npairs; base += NG) {
+        const int pi = base + grp;
+        int a = 0, b = 0;
+        if (pi < npairs) rr_pair(rnd, pi, dp, a, b);
+        const bool act = pi < npairs && b < d;
+        const c128 *ma = M + int64_t(a) * K, *mb = M + int64_t(b) * K;
         double al = 0.0, be = 0.0, gr = 0.0, gi = 0.0;
-        for (int k = lane; k < K; k += 32) {
-          const c128 x = ma[k], y = mb[k];
-          al += cabs2(x);
-          be += cabs2(y);
-          gr = fma(x.re, y.re, fma(x.im, y.im, gr));
-          gi = fma(x.re, y.im, fma(-x.im, y.re, gi));
+        if (act) {
+          for (int k = gl; k < K; k += JG) {
+            const c128 x = ma[k], y = mb[k];
+            al += cabs2(x);
+            be += cabs2(y);
+            gr = fma(x.re, y.re, fma(x.im, y.im, gr));
+            gi = fma(x.re, y.im, fma(-x.im, y.re, gi));
+          }
         }
-        al = warp_sum(al);
-        be = warp_sum(be);
-        gr = warp_sum(gr);
-        gi = warp_sum(gi);
+        al = grp_sum(al);
+        be = grp_sum(be);
+        gr = grp_sum(gr);
+        gi = grp_sum(gi);
+        if (!act) continue;
         const double gabs = hypot(gr, gi);
         if (!(gabs > JACOBI_TOL * sqrt(al) * sqrt(be)) || gabs == 0.0) continue;
         const double zeta = (be - al) / (2.0 * gabs);
         const double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
         const double c = 1.0 / sqrt(1.0 + t * t), s = c * t;
         const c128 ph = mk<double>(gr / gabs, -gi / gabs);  // e^{-i phi}
-        for (int k = lane; k < K; k += 32) {
-          const c128 x = ma[k], y = cmul(mb[k], ph);
-          ma[k] = mk<double>(c * x.re - s * y.re, c * x.im - s * y.im);
-          mb[k] = mk<double>(s * x.re + c * y.re, s * x.im + c * y.im);
+        c128 *wa = M + int64_t(a) * K, *wb = M + int64_t(b) * K;
+        for (int k = gl; k < K; k += JG) {
+          const c128 x = wa[k], y = cmul(wb[k], ph);
+          wa[k] = mk<double>(c * x.re - s * y.re, c * x.im - s * y.im);
+          wb[k] = mk<double>(s * x.re + c * y.re, s * x.im + c * y.im);
         }
         c128 *ja = J + int64_t(a) * d, *jb = J + int64_t(b) * d;
-        for (int k = lane; k < d; k += 32) {
+        for (int k = gl; k < d; k += JG) {
           const c128 x = ja[k], y = cmul(jb[k], ph);
           ja[k] = mk<double>(c * x.re - s * y.re, c * x.im - s * y.im);
           jb[k] = mk<double>(s * x.re + c * y.re, s * x.im + c * y.im);
         }
-        if (lane == 0) s_rot[sweep & 1] = 1;
+        if (gl == 0) s_rot[sweep & 1] = 1;
       }
       __syncthreads();
       // the next sweep's flag was last read before this sweep's first barrier
