@@ -1,6 +1,8 @@
 // K5 batched Hermitian inverse, K4 Woodbury update, the per-trial chain of
 // the batched runner, and the speculative sketch-cursor verifier.
 
+#include <stdlib.h>
+
 #include <cooperative_groups.h>
 
 #include "linalg.cuh"
@@ -309,7 +311,7 @@ LRZ_DEV void chain_cp16(void *smem, const void *gmem) {
 __global__ void __launch_bounds__(INV_THREADS)
     chain_kernel(int T, int K, int D, const uint8_t *plan, const c128 *G, const c128 *Ainv_prev,
                  c128 *Ainv_seq, c128 *A_state, const c128 *U, const c128 *V, const double *S,
-                 const int32_t *r, uint8_t *method, int32_t *info, c128 *ws) {
+                 const int32_t *r, uint8_t *method, int32_t *info, c128 *ws, int resident) {
   extern __shared__ __align__(16) char smem[];
   const int64_t b = blockIdx.x;
   const int64_t KK = int64_t(K) * K;
@@ -318,7 +320,7 @@ __global__ void __launch_bounds__(INV_THREADS)
   c128 *M;
   WbScratch sc;
   sc.inv = carve_inv(smem, n, &M, K, K <= INV_SMEM_KMAX);
-  const bool res = chain_resident(K, D);
+  const bool res = resident != 0;
   c128 *sAi = nullptr, *sA = nullptr, *sU = nullptr, *sV = nullptr;
   const int ld = K + 1;                   // resident stride (bank spread)
   const int64_t KL = int64_t(K) * ld;     // one resident A^-1 buffer
@@ -334,13 +336,8 @@ __global__ void __launch_bounds__(INV_THREADS)
   }
   c128 *Ast = A_state ? A_state + b * KK : nullptr;
   int cb = 0;  // resident: sAi + cb KL holds A^-1 of the previous step
-  if (res) {
-    for (int64_t e = tid; e < KK; e += NT) {
-      sAi[(e / K) * ld + e % K] = Ainv_prev[b * KK + e];
-      if (Ast) sA[e] = Ast[e];
-    }
-    __syncthreads();
-  }
+  // resident tiles are filled lazily (a chunk of full inversions never reads them)
+  bool have_ai = false, have_a = false;
   c128 *Acur = res ? (Ast ? sA : nullptr) : Ast;  // where the A state lives
   for (int t = 0; t < T; ++t) {
     const int64_t bt = b * T + t;
@@ -349,6 +346,14 @@ __global__ void __launch_bounds__(INV_THREADS)
     const c128 *prev = (t == 0) ? Ainv_prev + b * KK : out - KK;
     int m = LRZ_METHOD_FULL, st = LRZ_INFO_OK;
     bool reload = false;  // resident: A^-1 of this step is in `out` (global)
+    if (res && pl != 0 && !have_ai) {  // A^-1 of the previous step, from global
+      for (int64_t e = tid; e < KK; e += NT) sAi[cb * KL + (e / K) * ld + e % K] = prev[e];
+      if (Ast && !have_a)
+        for (int64_t e = tid; e < KK; e += NT) sA[e] = Ast[e];
+      have_ai = true;
+      have_a = true;
+      __syncthreads();
+    }
     if (pl == 1) {
       const c128 *Ub = U + bt * int64_t(D) * K, *Vb = V + bt * int64_t(D) * K;
       if (res) {
@@ -379,6 +384,7 @@ __global__ void __launch_bounds__(INV_THREADS)
           for (int64_t e = tid; e < KK; e += NT) Acur[e] = G[bt * KK + e];
         m = LRZ_METHOD_FULL;
         reload = true;
+        have_a = true;
       }
     } else if (pl == 2) {
       for (int64_t e = tid; e < KK; e += NT)
@@ -391,11 +397,13 @@ __global__ void __launch_bounds__(INV_THREADS)
       if (Acur && needed)
         for (int64_t e = tid; e < KK; e += NT) Acur[e] = G[bt * KK + e];
       st = info ? info[bt] : LRZ_INFO_OK;  // written by the batched inverse
-      reload = needed;
+      reload = needed && t + 1 < T;
+      if (needed) have_a = true;
     }
     __syncthreads();
     if (res && reload) {  // out was written by this CTA (fallback) or the batched inverse
       for (int64_t e = tid; e < KK; e += NT) sAi[cb * KL + (e / K) * ld + e % K] = out[e];
+      have_ai = true;
       __syncthreads();
     }
     if (tid == 0) {
@@ -403,7 +411,7 @@ __global__ void __launch_bounds__(INV_THREADS)
       if (info) info[bt] = st;
     }
   }
-  if (res && Ast) {
+  if (res && Ast && have_a) {
     for (int64_t e = tid; e < KK; e += NT) Ast[e] = sA[e];
   }
 }
@@ -930,12 +938,22 @@ extern "C" int lrz_chain(int64_t B, int T, int K, int d_max, const uint8_t *plan
     return LRZ_EINVAL;
   }
   if (B == 0) return LRZ_OK;
-  const size_t sm = lrz_chain_smem(K, d_max);
+  static int mode = -1;  // LRZ_CHAIN_RESIDENT=0: global-memory chain (A/B switch)
+  if (mode < 0) {
+    const char *e = getenv("LRZ_CHAIN_RESIDENT");
+    mode = (e && e[0] == '0') ? 0 : 1;
+    const char *c = getenv("LRZ_CHAIN_CARVEOUT");
+    if (c) cudaFuncSetAttribute((const void *)chain_kernel,
+                                cudaFuncAttributePreferredSharedMemoryCarveout, atoi(c));
+  }
+  const int resident = mode && chain_resident(K, d_max);
+  const size_t sm = resident ? lrz_chain_smem(K, d_max)
+                             : InvSmem::bytes(K, d_max, K <= INV_SMEM_KMAX) + wb_aux_smem(d_max);
   if (set_smem((const void *)chain_kernel, sm)) return LRZ_ELAUNCH;
   chain_kernel<<<unsigned(B), INV_THREADS, sm, (cudaStream_t)stream>>>(
       T, K, d_max, plan, (const c128 *)G, (const c128 *)A_inv_prev, (c128 *)A_inv_seq,
       (c128 *)A_state, (const c128 *)U, (const c128 *)V, S, r, method, info,
-      (c128 *)workspace);
+      (c128 *)workspace, resident);
   return lrz_launch_status("lrz_chain");
 }
 
