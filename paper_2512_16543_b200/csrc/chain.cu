@@ -748,7 +748,9 @@ __global__ void __launch_bounds__(128, KP > 16 ? 3 : 4)
     }
   }
   fa = warp_sum(fa);
-  __shared__ c128 prow[4][KP];
+  // the scaled pivot row is stored twice (slots lane and lane + KP), so the
+  // rotated read of slot (j + 1 + k) mod KP is a constant offset from pr_s + k + 1
+  __shared__ c128 prow[4][2 * KP];
   c128 *pr_s = prow[threadIdx.x >> 5];
   bool ok = true;
 #pragma unroll 1
@@ -764,15 +766,20 @@ __global__ void __launch_bounds__(128, KP > 16 ? 3 : 4)
     // this lane's entry of the scaled pivot row, M[k][lane] / p
     const c128 mk_l = (lane == k) ? mk<double>(pr, pi)
                                   : (lane > k ? cconj(ck) : mk<double>(-ck.re, ck.im));
-    if (lane < KP) pr_s[lane] = cmul(mk_l, pinv);
+    if (lane < KP) {
+      const c128 v = cmul(mk_l, pinv);
+      pr_s[lane] = v;
+      pr_s[lane + KP] = v;
+    }
     __syncwarp();
+    const c128 *prk = pr_s + k + 1;
     // row_i -= c_i r with c_k = p - 1 (so row k becomes r); column k is then
     // -c_i / p (i != k) and 1 / p (i = k), stored in the last slot
     const c128 c = (lane == k) ? mk<double>(ck.re - 1.0, ck.im) : ck;
     const c128 colv = (lane == k) ? pinv : cmul(mk<double>(-ck.re, -ck.im), pinv);
 #pragma unroll
     for (int j = 0; j < KP - 1; ++j) {
-      const c128 r = pr_s[(j + 1 + k) & (KP - 1)];
+      const c128 r = prk[j];
       c128 u = m[j + 1];
       u.re = fma(-c.re, r.re, u.re);
       u.re = fma(c.im, r.im, u.re);
