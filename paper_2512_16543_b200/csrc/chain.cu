@@ -289,6 +289,7 @@ __global__ void __launch_bounds__(INV_THREADS)
 // serial chain pays one global-load latency per step (U / V by cp.async)
 // instead of one per dependent product; the arithmetic and its order are the
 // global-memory path's, so the results are bit-identical.
+constexpr int CH_PLAN_BLK = 1024;  // plan entries staged per block of steps
 __host__ __device__ inline bool chain_resident(int K, int D) { return K <= 32 && D <= 32; }
 __host__ __device__ inline size_t chain_base_smem(int K, int D) {
   return (InvSmem::bytes(K, D, K <= INV_SMEM_KMAX) + wb_aux_smem(D) + 15) & ~size_t(15);
@@ -339,9 +340,18 @@ __global__ void __launch_bounds__(INV_THREADS)
   // resident tiles are filled lazily (a chunk of full inversions never reads them)
   bool have_ai = false, have_a = false;
   c128 *Acur = res ? (Ast ? sA : nullptr) : Ast;  // where the A state lives
+  // the trial's plan row is staged in shared memory block by block (with one
+  // entry of lookahead): a chunk of full inversions then costs no dependent
+  // global load per step
+  __shared__ uint8_t s_plan[CH_PLAN_BLK + 1];
   for (int t = 0; t < T; ++t) {
     const int64_t bt = b * T + t;
-    const int pl = plan[bt];
+    if (t % CH_PLAN_BLK == 0) {
+      __syncthreads();
+      for (int i = tid; i <= CH_PLAN_BLK && t + i < T; i += NT) s_plan[i] = plan[bt + i];
+      __syncthreads();
+    }
+    const int pl = s_plan[t % CH_PLAN_BLK];
     c128 *out = Ainv_seq + bt * KK;
     const c128 *prev = (t == 0) ? Ainv_prev + b * KK : out - KK;
     int m = LRZ_METHOD_FULL, st = LRZ_INFO_OK;
@@ -393,10 +403,10 @@ __global__ void __launch_bounds__(INV_THREADS)
     } else {
       // A = G_t; dead if the next step is another full inversion (it overwrites
       // A); needed before a Woodbury or 'none' step and at the chunk end
-      const bool needed = (t == T - 1) || plan[bt + 1] != 0;
+      const bool needed = (t == T - 1) || s_plan[t % CH_PLAN_BLK + 1] != 0;
       if (Acur && needed)
         for (int64_t e = tid; e < KK; e += NT) Acur[e] = G[bt * KK + e];
-      st = info ? info[bt] : LRZ_INFO_OK;  // written by the batched inverse
+      // info[bt] was written by the batched inverse and stays as it is
       reload = needed && t + 1 < T;
       if (needed) have_a = true;
     }
@@ -408,7 +418,7 @@ __global__ void __launch_bounds__(INV_THREADS)
     }
     if (tid == 0) {
       method[bt] = uint8_t(m);
-      if (info) info[bt] = st;
+      if (info && pl != 0) info[bt] = st;
     }
   }
   if (res && Ast && have_a) {

@@ -19,28 +19,35 @@ KEYS = ["Duration", "DRAM Throughput", "Memory Throughput", "Compute (SM) Throug
 
 
 def launches(path):
+    """Per-kernel launch count, time and DRAM bytes from a --metrics launch list
+    (one CSV row per (launch, metric))."""
     rows = list(csv.reader(open(path)))
     hi = [i for i, r in enumerate(rows) if "Kernel Name" in r][0]
     h, data = rows[hi], rows[hi + 1:]
     ki, vi, ui = h.index("Kernel Name"), h.index("Metric Value"), h.index("Metric Unit")
-    agg = collections.OrderedDict()
-    unit = None
+    mi = h.index("Metric Name")
+    tscale = {"ns": 1e-6, "nsecond": 1e-6, "us": 1e-3, "usecond": 1e-3, "ms": 1.0, "msecond": 1.0}
+    bscale = {"byte": 1e-6, "Kbyte": 1e-3, "Mbyte": 1.0, "Gbyte": 1e3}
+    agg = collections.OrderedDict()   # name -> [launches, ms, DRAM MB]
     for r in data:
         if len(r) <= vi:
             continue
         name = r[ki].split("(")[0]
-        agg.setdefault(name, [0, 0.0])
-        agg[name][0] += 1
-        agg[name][1] += float(r[vi].replace(",", ""))
-        unit = r[ui]
-    scale = {"ns": 1e-6, "nsecond": 1e-6, "us": 1e-3, "usecond": 1e-3, "ms": 1.0,
-             "msecond": 1.0}.get(unit, 1e-6)
+        v = float(r[vi].replace(",", ""))
+        e = agg.setdefault(name, [0, 0.0, 0.0])
+        if r[mi] == "gpu__time_duration.sum":
+            e[0] += 1
+            e[1] += v * tscale.get(r[ui], 1e-6)
+        elif r[mi].startswith("dram__bytes"):
+            e[2] += v * bscale.get(r[ui], 1e-6)
     tot = sum(v[1] for k, v in agg.items() if "cutlass" not in k)
-    print(f"{'launches':>8} {'total ms':>10} {'ms/launch':>10} {'share':>6}  kernel "
+    print(f"{'launches':>8} {'total ms':>10} {'ms/launch':>10} {'MB/launch':>10} {'share':>6}  kernel "
           "(cold-cache, serialised; cuBLAS peak-measurement GEMMs excluded from share)")
     for k, v in sorted(agg.items(), key=lambda x: -x[1][1]):
+        if v[0] == 0:
+            continue
         share = "" if "cutlass" in k else f"{100 * v[1] / tot:5.1f}%"
-        print(f"{v[0]:8d} {v[1] * scale:10.3f} {v[1] * scale / v[0]:10.4f} {share:>6}  {k[:90]}")
+        print(f"{v[0]:8d} {v[1]:10.3f} {v[1] / v[0]:10.4f} {v[2] / v[0]:10.1f} {share:>6}  {k[:90]}")
 
 
 def report(path):
