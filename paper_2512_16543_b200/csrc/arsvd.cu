@@ -753,7 +753,7 @@ __global__ void __launch_bounds__(128, 4) arsvd_screen_kernel(ArsvdArgs g, int64
         ok = false;
         break;
       }
-      const double l = sqrt(piv), il = 1.0 / l;
+      const double il = rsqrt(piv), l = piv * il;  // one MUFU + Newton, no divide
       lmin = fmin(lmin, l);
       lmax = fmax(lmax, l);
       __syncwarp();
@@ -804,7 +804,7 @@ __global__ void __launch_bounds__(128, 4) arsvd_screen_kernel(ArsvdArgs g, int64
             ok2 = false;
             break;
           }
-          const double l = sqrt(piv), il = 1.0 / l;
+          const double il = rsqrt(piv), l = piv * il;  // one MUFU + Newton, no divide
           __syncwarp();
           for (int a = jj + 1 + lane; a < d; a += 32) L[a * LD + jj] = cscale(L[a * LD + jj], il);
           if (lane == 0) L[jj * LD + jj] = mk<double>(l, 0.0);
@@ -928,7 +928,7 @@ LRZ_DEV bool warp_chol_tri(c128 *L, int d, int LD, const uint16_t *tri, double &
   for (int jj = 0; jj < d; ++jj) {
     const double piv = L[jj * LD + jj].re;
     if (!(piv > 0.0)) return false;
-    const double l = sqrt(piv), il = 1.0 / l;
+    const double il = rsqrt(piv), l = piv * il;  // one MUFU + Newton, no divide
     lmin = fmin(lmin, l);
     lmax = fmax(lmax, l);
     __syncwarp();
