@@ -116,10 +116,12 @@ LRZ_DEV void jacobi_sv(c128 *M, c128 *J, int K, int d, double *sval, int *perm, 
         if (!act) continue;
         const double gabs = hypot(gr, gi);
         if (!(gabs > JACOBI_TOL * sqrt(al) * sqrt(be)) || gabs == 0.0) continue;
-        const double zeta = (be - al) / (2.0 * gabs);
+        // one divide for the three quotients by |g|, rsqrt for the cosine
+        const double ig = 1.0 / gabs;
+        const double zeta = (be - al) * (0.5 * ig);
         const double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
-        const double c = 1.0 / sqrt(1.0 + t * t), s = c * t;
-        const c128 ph = mk<double>(gr / gabs, -gi / gabs);  // e^{-i phi}
+        const double c = rsqrt(1.0 + t * t), s = c * t;
+        const c128 ph = mk<double>(gr * ig, -gi * ig);  // e^{-i phi}
         c128 *wa = M + int64_t(a) * K, *wb = M + int64_t(b) * K;
         for (int k = gl; k < K; k += JG) {
           const c128 x = wa[k], y = cmul(wb[k], ph);
