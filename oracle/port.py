@@ -58,6 +58,10 @@ class Factor:
     consumed: int = 0
     s_all: np.ndarray | None = None        # full singular values of the last sketch
     e_target: float = 0.0
+    # smallest relative distance of any decision quantity to its threshold over
+    # every iteration run (cumsum(s^2) vs the energy target, and on the
+    # fallback tail s vs s_0 K eps): the near-tie indicator of SURVEY A.1
+    margin_min: float = np.inf
 
 
 @dataclass
@@ -203,6 +207,7 @@ def arsvd(dA, cfg: Cfg, rng) -> Factor:
     target = cfg.eta * energy
     k0, used = cfg.k_init, 0
     s = Uap = Vh = None
+    mmin = np.inf
     for it in range(cfg.i_max):
         d = min(k0 + cfg.p, K)
         om = SQRT_HALF * (rng.standard_normal((K, d)) + 1j * rng.standard_normal((K, d)))
@@ -211,16 +216,19 @@ def arsvd(dA, cfg: Cfg, rng) -> Factor:
         Uh, s, Vh = np.linalg.svd(Q.conj().T @ dA, full_matrices=False)
         Uap = Q @ Uh
         cum = np.cumsum(s ** 2)
+        mmin = min(mmin, float(np.min(np.abs(cum - target)) / target))
         hit = np.flatnonzero(cum >= target)
         if hit.size:
             r = int(hit[0]) + 1
             return Factor(Uap[:, :r], s[:r].copy(), Vh[:r].conj().T, r, False,
-                          it + 1, used, s.copy(), float(target))
+                          it + 1, used, s.copy(), float(target), mmin)
         k0 *= 2
     floor = s[0] * K * np.finfo(float).eps
     r = max(int(np.count_nonzero(s > floor)), 1)
+    if floor > 0:
+        mmin = min(mmin, float(np.min(np.abs(s - floor)) / floor))
     return Factor(Uap[:, :r], s[:r].copy(), Vh[:r].conj().T, r, True,
-                  cfg.i_max, used, s.copy(), float(target))
+                  cfg.i_max, used, s.copy(), float(target), mmin)
 
 
 # -- dispatcher (lowrank.py:319-373) ----------------------------------------------

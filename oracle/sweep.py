@@ -30,6 +30,7 @@ class SweepRecord:
     consumed: np.ndarray         # (T,) normals consumed
     fallback: np.ndarray         # (T,) bool
     margin: np.ndarray           # (T,) relative distance of the deciding cum to the target
+    margin_min: np.ndarray = None  # (T,) smallest decision margin over every iteration
     A_inv: list = field(default_factory=list)
     F_BB: list = field(default_factory=list)
 
@@ -52,7 +53,8 @@ def sweep_trial(H_seq, alpha, noise, P_t, cfg: port.Cfg | None, sketch,
     T, K, _ = H_seq.shape
     rec = SweepRecord(np.zeros(T), np.zeros((T, K)), np.zeros(T, np.uint8),
                       np.zeros(T, np.int64), np.zeros(T), np.zeros(T, np.int64),
-                      np.zeros(T, np.int64), np.zeros(T, bool), np.full(T, np.inf))
+                      np.zeros(T, np.int64), np.zeros(T, bool), np.full(T, np.inf),
+                      np.full(T, np.inf))
     st = None
     prev = None
     for i in range(T):
@@ -64,6 +66,7 @@ def sweep_trial(H_seq, alpha, noise, P_t, cfg: port.Cfg | None, sketch,
             st, method, k, cost, f = port.update_inverse(st, prev, H - prev, cfg, sketch)
             rec.iters[i], rec.consumed[i] = f.iters, f.consumed
             rec.fallback[i], rec.margin[i] = f.used_fallback, _margin(f)
+            rec.margin_min[i] = f.margin_min
         F_BB, _ = port.rzf_precoder(H, st.A_inv, F_RF, P_t)
         rates, total, _ = port.sum_rate(H, F_RF, F_BB, noise)
         rec.rates[i], rec.per_ut[i] = total, rates

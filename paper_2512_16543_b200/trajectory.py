@@ -94,6 +94,8 @@ class TrajectoryResult:
     consumed: np.ndarray
     spec_passes: list = field(default_factory=list)
     A_inv: np.ndarray | None = None
+    W: np.ndarray | None = None          # [B, T, N, K] power-normalised precoder F_BB
+    scale: np.ndarray | None = None      # [B, T] power normalisation s (F_BB = s F_raw)
 
 
 _MASKS: dict = {}   # dispatcher-step masks by (B, reset pattern, device)
@@ -418,7 +420,7 @@ def step_costs(method: np.ndarray, k_est: np.ndarray, is_sketch: np.ndarray, K: 
 
 def run_trajectory(H, noise, cfg: TrajectoryConfig, streams: OmegaStreams | None = None,
                    chunk: int | None = None, keep_A_inv: bool = False,
-                   device=None) -> TrajectoryResult:
+                   device=None, keep_W: bool = False) -> TrajectoryResult:
     """Run B trials x T steps.  H: numpy or torch [B, T, K, N]; noise [K] or
     [B, K]; streams: per-trial sketch streams (required for WB): host
     ``OmegaStreams`` or GPU-generated ``DeviceOmegaStreams`` (same normals)."""
@@ -447,7 +449,10 @@ def run_trajectory(H, noise, cfg: TrajectoryConfig, streams: OmegaStreams | None
             om = streams.window(L)
             if isinstance(om, np.ndarray):  # host streams (OmegaStreams); device streams stay put
                 om = torch.from_numpy(om).to(dev)
-        r = runner.run_chunk(Hc, noise_d, om, keep_A_inv=keep_A_inv)
+        r = runner.run_chunk(Hc, noise_d, om, keep_A_inv=keep_A_inv, keep_W=keep_W)
+        if keep_W:
+            # F_BB = s F_raw (precoding.py:47-52), moved to the host chunk by chunk
+            r.W = (r.W * r.scale[..., None, None].to(r.W.dtype)).cpu()
         if cfg.eta is not None:
             used = r.consumed.cpu().numpy()
             streams.advance(r.consumed if isinstance(om, torch.Tensor) and
@@ -475,7 +480,9 @@ def run_trajectory(H, noise, cfg: TrajectoryConfig, streams: OmegaStreams | None
         per_ut=torch.cat([o.per_ut for o in outs], 1).cpu().numpy(),
         method=method, k_est=k_est, iters=iters,
         cost=step_costs(method, k_est, sk_mask, K), consumed=cons, spec_passes=passes,
-        A_inv=(torch.cat([o.A_inv for o in outs], 1).cpu().numpy() if keep_A_inv else None))
+        A_inv=(torch.cat([o.A_inv for o in outs], 1).cpu().numpy() if keep_A_inv else None),
+        W=(torch.cat([o.W for o in outs], 1).numpy() if keep_W else None),
+        scale=torch.cat([o.scale for o in outs], 1).cpu().numpy())
 
 
 def run_campaign_device(spec, eta, trials, device=None, chunk: int | None = None,

@@ -1,6 +1,6 @@
 """Stage split (CUDA events between stages) of one chunk of a BASELINE config.
 
-    python scripts/stage_probe_cfg.py C3 [chunk]
+    python scripts/stage_probe_cfg.py C3 [chunk] [dtype] [eta]
 """
 
 import sys
@@ -17,12 +17,15 @@ from paper_2512_16543_b200.trajectory import TrajectoryConfig, TrajectoryRunner 
 name = sys.argv[1]
 chunk = int(sys.argv[2]) if len(sys.argv) > 2 else 50
 spec = S.CONFIGS[name]
+if len(sys.argv) > 3:
+    spec = spec.with_(dtype=sys.argv[3])
+eta_wb = float(sys.argv[4]) if len(sys.argv) > 4 else spec.eta
 dev = torch.device("cuda", 0)
 trials = list(range(spec.B))
 chans = S.DeviceChannels(spec, trials, dev)
 tdt = torch.complex64 if spec.dtype == "c64" else torch.complex128
 noise = torch.full((spec.B, spec.K), spec.noise_var, dtype=torch.float64, device=dev)
-for eta in (spec.eta, None):
+for eta in (eta_wb, None):
     cfg = TrajectoryConfig(alpha=spec.alpha, eta=eta, k_init=spec.k_init, p=spec.p,
                            i_max=spec.i_max)
     rn = TrajectoryRunner(spec.B, spec.K, spec.N, tdt, cfg, dev)
@@ -39,6 +42,6 @@ for eta in (spec.eta, None):
     tot = {}
     for nm, a, b in rn.prof:
         tot[nm] = tot.get(nm, 0.0) + a.elapsed_time(b)
-    print(name, "eta", eta, {k: round(v, 3) for k, v in tot.items()},
+    print(name, spec.dtype, "eta", eta, {k: round(v, 3) for k, v in tot.items()},
           "sum", round(sum(tot.values()), 3), "ms per", spec.B * chunk, "updates",
           "passes", r.spec_passes)
