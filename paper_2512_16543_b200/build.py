@@ -55,9 +55,27 @@ def build(force: bool = False, verbose: bool = True) -> Path:
     if not force and not _stale():
         return LIB
     OUT_DIR.mkdir(exist_ok=True)
+    obj_dir = OUT_DIR / "obj"
+    obj_dir.mkdir(exist_ok=True)
     tmp = LIB.with_suffix(".so.tmp")
-    cmd = [_nvcc(), *ARCH, *FLAGS, "-I", str(PKG.parent / "include"), "-o", str(tmp),
-           *map(str, sources()), "-lcudart"]
+    # one nvcc per translation unit, in parallel (no relocatable device code:
+    # every .cu is self-contained), then one link
+    cflags = [f for f in FLAGS if f != "-shared"]
+
+    def compile_one(src: Path) -> Path:
+        obj = obj_dir / (src.stem + ".o")
+        cmd = [_nvcc(), *ARCH, *cflags, "-I", str(PKG.parent / "include"), "-c", str(src),
+               "-o", str(obj)]
+        if verbose:
+            print(" ".join(cmd), file=sys.stderr)
+        subprocess.run(cmd, check=True)
+        return obj
+
+    from concurrent.futures import ThreadPoolExecutor
+    with ThreadPoolExecutor(max_workers=min(len(sources()), os.cpu_count() or 4)) as ex:
+        objs = list(ex.map(compile_one, sources()))
+    cmd = [_nvcc(), *ARCH, "-shared", "-Xcompiler", "-fPIC", "-o", str(tmp),
+           *map(str, objs), "-lcudart"]
     if verbose:
         print(" ".join(cmd), file=sys.stderr)
     subprocess.run(cmd, check=True)

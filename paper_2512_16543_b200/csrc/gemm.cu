@@ -891,6 +891,10 @@ static int ntiles(int K) { return (K + TM - 1) / TM; }
 // SIMT kernels instead (A/B measurements)
 int lrz_gram_dmma(int dtype, int64_t B, int K, int N, const void *H, int64_t hs, double alpha,
                   void *A, int64_t as, cudaStream_t s);
+int lrz_dmma_hn_tiles(int NN, int J);
+int lrz_dmma_hn(int dtype, int64_t B, int NN, int J, int Kd, const void *X, int64_t xs, int ldx,
+                const void *Y, int64_t ys, void *out, int64_t os, double *parts,
+                cudaStream_t s);
 int lrz_precode_dmma32(int dtype, int64_t B, int K, int N, const void *H, int64_t hs, const void *A_inv,
                        int64_t ais, const void *G_true, double alpha, double P_t,
                        const double *noise, int64_t noise_div, void *W, int64_t wst,
@@ -1104,6 +1108,21 @@ extern "C" int lrz_precode_rate(int dtype, int64_t B, int K, int N, const void *
                                 noise, noise_div, W, w_stride, scale, rates, sinr, sum_rate,
                                 info, s);
     int nparts = tm * tn;
+    if (K > 32 && use_dmma()) {
+      // FP64 tensor pipe, 64 x 64 output tiles, k streamed (dmma_tiled.cu):
+      // W = H^H A^-1 with per-CTA norm partials, then the coupling G A^-1
+      if (int rc = lrz_dmma_hn(dtype, B, N, K, K, H, h_stride, N, A_inv, ai_stride, W, w_stride,
+                               parts, s))
+        return rc;
+      if (int rc = lrz_dmma_hn(LRZ_C128, B, K, K, K, G_true, int64_t(K) * K, K, A_inv,
+                               ai_stride, Gc, int64_t(K) * K, nullptr, s))
+        return rc;
+      sinr_kernel<double><<<unsigned(B), 256, 0, s>>>(
+          K, (const c128 *)Gc, int64_t(K) * K, nullptr, parts, lrz_dmma_hn_tiles(N, K), P_t,
+          scale, noise, noise_div, rates, sinr, sum_rate, info, (const c128 *)A_inv, ai_stride,
+          alpha);
+      return lrz_launch_status("lrz_precode_rate");
+    }
     if (K <= 32) {
       const size_t es = dtype == LRZ_C64 ? 8 : 16;
       const size_t sm = (32 * 32 + 2 * PW_KC * PW_ROWS) * es;
