@@ -1,24 +1,41 @@
 #!/usr/bin/env python
-"""RZF precoder updates/s (WB-arSVD vs full inverse) on one B200 -- BASELINE.json metric.
+"""RZF precoder updates/s (WB-arSVD vs full inverse) and % of roofline on one B200
+-- the BASELINE.json metric.
 
-Workload (BASELINE.json configs[1], SURVEY.md 8(d) "C2"): N = 256 (16x16 UPA),
-K = 32 users, T = 200 orbit steps, B = 64 Monte-Carlo trials per GPU, SNR
-10 dB (alpha = K/SNR), arSVD tolerance 1e-3 (eta = 0.999), rank cap 16
-(i_max = 4), oversampling p = 5, complex128.  One bench "step" = one pass
-of the hot path over the whole batch: B * T = 12,800 precoder updates, each
-producing A^-1_t, W_t and the sum-rate (harness._sweep_trial semantics).
+Headline workload (BASELINE.json configs[4], SURVEY.md 8(d) "C5", the largest
+config whose channel tensor fits HBM): N = 4096 (64 x 64 UPA), K = 256 users,
+T = 100 orbit steps, B = 64 Monte-Carlo trials per GPU, kappa 10 dB, drift
+0.05 deg/step, SNR 10 dB (alpha = K / SNR), arSVD tolerance 1e-3 (eta =
+0.999), rank cap 32 (i_max = 5), oversampling p = 5, complex128 (the
+reference's own precision).  One bench "step" = one pass of the hot path over
+the whole batch: B * T = 6,400 precoder updates, each producing A^-1_t, the
+precoder W_t = H_t^H A^-1_t (written to HBM), its power normalisation and the
+sum-rate (harness._sweep_trial semantics, harness.py:221-255; every C5 step
+after the first is a rank-37 Woodbury update).  The channel tensor
+H (107 GB) is resident in HBM before timing; the sketch normals are generated
+on the device inside each step from the harness's per-(method, trial) PCG64
+streams.
 
-  python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+Beside the headline the line carries: the full-inversion method on the same
+workload, per-kernel CUDA-event times over the timed region with the dominant
+kernel's roofline, the end-to-end number through the public batched API with
+host channels, and per-config keys for every other BASELINE config (C1, C2
+c128/c64 incl. the paper's eta = 0.9 Woodbury regime, C3, the 12 C4 cap x tol
+runs, C5 c64), each with its dominant-kernel roofline and CPU baseline.
+
+  python bench.py [--gpus N --steps K --warmup W] [--impl reference] [--quick]
 
 --impl reference times the reference algorithm on the host CPU (the numpy
-oracle port in oracle/, all cores, BLAS pinned to one thread per worker like
-harness.py:284-293).  Multi-GPU: torchrun, one rank per GPU, trials sharded
-by rank (weak scaling, no data-path collective), max-over-ranks timing.
+oracle port of leorzf in oracle/, all cores, BLAS pinned to one thread per
+worker like harness.py:284-293) on a bounded sample of the same workload.
+Multi-GPU: torchrun, one rank per GPU, trials sharded by rank (weak scaling,
+no data-path collective), max-over-ranks timing.
 """
 
 from __future__ import annotations
 
 import argparse
+import dataclasses
 import json
 import math
 import os
@@ -36,6 +53,9 @@ sys.path.insert(0, str(ROOT))
 
 METRIC = "RZF precoder updates/s (WB-arSVD vs full inverse) and % of roofline, 1 B200"
 
+# default T-chunk per config (HBM budget of the per-chunk working set)
+CHUNK = {"C1": 50, "C2": 200, "C3": 50, "C4": 20, "C5": 20}
+
 
 def parse():
     ap = argparse.ArgumentParser()
@@ -43,23 +63,23 @@ def parse():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--config", default="C2")
+    ap.add_argument("--config", default="C5")
     ap.add_argument("--dtype", default="c128", choices=["c128", "c64"])
-    ap.add_argument("--snr", type=float, default=10.0)
     ap.add_argument("--eta", type=float, default=None)
     ap.add_argument("--trials", type=int, default=None, help="trials per GPU (default: config B)")
     ap.add_argument("--T", type=int, default=None)
-    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--chunk", type=int, default=None)
+    ap.add_argument("--e2e-trials", type=int, default=16)
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline legs")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--no-extra", action="store_true", help="skip the c64 side measurement")
-    ap.add_argument("--no-graph", action="store_true",
-                    help="launch every step eagerly instead of replaying its CUDA graph")
+    ap.add_argument("--no-extra", action="store_true", help="skip the per-config keys")
+    ap.add_argument("--quick", action="store_true", help="per-config keys at reduced T")
     return ap.parse_args()
 
 
 def _spec(args):
     from paper_2512_16543_b200 import scenario as S
-    spec = S.CONFIGS[args.config].with_(dtype=args.dtype, snr_db=args.snr)
+    spec = S.CONFIGS[args.config].with_(dtype=args.dtype)
     if args.trials:
         spec = spec.with_(B=args.trials)
     if args.T:
@@ -72,6 +92,23 @@ def workload_desc(spec, eta):
     return (f"{spec.name}: N={spec.N} ({spec.n_side}x{spec.n_side} UPA), K={spec.K}, "
             f"T={spec.T}, B={spec.B} trials/GPU, SNR {spec.snr_db:g} dB, tol {1 - eta:.0e} "
             f"(eta={eta:g}), cap {spec.cap} (i_max={spec.i_max}), p={spec.p}, {spec.dtype}")
+
+
+def cpu_model() -> str:
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def _cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
 
 
 # --------------------------------------------------------------------------- CPU legs
@@ -90,21 +127,20 @@ def _cpu_init(spec_kw=None):
         pass
     if spec_kw is not None:
         kw = dict(spec_kw)
-        kw["T"] = 3
-        _cpu_trial((kw, 0, 1.0 - kw["tol"]))
-        _cpu_trial((kw, 0, None))
+        kw["T"] = 2
+        _cpu_trial((kw, 0, 1.0 - kw["tol"], 2))
 
 
-def _cpu_pool(cores, spec):
+def _cpu_pool(cores, spec=None):
     """Spawned worker pool with BLAS pinned to one thread per process."""
-    import dataclasses
     import multiprocessing as mp
     saved = {k: os.environ.get(k) for k in _BLAS_ENV}
     for k in _BLAS_ENV:
         os.environ[k] = "1"
     try:
-        return mp.get_context("spawn").Pool(cores, initializer=_cpu_init,
-                                            initargs=(dataclasses.asdict(spec),))
+        return mp.get_context("spawn").Pool(
+            cores, initializer=_cpu_init,
+            initargs=(dataclasses.asdict(spec) if spec is not None else None,))
     finally:
         for k, v in saved.items():
             if v is None:
@@ -114,23 +150,86 @@ def _cpu_pool(cores, spec):
 
 
 def _cpu_trial(job):
-    """One trial of the reference algorithm (oracle port) on one core; channel
-    generation is outside the timed region, F_RF = I_N verbatim."""
-    spec_kw, trial, eta = job
+    """The first `steps` steps of one trial of the reference algorithm (oracle
+    port of lowrank/precoding through the _sweep_trial loop) on one core;
+    channel generation is outside the timed region.  F_RF = I_N verbatim for
+    N <= 1024, identity-elided at N = 4096."""
+    spec_kw, trial, eta, steps = job
     from oracle import port, sweep
     from paper_2512_16543_b200 import scenario as S
     spec = S.ScenarioSpec(**spec_kw)
-    H = S.trial_channels(spec, trial)
+    H = S.trial_channels(spec, trial, 0, steps)
     if spec.dtype == "c64":
         H = H.astype(np.complex64)
-    F = np.eye(spec.N)
+    F = np.eye(spec.N) if spec.N <= 1024 else None
     cfg = None if eta is None else port.Cfg(eta, spec.k_init, spec.p, spec.i_max)
     sk = None if eta is None else np.random.default_rng(
         S.stream_seed(spec.seed, S.method_label(eta), trial))
     t0 = time.perf_counter()
     sweep.sweep_trial(H, spec.alpha, S.noise_vector(spec), 1.0, cfg, sk, F_RF=F)
-    return spec.T, time.perf_counter() - t0
+    return steps, time.perf_counter() - t0
 
+
+# CPU sample per config: steps per trial, so that one worker runs ~2-6 s
+CPU_STEPS = {"C1": 50, "C2": 100, "C3": 40, "C4": 20, "C5": 8}
+
+
+def cpu_rate(spec, eta, pool, steps, n_trials):
+    """updates/s of the reference algorithm: n_trials trials x `steps` steps,
+    one trial per worker process concurrently; total updates / busiest worker."""
+    kw = dataclasses.asdict(spec)
+    res = pool.map(_cpu_trial, [(kw, t, eta, steps) for t in range(n_trials)], chunksize=1)
+    workers = pool._processes
+    busy = [0.0] * workers
+    for i, (_, sec) in enumerate(res):
+        busy[i % workers] += sec
+    return sum(r[0] for r in res) / max(busy)
+
+
+def cpu_baseline(spec, eta, pool, cores):
+    steps = min(spec.T, CPU_STEPS.get(spec.name, 20))
+    n = cores
+    v = cpu_rate(spec, eta, pool, steps, n)
+    return {"value": v, "unit": "updates/s", "cores": cores, "kind": "port",
+            "cpu_model": cpu_model(),
+            "sample": f"{n} trials x first {steps} steps of {spec.name} {spec.dtype} "
+                      f"({'conventional' if eta is None else f'eta={eta:g}'}), one trial per "
+                      "worker process, oracle port of leorzf lowrank/precoding through the "
+                      "_sweep_trial loop, BLAS 1 thread/worker, channel generation untimed"}
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    spec, eta = _spec(args)
+    cores = _cores()
+    steps = min(spec.T, CPU_STEPS.get(spec.name, 20))
+    with _cpu_pool(cores, spec) as pool:
+        for _ in range(args.warmup):
+            cpu_rate(spec, eta, pool, 2, cores)
+        wb = [cpu_rate(spec, eta, pool, steps, cores) for _ in range(args.steps)]
+    v = statistics.median(wb)
+    sample = (f"per step {cores} trials x first {steps} steps (one trial per worker), oracle "
+              f"port of leorzf lowrank/precoding through the _sweep_trial loop, "
+              f"{'F_RF = I_N verbatim' if spec.N <= 1024 else 'identity-elided F_RF (N = 4096)'}"
+              f", BLAS 1 thread/worker; CPU {cpu_model()}")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": "updates/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * cores * steps / v, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": spec.dtype,
+        "data": "synthetic (SURVEY.md 8(d) seeded Rician drift channels)",
+        "config": {"workload": workload_desc(spec, eta)},
+        "cpu_baseline": {"value": v, "unit": "updates/s", "cores": cores, "kind": "port",
+                         "cpu_model": cpu_model(), "sample": sample},
+        "e2e": {"value": v, "unit": "updates/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# --------------------------------------------------------------------------- GPU leg
 
 def _leo_cpu_job(job):
     """One LEO pass prefix of every method (oracle port of harness._sweep_trial
@@ -195,59 +294,6 @@ def leo_side(args, dev, world, max_over_ranks):
     return out
 
 
-def _cores():
-    try:
-        return len(os.sched_getaffinity(0))
-    except Exception:
-        return os.cpu_count() or 1
-
-
-def cpu_rate(spec, eta, n_trials, pool):
-    """updates/s of the reference algorithm over n_trials trials run one per
-    worker process concurrently: total updates / busiest worker's time."""
-    import dataclasses
-    kw = dataclasses.asdict(spec)
-    jobs = [(kw, t, eta) for t in range(n_trials)]
-    res = pool.map(_cpu_trial, jobs, chunksize=1)
-    workers = pool._processes
-    busy = [0.0] * workers
-    for i, (_, sec) in enumerate(res):
-        busy[i % workers] += sec
-    return sum(r[0] for r in res) / max(busy)
-
-
-def run_reference(args):
-    rank = int(os.environ.get("RANK", "0"))
-    if rank != 0:
-        return
-    spec, eta = _spec(args)
-    cores = _cores()
-    n_trials = min(spec.B, cores)
-    with _cpu_pool(cores, spec) as pool:
-        for _ in range(args.warmup):
-            cpu_rate(spec.with_(T=min(spec.T, 20)), eta, min(n_trials, cores), pool)
-        wb = [cpu_rate(spec, eta, n_trials, pool) for _ in range(args.steps)]
-        full = [cpu_rate(spec, None, n_trials, pool) for _ in range(max(1, args.steps // 2))]
-    v = statistics.median(wb)
-    sample = (f"{n_trials} trials x {spec.T} steps per step (one trial per worker), oracle port "
-              f"of leorzf lowrank/precoding with F_RF = I_N verbatim, BLAS 1 thread/worker")
-    line = {
-        "impl": "reference", "metric": METRIC, "value": v, "unit": "updates/s",
-        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": 1e3 * n_trials * spec.T / v, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": spec.dtype,
-        "data": "synthetic (SURVEY.md 8(d) seeded Rician drift channels)",
-        "config": {"workload": workload_desc(spec, eta)},
-        "full_inverse": {"value": statistics.median(full), "unit": "updates/s"},
-        "cpu_baseline": {"value": v, "unit": "updates/s", "cores": cores, "kind": "port",
-                         "sample": sample},
-        "e2e": {"value": v, "unit": "updates/s", "h2d_bytes_per_step": 0,
-                "d2h_bytes_per_step": 0},
-    }
-    print(json.dumps(line), flush=True)
-
-
-# --------------------------------------------------------------------------- GPU leg
 
 class Clocks:
     """nvidia-smi sampler running during the timed region (B200_PROFILING.md)."""
@@ -328,73 +374,42 @@ def measured_peaks(torch, dev):
     return out
 
 
-def stage_model(spec, T, B, k_mean, iters_hist, wb_steps):
-    """Algorithmic flops / compulsory HBM bytes per stage for one bench step
-    (SURVEY.md 8(d) 'Algorithmic counts'; c = bytes per complex element of H;
-    K x K matrices are complex128 = 16 B)."""
+def kernel_model(name: str, spec, items: int, D: int, Dtot: int, r_mean: float,
+                 n_full: int, n_wb: int):
+    """Algorithmic (flops, compulsory HBM bytes) of ONE launch of an
+    instrumented kernel processing `items` (trial, step) items (SURVEY.md 8(d)
+    'Algorithmic counts'; complex MAC = 8 flops, Hermitian outputs counted
+    once; c = bytes per element of H; K x K matrices complex128)."""
     K, N = spec.K, spec.N
     c = 8 if spec.dtype == "c64" else 16
-    BT = B * T
-    n_sk = B * (T - 1)
-    m = {}
-    m["gram"] = (4 * K * (K + 1) * N * BT, (K * N * c + K * K * 16) * BT)
-    # difference form G_t - G_{t-1} of the fp64 Grams (TrajectoryConfig.delta "auto":
-    # the DMMA Grams accumulate in fp64 for both dtypes)
-    # (each Gram is read once as G_t and once as G_{t-1}: compulsory = one read + dA out)
-    m["gram_delta"] = (2 * K * K * n_sk, 2 * K * K * 16 * n_sk)
-    widths = []
-    k0 = spec.k_init
-    for _ in range(spec.i_max):
-        widths.append(min(k0 + spec.p, K))
-        k0 *= 2
-    f_ar = 0.0
-    b_ar = 0.0
-    for it, cnt in iters_hist.items():
-        ds = widths[:it]
-        f_ar += cnt * (4 * K * K + sum(16 * K * K * d + 32 * K * d * d for d in ds))
-        b_ar += cnt * sum(K * K * 16 + 2 * K * d * 8 for d in ds)
-    m["arsvd"] = (f_ar, b_ar)
-    n_full = BT - wb_steps
-    m["inverse"] = ((4 / 3 + 8 / 3) * K ** 3 * n_full, 2 * K * K * 16 * n_full)
-    r = max(k_mean, 1.0)
-    m["chain"] = ((24 * K * K * r + 16 * K * r * r + 8 * r ** 3 + 8 * K * K * r) * wb_steps,
-                  (2 * K * K * 16 + 2 * K * r * 16) * wb_steps)
-    # W = H^H A^-1, ||W||_F^2, H W from the Gram shortcut (G - alpha I) A^-1 (K^3,
-    # SURVEY A.6 -- the flops actually executed, not the 8 K^2 N product it replaces), SINR
-    m["precode_rate"] = ((8 * K * K * N + 8 * N * K + 8 * K ** 3 + 8 * K * K) * BT,
-                         (K * N * c + N * K * c + 2 * K * K * 16) * BT)
-    return m
-
-
-# kernels (name fragment, launches per WB step) behind each bench stage
-STAGE_KERNELS = {
-    "arsvd": [("sketch_dmma_kernel", 1), ("arsvd_screen_kernel", 1), ("arsvd_kernel", 1)],
-    "gram": [("gram_dmma_kernel", 1)],
-    "precode_rate": [("precode_dmma32_kernel", 1)],
-    "inverse": [("herm_inverse_warp_kernel", 1), ("herm_inverse_kernel", 1)],
-    "omega_rng": [("rng_pass_a", 1), ("rng_pass_b", 1), ("rng_pass_c", 1)],
-}
-
-
-# kernels that carry a stage's work (for picking the dominant kernel)
-STAGE_MAIN_KERNELS = {"arsvd": 2, "omega_rng": 3}
-
-
-def stage_traffic(stage, spec):
-    """DRAM bytes per step of a stage (sum over its kernels, per launch x launches)
-    from the committed ncu capture of the same command (profiles/, C2 c128 only)."""
-    path = ROOT / "profiles" / "r01_traffic_C2_c128.json"
-    if spec.name != "C2" or spec.dtype != "c128" or not path.exists() or stage not in STAGE_KERNELS:
-        return None
-    tab = json.loads(path.read_text())
-    tot = 0.0
-    for frag, n in STAGE_KERNELS[stage]:
-        hits = [v for k, v in tab.items() if k.split("<")[0].endswith(frag)]
-        if not hits:
-            return None
-        tot += hits[0]["dram_bytes_per_launch"] * n
-    return {"bytes_per_step": tot, "source": f"ncu dram__bytes_read.sum + dram__bytes_write.sum, "
-                                               f"{path.relative_to(ROOT)}"}
+    nb = (K + 31) // 32
+    if name == "dmma_hn_kernel:W":                 # W = H^H A^-1 + ||W||^2
+        return (8 * K * K * N + 8 * N * K) * items, (K * N * c + K * K * 16 + N * K * c) * items
+    if name == "dmma_hn_kernel:coupling":          # (G - alpha I) A^-1, SURVEY A.6
+        return 8 * K ** 3 * items, 3 * K * K * 16 * items
+    if name == "precode_dmma32_kernel":            # W + norm + coupling + SINR fused
+        return ((8 * K * K * N + 8 * N * K + 8 * K ** 3 + 8 * K * K) * items,
+                (K * N * c + N * K * c + 2 * K * K * 16) * items)
+    if name == "gram_dmma_kernel":                 # diagonal 32-row blocks (lower incl. diag)
+        kd = min(K, 32)
+        return nb * 4 * kd * (kd + 1) * N * items, (K * N * c + K * K * 16) * items
+    if name == "gram_dmma_off_kernel":             # K > 32: every lower 32 x 32 block
+        # algorithmic Hermitian count 4 K (K + 1) N (executed: nb (nb + 1) / 2 full blocks)
+        return 4 * K * (K + 1) * N * items, (K * N * c + K * K * 16) * items
+    if name in ("dmma_hn_kernel:sketch_Y", "dmma_hn_kernel:sketch_W"):
+        return 8 * K * K * Dtot * items, (K * K * 16 + 2 * K * Dtot * 16) * items
+    if name == "sketch_dmma_kernel":               # Y = dA Omega and W = dA Y, K <= 32
+        return 16 * K * K * Dtot * items, (K * K * 16 + 2 * K * Dtot * 8 + 2 * K * Dtot * 16) * items
+    if name == "arsvd_screen_kernel":              # per iteration: Gram, Cholesky, X rows
+        return 12 * K * Dtot * D * items, (2 * K * Dtot * 16 + K * K * 16) * items
+    if name in ("chain_steps (all kernels)", "chain_kernel"):
+        r = max(r_mean, 1.0)
+        return ((24 * K * K * r + 16 * K * r * r + 8 * r ** 3 + 8 * K * K * r) * n_wb,
+                (3 * K * K * 16 + 2 * K * r * 16) * n_wb)
+    if name.startswith("herm_inverse") and name != "herm_inverse_kernel":
+        # (herm_inverse_kernel only re-does the items the fast path flagged)
+        return 4 * K ** 3 * n_full, 2 * K * K * 16 * n_full
+    return None
 
 
 def run_b200(args):
@@ -414,7 +429,10 @@ def run_b200(args):
     dev = torch.device("cuda", local)
     spec, eta = _spec(args)
     B, T, K, Nn = spec.B, spec.T, spec.K, spec.N
+    chunk = args.chunk or CHUNK.get(spec.name, T)
     trials = list(range(rank * B, (rank + 1) * B))
+    tdt = torch.complex64 if spec.dtype == "c64" else torch.complex128
+    stream = torch.cuda.current_stream(dev)
 
     def barrier():
         if world > 1:
@@ -427,329 +445,371 @@ def run_b200(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
-    # ---- inputs (synthetic, seeded); resident in HBM before timing
-    H_host = S.channels(spec, trials=trials)
-    tdt = torch.complex64 if spec.dtype == "c64" else torch.complex128
-    H_pin = torch.from_numpy(H_host).pin_memory()
-    del H_host
-    H_dev = H_pin.to(dev)
-    noise = torch.from_numpy(np.ascontiguousarray(
-        np.broadcast_to(S.noise_vector(spec), (B, K)))).to(dev)
-    cfg_wb = TrajectoryConfig(alpha=spec.alpha, eta=eta, k_init=spec.k_init, p=spec.p,
-                              i_max=spec.i_max)
-    cfg_full = TrajectoryConfig(alpha=spec.alpha, eta=None)
-    L = T * TrajectoryRunner(B, K, Nn, tdt, cfg_wb, dev).normals_per_step_max()
-    # sketch streams: the harness's per-(method, trial) PCG64 Generators
-    # (harness.py:88-92), reproduced on the device; each step regenerates its
-    # window from the stream start so every timed step does identical work
-    streams = DeviceOmegaStreams.for_method(spec.seed, eta, trials, dev)
-    stream = torch.cuda.current_stream(dev)
+    def cfg_for(sp, e):
+        return TrajectoryConfig(alpha=sp.alpha, eta=e, k_init=sp.k_init, p=sp.p, i_max=sp.i_max)
 
-    # LRZ_RNG_PRIO=-1 puts the sketch RNG on a high-priority stream (its CTAs are
-    # dispatched first as SM slots free up beside the Gram)
-    rng_stream = torch.cuda.Stream(dev, priority=int(os.environ.get("LRZ_RNG_PRIO", "0")))
-
-    def one(cfg, prof=None, Hd=H_dev, st=streams, sl=slice(None), sync=True):
-        nb = Hd.shape[0]
-        rn = TrajectoryRunner(nb, K, Nn, tdt, cfg, dev)
+    def one_pass(sp, e, Hs, streams, noise, ch, prof=None, on_chunk=None):
+        """One pass of the hot path over B trials x T steps (T in chunks of ch):
+        fresh runner, sketch windows regenerated on the device from the stream
+        start, results of the last chunk returned.  Hs: list of per-chunk
+        device channel tensors, or a callable (t0, t1) -> tensor."""
+        b = noise.shape[0]
+        rn = TrajectoryRunner(b, sp.K, sp.N, tdt if sp is spec else
+                              (torch.complex64 if sp.dtype == "c64" else torch.complex128),
+                              cfg_for(sp, e), dev)
         rn.prof = prof
-        om = None
-        if cfg.eta is not None:
-            st.raw.zero_()
-            if prof is not None:   # stage profile: serialised so the RNG's own time is seen
-                e0 = rn._ev()
-                om = st.window(L)
-                rn._stage("omega_rng", e0)
-            else:                  # the step: Omega generated on a side stream under the Gram
-                om = st.window(L, stream=rng_stream)
-        return rn.run_chunk(Hd, noise[sl], om, omega_ready=st.ready, sync=sync)
+        if e is not None:
+            streams.raw.zero_()
+            streams.consumed_total.zero_()
+        outs = []
+        for i, t0 in enumerate(range(0, sp.T, ch)):
+            t1 = min(sp.T, t0 + ch)
+            H = Hs[i] if isinstance(Hs, list) else Hs(t0, t1)
+            if on_chunk is not None:
+                on_chunk(i, "start")
+            om = None if e is None else streams.window((t1 - t0) * rn.normals_per_step_max())
+            r = rn.run_chunk(H, noise, om)
+            if e is not None:
+                streams.advance(r.consumed)
+            if on_chunk is not None:
+                on_chunk(i, "end")
+            outs.append(r)
+        return outs
 
-    use_graph = not args.no_graph
+    def summarize(outs):
+        method = torch.cat([o.method for o in outs], 1).cpu().numpy()
+        k_est = torch.cat([o.k_est for o in outs], 1).cpu().numpy()
+        iters = torch.cat([o.iters for o in outs], 1).cpu().numpy()
+        rates = torch.cat([o.rates for o in outs], 1).cpu().numpy()
+        info = torch.cat([o.info for o in outs], 1).cpu().numpy()
+        wb = int((method == 1).sum())
+        return {"method_counts": {"full": int((method == 0).sum()), "woodbury": wb,
+                                  "none": int((method == 2).sum())},
+                "k_mean_woodbury": float(k_est[method == 1].mean()) if wb else 0.0,
+                "iters_hist": {int(i): int(c) for i, c in zip(*np.unique(iters[iters > 0],
+                                                                         return_counts=True))},
+                "mean_sum_rate": float(rates.mean()), "finite": bool(np.isfinite(rates).all()),
+                "singular_steps": int((info == 1).sum()), "_wb": wb,
+                "_r": float(k_est[method == 1].mean()) if wb else 0.0,
+                "_full": int((method == 0).sum())}
 
-    def capture(cfg):
-        """The whole step (fresh runner, Omega window, Gram ... rate) as one CUDA
-        graph; the verifier flags of every replay accumulate on the device."""
-        acc = torch.zeros(2, dtype=torch.int32, device=dev)
-        g = torch.cuda.CUDAGraph()
-        torch.cuda.synchronize(dev)
-        with torch.cuda.graph(g):
-            r = one(cfg, sync=False)
-            if r.flags is not None:
-                acc.add_(r.flags)
-        torch.cuda.synchronize(dev)
-        return g, r, acc
-
-    def timed(cfg, steps, graph=None):
+    def timed(fn, steps):
         barrier()
         torch.cuda.synchronize(dev)
-        l0 = ops.LAUNCHES[0]
-        last = one(cfg)                      # eager step: kernel count, verified results
-        torch.cuda.synchronize(dev)
-        n_launch = ops.LAUNCHES[0] - l0
-        if graph is not None:
-            g, gres, acc = graph
-            acc.zero_()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        torch.cuda.synchronize(dev)
         e0.record(stream)
+        last = None
         for _ in range(steps):
-            if graph is not None:
-                g.replay()
-            else:
-                last = one(cfg)
+            last = fn()
         e1.record(stream)
         torch.cuda.synchronize(dev)
         barrier()
-        if graph is not None:
-            if int(acc.abs().sum().item()):
-                raise RuntimeError("graph replay left unverified arSVD steps; rerun with --no-graph")
-            # the replayed results equal the eager step's (same inputs, same streams)
-            if not torch.equal(gres.method, last.method) or \
-                    not torch.allclose(gres.rates, last.rates, rtol=0, atol=0):
-                raise RuntimeError("graph replay differs from the eager step")
-            last = gres
-        ms = max_over_ranks(e0.elapsed_time(e1)) / steps
-        return ms, n_launch, last
+        return max_over_ranks(e0.elapsed_time(e1)) / steps, last
 
-    for _ in range(args.warmup):
-        one(cfg_wb)
-        one(cfg_full)
-    graphs = {}
-    if use_graph:
-        graphs = {"wb": capture(cfg_wb), "full": capture(cfg_full)}
-        for g, _, _ in graphs.values():     # warm replays
-            g.replay()
-        torch.cuda.synchronize(dev)
-    with Clocks(local) as clk:
-        ms_wb, launches, last = timed(cfg_wb, args.steps, graphs.get("wb"))
-        ms_full, launches_full, _ = timed(cfg_full, args.steps, graphs.get("full"))
-    # stage split: separate eager steps with CUDA events between stages (serialised RNG)
-    prof = []
-    n_prof = min(args.steps, 3)
-    for _ in range(n_prof):
-        one(cfg_wb, prof)
-    torch.cuda.synchronize(dev)
-    updates = B * T
-    value = world * updates / (ms_wb / 1e3)
-    value_full = world * updates / (ms_full / 1e3)
-
-    # per-stage device time over the timed WB steps (CUDA events on the stream)
-    stage_ms = {}
-    for name, a, b in prof:
-        stage_ms[name] = stage_ms.get(name, 0.0) + a.elapsed_time(b)
-    stage_ms = {k: v / n_prof for k, v in stage_ms.items()}
-    if world > 1:
-        # one gather of the per-trial results, merged by trial index (SURVEY 8(e))
-        from paper_2512_16543_b200.dist import gather_results
-        merged = gather_results({"rates": last.rates.cpu().numpy(),
-                                 "k_est": last.k_est.cpu().numpy(),
-                                 "method": last.method.cpu().numpy()},
-                                trials, world * B, device=dev)
-        assert merged["rates"].shape == (world * B, T)
-    method = last.method.cpu().numpy()
-    k_est = last.k_est.cpu().numpy()
-    iters = last.iters.cpu().numpy()
-    wb_steps = int((method == 1).sum())
-    k_mean = float(k_est[method == 1].mean()) if wb_steps else 0.0
-    hist = {int(i): int(c) for i, c in zip(*np.unique(iters[iters > 0], return_counts=True))}
-    model = stage_model(spec, T, B, k_mean, hist, wb_steps)
     peaks = measured_peaks(torch, dev)
     mp_path = ROOT / "MEASURED_PEAKS.json"
     hbm = json.loads(mp_path.read_text())["hbm_gbs"] if mp_path.exists() else 6650.0
-    fpk = peaks["fp64"] if spec.dtype == "c128" else peaks["fp32"]
-    # dominant kernel: a stage of n main kernels is credited stage_ms / n per kernel
-    # (arSVD = sketch GEMM + screen; the launch list in profiles/ has the split),
-    # so a single-kernel stage longer than that wins
-    per_kernel = {k: stage_ms[k] / STAGE_MAIN_KERNELS.get(k, 1) for k in stage_ms if k in model}
-    dom = max(per_kernel, key=lambda k: per_kernel[k])
-    flops, byts = model[dom]
-    launches_dom = {"arsvd": max(last.spec_passes, 1), "gram_delta": 2}.get(dom, 1)
-    t = stage_ms[dom] / 1e3
-    t_f, t_b = flops / (fpk * 1e12), byts / (hbm * 1e9)
-    if t_f >= t_b:
-        roof = {"bound": "tensor", "achieved": flops / t / 1e12, "peak": fpk, "unit": "TFLOP/s",
-                "peak_source": f"measured now: cuBLAS {'DGEMM' if spec.dtype == 'c128' else 'SGEMM (TF32 off)'} 8192^3 via torch.matmul (MEASURED_PEAKS.json has no fp64/fp32 entry)"}
-    else:
-        roof = {"bound": "hbm", "achieved": byts / t / 1e9, "peak": hbm, "unit": "GB/s",
-                "peak_source": "MEASURED_PEAKS.json hbm_gbs"}
-    roof["frac"] = roof["achieved"] / roof["peak"]
-    roof["kernel"] = dom
-    roof["kernels"] = [frag for frag, _ in STAGE_KERNELS.get(dom, [])]
-    roof["launches_per_step"] = launches_dom
-    tr = stage_traffic(dom, spec)
-    roof["traffic"] = tr["bytes_per_step"] if tr else None
-    roof["traffic_note"] = (tr["source"] + "; per step, like 'algorithmic' (compulsory "
-                            "bytes: H in, W out, A^-1 and G in for the precoder; dA + Omega "
-                            "for the arSVD front end)") if tr else None
-    roof["algorithmic"] = {"flops_per_step": flops, "bytes_per_step": byts}
-    all_stages = {}
-    for k, v in stage_ms.items():
-        if k in model and v > 0:
-            f, b_ = model[k]
-            # roofline fraction of the stage: the slower of its flops at the FP64 (c64:
-            # FP32) peak and its compulsory bytes at HBM bandwidth, over its time
-            tb = max(f / (fpk * 1e12), b_ / (hbm * 1e9))
-            all_stages[k] = {"ms": v, "tflops": f / (v / 1e3) / 1e12, "gbs": b_ / (v / 1e3) / 1e9,
-                             "bound": "tensor" if f / (fpk * 1e12) >= b_ / (hbm * 1e9) else "hbm",
-                             "frac": tb / (v / 1e3)}
-        else:
-            all_stages[k] = {"ms": v}
 
-    # ---- e2e: host (pinned) channels -> device -> results back, every step.
-    # Trials are split into groups, each with its own device buffer; all H2D
-    # copies are queued back to back on a copy stream (PCIe is the bound) and
-    # group g's compute starts as soon as its copy lands.  Groups run without
-    # a host round trip (sync=False); their verifier flags accumulate on the
-    # device and are checked after the timed region.  Omega is generated on
-    # the device.
+    def roofline_table(kprof, sp, steps, items_per_launch, summ, Dtot, D):
+        """Per-kernel (per launch) achieved vs roofline from CUDA-event times over
+        the timed region; the dominant kernel (largest total time) first."""
+        fpk = peaks["fp64"]   # every N-sized product runs on the FP64 pipe (DMMA / DFMA)
+        rows = {}
+        for name, (ms, n) in kprof.items():
+            if n == 0 or ms <= 0:
+                continue
+            per_launch = ms / n
+            per_pass = n / max(steps, 1)
+            m = kernel_model(name, sp, items_per_launch, D, Dtot, summ["_r"],
+                             summ["_full"] / per_pass, summ["_wb"] / per_pass)
+            row = {"ms_total_per_step": ms / steps, "launches_per_step": n / steps,
+                   "ms_per_launch": per_launch}
+            if m is not None:
+                f, b_ = m
+                t = per_launch / 1e3
+                t_f, t_b = f / (fpk * 1e12), b_ / (hbm * 1e9)
+                if t_f >= t_b:
+                    row.update(bound="tensor", achieved=f / t / 1e12, peak=fpk, unit="TFLOP/s")
+                else:
+                    row.update(bound="hbm", achieved=b_ / t / 1e9, peak=hbm, unit="GB/s")
+                row["frac"] = row["achieved"] / row["peak"]
+                row["flops_per_launch"] = f
+                row["bytes_per_launch"] = b_
+            rows[name] = row
+        return dict(sorted(rows.items(), key=lambda kv: -kv[1]["ms_total_per_step"]))
+
+    def dominant(rows):
+        for name, r in rows.items():
+            if "frac" in r:
+                out = {k: r[k] for k in ("bound", "achieved", "peak", "unit", "frac")}
+                out.update(kernel=name, ms_per_launch=r["ms_per_launch"],
+                           launches_per_step=r["launches_per_step"],
+                           algorithmic={"flops_per_launch": r["flops_per_launch"],
+                                        "bytes_per_launch": r["bytes_per_launch"]},
+                           peak_source=("measured now: cuBLAS DGEMM 8192^3 via torch.matmul "
+                                        "(MEASURED_PEAKS.json has no FP64 entry)")
+                           if r["unit"] == "TFLOP/s" else "MEASURED_PEAKS.json hbm_gbs",
+                           traffic=None)
+                return out
+        return None
+
+    def sketch_dims(sp):
+        ds, k0 = [], sp.k_init
+        for _ in range(sp.i_max):
+            ds.append(min(k0 + sp.p, sp.K))
+            k0 *= 2
+        return sum(ds), max(ds)
+
+    # ================================================================ headline
+    noise = torch.full((B, K), spec.noise_var, dtype=torch.float64, device=dev)
+    chans = S.DeviceChannels(spec, trials, dev)
+    # inputs resident in HBM before timing (device synthesis = the host generator's
+    # channels, tests/test_gpu_rng.py); one tensor per T-chunk so each is contiguous
+    H_chunks = [chans.generate(t0, min(T, t0 + chunk)) for t0 in range(0, T, chunk)]
+    torch.cuda.synchronize(dev)
+    h_bytes = sum(h.numel() * h.element_size() for h in H_chunks)
+    streams = DeviceOmegaStreams.for_method(spec.seed, eta, trials, dev)
+    wb = lambda: one_pass(spec, eta, H_chunks, streams, noise, chunk)          # noqa: E731
+    full = lambda: one_pass(spec, None, H_chunks, None, noise, chunk)          # noqa: E731
+    for _ in range(args.warmup):
+        wb()
+        full()
+    torch.cuda.synchronize(dev)
+    l0 = ops.LAUNCHES[0]
+    ref_outs = wb()
+    launches = ops.LAUNCHES[0] - l0
+    summ = summarize(ref_outs)
+    l0 = ops.LAUNCHES[0]
+    full()
+    launches_full = ops.LAUNCHES[0] - l0
+    with Clocks(local) as clk:
+        ops.prof_enable(True, dev)
+        ms_wb, outs = timed(wb, args.steps)
+        kprof = ops.prof_collect(dev)
+        ops.prof_enable(False, dev)
+        ms_full, _ = timed(full, args.steps)
+    summ_t = summarize(outs)
+    if summ_t["method_counts"] != summ["method_counts"]:
+        raise RuntimeError("timed passes differ from the reference pass")
+    updates = B * T
+    value = world * updates / (ms_wb / 1e3)
+    value_full = world * updates / (ms_full / 1e3)
+    Dtot, D = sketch_dims(spec)
+    ktab = roofline_table(kprof, spec, args.steps, B * chunk, summ, Dtot, D)
+    roof = dominant(ktab)
+    # stage split: one more pass with events between the runner's stages
+    prof = []
+    one_pass(spec, eta, H_chunks, streams, noise, chunk, prof=prof)
+    torch.cuda.synchronize(dev)
+    stages = {}
+    for name, a, b_ in prof:
+        stages[name] = stages.get(name, 0.0) + a.elapsed_time(b_)
+    del H_chunks
+    torch.cuda.empty_cache()
+
+    # ================================================================ e2e
     e2e = None
     if not args.no_e2e:
-        ng = 8 if B % 8 == 0 else 1
-        bs = B // ng
-        gstreams = [DeviceOmegaStreams.for_method(spec.seed, eta, trials[g * bs:(g + 1) * bs], dev)
-                    for g in range(ng)]
-        bufs = [torch.empty((bs,) + tuple(H_dev.shape[1:]), dtype=H_dev.dtype, device=dev)
-                for _ in range(ng)]
+        be = min(args.e2e_trials, B)
+        ch_e = chunk
+        ech = S.DeviceChannels(spec, trials[:be], dev)
+        n_chunks = (T + ch_e - 1) // ch_e
+        host = []
+        for i in range(n_chunks):     # pinned host channels (the caller's inputs)
+            t0, t1 = i * ch_e, min(T, (i + 1) * ch_e)
+            hd = ech.generate(t0, t1)
+            hp = torch.empty(hd.shape, dtype=hd.dtype).pin_memory()
+            hp.copy_(hd)
+            host.append(hp)
+            del hd
+        bufs = [torch.empty(host[0].shape, dtype=tdt, device=dev) for _ in range(2)]
+        noise_e = noise[:be].contiguous()
+        st_e = DeviceOmegaStreams.for_method(spec.seed, eta, trials[:be], dev)
         copy_s = torch.cuda.Stream(dev)
-        outs_pin = {}
-        acc = torch.zeros(2, dtype=torch.int32, device=dev)
-        n_e2e = max(2, min(args.steps, 3))
+        out_pin = {}
+        d2h = [0]
 
-        def e2e_step():
-            copied = []
-            for g in range(ng):
+        def e2e_pass():
+            rn = TrajectoryRunner(be, K, Nn, tdt, cfg_for(spec, eta), dev)
+            st_e.raw.zero_()
+            st_e.consumed_total.zero_()
+            ready = []
+
+            def enqueue(i):
+                buf = bufs[i % 2]
+                if buf.shape[1] != host[i].shape[1]:
+                    buf = bufs[i % 2] = torch.empty(host[i].shape, dtype=tdt, device=dev)
                 with torch.cuda.stream(copy_s):
-                    copy_s.wait_stream(stream)        # previous step's readers of bufs[g]
-                    bufs[g].copy_(H_pin[g * bs:(g + 1) * bs], non_blocking=True)
+                    copy_s.wait_stream(stream)      # the buffer's previous reader is done
+                    buf.copy_(host[i], non_blocking=True)
                     ev = torch.cuda.Event()
                     ev.record(copy_s)
-                    copied.append(ev)
-            for g in range(ng):
-                stream.wait_event(copied[g])
-                r = one(cfg_wb, None, bufs[g], gstreams[g], slice(g * bs, (g + 1) * bs),
-                        sync=False)
-                if r.flags is not None:
-                    acc.add_(r.flags)
-                for name in ("rates", "per_ut", "method", "k_est"):
-                    t = getattr(r, name)
-                    key = (name, g)
-                    if key not in outs_pin:
-                        outs_pin[key] = torch.empty(t.shape, dtype=t.dtype).pin_memory()
-                    outs_pin[key].copy_(t, non_blocking=True)
+                ready.append(ev)
 
-        e2e_step()
-        barrier()
-        torch.cuda.synchronize(dev)
-        acc.zero_()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        for _ in range(n_e2e):
-            e2e_step()
-        e1.record(stream)
-        torch.cuda.synchronize(dev)
-        barrier()
-        if int(acc.abs().sum().item()):
-            raise RuntimeError("e2e groups left unverified arSVD steps")
-        ms_e2e = max_over_ranks(e0.elapsed_time(e1)) / n_e2e
-        d2h = sum(t.numel() * t.element_size() for t in outs_pin.values())
-        e2e = {"value": world * updates / (ms_e2e / 1e3), "unit": "updates/s",
-               "h2d_bytes_per_step": H_pin.numel() * H_pin.element_size(),
-               "d2h_bytes_per_step": d2h, "ms_per_step": ms_e2e,
-               "path": "TrajectoryRunner.run_chunk (public batched API over the C ABI): pinned "
-                       f"host H copied in per step in {ng} trial groups queued back to back "
-                       "on a copy stream, each group's compute starting when its copy lands; "
-                       "Omega generated on the device from the harness's PCG64 streams; "
-                       "rates/per-UT rates/method/k_est copied out"}
-        del bufs
+            enqueue(0)
+            nbytes = 0
+            for i in range(n_chunks):
+                if i + 1 < n_chunks:
+                    enqueue(i + 1)
+                stream.wait_event(ready[i])
+                t1 = min(T, (i + 1) * ch_e)
+                om = st_e.window((t1 - i * ch_e) * rn.normals_per_step_max())
+                r = rn.run_chunk(bufs[i % 2], noise_e, om)
+                st_e.advance(r.consumed)
+                for nm in ("rates", "per_ut", "method", "k_est"):
+                    t_ = getattr(r, nm)
+                    key = (nm, i)
+                    if key not in out_pin or out_pin[key].shape != t_.shape:
+                        out_pin[key] = torch.empty(t_.shape, dtype=t_.dtype).pin_memory()
+                    out_pin[key].copy_(t_, non_blocking=True)
+                    nbytes += t_.numel() * t_.element_size()
+            d2h[0] = nbytes
 
-    # ---- c64 side measurement (same workload, complex64 inputs)
-    extra = None
-    if not args.no_extra and spec.dtype == "c128":
-        H64 = H_dev.to(torch.complex64)
-        torch.cuda.synchronize(dev)
+        e2e_pass()
+        ms_e2e, _ = timed(e2e_pass, max(2, min(args.steps, 3)))
+        e2e = {"value": world * be * T / (ms_e2e / 1e3), "unit": "updates/s",
+               "h2d_bytes_per_step": int(sum(h.numel() * h.element_size() for h in host)),
+               "d2h_bytes_per_step": int(d2h[0]), "ms_per_step": ms_e2e,
+               "trials_per_gpu": be,
+               "path": "TrajectoryRunner.run_chunk (public batched API over the C ABI) on "
+                       f"{be} of the {B} trials x all {T} steps: each {ch_e}-step chunk of "
+                       "pinned host channels copied H2D on a copy stream (double-buffered, "
+                       "overlapping the previous chunk's compute), sketch normals from the "
+                       "harness's PCG64 streams on the device, rates / per-UT rates / methods / "
+                       "ranks copied back to pinned host memory"}
+        del host, bufs
+        torch.cuda.empty_cache()
 
-        def one64(cfg):
-            rn = TrajectoryRunner(B, K, Nn, torch.complex64, cfg, dev)
-            om = None
-            if cfg.eta is not None:
-                streams.raw.zero_()
-                om = streams.window(L)
-            return rn.run_chunk(H64, noise, om)
+    # ================================================================ per-config keys
+    configs = {}
+    if not args.no_extra:
+        cores = _cores()
+        runs = [
+            ("C1_c128", "C1", {}, [spec_eta_default, None], 2),
+            ("C2_c128", "C2", {}, [spec_eta_default, None], 3),
+            ("C2_c128_eta0.9", "C2", {}, [0.9], 3),
+            ("C2_c64", "C2", {"dtype": "c64"}, [spec_eta_default, None], 3),
+            ("C3_c64", "C3", {}, [spec_eta_default, None], 1),
+            ("C5_c64", "C5", {"dtype": "c64"}, [spec_eta_default, None], 1),
+        ]
+        for cap in (4, 8, 16, 32):
+            for tol in (1e-2, 1e-3, 1e-4):
+                lab = f"C4_cap{cap}_tol{tol:g}"
+                runs.append((lab, "C4", {"cap": cap, "tol": tol},
+                             [spec_eta_default] + ([None] if (cap, tol) == (16, 1e-3) else []),
+                             1))
+        for lab, name, ov, etas, reps in runs:
+            sp = S.CONFIGS[name].with_(**ov)
+            if args.quick:
+                sp = sp.with_(T=min(sp.T, 2 * CHUNK[name]))
+            configs[lab] = run_config(sp, etas, reps, rank, world, dev, one_pass, summarize,
+                                      roofline_table, dominant, sketch_dims, timed, ops, S,
+                                      DeviceOmegaStreams, torch)
+            torch.cuda.empty_cache()
+        if rank == 0 and world == 1 and not args.no_cpu:
+            for lab, name, ov, etas, _ in runs:
+                if lab.startswith("C4") and lab != "C4_cap16_tol0.001":
+                    continue
+                sp = S.CONFIGS[name].with_(**ov)
+                e = etas[0] if etas[0] is not None else sp.eta
+                e = sp.eta if e == "default" else e
+                with _cpu_pool(cores, sp) as pool:
+                    configs[lab]["cpu_baseline"] = cpu_baseline(sp, e, pool, cores)
 
-        for cfg in (cfg_wb, cfg_full):
-            one64(cfg)
-        res64 = {}
-        for name, cfg in (("wb", cfg_wb), ("full", cfg_full)):
-            torch.cuda.synchronize(dev)
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record(stream)
-            for _ in range(args.steps):
-                one64(cfg)
-            e1.record(stream)
-            torch.cuda.synchronize(dev)
-            res64[name] = world * updates / (max_over_ranks(e0.elapsed_time(e1)) / args.steps / 1e3)
-        extra = {"c64_wb_updates_per_s": res64["wb"], "c64_full_updates_per_s": res64["full"]}
-        del H64
-
-    # ---- the reference's own LEO campaign (hybrid beams), SURVEY 8(f) #3/#4
     leo = None
     if not args.no_extra:
-        # the campaign allocates its own multi-GB chunk buffers: hand back the
-        # graph pools and cached blocks of the C2 measurements first
-        graphs.clear()
-        torch.cuda.synchronize(dev)
-        torch.cuda.empty_cache()
         leo = leo_side(args, dev, world, max_over_ranks)
 
-    # ---- CPU baseline (rank 0, N = 1 only)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         cores = _cores()
-        n_trials = min(B, cores)
         with _cpu_pool(cores, spec) as pool:
-            v_cpu = cpu_rate(spec, eta, n_trials, pool)
-        cpu = {"value": v_cpu, "unit": "updates/s", "cores": cores, "kind": "port",
-               "sample": f"{n_trials} trials x {spec.T} steps of the WB-arSVD method, one trial "
-                         f"per worker process, oracle port with F_RF = I_N verbatim, "
-                         f"BLAS 1 thread/worker"}
+            cpu = cpu_baseline(spec, eta, pool, cores)
 
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "updates/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_wb,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-            "dtype": spec.dtype + (" (fp64 arithmetic)" if spec.dtype == "c128" else
-                                   " (fp32 N-sized products, fp64 K x K chain)"),
-            "data": "synthetic (SURVEY.md 8(d) seeded Rician drift channels; the reference has "
-                    "no public dataset)",
-            "config": {"workload": workload_desc(spec, eta),
-                       "parallelism": f"trials sharded over {world} GPU(s)",
-                       "l2": "inputs larger than L2 (H = %.2f GB per GPU), no flush needed"
-                             % (H_pin.numel() * H_pin.element_size() / 1e9),
-                       "updates_per_step": updates * world},
+            "dtype": spec.dtype,
+            "data": "synthetic (SURVEY.md 8(d) seeded Rician drift channels, synthesised on the "
+                    "device = the host generator's values; the reference has no public dataset)",
+            "config": {"workload": workload_desc(spec, eta)},
+            "l2": "inputs larger than L2 (H = %.1f GB per GPU resident in HBM), no flush needed"
+                  % (h_bytes / 1e9),
+            "updates_per_step": updates * world,
+            "method": "WB-arSVD (eta = 1 - tol, SURVEY D3), every step after the first a "
+                      "Woodbury update; Omega generated on the device inside every step; W "
+                      "written to HBM",
             "full_inverse": {"value": value_full, "unit": "updates/s", "ms_per_step": ms_full,
                              "gpu_launches": launches_full},
             "roofline": roof,
-            "stages": all_stages,
+            "kernels": ktab,
+            "stages_ms_per_step": stages,
             "peaks_measured": peaks,
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": launches,
-            "spec_passes": last.spec_passes,
-            "omega": "generated on the device each step (PCG64 + numpy ziggurat, the "
-                     "harness's per-(method, trial) streams; bit-exact except ulp-level "
-                     "log1p tail values)",
-            "method_counts": {"full": int((method == 0).sum()), "woodbury": wb_steps,
-                              "none": int((method == 2).sum())},
             "clocks": clk.summary(),
+            **{k: v for k, v in summ.items() if not k.startswith("_")},
+            "configs": configs,
         }
-        if extra:
-            line["c64"] = extra
         if leo:
             line["leo_campaign"] = leo
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+spec_eta_default = "default"
+
+
+def run_config(sp, etas, reps, rank, world, dev, one_pass, summarize, roofline_table, dominant,
+               sketch_dims, timed, ops, S, DeviceOmegaStreams, torch):
+    """One BASELINE config: full trial count and T, channels synthesised on the
+    device per T-chunk (C4's 215 GB pass is streamed); each method timed over
+    `reps` passes after one warm-up pass.  `updates_per_s` counts the runner
+    (CUDA events around every run_chunk), `updates_per_s_with_channels` the
+    whole pass including the channel synthesis."""
+    B, T = sp.B, sp.T
+    trials = list(range(rank * B, (rank + 1) * B))
+    ch = min(T, CHUNK.get(sp.name, T))
+    chans = S.DeviceChannels(sp, trials, dev)
+    noise = torch.full((B, sp.K), sp.noise_var, dtype=torch.float64, device=dev)
+    stream = torch.cuda.current_stream(dev)
+    out = {"workload": None, "B": B, "T": T, "chunk": ch, "dtype": sp.dtype}
+    for e in etas:
+        e = sp.eta if e == "default" else e
+        streams = None if e is None else DeviceOmegaStreams.for_method(sp.seed, e, trials, dev)
+        evs = []
+
+        def mark(i, what):
+            ev = torch.cuda.Event(enable_timing=True)
+            ev.record(stream)
+            evs.append(ev)
+
+        run = lambda: one_pass(sp, e, chans.generate, streams, noise, ch, on_chunk=mark)  # noqa
+        run()
+        torch.cuda.synchronize(dev)
+        evs.clear()
+        ops.prof_enable(True, dev)
+        ms, outs = timed(run, reps)
+        kprof = ops.prof_collect(dev)
+        ops.prof_enable(False, dev)
+        runner_ms = sum(evs[i].elapsed_time(evs[i + 1]) for i in range(0, len(evs), 2)) / reps
+        summ = summarize(outs)
+        Dtot, D = sketch_dims(sp)
+        ktab = roofline_table(kprof, sp, reps, B * ch, summ, Dtot, D)
+        key = "conventional" if e is None else f"wb_eta{e:g}"
+        out[key] = {
+            "updates_per_s": world * B * T / (runner_ms / 1e3),
+            "updates_per_s_with_channels": world * B * T / (ms / 1e3),
+            "ms_per_pass": runner_ms, "roofline": dominant(ktab),
+            "kernels_top": dict(list(ktab.items())[:6]),
+            **{k: v for k, v in summ.items() if not k.startswith("_")}}
+        out["workload"] = workload_desc(sp, e if e is not None else sp.eta)
+    return out
+
 
 
 def main():

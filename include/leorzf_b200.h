@@ -20,9 +20,8 @@
  *    lrz_last_error()).  Per-item numerical outcomes go to `info[item]`
  *    (LRZ_INFO_*), which the Python layer maps to the reference exceptions
  *    (pkg/src/leorzf/errors.py:28-50).
- *  - No host synchronisation inside calls except lrz_traj_* (see below), no
- *    allocation, deterministic (fixed reduction orders, no atomics on
- *    values).
+ *  - No host synchronisation inside calls, no allocation, deterministic
+ *    (fixed reduction orders, no atomics on values).
  */
 #ifndef LEORZF_B200_H
 #define LEORZF_B200_H
@@ -57,6 +56,13 @@ int lrz_version(void);
 const char *lrz_last_error(void);
 /* 0 if `device` is a compute-capability 10.0 part this library was built for. */
 int lrz_device_check(int device);
+
+/* Per-kernel device timing: lrz_prof_enable(1) brackets every instrumented
+ * launch with CUDA events on its stream (0 turns it off); lrz_prof_collect()
+ * waits for them and returns "kernel=ms_total:launches;..." for the launches
+ * since the last enable/collect (bench.py's per-kernel roofline timing). */
+int lrz_prof_enable(int on);
+const char *lrz_prof_collect(void);
 
 /* K1  Gram + regularisation: A[i] = 0.5 (H H^H + (H H^H)^H) + alpha I.
  *     Replaces lowrank.py:160-162 (and :365-366).  H: [B][K][N] dtype,

@@ -43,6 +43,8 @@ _SIGS = {
     "lrz_version": (C.c_int, []),
     "lrz_last_error": (C.c_char_p, []),
     "lrz_device_check": (C.c_int, [C.c_int]),
+    "lrz_prof_enable": (C.c_int, [C.c_int]),
+    "lrz_prof_collect": (C.c_char_p, []),
     "lrz_gram": (C.c_int, [C.c_int, I64, C.c_int, C.c_int, P, I64, F64, P, I64, P]),
     "lrz_gram_delta": (C.c_int, [C.c_int, I64, C.c_int, C.c_int, P, I64, P, I64, C.c_int, P,
                                  I64, P]),

@@ -21,6 +21,12 @@ int lrz_sketch_gemm(int64_t B, int K, int Dtot, const void *dA, int64_t a_stride
                     int64_t orow_div, const int64_t *cursor, int k_init, int p,
                     const uint8_t *mask, void *Y, void *W, void *stream);
 
+int lrz_use_dmma();
+int lrz_sketch_dmma_large(int64_t B, int K, int Dtot, const void *dA, int64_t a_stride,
+                          const double *omega, int64_t omega_stride, const int32_t *omega_row,
+                          int64_t orow_div, const int64_t *cursor, int k_init, int p,
+                          const uint8_t *mask, void *Om, void *Y, void *W, cudaStream_t s);
+
 namespace lrz {
 
 constexpr int ARSVD_THREADS = 256;
@@ -43,6 +49,8 @@ struct ArsvdArgs {
   int k_init, p, i_max, D;
   int want;  // 1: always produce U/S/V; 0: only when 2 k_est <= K (Woodbury candidate)
   const int32_t *start_it;  // nullable: iteration to resume at (warp front end), < 0 = skip
+  const c128 *ya;           // nullable: the front end's Y_all [item][K][ydtot]; a resumed
+  int ydtot;                //   iteration takes its sketch Y from there
   c128 *U, *V;
   double *S;
   int32_t *k_est, *iters, *fallback;
@@ -219,6 +227,97 @@ LRZ_DEV bool gram_certificate(const c128 *M, int K, int d, double trC, c128 *Cw,
   return isfinite(F) && F * trC <= 1e9;
 }
 
+// In-place Householder QR of the d columns (length K, column-major [d][K]) of
+// X: reflector j = (v0 at X[j][j], X[j][j+1..K-1]) with tau[j]; the strictly
+// upper part of R stays in X[c][r], r < c; R's diagonal goes to rdiag.
+// Block-cooperative (barriers inside).
+LRZ_DEV void hh_qr(c128 *X, int K, int d, double *tau, c128 *rdiag, c128 *rbuf) {
+  const int tid = threadIdx.x, NT = blockDim.x, lane = tid & 31, wid = tid >> 5, NW = NT >> 5;
+  for (int j = 0; j < d; ++j) {
+    c128 *wj = X + int64_t(j) * K;
+    if (wid == 0) {
+      double sig2 = 0.0;
+      for (int k = j + 1 + lane; k < K; k += 32) sig2 += cabs2(wj[k]);
+      sig2 = warp_sum(sig2);
+      if (lane == 0) {
+        const c128 x0 = wj[j];
+        const double ax = sqrt(cabs2(x0));
+        const double nrm = sqrt(ax * ax + sig2);
+        if (nrm == 0.0) {
+          tau[j] = 0.0;
+          rdiag[j] = czero<double>();
+        } else {
+          const c128 e = ax > 0.0 ? mk<double>(x0.re / ax, x0.im / ax) : mk<double>(1.0, 0.0);
+          const c128 v0 = mk<double>(e.re * (ax + nrm), e.im * (ax + nrm));
+          tau[j] = 2.0 / (cabs2(v0) + sig2);
+          rdiag[j] = mk<double>(-e.re * nrm, -e.im * nrm);
+          wj[j] = v0;
+        }
+      }
+    }
+    __syncthreads();
+    const double tj = tau[j];
+    if (tj != 0.0) {
+      for (int c = j + 1 + wid; c < d; c += NW) {
+        const c128 *wc = X + int64_t(c) * K;
+        double re = 0.0, im = 0.0;
+        for (int k = j + lane; k < K; k += 32) {
+          const c128 a = wj[k], b = wc[k];
+          re = fma(a.re, b.re, fma(a.im, b.im, re));
+          im = fma(a.re, b.im, fma(-a.im, b.re, im));
+        }
+        re = warp_sum(re);
+        im = warp_sum(im);
+        if (lane == 0) rbuf[c] = mk<double>(tj * re, tj * im);
+      }
+      __syncthreads();
+      const int rows = K - j, ncol = d - j - 1;
+      for (int e = tid; e < rows * ncol; e += NT) {
+        const int c = j + 1 + e / rows, k = j + e % rows;
+        const c128 v = wj[k], w = rbuf[c];
+        c128 &x = X[int64_t(c) * K + k];
+        x.re -= v.re * w.re - v.im * w.im;
+        x.im -= v.re * w.im + v.im * w.re;
+      }
+      __syncthreads();
+    }
+  }
+}
+
+// C <- Q C for the Q of hh_qr (reflectors in X, tau), C: nc columns of length K
+// (column-major [nc][K]).  Block-cooperative.
+LRZ_DEV void hh_apply(const c128 *X, int K, int d, const double *tau, c128 *C, int nc,
+                      c128 *rbuf) {
+  const int tid = threadIdx.x, NT = blockDim.x, lane = tid & 31, wid = tid >> 5, NW = NT >> 5;
+  for (int j = d - 1; j >= 0; --j) {
+    const double tj = tau[j];
+    if (tj == 0.0) continue;  // block-uniform
+    const c128 *vj = X + int64_t(j) * K;
+    for (int c = wid; c < nc; c += NW) {
+      const c128 *qc = C + int64_t(c) * K;
+      double re = 0.0, im = 0.0;
+      for (int k = j + lane; k < K; k += 32) {
+        const c128 a = vj[k], b = qc[k];
+        re = fma(a.re, b.re, fma(a.im, b.im, re));
+        im = fma(a.re, b.im, fma(-a.im, b.re, im));
+      }
+      re = warp_sum(re);
+      im = warp_sum(im);
+      if (lane == 0) rbuf[c] = mk<double>(tj * re, tj * im);
+    }
+    __syncthreads();
+    const int rows = K - j;
+    for (int e = tid; e < rows * nc; e += NT) {
+      const int c = e / rows, k = j + e % rows;
+      const c128 v = vj[k], w = rbuf[c];
+      c128 &x = C[int64_t(c) * K + k];
+      x.re -= v.re * w.re - v.im * w.im;
+      x.im -= v.re * w.im + v.im * w.re;
+    }
+    __syncthreads();
+  }
+}
+
 // One arsvd call (item) by the whole CTA, sketch stream read from `cur`,
 // resuming at iteration it0.  Returns the normals consumed (block-uniform).
 LRZ_DEV int64_t arsvd_item(const ArsvdArgs &g, const int64_t item, int64_t cur, const int it0) {
@@ -262,8 +361,10 @@ LRZ_DEV int64_t arsvd_item(const ArsvdArgs &g, const int64_t item, int64_t cur, 
   const double SQH = 0.7071067811865476;  // np.sqrt(0.5)
   int k0 = g.k_init, d = 0, it = 0, r = -1;
   bool have_sv = false, hit_found = false;
+  int yo = 0;                      // column offset of iteration it0 in Y_all
   for (int i = 0; i < it0; ++i) {  // resume: skip iterations the front end already ran
     cur += int64_t(2) * K * min(k0 + g.p, K);
+    yo += min(k0 + g.p, K);
     k0 *= 2;
   }
 
@@ -282,7 +383,15 @@ LRZ_DEV int64_t arsvd_item(const ArsvdArgs &g, const int64_t item, int64_t cur, 
     const double *zre = om + cur;
     const double *zim = zre + int64_t(K) * d;
     cur += int64_t(2) * K * d;
-    // ---- Y = dA Omega  (threads: k slow, j fast -> Omega row contiguous)
+    // ---- Y = dA Omega  (threads: k slow, j fast -> Omega row contiguous); a
+    //      resumed iteration takes the front end's Y block (same Omega, DMMA product)
+    if (g.ya && it == it0) {
+      const c128 *ys = g.ya + item * int64_t(K) * g.ydtot + yo;
+      for (int e = tid; e < K * d; e += NT) {
+        const int k = e / d, j = e - k * d;
+        Q[int64_t(j) * K + k] = ys[int64_t(k) * g.ydtot + j];
+      }
+    } else
     for (int e = tid; e < K * d; e += NT) {
       const int k = e / d, j = e - k * d;
       c128 a = czero<double>();
@@ -415,7 +524,29 @@ LRZ_DEV int64_t arsvd_item(const ArsvdArgs &g, const int64_t item, int64_t cur, 
         break;
       }
     }
-    jacobi_sv(M, J, K, d, sval, perm, s_rot);
+    if (K >= 64 && K >= 2 * d) {
+      // QR-preconditioned one-sided Jacobi: M = Q2 R2 (Householder), rotate the
+      // d x d R2 (columns of length d instead of K), then M J = Q2 (R2 J).  The
+      // rotations and singular values are those of M (M^H M = R2^H R2).
+      c128 *Rb = V, *Ub = U;   // the item's factor outputs as scratch (written below)
+      hh_qr(M, K, d, s_tau, s_ph, rbuf);
+      for (int e = tid; e < d * d; e += NT) {
+        const int c = e / d, r = e - c * d;
+        Rb[e] = r < c ? M[int64_t(c) * K + r] : (r == c ? s_ph[c] : czero<double>());
+      }
+      __syncthreads();
+      jacobi_sv(Rb, J, d, d, sval, perm, s_rot);
+      for (int e = tid; e < K * d; e += NT) {
+        const int c = e / K, k = e - c * K;
+        Ub[e] = k < d ? Rb[int64_t(c) * d + k] : czero<double>();
+      }
+      __syncthreads();
+      hh_apply(M, K, d, s_tau, Ub, d, rbuf);
+      for (int e = tid; e < K * d; e += NT) M[e] = Ub[e];
+      __syncthreads();
+    } else {
+      jacobi_sv(M, J, K, d, sval, perm, s_rot);
+    }
     have_sv = true;
     // ---- energy test on the exact singular values (lowrank.py:290-301)
     if (tid == 0) {
@@ -524,7 +655,7 @@ arsvd_seq_kernel(ArsvdArgs g, int T, const uint8_t *__restrict__ is_sketch,
 // the s_max K eps floor).  Everything else is handed to arsvd_kernel, which
 // redoes that iteration with Householder QR + one-sided Jacobi.
 // ---------------------------------------------------------------------------
-constexpr int SCR_DMAX = 32;
+constexpr int SCR_DMAX = 40;
 
 // Lower triangle of P^H P (d x d, d <= 32) for the K x d block P (row stride
 // ld) on the FP64 tensor pipe, one warp: lane (g, t) loads P[k0 + t][8a + g],
@@ -581,9 +712,14 @@ LRZ_DEV void warp_gram_dmma(const c128 *P, int64_t ld, int K, int d, c128 *L, in
     case 1: warp_gram_dmma_nb<1, 0, 1>(P, ld, K, d, L, LD); break;
     case 2: warp_gram_dmma_nb<2, 0, 2>(P, ld, K, d, L, LD); break;
     case 3: warp_gram_dmma_nb<3, 0, 3>(P, ld, K, d, L, LD); break;
-    default:  // 10 tiles in two passes (register budget of the 4-CTA/SM screen)
+    case 4:  // 10 tiles in two passes (register budget of the 4-CTA/SM screen)
       warp_gram_dmma_nb<4, 0, 3>(P, ld, K, d, L, LD);
       warp_gram_dmma_nb<4, 3, 4>(P, ld, K, d, L, LD);
+      break;
+    default:  // d <= 40 (large K, cap 32 + p): 15 tiles in three passes
+      warp_gram_dmma_nb<5, 0, 3>(P, ld, K, d, L, LD);
+      warp_gram_dmma_nb<5, 3, 4>(P, ld, K, d, L, LD);
+      warp_gram_dmma_nb<5, 4, 5>(P, ld, K, d, L, LD);
       break;
   }
 }
@@ -1163,6 +1299,8 @@ extern "C" int lrz_arsvd(int64_t B, int K, const void *dA, int64_t a_stride,
   g.D = cfg->d_max;
   g.want = want_factor;
   g.start_it = nullptr;
+  g.ya = nullptr;
+  g.ydtot = 0;
   g.U = (c128 *)U;
   g.V = (c128 *)V;
   g.S = S;
@@ -1201,11 +1339,18 @@ extern "C" int lrz_arsvd(int64_t B, int K, const void *dA, int64_t a_stride,
     c128 *Om = (c128 *)wp;
     c128 *Ya = (c128 *)(wp + blk);
     c128 *Wa = (c128 *)(wp + 2 * blk);
-    // Y = dA Omega_all; for K <= 32 the same kernel also forms W = dA Y per tile
-    int rc = lrz_sketch_gemm(B, K, Dtot, dA, a_stride, omega, omega_stride, omega_row, 1, cursor,
-                             cfg->k_init, cfg->p, item_mask, Ya, K <= 32 ? Wa : nullptr, stream);
+    // Y = dA Omega_all; for K <= 32 the same kernel also forms W = dA Y per tile;
+    // K > 32: Omega gathered, both products on the FP64 tensor pipe (dmma_tiled.cu)
+    const bool large_dmma = K > 32 && lrz_use_dmma();
+    int rc = large_dmma
+                 ? lrz_sketch_dmma_large(B, K, Dtot, dA, a_stride, omega, omega_stride,
+                                         omega_row, 1, cursor, cfg->k_init, cfg->p, item_mask,
+                                         Om, Ya, Wa, st)
+                 : lrz_sketch_gemm(B, K, Dtot, dA, a_stride, omega, omega_stride, omega_row, 1,
+                                   cursor, cfg->k_init, cfg->p, item_mask, Ya,
+                                   K <= 32 ? Wa : nullptr, stream);
     if (rc) return rc;
-    if (K > 32) {
+    if (K > 32 && !large_dmma) {
       rc = lrz_cgemm(LRZ_C128, B, K, Dtot, K, 0, dA, K, a_stride, 0, Ya, Dtot, int64_t(K) * Dtot,
                      Wa, Dtot, int64_t(K) * Dtot, stream);
       if (rc) return rc;
@@ -1216,9 +1361,16 @@ extern "C" int lrz_arsvd(int64_t B, int K, const void *dA, int64_t a_stride,
       lrz_set_error("lrz_arsvd: cannot reserve %zu bytes of shared memory", sm);
       return LRZ_ELAUNCH;
     }
-    arsvd_screen_kernel<<<unsigned((B + 3) / 4), 128, sm, st>>>(g, B, Dtot, Ya, Wa, Om, resume);
+    {
+      LrzProf prof("arsvd_screen_kernel", st);
+      arsvd_screen_kernel<<<unsigned((B + 3) / 4), 128, sm, st>>>(g, B, Dtot, Ya, Wa, Om,
+                                                                  resume);
+    }
     g.start_it = resume;
+    g.ya = Ya;
+    g.ydtot = Dtot;
   }
+  LrzProf prof("arsvd_kernel", st);
   arsvd_kernel<<<unsigned(B), ARSVD_THREADS, 0, st>>>(g);
   return lrz_launch_status("lrz_arsvd");
 }
@@ -1259,6 +1411,8 @@ extern "C" int lrz_arsvd_seq(int64_t B, int T, int K, const void *dA, const doub
   g.D = cfg->d_max;
   g.want = want_factor;
   g.start_it = nullptr;
+  g.ya = nullptr;
+  g.ydtot = 0;
   g.U = (c128 *)U;
   g.V = (c128 *)V;
   g.S = S;
@@ -1268,6 +1422,7 @@ extern "C" int lrz_arsvd_seq(int64_t B, int T, int K, const void *dA, const doub
   g.consumed = consumed;
   g.mask = nullptr;
   g.ws = (c128 *)workspace;
+  LrzProf prof("arsvd_seq_kernel", (cudaStream_t)stream);
   arsvd_seq_kernel<<<unsigned(B), ARSVD_THREADS, 0, (cudaStream_t)stream>>>(
       g, T, is_sketch, first_unverified, cursor, iters_pred);
   return lrz_launch_status("lrz_arsvd_seq");
@@ -1312,6 +1467,7 @@ extern "C" int lrz_arsvd_walk(int64_t B, int T, int K, const void *dA, const dou
     lrz_set_error("lrz_arsvd_walk: cannot reserve %zu bytes of shared memory", sm);
     return LRZ_ELAUNCH;
   }
+  LrzProf prof("arsvd_walk_kernel", (cudaStream_t)stream);
   arsvd_walk_kernel<<<unsigned(B), 32, sm, (cudaStream_t)stream>>>(g, T, is_sketch,
                                                                    first_unverified, cursor,
                                                                    iters_pred);

@@ -63,3 +63,78 @@ extern "C" size_t lrz_workspace_bytes(int op, int dtype, int64_t B, int K, int N
       return 0;
   }
 }
+
+// ---- per-kernel event profiler (prof.cuh) -----------------------------------
+#include <map>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "prof.cuh"
+
+namespace {
+struct ProfState {
+  std::mutex mu;
+  int on = 0;
+  std::vector<cudaEvent_t> pool;  // events handed out since the last collect
+  size_t next = 0;
+  std::vector<std::pair<std::string, std::pair<cudaEvent_t, cudaEvent_t>>> recs;
+  std::string out;
+};
+ProfState &prof() {
+  static ProfState p;
+  return p;
+}
+}  // namespace
+
+int lrz_prof_on() { return prof().on; }
+
+cudaEvent_t lrz_prof_event() {
+  ProfState &p = prof();
+  std::lock_guard<std::mutex> lk(p.mu);
+  if (p.next == p.pool.size()) {
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    p.pool.push_back(e);
+  }
+  return p.pool[p.next++];
+}
+
+void lrz_prof_record(const char *name, cudaEvent_t a, cudaEvent_t b) {
+  ProfState &p = prof();
+  std::lock_guard<std::mutex> lk(p.mu);
+  p.recs.push_back({name, {a, b}});
+}
+
+extern "C" int lrz_prof_enable(int on) {
+  ProfState &p = prof();
+  std::lock_guard<std::mutex> lk(p.mu);
+  p.on = on;
+  p.recs.clear();
+  p.next = 0;
+  return LRZ_OK;
+}
+
+extern "C" const char *lrz_prof_collect(void) {
+  ProfState &p = prof();
+  std::lock_guard<std::mutex> lk(p.mu);
+  std::map<std::string, std::pair<double, int>> agg;
+  for (auto &r : p.recs) {
+    cudaEventSynchronize(r.second.second);
+    float ms = 0.f;
+    if (cudaEventElapsedTime(&ms, r.second.first, r.second.second) != cudaSuccess) ms = -1.f;
+    auto &a = agg[r.first];
+    a.first += ms;
+    a.second += 1;
+  }
+  p.recs.clear();
+  p.next = 0;
+  p.out.clear();
+  char buf[256];
+  for (auto &kv : agg) {
+    snprintf(buf, sizeof(buf), "%s=%.6f:%d;", kv.first.c_str(), kv.second.first,
+             kv.second.second);
+    p.out += buf;
+  }
+  return p.out.c_str();
+}

@@ -880,6 +880,7 @@ extern "C" int lrz_herm_inverse(int64_t B, int K, const void *A, int64_t a_strid
   if (K <= 32 && workspace) {
     // warp-per-matrix fast path; the CTA kernel re-does only flagged items
     uint8_t *redo = (uint8_t *)workspace;
+    LrzProf prof("herm_inverse_warp_kernel", st);
     if (K <= 16)
       herm_inverse_warp_kernel<16><<<unsigned((B + 3) / 4), 128, 0, st>>>(
           B, K, (const c128 *)A, a_stride, (c128 *)A_inv, ai_stride, info, cond_limit,
@@ -916,12 +917,14 @@ extern "C" int lrz_herm_inverse(int64_t B, int K, const void *A, int64_t a_strid
     at[0].val.clusterDim.z = 1;
     lc.attrs = at;
     lc.numAttrs = 1;
+    LrzProf prof("herm_inverse_cluster_kernel", st);
     if (cudaLaunchKernelEx(&lc, herm_inverse_cluster_kernel, K, CS, bsz, (const c128 *)A, a_stride,
                            (c128 *)A_inv, ai_stride, info, cond_limit, item_mask, redo) !=
         cudaSuccess)
       return lrz_launch_status("herm_inverse_cluster_kernel");
     mask = redo;
   }
+  LrzProf prof("herm_inverse_kernel", st);
   herm_inverse_kernel<<<unsigned(B), INV_THREADS, sm, st>>>(
       K, (const c128 *)A, a_stride, (c128 *)A_inv, ai_stride, info, cond_limit, mask);
   return lrz_launch_status("lrz_herm_inverse");
@@ -967,6 +970,7 @@ extern "C" int lrz_chain(int64_t B, int T, int K, int d_max, const uint8_t *plan
   const size_t sm = resident ? lrz_chain_smem(K, d_max)
                              : InvSmem::bytes(K, d_max, K <= INV_SMEM_KMAX) + wb_aux_smem(d_max);
   if (set_smem((const void *)chain_kernel, sm)) return LRZ_ELAUNCH;
+  LrzProf prof("chain_kernel", (cudaStream_t)stream);
   chain_kernel<<<unsigned(B), INV_THREADS, sm, (cudaStream_t)stream>>>(
       T, K, d_max, plan, (const c128 *)G, (const c128 *)A_inv_prev, (c128 *)A_inv_seq,
       (c128 *)A_state, (const c128 *)U, (const c128 *)V, S, r, method, info,
@@ -987,6 +991,7 @@ extern "C" int lrz_chain_steps(int64_t B, int T, int K, int d_max, const uint8_t
   }
   if (B == 0) return LRZ_OK;
   cudaStream_t st = (cudaStream_t)stream;
+  LrzProf prof("chain_steps (all kernels)", st);
   {
     // step-parallel chain: the trials advance together, products batched over them
     c128 *ws = (c128 *)workspace;

@@ -83,6 +83,7 @@ extern "C" int lrz_channels(int dtype, int64_t B, int t0, int T, int K, int N, i
   const int64_t rows = B * int64_t(T) * K;  // one warp per row
   const unsigned nb = unsigned(std::min<int64_t>((rows + 7) / 8, 148 * 64));
   cudaStream_t s = (cudaStream_t)stream;
+  LrzProf prof("channel_kernel", s);
   if (dtype == LRZ_C64)
     channel_kernel<float><<<nb, 256, 0, s>>>(B, t0, T, K, N, n_side, params, scatter,
                                              scatter_stride, (c64 *)H);

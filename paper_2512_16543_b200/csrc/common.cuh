@@ -6,6 +6,7 @@
 #include <stdint.h>
 
 #include "../../include/leorzf_b200.h"
+#include "prof.cuh"
 
 #define LRZ_DEV __device__ __forceinline__
 

@@ -109,14 +109,18 @@ __global__ void __launch_bounds__(32 * GD_WARPS, 3)
 template <typename T>
 __global__ void __launch_bounds__(32 * GD_WARPS)
     gram_dmma_off_kernel(int64_t B, int K, int N, const cplx<T> *__restrict__ H, int64_t hs,
-                         c128 *__restrict__ A, int64_t as, int npair) {
+                         c128 *__restrict__ A, int64_t as, int npair, double alpha,
+                         int diag) {
   const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
   const int64_t wid = int64_t(blockIdx.x) * GD_WARPS + (threadIdx.x >> 5);
   if (wid >= B * npair) return;
   const int64_t item = wid / npair;
-  int p = int(wid - item * npair), I = 1;
-  while (p >= I) {  // pairs (I, J), J < I, in row order
-    p -= I;
+  // pairs (I, J) in row order: J < I, or J <= I with diag (the diagonal blocks
+  // as full 32 x 32 products: for N in the thousands the 16-tile warp streams
+  // H at the DMMA rate, the 10-tile diagonal kernel does not)
+  int p = int(wid - item * npair), I = diag ? 0 : 1;
+  while (p >= I + diag) {
+    p -= I + diag;
     ++I;
   }
   const int J = p;
@@ -167,10 +171,16 @@ __global__ void __launch_bounds__(32 * GD_WARPS)
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
         const int row = 32 * I + 8 * ib + g, col = 32 * J + 8 * jb + 2 * t + e;
-        if (row < K && col < K) {
-          const c128 z = mk<double>(cr[4 * ib + jb][e], ci[4 * ib + jb][e]);
-          a[int64_t(row) * K + col] = z;
-          a[int64_t(col) * K + row] = cconj(z);
+        if (row < K && col < K && col <= row) {
+          c128 z = mk<double>(cr[4 * ib + jb][e], ci[4 * ib + jb][e]);
+          if (row == col) {  // exactly Hermitian: real diagonal + alpha (lowrank.py:160-162)
+            z.im = 0.0;
+            z.re += alpha;
+            a[int64_t(row) * K + col] = z;
+          } else {
+            a[int64_t(row) * K + col] = z;
+            a[int64_t(col) * K + row] = cconj(z);
+          }
         }
       }
 }
@@ -361,17 +371,21 @@ template <typename T>
 static void gram_dmma_launch(int64_t B, int K, int N, const cplx<T> *h, int64_t hs, double alpha,
                              c128 *a, int64_t as, cudaStream_t s) {
   const int nb = (K + 31) / 32;
+  if (nb > 1) {
+    // K > 32: every lower 32 x 32 block (diagonal ones included) by the 16-tile kernel
+    LrzProf prof_o("gram_dmma_off_kernel", s);
+    const int np = nb * (nb + 1) / 2;
+    const unsigned no = unsigned((B * np + GD_WARPS - 1) / GD_WARPS);
+    gram_dmma_off_kernel<T><<<no, 32 * GD_WARPS, 0, s>>>(B, K, N, h, hs, a, as, np, alpha, 1);
+    return;
+  }
   const unsigned nd = unsigned((B * nb + GD_WARPS - 1) / GD_WARPS);
+  LrzProf prof_d("gram_dmma_kernel", s);
   switch (K > 32 ? 4 : (K + 7) / 8) {
     case 1: gram_dmma_kernel<1, T><<<nd, 32 * GD_WARPS, 0, s>>>(B, K, N, h, hs, alpha, a, as, nb); break;
     case 2: gram_dmma_kernel<2, T><<<nd, 32 * GD_WARPS, 0, s>>>(B, K, N, h, hs, alpha, a, as, nb); break;
     case 3: gram_dmma_kernel<3, T><<<nd, 32 * GD_WARPS, 0, s>>>(B, K, N, h, hs, alpha, a, as, nb); break;
     default: gram_dmma_kernel<4, T><<<nd, 32 * GD_WARPS, 0, s>>>(B, K, N, h, hs, alpha, a, as, nb); break;
-  }
-  if (nb > 1) {
-    const int np = nb * (nb - 1) / 2;
-    const unsigned no = unsigned((B * np + GD_WARPS - 1) / GD_WARPS);
-    gram_dmma_off_kernel<T><<<no, 32 * GD_WARPS, 0, s>>>(B, K, N, h, hs, a, as, np);
   }
 }
 
@@ -389,6 +403,7 @@ int lrz_precode_dmma32(int dtype, int64_t B, int K, int N, const void *H, int64_
                        double P_t, const double *noise, int64_t noise_div, void *W, int64_t wst,
                        double *scale, double *rates, double *sinr, double *sum_rate,
                        int32_t *info, cudaStream_t s) {
+  LrzProf prof("precode_dmma32_kernel", s);
   if (dtype == LRZ_C64)
     precode_dmma32_kernel<float><<<unsigned(B), 32 * PD_WARPS, 0, s>>>(
         K, N, (const c64 *)H, hs, (const c128 *)A_inv, ais, (const c128 *)G_true,

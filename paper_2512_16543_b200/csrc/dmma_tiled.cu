@@ -52,11 +52,13 @@ template <typename T>
 __global__ void __launch_bounds__(DT_THREADS, 2)
     dmma_hn_kernel(int NN, int J, int Kd, const cplx<T> *__restrict__ X, int64_t xs, int ldx,
                    const c128 *__restrict__ Y, int64_t ys, cplx<T> *__restrict__ out,
-                   int64_t os, double *__restrict__ parts, int tiles_n, int tiles_j) {
+                   int64_t os, double *__restrict__ parts, int tiles_n, int tiles_j,
+                   const uint8_t *__restrict__ mask) {
   using S = DtSmem<T>;
   extern __shared__ __align__(16) unsigned char dt_smem[];
   const int ntile = tiles_n * tiles_j;
   const int64_t item = blockIdx.x / ntile;
+  if (mask && !mask[item]) return;
   const int tile = int(blockIdx.x - item * ntile);
   const int n0 = (tile / tiles_j) * DT_BN, j0 = (tile % tiles_j) * DT_BJ;
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5, g = lane >> 2, t = lane & 3;
@@ -167,7 +169,8 @@ __global__ void __launch_bounds__(DT_THREADS, 2)
 template <typename T>
 static int dmma_hn_launch(int64_t B, int NN, int J, int Kd, const cplx<T> *X, int64_t xs, int ldx,
                           const c128 *Y, int64_t ys, cplx<T> *out, int64_t os, double *parts,
-                          cudaStream_t s) {
+                          const uint8_t *mask, cudaStream_t s, const char *what) {
+  LrzProf prof(what, s);
   const int tn = (NN + DT_BN - 1) / DT_BN, tj = (J + DT_BJ - 1) / DT_BJ;
   const size_t sm = DtSmem<T>::bytes;
   static bool attr = false;
@@ -186,7 +189,7 @@ static int dmma_hn_launch(int64_t B, int NN, int J, int Kd, const cplx<T> *X, in
     const int64_t bb = B - b0 < per ? B - b0 : per;
     dmma_hn_kernel<T><<<unsigned(bb * tn * tj), DT_THREADS, sm, s>>>(
         NN, J, Kd, X + b0 * xs, xs, ldx, Y + b0 * ys, ys, out + b0 * os, os,
-        parts ? parts + b0 * tn * tj : nullptr, tn, tj);
+        parts ? parts + b0 * tn * tj : nullptr, tn, tj, mask ? mask + b0 : nullptr);
   }
   (void)nb;
   return lrz_launch_status("dmma_hn_kernel");
@@ -205,10 +208,72 @@ int lrz_dmma_hn_tiles(int NN, int J) {
 // out in dtype with row length J; parts (nullable): per-CTA ||out||^2.
 int lrz_dmma_hn(int dtype, int64_t B, int NN, int J, int Kd, const void *X, int64_t xs, int ldx,
                 const void *Y, int64_t ys, void *out, int64_t os, double *parts,
-                cudaStream_t s) {
+                cudaStream_t s, const uint8_t *mask, const char *what) {
   if (dtype == LRZ_C64)
     return dmma_hn_launch<float>(B, NN, J, Kd, (const c64 *)X, xs, ldx, (const c128 *)Y, ys,
-                                 (c64 *)out, os, parts, s);
+                                 (c64 *)out, os, parts, mask, s, what);
   return dmma_hn_launch<double>(B, NN, J, Kd, (const c128 *)X, xs, ldx, (const c128 *)Y, ys,
-                                (c128 *)out, os, parts, s);
+                                (c128 *)out, os, parts, mask, s, what);
+}
+
+// Omega_all [B][K][Dtot] (complex128) gathered from the normal window: column c
+// of block i (offset o_i, width d_i) is sqrt(1/2) (zre[k d_i + j] + i zim[k d_i + j])
+// at the item's cursor, blocks back to back in the stream (lowrank.py:284-286).
+__global__ void omega_gather_kernel(int K, int Dtot, const double *__restrict__ omega,
+                                    int64_t os, const int32_t *__restrict__ orow,
+                                    int64_t orow_div, const int64_t *__restrict__ cursor,
+                                    int k_init, int p, const uint8_t *__restrict__ mask,
+                                    c128 *__restrict__ Om) {
+  const int64_t item = blockIdx.x;
+  if (mask && !mask[item]) return;
+  __shared__ int s_off[256], s_d[256], s_j[256];
+  for (int c = threadIdx.x; c < Dtot; c += blockDim.x) {
+    int o = 0, k0 = k_init, d = min(k0 + p, K), off = 0;
+    while (c >= o + d) {
+      o += d;
+      off += 2 * K * d;
+      k0 *= 2;
+      d = min(k0 + p, K);
+    }
+    s_off[c] = off;
+    s_d[c] = d;
+    s_j[c] = c - o;
+  }
+  __syncthreads();
+  const int64_t row = orow ? int64_t(orow[item]) : item / orow_div;
+  const double *z = omega + row * os + (cursor ? cursor[item] : 0);
+  const double SQH = 0.7071067811865476;
+  c128 *o = Om + item * int64_t(K) * Dtot;
+  for (int e = threadIdx.x; e < K * Dtot; e += blockDim.x) {
+    const int k = e / Dtot, c = e - k * Dtot, d = s_d[c];
+    const double *zb = z + s_off[c] + int64_t(k) * d + s_j[c];
+    o[e] = mk<double>(SQH * zb[0], SQH * zb[int64_t(K) * d]);
+  }
+}
+
+// lrz_arsvd's front end for K > 32 on the FP64 tensor pipe: Omega_all gathered,
+// Y = dA Omega_all and W = dA Y as two dmma_hn passes (dA is Hermitian, so
+// conj(dA)^T = dA).  Om, Y, W: [B][K][Dtot] complex128.
+int lrz_sketch_dmma_large(int64_t B, int K, int Dtot, const void *dA, int64_t a_stride,
+                          const double *omega, int64_t omega_stride, const int32_t *omega_row,
+                          int64_t orow_div, const int64_t *cursor, int k_init, int p,
+                          const uint8_t *mask, void *Om, void *Y, void *W, cudaStream_t s) {
+  if (Dtot > 256) {
+    lrz_set_error("lrz_sketch_dmma_large: Dtot %d > 256", Dtot);
+    return LRZ_EINVAL;
+  }
+  {
+    LrzProf prof("omega_gather_kernel", s);
+    omega_gather_kernel<<<unsigned(B), 256, 0, s>>>(K, Dtot, omega, omega_stride, omega_row,
+                                                    orow_div, cursor, k_init, p, mask,
+                                                    (c128 *)Om);
+  }
+  if (int rc = lrz_launch_status("omega_gather_kernel")) return rc;
+  const int64_t st = int64_t(K) * Dtot;
+  if (int rc = dmma_hn_launch<double>(B, K, Dtot, K, (const c128 *)dA, a_stride, K,
+                                      (const c128 *)Om, st, (c128 *)Y, st, nullptr, mask, s,
+                                      "dmma_hn_kernel:sketch_Y"))
+    return rc;
+  return dmma_hn_launch<double>(B, K, Dtot, K, (const c128 *)dA, a_stride, K, (const c128 *)Y,
+                                st, (c128 *)W, st, nullptr, mask, s, "dmma_hn_kernel:sketch_W");
 }

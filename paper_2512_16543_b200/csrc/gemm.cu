@@ -877,6 +877,7 @@ extern "C" int lrz_axpby(int dtype, int64_t n, double a, const void *X, double b
   if (n == 0) return LRZ_OK;
   const unsigned nb = unsigned(std::min<int64_t>((n + 255) / 256, 148 * 32));
   cudaStream_t s = (cudaStream_t)stream;
+  LrzProf prof("axpby_kernel", s);
   if (dtype == LRZ_C64)
     axpby_kernel<float><<<nb, 256, 0, s>>>(n, a, (const c64 *)X, b, (const c64 *)Y, (c64 *)Z);
   else
@@ -894,13 +895,16 @@ int lrz_gram_dmma(int dtype, int64_t B, int K, int N, const void *H, int64_t hs,
 int lrz_dmma_hn_tiles(int NN, int J);
 int lrz_dmma_hn(int dtype, int64_t B, int NN, int J, int Kd, const void *X, int64_t xs, int ldx,
                 const void *Y, int64_t ys, void *out, int64_t os, double *parts,
-                cudaStream_t s);
+                cudaStream_t s, const uint8_t *mask = nullptr,
+                const char *what = "dmma_hn_kernel");
 int lrz_precode_dmma32(int dtype, int64_t B, int K, int N, const void *H, int64_t hs, const void *A_inv,
                        int64_t ais, const void *G_true, double alpha, double P_t,
                        const double *noise, int64_t noise_div, void *W, int64_t wst,
                        double *scale, double *rates, double *sinr, double *sum_rate,
                        int32_t *info, cudaStream_t s);
-static bool use_dmma() {
+int lrz_use_dmma();
+static bool use_dmma() { return lrz_use_dmma() != 0; }
+int lrz_use_dmma() {
   static const int v = [] {
     const char *e = getenv("LRZ_SIMT_FP64");
     return (e && e[0] == '1') ? 0 : 1;
@@ -956,6 +960,7 @@ extern "C" int lrz_gram_delta(int dtype, int64_t B, int K, int N, const void *P,
   const int nt = ntiles(K), ntl = nt * (nt + 1) / 2;
   const dim3 grid(unsigned(B * ntl));
   cudaStream_t s = (cudaStream_t)stream;
+  LrzProf prof("gram_delta_kernel", s);
   if (dtype == LRZ_C64)
     gram_delta_kernel<float, 16><<<grid, GEMM_THREADS, 0, s>>>(
         K, N, (const c64 *)P, p_stride, (const c64 *)Q, q_stride, mode, (c128 *)dA, a_stride,
@@ -976,6 +981,7 @@ int lrz_sketch_gemm(int64_t B, int K, int Dtot, const void *dA, int64_t a_stride
   SketchOperand so{omega, omega_stride, omega_row, orow_div, cursor, k_init, p};
   const bool fuse = W != nullptr && K <= TM;
   if (fuse && use_dmma()) {
+    LrzProf prof("sketch_dmma_kernel", (cudaStream_t)stream);
     sketch_dmma_kernel<<<unsigned(B * tn), 128, 0, (cudaStream_t)stream>>>(
         K, Dtot, (const c128 *)dA, a_stride, so, mask, (c128 *)Y, tn, (c128 *)W);
     return lrz_launch_status("sketch_dmma_kernel");
@@ -983,6 +989,7 @@ int lrz_sketch_gemm(int64_t B, int K, int Dtot, const void *dA, int64_t a_stride
   const size_t sm = fuse ? 2 * size_t(TM) * (TM + 1) * sizeof(c128) : 0;
   if (fuse)
     cudaFuncSetAttribute(sketch_cgemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
+  LrzProf prof("sketch_cgemm_kernel", (cudaStream_t)stream);
   sketch_cgemm_kernel<<<unsigned(B * tm * tn), GEMM_THREADS, sm, (cudaStream_t)stream>>>(
       K, Dtot, (const c128 *)dA, a_stride, so, mask, (c128 *)Y, tn,
       fuse ? (c128 *)W : nullptr);
@@ -1112,11 +1119,13 @@ extern "C" int lrz_precode_rate(int dtype, int64_t B, int K, int N, const void *
       // FP64 tensor pipe, 64 x 64 output tiles, k streamed (dmma_tiled.cu):
       // W = H^H A^-1 with per-CTA norm partials, then the coupling G A^-1
       if (int rc = lrz_dmma_hn(dtype, B, N, K, K, H, h_stride, N, A_inv, ai_stride, W, w_stride,
-                               parts, s))
+                               parts, s, nullptr, "dmma_hn_kernel:W"))
         return rc;
       if (int rc = lrz_dmma_hn(LRZ_C128, B, K, K, K, G_true, int64_t(K) * K, K, A_inv,
-                               ai_stride, Gc, int64_t(K) * K, nullptr, s))
+                               ai_stride, Gc, int64_t(K) * K, nullptr, s, nullptr,
+                               "dmma_hn_kernel:coupling"))
         return rc;
+      LrzProf prof("sinr_kernel", s);
       sinr_kernel<double><<<unsigned(B), 256, 0, s>>>(
           K, (const c128 *)Gc, int64_t(K) * K, nullptr, parts, lrz_dmma_hn_tiles(N, K), P_t,
           scale, noise, noise_div, rates, sinr, sum_rate, info, (const c128 *)A_inv, ai_stride,

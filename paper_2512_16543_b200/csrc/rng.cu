@@ -523,6 +523,7 @@ extern "C" int lrz_rng_normals(int64_t B, int64_t L, const uint64_t *state, cons
   a.status = status;
   const int64_t n = B * a.nseg;
   cudaStream_t s = (cudaStream_t)stream;
+  LrzProf prof("rng_pass_abc", s);
   rng_pass_a<<<unsigned((n + RNG_A_THREADS - 1) / RNG_A_THREADS), RNG_A_THREADS, 0, s>>>(a);
   rng_pass_b<<<unsigned(B), RNG_B_THREADS, 0, s>>>(a);
   rng_pass_c<<<unsigned((n + RNG_C_THREADS - 1) / RNG_C_THREADS), RNG_C_THREADS, 0, s>>>(a);

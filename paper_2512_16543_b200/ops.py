@@ -94,7 +94,7 @@ def gram(H: torch.Tensor, alpha: float, out: torch.Tensor | None = None) -> torc
     lib = N.lib_for(H.device)
     N.check(lib.lrz_gram(_dt(H), B, K, Nn, H.data_ptr(), K * Nn, float(alpha), A.data_ptr(),
                          K * K, N.stream_ptr(H.device)), "lrz_gram")
-    _count(2 if (K > 32 and dmma_active()) else 1)  # diagonal + off-diagonal blocks
+    _count(1)  # K <= 32: warp per item; K > 32: warp per lower 32 x 32 block
     return A
 
 
@@ -189,8 +189,10 @@ def arsvd(dA: torch.Tensor, omega: torch.Tensor, cursor: torch.Tensor, eta, k_in
                           out["consumed"].data_ptr(), N.ptr(mask), int(want_factor),
                           int(hermitian), ws.data_ptr(), N.stream_ptr(dev)), "lrz_arsvd")
     # screening front end (sketch GEMM [+ W GEMM for K > 32] + screen) + the exact kernel
-    front = hermitian and not want_factor and D <= 32
-    _count((3 if K <= 32 else 4) if front else 1)
+    front = hermitian and not want_factor and D <= 40
+    # K <= 32: fused sketch + screen + exact; K > 32: Omega gather + Y + W GEMMs on
+    # DMMA (SIMT: sketch + W GEMM) + screen + exact
+    _count((3 if K <= 32 else (5 if dmma_active() else 4)) if front else 1)
     out["D"] = D
     return out
 
@@ -490,3 +492,25 @@ def campaign_reduce(method: torch.Tensor, k_est: torch.Tensor, t_base: int, K: i
                                     N.stream_ptr(method.device)), "lrz_campaign_reduce")
     _count(1)
     return stats
+
+
+# -- per-kernel event timing (lrz_prof_*) ------------------------------------------------
+
+def prof_enable(on: bool = True, device=None) -> None:
+    """Bracket every instrumented launch with CUDA events on its stream."""
+    lib = N.lib_for(device if device is not None else torch.device("cuda", 0))
+    lib.lrz_prof_enable(1 if on else 0)
+
+
+def prof_collect(device=None) -> dict:
+    """{kernel: (total ms, launches)} of the launches since prof_enable."""
+    lib = N.lib_for(device if device is not None else torch.device("cuda", 0))
+    out = {}
+    raw = lib.lrz_prof_collect()
+    for part in (raw.decode() if raw else "").split(";"):
+        if "=" not in part:
+            continue
+        name, v = part.split("=", 1)
+        ms, n = v.split(":")
+        out[name] = (float(ms), int(n))
+    return out
