@@ -897,6 +897,25 @@ int lrz_dmma_hn(int dtype, int64_t B, int NN, int J, int Kd, const void *X, int6
                 const void *Y, int64_t ys, void *out, int64_t os, double *parts,
                 cudaStream_t s, const uint8_t *mask = nullptr,
                 const char *what = "dmma_hn_kernel");
+int lrz_tc_w_ok(int K, int N, int64_t h_stride);
+int lrz_tc_w_tiles(int N);
+size_t lrz_tc_w_ws(int64_t B, int K);
+int lrz_tc_precoder_w(int64_t B, int K, int N, const void *H, const void *A_inv, int64_t ais,
+                      void *W, double *parts, void *ws, cudaStream_t s);
+// complex64 K > 32 precoder on tcgen05 (3xTF32, tc_tf32.cu) unless LRZ_TC=0 (A/B runs)
+static bool use_tc() {
+  static const int v = [] {
+    const char *e = getenv("LRZ_TC");
+    return (e && e[0] == '0') ? 0 : 1;
+  }();
+  return v != 0;
+}
+// items per tcgen05 precoder launch group: the pre-split A^-1 operand of a
+// group (8 (2K)^2 bytes per item) stays within 1 GB of workspace
+static int64_t tc_group(int K) {
+  const int64_t per = int64_t(8) * (2 * K) * (2 * K);
+  return std::max<int64_t>(1, (int64_t(1) << 30) / per);
+}
 int lrz_precode_dmma32(int dtype, int64_t B, int K, int N, const void *H, int64_t hs, const void *A_inv,
                        int64_t ais, const void *G_true, double alpha, double P_t,
                        const double *noise, int64_t noise_div, void *W, int64_t wst,
@@ -1080,6 +1099,9 @@ size_t lrz_precode_ws(int dtype, int64_t B, int K, int N) {
   bytes += size_t(B) * tiles * sizeof(double);
   bytes = (bytes + 255) & ~size_t(255);
   bytes += size_t(B) * N * K * es;
+  bytes = (bytes + 1023) & ~size_t(1023);
+  if (dtype == LRZ_C64 && K > 32 && K <= 256)  // tcgen05 precoder: pre-split A^-1 operand
+    bytes += lrz_tc_w_ws(std::min<int64_t>(B, tc_group(K)), K);
   return bytes;
 }
 
@@ -1101,10 +1123,12 @@ extern "C" int lrz_precode_rate(int dtype, int64_t B, int K, int N, const void *
   const int tm = ntiles(N), tn = ntiles(K);
   off += size_t(B) * tm * tn * sizeof(double);
   off = (off + 255) & ~size_t(255);
+  size_t off_w = off;
   if (!W) {
     W = ws + off;
     w_stride = int64_t(N) * K;
   }
+  void *tc_ws = ws + ((off_w + size_t(B) * N * K * 16 + 1023) & ~size_t(1023));
   cudaStream_t s = (cudaStream_t)stream;
   const dim3 g1(unsigned(B * tm * tn)), g2(unsigned(B * tn * tn));
   if (G_true) {
@@ -1116,18 +1140,32 @@ extern "C" int lrz_precode_rate(int dtype, int64_t B, int K, int N, const void *
                                 info, s);
     int nparts = tm * tn;
     if (K > 32 && use_dmma()) {
-      // FP64 tensor pipe, 64 x 64 output tiles, k streamed (dmma_tiled.cu):
-      // W = H^H A^-1 with per-CTA norm partials, then the coupling G A^-1
-      if (int rc = lrz_dmma_hn(dtype, B, N, K, K, H, h_stride, N, A_inv, ai_stride, W, w_stride,
-                               parts, s, nullptr, "dmma_hn_kernel:W"))
+      int np_w = lrz_dmma_hn_tiles(N, K);
+      if (dtype == LRZ_C64 && use_tc() && lrz_tc_w_ok(K, N, h_stride) &&
+          w_stride == int64_t(N) * K) {
+        // complex64: W = H^H A^-1 on tcgen05 (3xTF32, TMA tiles, TMEM accumulator)
+        np_w = lrz_tc_w_tiles(N);
+        const int64_t G = tc_group(K);
+        for (int64_t b0 = 0; b0 < B; b0 += G) {
+          const int64_t g = std::min<int64_t>(G, B - b0);
+          if (int rc = lrz_tc_precoder_w(g, K, N, (const c64 *)H + b0 * h_stride,
+                                         (const c128 *)A_inv + b0 * ai_stride, ai_stride,
+                                         (c64 *)W + b0 * w_stride, parts + b0 * np_w, tc_ws, s))
+            return rc;
+        }
+      } else if (int rc = lrz_dmma_hn(dtype, B, N, K, K, H, h_stride, N, A_inv, ai_stride, W,
+                                      w_stride, parts, s, nullptr, "dmma_hn_kernel:W")) {
+        // FP64 tensor pipe, 64 x 64 output tiles, k streamed (dmma_tiled.cu):
+        // W = H^H A^-1 with per-CTA norm partials, then the coupling G A^-1
         return rc;
+      }
       if (int rc = lrz_dmma_hn(LRZ_C128, B, K, K, K, G_true, int64_t(K) * K, K, A_inv,
                                ai_stride, Gc, int64_t(K) * K, nullptr, s, nullptr,
                                "dmma_hn_kernel:coupling"))
         return rc;
       LrzProf prof("sinr_kernel", s);
       sinr_kernel<double><<<unsigned(B), 256, 0, s>>>(
-          K, (const c128 *)Gc, int64_t(K) * K, nullptr, parts, lrz_dmma_hn_tiles(N, K), P_t,
+          K, (const c128 *)Gc, int64_t(K) * K, nullptr, parts, np_w, P_t,
           scale, noise, noise_div, rates, sinr, sum_rate, info, (const c128 *)A_inv, ai_stride,
           alpha);
       return lrz_launch_status("lrz_precode_rate");

@@ -309,6 +309,12 @@ def precode_rate(H: torch.Tensor, A_inv: torch.Tensor, P_t: float, noise: torch.
     row = item // noise_div.  Returns dict(W (unscaled F_raw or None), scale,
     rates [B,K], sinr, sum [B], info)."""
     _chk(H, "H")
+    _chk(A_inv, "A_inv")
+    _chk(noise, "noise")
+    if G_true is not None:
+        _chk(G_true, "G_true")
+    if W is not None:
+        _chk(W, "W")
     B, K, Nn = H.shape
     dev = H.device
     lib = N.lib_for(dev)

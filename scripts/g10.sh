@@ -1,0 +1,5 @@
+mkdir -p gpurun_out
+timeout 900 python bench.py --steps 2 --warmup 1 --no-e2e --no-cpu --quick > gpurun_out/g10_bench.json 2> gpurun_out/g10_bench.err
+echo "bench rc=$?"; tail -3 gpurun_out/g10_bench.err
+timeout 1200 python -m pytest tests -q -m gpu -x --timeout=600 > gpurun_out/g10_pytest.txt 2>&1
+tail -5 gpurun_out/g10_pytest.txt

@@ -156,3 +156,20 @@ def test_larger_configs_vs_oracle(cuda, name, B, T, dtype, etas):
             err = max(rel(res.A_inv[b, t], ref.A_inv[t]) for t in range(T))
             assert err < tol, (name, eta, err)
             assert np.max(np.abs(res.rates[b] / ref.rates - 1)) < tol, (name, eta)
+
+
+def test_per_user_noise_vector_reaches_every_trial(cuda):
+    """sigma_k^2 differs per user (precoding.py:55-80 takes a noise vector): the
+    batched runner must apply the same [K] vector to every trial (regression:
+    a broadcast [B, K] host array used to reach the kernels Fortran-ordered)."""
+    spec = S.C2.with_(B=3, T=10)
+    H = S.channels(spec)
+    noise = np.linspace(0.05, 0.3, spec.K)
+    cfg = _cfg(spec, 0.9)
+    res = run_trajectory(H, noise, cfg, OmegaStreams.for_method(spec.seed, 0.9, [0, 1, 2]))
+    for b in range(3):
+        sk = np.random.default_rng(S.stream_seed(spec.seed, S.method_label(0.9), b))
+        ref = sweep.sweep_trial(H[b], spec.alpha, noise, 1.0,
+                                port.Cfg(0.9, spec.k_init, spec.p, spec.i_max), sk)
+        assert np.array_equal(res.k_est[b], ref.k_est)
+        np.testing.assert_allclose(res.rates[b], ref.rates, rtol=1e-10)
