@@ -42,6 +42,12 @@ LRZ_DEV InvScratch carve_inv(char *sm, int n, c128 **matrix, int K, bool want_ma
 constexpr int WB_SMEM_DMAX = 40;  // aux / aux^-1 in shared memory up to this rank
 
 __host__ __device__ inline int64_t wb_ws_elems(int K, int D) {
+  // AiU, T, VhAi (K x D each) [+ aux, aux^-1 when they do not fit shared memory]
+  // + the DMMA chain's aux and aux^-1 in global memory (D x D each)
+  return 3 * int64_t(K) * D + (D > WB_SMEM_DMAX ? 2 * int64_t(D) * D : 0) + 2 * int64_t(D) * D;
+}
+// offset of the DMMA chain's global aux (then aux^-1) inside a trial's workspace
+__host__ __device__ inline int64_t wb_ws_aux_off(int K, int D) {
   return 3 * int64_t(K) * D + (D > WB_SMEM_DMAX ? 2 * int64_t(D) * D : 0);
 }
 __host__ __device__ inline size_t wb_aux_smem(int D) {
@@ -445,10 +451,14 @@ __global__ void __launch_bounds__(INV_THREADS)
     wb_core_kernel(int T, int t, int K, int D, const uint8_t *__restrict__ plan,
                    const c128 *__restrict__ V, const double *__restrict__ S,
                    const int32_t *__restrict__ r, c128 *__restrict__ ws, uint8_t *__restrict__ fb,
-                   uint8_t *__restrict__ method, int32_t *__restrict__ info) {
+                   uint8_t *__restrict__ method, int32_t *__restrict__ info, int dmma) {
   extern __shared__ __align__(16) char wbc_smem[];
   const int64_t b = blockIdx.x, bt = b * T + t;
-  if (plan[bt] != 1) return;
+  const int64_t nB = gridDim.x;
+  if (plan[bt] != 1) {
+    if (threadIdx.x == 0) fb[nB + b] = 0;  // act: no Woodbury apply for this trial
+    return;
+  }
   const int tid = threadIdx.x, NT = blockDim.x;
   const int rr = r[bt];
   WbScratch sc;
@@ -458,15 +468,20 @@ __global__ void __launch_bounds__(INV_THREADS)
   const c128 *Vb = V + bt * int64_t(D) * K;
   const double *Sb = S + bt * D;
   bool ok = rr >= 1 && rr <= D;
+  c128 *aux_g = ws + b * wb_ws_elems(K, D) + wb_ws_aux_off(K, D);  // DMMA path: V^H AiU in
   if (ok) {
     // aux = diag(1/S) + V^H AiU (lowrank.py:208-211)
     double loc = 0.0;
     for (int e = tid; e < rr * rr; e += NT) {
       const int i = e / rr, j = e - i * rr;
       c128 a = czero<double>();
-      const c128 *vc = Vb + int64_t(i) * K;
-      const c128 *au = sc.AiU + int64_t(j) * K;
-      for (int k = 0; k < K; ++k) cfma_ca(a, vc[k], au[k]);
+      if (dmma) {
+        a = aux_g[i * D + j];
+      } else {
+        const c128 *vc = Vb + int64_t(i) * K;
+        const c128 *au = sc.AiU + int64_t(j) * K;
+        for (int k = 0; k < K; ++k) cfma_ca(a, vc[k], au[k]);
+      }
       if (i == j) a.re = 1.0 / Sb[i] + a.re;
       sc.aux[e] = a;
       sc.auxinv[e] = a;
@@ -480,11 +495,18 @@ __global__ void __launch_bounds__(INV_THREADS)
       ok = false;
     } else {
       const double fi = cta_fro2(sc.auxinv, rr, rr, sc.inv.red);
-      ok = cta_cond_ok(sc.aux, sc.auxinv, rr, rr, rr, fa, fi, 1e12, sc.inv.v, sc.inv.w,
-                       sc.inv.red);
+      ok = cta_cond_ok(fa, fi, 1e12, sc.aux, rr, rr, sc.inv.red, sc.inv.ired);
     }
   }
-  if (ok) {
+  if (ok && dmma) {
+    // aux^-1 to global memory (D x D, zero beyond r) for the T = AiU aux^-1 GEMM
+    __syncthreads();
+    c128 *ai_g = aux_g + int64_t(D) * D;
+    for (int e = tid; e < D * D; e += NT) {
+      const int i = e / D, j = e - i * D;
+      ai_g[e] = (i < rr && j < rr) ? sc.auxinv[i * rr + j] : czero<double>();
+    }
+  } else if (ok) {
     // T = AiU aux^-1 (K x r), zero beyond r; VhAi rows beyond r zeroed too, so the
     // apply stage can run its inner loop over all D columns
     for (int e = tid; e < K * D; e += NT) {
@@ -498,6 +520,7 @@ __global__ void __launch_bounds__(INV_THREADS)
   }
   if (tid == 0) {
     fb[b] = ok ? 0 : 1;
+    fb[nB + b] = ok ? 1 : 0;  // act[b]: the Woodbury products apply (DMMA path)
     if (ok) {
       method[bt] = uint8_t(LRZ_METHOD_WOODBURY);
       info[bt] = LRZ_INFO_OK;
@@ -514,7 +537,7 @@ __global__ void __launch_bounds__(256)
                     const c128 *__restrict__ U, const c128 *__restrict__ V,
                     const double *__restrict__ S, const int32_t *__restrict__ r,
                     const c128 *__restrict__ ws, const uint8_t *__restrict__ fb,
-                    uint8_t *__restrict__ method) {
+                    uint8_t *__restrict__ method, int skip_wb) {
   __shared__ c128 Ts[8][WBA_TILE + 1], Ws[8][WBA_TILE + 1];
   const int nt = (K + WBA_TILE - 1) / WBA_TILE, ntile = nt * nt;
   const int64_t b = blockIdx.x / ntile;
@@ -548,6 +571,7 @@ __global__ void __launch_bounds__(256)
     if (pl == 0 && tile == 0 && tid == 0) method[bt] = uint8_t(LRZ_METHOD_FULL);
     return;
   }
+  if (skip_wb) return;  // the Woodbury products run on DMMA (lrz_chain_apply_dmma)
   const c128 *w = ws + b * wb_ws_elems(K, D);
   const c128 *Tm = w + int64_t(K) * D, *VhAi = w + 2 * int64_t(K) * D;
   const c128 *Ub = U + bt * int64_t(D) * K, *Vb = V + bt * int64_t(D) * K;
@@ -742,7 +766,12 @@ __global__ void __launch_bounds__(128, KP > 16 ? 3 : 4)
   const int lane = threadIdx.x & 31;
   const int64_t item = blockIdx.x * int64_t(blockDim.x >> 5) + (threadIdx.x >> 5);
   if (item >= B) return;
-  if (mask && !mask[item]) return;
+  if (mask && !mask[item]) {
+    // masked out: nothing for the CTA kernel to redo either (the redo array
+    // lives in a reused workspace and must not carry a stale flag)
+    if (lane == 0) redo[item] = 0;
+    return;
+  }
   const c128 *a = A + item * as;
   c128 m[KP];
   double fa = 0.0;
@@ -848,7 +877,7 @@ size_t lrz_chain_smem(int K, int D) {
 }
 size_t lrz_wb_ws(int64_t B, int K, int D) {
   // + per-trial SingularAuxiliary flags of the step-parallel chain
-  return size_t(B) * wb_ws_elems(K, D) * sizeof(c128) + size_t(B);
+  return size_t(B) * wb_ws_elems(K, D) * sizeof(c128) + 2 * size_t(B);  // + fb[B], act[B]
 }
 int lrz_zgemm_internal(int64_t batch, int M, int N, int Kd, int opA, const void *A, int64_t lda,
                        int64_t sA, int opB, const void *Bm, int64_t ldb, int64_t sB, void *C,
@@ -979,6 +1008,18 @@ extern "C" int lrz_chain(int64_t B, int T, int K, int d_max, const uint8_t *plan
 }
 
 
+int lrz_use_dmma();
+int lrz_chain_gemms_dmma(int64_t B, int T, int t, int K, int D, const uint8_t *plan,
+                         const void *U, const void *V, const void *prev, int64_t pst,
+                         void *AiUt, void *VhAi, void *aux, int64_t ws_stride, cudaStream_t s);
+int lrz_chain_T_dmma(int64_t B, int T, int t, int K, int D, const uint8_t *act,
+                     const int32_t *r, const void *auxinv, const void *AiUt, void *Tm,
+                     int64_t ws_stride, cudaStream_t s);
+int lrz_chain_apply_dmma(int64_t B, int T, int t, int K, int D, const uint8_t *act,
+                         const void *Tm, const void *VhAi, int64_t ws_stride, const void *prev,
+                         int64_t pst, void *Ainv_seq, void *A_state, const void *U,
+                         const void *V, const double *S, const int32_t *r, cudaStream_t s);
+
 extern "C" int lrz_chain_steps(int64_t B, int T, int K, int d_max, const uint8_t *plan,
                                const void *G, const void *A_inv_prev, void *A_inv_seq,
                                void *A_state, const void *U, const void *V, const double *S,
@@ -1002,26 +1043,57 @@ extern "C" int lrz_chain_steps(int64_t B, int T, int K, int d_max, const uint8_t
         set_smem((const void *)wb_fallback_kernel, smf))
       return LRZ_ELAUNCH;
     const int nt = (K + WBA_TILE - 1) / WBA_TILE;
+    const bool dmma = lrz_use_dmma() != 0;
     for (int t = 0; t < T; ++t) {
       const c128 *prev = t == 0 ? (const c128 *)A_inv_prev : (const c128 *)A_inv_seq + (t - 1) * KK;
       const int64_t pst = t == 0 ? KK : int64_t(T) * KK;
       // AiU^T = U^T (A^-1)^T  (D x K)  and  VhAi = conj(V^T) A^-1  (D x K)
-      int rc = lrz_zgemm_internal(B, d_max, K, K, 0, (const c128 *)U + t * int64_t(d_max) * K, K,
-                                  int64_t(T) * d_max * K, 1, prev, K, pst, ws, K, E, st);
-      if (!rc)
-        rc = lrz_zgemm_internal(B, d_max, K, K, 3, (const c128 *)V + t * int64_t(d_max) * K, K,
-                                int64_t(T) * d_max * K, 0, prev, K, pst,
-                                ws + 2 * int64_t(K) * d_max, K, E, st);
+      int rc;
+      if (dmma) {
+        rc = lrz_chain_gemms_dmma(B, T, t, K, d_max, plan, U, V, prev, pst, ws,
+                                  ws + 2 * int64_t(K) * d_max, ws + wb_ws_aux_off(K, d_max), E,
+                                  st);
+      } else {
+        LrzProf p1("chain:gemms", st);
+        rc = lrz_zgemm_internal(B, d_max, K, K, 0, (const c128 *)U + t * int64_t(d_max) * K, K,
+                                int64_t(T) * d_max * K, 1, prev, K, pst, ws, K, E, st);
+        if (!rc)
+          rc = lrz_zgemm_internal(B, d_max, K, K, 3, (const c128 *)V + t * int64_t(d_max) * K, K,
+                                  int64_t(T) * d_max * K, 0, prev, K, pst,
+                                  ws + 2 * int64_t(K) * d_max, K, E, st);
+      }
       if (rc) return rc;
-      wb_core_kernel<<<unsigned(B), INV_THREADS, smc, st>>>(T, t, K, d_max, plan,
-                                                            (const c128 *)V, S, r, ws, fb,
-                                                            method, info);
-      wb_apply_kernel<<<unsigned(B * nt * nt), 256, 0, st>>>(
-          T, t, K, d_max, plan, (const c128 *)G, prev, pst, (c128 *)A_inv_seq, (c128 *)A_state,
-          (const c128 *)U, (const c128 *)V, S, r, ws, fb, method);
-      wb_fallback_kernel<<<unsigned(B), INV_THREADS, smf, st>>>(T, t, K, plan, (const c128 *)G,
-                                                                (c128 *)A_inv_seq, fb, method,
-                                                                info);
+      {
+        LrzProf p2("chain:wb_core_kernel", st);
+        wb_core_kernel<<<unsigned(B), INV_THREADS, smc, st>>>(T, t, K, d_max, plan,
+                                                              (const c128 *)V, S, r, ws, fb,
+                                                              method, info, dmma ? 1 : 0);
+      }
+      if (dmma) {
+        rc = lrz_chain_T_dmma(B, T, t, K, d_max, fb + B, r, ws + wb_ws_aux_off(K, d_max) +
+                              int64_t(d_max) * d_max, ws, ws + int64_t(K) * d_max, E, st);
+        if (rc) return rc;
+      }
+      {
+        LrzProf p3("chain:wb_apply_kernel", st);
+        wb_apply_kernel<<<unsigned(B * nt * nt), 256, 0, st>>>(
+            T, t, K, d_max, plan, (const c128 *)G, prev, pst, (c128 *)A_inv_seq,
+            (c128 *)A_state, (const c128 *)U, (const c128 *)V, S, r, ws, fb, method,
+            dmma ? 1 : 0);
+      }
+      if (dmma) {
+        rc = lrz_chain_apply_dmma(B, T, t, K, d_max, fb + B, ws + int64_t(K) * d_max,
+                                  ws + 2 * int64_t(K) * d_max, E, prev, pst, A_inv_seq, A_state,
+                                  U, V, S, r, st);
+        if (rc) return rc;
+      }
+      {
+        LrzProf p4("chain:wb_fallback_kernel", st);
+        wb_fallback_kernel<<<unsigned(B), INV_THREADS, smf, st>>>(T, t, K, plan,
+                                                                  (const c128 *)G,
+                                                                  (c128 *)A_inv_seq, fb, method,
+                                                                  info);
+      }
       if (int rc2 = lrz_launch_status("lrz_chain (step-parallel)")) return rc2;
     }
     return LRZ_OK;

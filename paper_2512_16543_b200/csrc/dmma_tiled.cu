@@ -48,23 +48,52 @@ LRZ_DEV void cpa(void *smem, const void *gmem, int bytes, bool pred) {
                  "r"(pred ? 8 : 0));
 }
 
-template <typename T>
-__global__ void __launch_bounds__(DT_THREADS, 2)
-    dmma_hn_kernel(int NN, int J, int Kd, const cplx<T> *__restrict__ X, int64_t xs, int ldx,
-                   const c128 *__restrict__ Y, int64_t ys, cplx<T> *__restrict__ out,
-                   int64_t os, double *__restrict__ parts, int tiles_n, int tiles_j,
-                   const uint8_t *__restrict__ mask) {
+// Generalised form used by the Woodbury chain as well:
+//   out[n][j] (MODE 0 =, 1 = base -, 2 +=) sum_k opX(k, n) opY(k, j)
+// with X(k, n) at XT ? n ldx + k : k ldx + n, opX = conj when XC (the
+// precoder's H^H), likewise Y / YT / YC; optional per-k real scale of Y
+// (kscale, the Woodbury S) and per-item reduction length (kd_item).
+struct ZgArgs {
+  int NN, J, Kd;
+  const void *X;
+  int64_t xs;
+  int ldx;
+  const c128 *Y;
+  int64_t ys;
+  int ldy;
+  void *out;
+  int64_t os;
+  int ldo;
+  const c128 *base;  // MODE 1
+  int64_t bs;
+  double *parts;
+  const uint8_t *mask;  // item active iff mask[item * mstride] == mval
+  int64_t mstride;
+  int mval;
+  const int32_t *kd_item;  // nullable: reduction length of item = min(Kd, kd_item[item * kstride])
+  int64_t kstride;
+  const double *kscale;  // nullable: Y row k scaled by kscale[item * kss + k]
+  int64_t kss;
+  int tiles_n, tiles_j;
+};
+
+template <typename T, bool XT, bool XC, bool YT, bool YC, int MODE>
+__global__ void __launch_bounds__(DT_THREADS, 2) zgemm_dmma_kernel(ZgArgs a) {
   using S = DtSmem<T>;
   extern __shared__ __align__(16) unsigned char dt_smem[];
-  const int ntile = tiles_n * tiles_j;
+  __shared__ double s_ks[DT_ST][DT_KC];
+  const int ntile = a.tiles_n * a.tiles_j;
   const int64_t item = blockIdx.x / ntile;
-  if (mask && !mask[item]) return;
+  if (a.mask && a.mask[item * a.mstride] != a.mval) return;
   const int tile = int(blockIdx.x - item * ntile);
-  const int n0 = (tile / tiles_j) * DT_BN, j0 = (tile % tiles_j) * DT_BJ;
+  const int n0 = (tile / a.tiles_j) * DT_BN, j0 = (tile % a.tiles_j) * DT_BJ;
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5, g = lane >> 2, t = lane & 3;
   const int wn = w & 3, wj = w >> 2;
-  const cplx<T> *x = X + item * xs;
-  const c128 *y = Y + item * ys;
+  const int NN = a.NN, J = a.J;
+  const int Kd = a.kd_item ? min(a.Kd, int(a.kd_item[item * a.kstride])) : a.Kd;
+  const cplx<T> *x = reinterpret_cast<const cplx<T> *>(a.X) + item * a.xs;
+  const c128 *y = a.Y + item * a.ys;
+  const double *ksc = a.kscale ? a.kscale + item * a.kss : nullptr;
 
   auto xslab = [&](int s) {
     return reinterpret_cast<cplx<T> *>(dt_smem + size_t(s) * S::stage);
@@ -77,25 +106,30 @@ __global__ void __launch_bounds__(DT_THREADS, 2)
     c128 *ysl = yslab(s);
 #pragma unroll
     for (int i = 0; i < (DT_KC * DT_BN) / DT_THREADS; ++i) {
-      const int e = tid + i * DT_THREADS, r = e / DT_BN, c = e % DT_BN;
+      const int e = tid + i * DT_THREADS;
+      const int r = XT ? e % DT_KC : e / DT_BN, c = XT ? e / DT_KC : e % DT_BN;
       const int k = k0 + r, n = n0 + c;
       const bool ok = k < Kd && n < NN;
-      cpa(xsl + r * S::XLD + c, x + (ok ? int64_t(k) * ldx + n : 0), sizeof(cplx<T>), ok);
+      const int64_t off = XT ? int64_t(n) * a.ldx + k : int64_t(k) * a.ldx + n;
+      cpa(xsl + r * S::XLD + c, x + (ok ? off : 0), sizeof(cplx<T>), ok);
     }
 #pragma unroll
     for (int i = 0; i < (DT_KC * DT_BJ) / DT_THREADS; ++i) {
-      const int e = tid + i * DT_THREADS, r = e / DT_BJ, c = e % DT_BJ;
+      const int e = tid + i * DT_THREADS;
+      const int r = YT ? e % DT_KC : e / DT_BJ, c = YT ? e / DT_KC : e % DT_BJ;
       const int k = k0 + r, j = j0 + c;
       const bool ok = k < Kd && j < J;
-      cpa(ysl + r * S::YLD + c, y + (ok ? int64_t(k) * J + j : 0), 16, ok);
+      const int64_t off = YT ? int64_t(j) * a.ldy + k : int64_t(k) * a.ldy + j;
+      cpa(ysl + r * S::YLD + c, y + (ok ? off : 0), 16, ok);
     }
+    if (ksc && tid < DT_KC) s_ks[s][tid] = (k0 + tid < Kd) ? ksc[k0 + tid] : 0.0;
   };
 
   double acr[2][4][2], aci[2][4][2];
 #pragma unroll
-  for (int a = 0; a < 2; ++a)
+  for (int q = 0; q < 2; ++q)
 #pragma unroll
-    for (int b = 0; b < 4; ++b) acr[a][b][0] = acr[a][b][1] = aci[a][b][0] = aci[a][b][1] = 0.0;
+    for (int b = 0; b < 4; ++b) acr[q][b][0] = acr[q][b][1] = aci[q][b][0] = aci[q][b][1] = 0.0;
 
   const int nslab = (Kd + DT_KC - 1) / DT_KC;
 #pragma unroll
@@ -118,13 +152,14 @@ __global__ void __launch_bounds__(DT_THREADS, 2)
       for (int nb = 0; nb < 2; ++nb) {
         const cplx<T> v = xsl[(kk + t) * S::XLD + 16 * wn + 8 * nb + g];
         hr[nb] = double(v.re);
-        hi[nb] = double(v.im);
+        hi[nb] = XC ? double(v.im) : -double(v.im);  // the product below conjugates x
       }
+      const double ks = ksc ? s_ks[it % DT_ST][kk + t] : 1.0;
 #pragma unroll
       for (int jb = 0; jb < 4; ++jb) {
         const c128 v = ysl[(kk + t) * S::YLD + 32 * wj + 8 * jb + g];
-        br[jb] = v.re;
-        bi[jb] = v.im;
+        br[jb] = ksc ? ks * v.re : v.re;
+        bi[jb] = ksc ? ks * (YC ? -v.im : v.im) : (YC ? -v.im : v.im);
       }
 #pragma unroll
       for (int nb = 0; nb < 2; ++nb) {
@@ -142,7 +177,8 @@ __global__ void __launch_bounds__(DT_THREADS, 2)
   }
   asm volatile("cp.async.wait_group 0;\n" ::);
 
-  cplx<T> *o = out + item * os;
+  cplx<T> *o = reinterpret_cast<cplx<T> *>(a.out) + item * a.os;
+  const c128 *bse = MODE == 1 ? a.base + item * a.bs : nullptr;
   double nrm = 0.0;
 #pragma unroll
   for (int nb = 0; nb < 2; ++nb) {
@@ -153,46 +189,85 @@ __global__ void __launch_bounds__(DT_THREADS, 2)
       for (int e = 0; e < 2; ++e) {
         const int j = j0 + 32 * wj + 8 * jb + 2 * t + e;
         if (n < NN && j < J) {
-          const cplx<T> z = mk<T>(T(acr[nb][jb][e]), T(aci[nb][jb][e]));
-          o[int64_t(n) * J + j] = z;
+          const int64_t idx = int64_t(n) * a.ldo + j;
+          double zr = acr[nb][jb][e], zi = aci[nb][jb][e];
+          if (MODE == 1) {
+            const c128 b = bse[idx];
+            zr = b.re - zr;
+            zi = b.im - zi;
+          } else if (MODE == 2) {
+            const cplx<T> b = o[idx];
+            zr = double(b.re) + zr;
+            zi = double(b.im) + zi;
+          }
+          const cplx<T> z = mk<T>(T(zr), T(zi));
+          o[idx] = z;
           nrm += double(z.re) * double(z.re) + double(z.im) * double(z.im);
         }
       }
   }
-  if (parts) {
+  if (a.parts) {
     double *red = reinterpret_cast<double *>(dt_smem + S::stage * DT_ST);
     const double s = block_sum(nrm, red);
-    if (tid == 0) parts[item * ntile + tile] = s;
+    if (tid == 0) a.parts[item * ntile + tile] = s;
   }
+}
+
+template <typename T, bool XT, bool XC, bool YT, bool YC, int MODE>
+static int zgemm_dmma_launch(int64_t B, ZgArgs a, cudaStream_t s, const char *what) {
+  LrzProf prof(what, s);
+  a.tiles_n = (a.NN + DT_BN - 1) / DT_BN;
+  a.tiles_j = (a.J + DT_BJ - 1) / DT_BJ;
+  const size_t sm = DtSmem<T>::bytes;
+  static bool attr = false;
+  if (!attr) {
+    if (cudaFuncSetAttribute(zgemm_dmma_kernel<T, XT, XC, YT, YC, MODE>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)) != cudaSuccess) {
+      lrz_set_error("zgemm_dmma_kernel: cannot reserve %zu bytes of shared memory", sm);
+      return LRZ_ELAUNCH;
+    }
+    attr = true;
+  }
+  const int64_t nt = int64_t(a.tiles_n) * a.tiles_j;
+  const int64_t per = (int64_t(1) << 30) / nt;
+  for (int64_t b0 = 0; b0 < B; b0 += per) {
+    const int64_t bb = B - b0 < per ? B - b0 : per;
+    ZgArgs c = a;
+    c.X = reinterpret_cast<const cplx<T> *>(a.X) + b0 * a.xs;
+    c.Y = a.Y + b0 * a.ys;
+    c.out = reinterpret_cast<cplx<T> *>(a.out) + b0 * a.os;
+    if (a.base) c.base = a.base + b0 * a.bs;
+    if (a.parts) c.parts = a.parts + b0 * nt;
+    if (a.mask) c.mask = a.mask + b0 * a.mstride;
+    if (a.kd_item) c.kd_item = a.kd_item + b0 * a.kstride;
+    if (a.kscale) c.kscale = a.kscale + b0 * a.kss;
+    zgemm_dmma_kernel<T, XT, XC, YT, YC, MODE><<<unsigned(bb * nt), DT_THREADS, sm, s>>>(c);
+  }
+  return lrz_launch_status(what);
 }
 
 template <typename T>
 static int dmma_hn_launch(int64_t B, int NN, int J, int Kd, const cplx<T> *X, int64_t xs, int ldx,
                           const c128 *Y, int64_t ys, cplx<T> *out, int64_t os, double *parts,
                           const uint8_t *mask, cudaStream_t s, const char *what) {
-  LrzProf prof(what, s);
-  const int tn = (NN + DT_BN - 1) / DT_BN, tj = (J + DT_BJ - 1) / DT_BJ;
-  const size_t sm = DtSmem<T>::bytes;
-  static bool attr = false;
-  if (!attr) {
-    if (cudaFuncSetAttribute(dmma_hn_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             int(sm)) != cudaSuccess) {
-      lrz_set_error("dmma_hn_kernel: cannot reserve %zu bytes of shared memory", sm);
-      return LRZ_ELAUNCH;
-    }
-    attr = true;
-  }
-  const int64_t nb = B * tn * tj;
-  // grid.x limit is 2^31 - 1; chunk the batch if it would overflow
-  const int64_t per = (int64_t(1) << 30) / (int64_t(tn) * tj);
-  for (int64_t b0 = 0; b0 < B; b0 += per) {
-    const int64_t bb = B - b0 < per ? B - b0 : per;
-    dmma_hn_kernel<T><<<unsigned(bb * tn * tj), DT_THREADS, sm, s>>>(
-        NN, J, Kd, X + b0 * xs, xs, ldx, Y + b0 * ys, ys, out + b0 * os, os,
-        parts ? parts + b0 * tn * tj : nullptr, tn, tj, mask ? mask + b0 : nullptr);
-  }
-  (void)nb;
-  return lrz_launch_status("dmma_hn_kernel");
+  ZgArgs a{};
+  a.NN = NN;
+  a.J = J;
+  a.Kd = Kd;
+  a.X = X;
+  a.xs = xs;
+  a.ldx = ldx;
+  a.Y = Y;
+  a.ys = ys;
+  a.ldy = J;
+  a.out = out;
+  a.os = os;
+  a.ldo = J;
+  a.parts = parts;
+  a.mask = mask;
+  a.mstride = 1;
+  a.mval = 1;
+  return zgemm_dmma_launch<T, false, true, false, false, 0>(B, a, s, what);
 }
 
 }  // namespace lrz
@@ -276,4 +351,128 @@ int lrz_sketch_dmma_large(int64_t B, int K, int Dtot, const void *dA, int64_t a_
     return rc;
   return dmma_hn_launch<double>(B, K, Dtot, K, (const c128 *)dA, a_stride, K, (const c128 *)Y,
                                 st, (c128 *)W, st, nullptr, mask, s, "dmma_hn_kernel:sketch_W");
+}
+
+// Woodbury chain products for one time step t of the step-parallel chain
+// (chain.cu), all trials at once on the FP64 tensor pipe.  U, V: [B][T][D][K]
+// (factor column f of item (b, t) contiguous); prev: A^-1_{t-1} per trial.
+//   AiUt[f][k] = (A^-1 U)[k][f] = sum_m U[m][f] A^-1[k][m]        (lowrank.py:209)
+//   VhAi[f][j] = (V^H A^-1)[f][j] = sum_k conj(V[k][f]) A^-1[k][j]  (lowrank.py:219)
+int lrz_chain_gemms_dmma(int64_t B, int T, int t, int K, int D, const uint8_t *plan,
+                         const void *U, const void *V, const void *prev, int64_t pst,
+                         void *AiUt, void *VhAi, void *aux, int64_t ws_stride, cudaStream_t s) {
+  ZgArgs a{};
+  a.NN = D;
+  a.J = K;
+  a.Kd = K;
+  a.X = (const c128 *)U + int64_t(t) * D * K;
+  a.xs = int64_t(T) * D * K;
+  a.ldx = K;
+  a.Y = (const c128 *)prev;
+  a.ys = pst;
+  a.ldy = K;
+  a.out = AiUt;
+  a.os = ws_stride;
+  a.ldo = K;
+  a.mask = plan + t;
+  a.mstride = T;
+  a.mval = 1;
+  if (int rc = zgemm_dmma_launch<double, true, false, true, false, 0>(B, a, s, "chain:AiU_dmma"))
+    return rc;
+  a.X = (const c128 *)V + int64_t(t) * D * K;
+  a.out = VhAi;
+  if (int rc = zgemm_dmma_launch<double, true, true, false, false, 0>(B, a, s,
+                                                                        "chain:VhAi_dmma"))
+    return rc;
+  // aux' = V^H AiU (D x D; lowrank.py:210 before the 1/S diagonal):
+  //   aux'[i][j] = sum_k conj(V[k][i]) AiU[k][j],  AiU[k][j] = AiUt[j][k]
+  ZgArgs c = a;
+  c.NN = D;
+  c.J = D;
+  c.Y = (const c128 *)AiUt;
+  c.ys = ws_stride;
+  c.ldy = K;
+  c.out = aux;
+  c.os = ws_stride;
+  c.ldo = D;
+  return zgemm_dmma_launch<double, true, true, true, false, 0>(B, c, s, "chain:aux_dmma");
+}
+
+// T = AiU aux^-1 (stored [D][K]: T[j][k] = sum_{i < r} aux^-1[i][j] AiU[k][i])
+int lrz_chain_T_dmma(int64_t B, int T, int t, int K, int D, const uint8_t *act,
+                     const int32_t *r, const void *auxinv, const void *AiUt, void *Tm,
+                     int64_t ws_stride, cudaStream_t s) {
+  ZgArgs a{};
+  a.NN = D;
+  a.J = K;
+  a.Kd = D;
+  a.X = auxinv;
+  a.xs = ws_stride;
+  a.ldx = D;
+  a.Y = (const c128 *)AiUt;
+  a.ys = ws_stride;
+  a.ldy = K;
+  a.out = Tm;
+  a.os = ws_stride;
+  a.ldo = K;
+  a.mask = act;
+  a.mstride = 1;
+  a.mval = 1;
+  a.kd_item = r + t;
+  a.kstride = T;
+  return zgemm_dmma_launch<double, false, false, false, false, 0>(B, a, s, "chain:T_dmma");
+}
+
+// A^-1_t = prev - T VhAi and A_t = A_{t-1} + (U S) V^H for the trials whose
+// Woodbury step went through (act[b] == 1); T, VhAi: [D][K] per trial.
+int lrz_chain_apply_dmma(int64_t B, int T, int t, int K, int D, const uint8_t *act,
+                         const void *Tm, const void *VhAi, int64_t ws_stride, const void *prev,
+                         int64_t pst, void *Ainv_seq, void *A_state, const void *U,
+                         const void *V, const double *S, const int32_t *r, cudaStream_t s) {
+  const int64_t KK = int64_t(K) * K;
+  ZgArgs a{};
+  a.NN = K;
+  a.J = K;
+  a.Kd = D;
+  a.X = Tm;
+  a.xs = ws_stride;
+  a.ldx = K;
+  a.Y = (const c128 *)VhAi;
+  a.ys = ws_stride;
+  a.ldy = K;
+  a.out = (c128 *)Ainv_seq + int64_t(t) * KK;
+  a.os = int64_t(T) * KK;
+  a.ldo = K;
+  a.base = (const c128 *)prev;
+  a.bs = pst;
+  a.mask = act;
+  a.mstride = 1;
+  a.mval = 1;
+  a.kd_item = r + t;  // T / VhAi rows beyond the rank are not read
+  a.kstride = T;
+  if (int rc = zgemm_dmma_launch<double, false, false, false, false, 1>(B, a, s,
+                                                                          "chain:apply_dmma"))
+    return rc;
+  if (!A_state) return LRZ_OK;
+  ZgArgs b{};
+  b.NN = K;
+  b.J = K;
+  b.Kd = D;
+  b.X = (const c128 *)U + int64_t(t) * D * K;
+  b.xs = int64_t(T) * D * K;
+  b.ldx = K;
+  b.Y = (const c128 *)V + int64_t(t) * D * K;
+  b.ys = int64_t(T) * D * K;
+  b.ldy = K;
+  b.out = A_state;
+  b.os = KK;
+  b.ldo = K;
+  b.mask = act;
+  b.mstride = 1;
+  b.mval = 1;
+  b.kd_item = r + t;
+  b.kstride = T;
+  b.kscale = S + int64_t(t) * D;
+  b.kss = int64_t(T) * D;
+  return zgemm_dmma_launch<double, false, false, false, true, 2>(B, b, s, "chain:Aupdate_dmma");
 }

@@ -151,17 +151,102 @@ LRZ_DEV double cta_sigma_max(const c128 *X, int K, int ld, c128 *v, c128 *w, dou
   return sqrt(lam);
 }
 
-// Condition guard shared by direct_inverse (1e14) and the Woodbury aux (1e12):
-// ||X||_F ||X^-1||_F bounds cond_2 from above; only when that bound exceeds
-// the limit is cond_2 estimated by power iteration (lowrank.py:135,212).
-LRZ_DEV bool cta_cond_ok(const c128 *X, const c128 *Xinv, int K, int ldx, int ldi, double fx,
-                         double fi, double limit, c128 *v, c128 *w, double *red) {
+// Exact 2-norm condition number of the n x n matrix X (row stride ld) by
+// one-sided Jacobi (Hestenes) on its columns, in place (X is destroyed):
+// sigma_max / sigma_min of the converged column norms, the quantity
+// np.linalg.cond computes (lowrank.py:135,212).  Block-cooperative; one warp
+// per column pair, round-robin ordering.  inf when sigma_min == 0.
+LRZ_DEV double cta_jacobi_cond(c128 *X, int n, int ld, double *red, int *flag) {
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, NW = blockDim.x >> 5;
+  const int dp = n + (n & 1), npairs = dp / 2;
+  for (int sweep = 0; sweep < 60; ++sweep) {
+    if (tid == 0) *flag = 0;
+    __syncthreads();
+    for (int rnd = 0; rnd < dp - 1; ++rnd) {
+      for (int pi = wid; pi < npairs; pi += NW) {
+        int a, b;
+        if (pi == 0) {
+          a = rnd;
+          b = dp - 1;
+        } else {
+          a = (rnd + pi) % (dp - 1);
+          b = (rnd - pi + dp - 1) % (dp - 1);
+        }
+        if (a > b) {
+          const int t_ = a;
+          a = b;
+          b = t_;
+        }
+        if (b >= n) continue;  // warp-uniform
+        double al = 0.0, be = 0.0, gr = 0.0, gi = 0.0;
+        for (int k = lane; k < n; k += 32) {
+          const c128 x = X[int64_t(k) * ld + a], y = X[int64_t(k) * ld + b];
+          al += cabs2(x);
+          be += cabs2(y);
+          gr += x.re * y.re + x.im * y.im;  // (x^H y)
+          gi += x.re * y.im - x.im * y.re;
+        }
+        al = warp_sum(al);
+        be = warp_sum(be);
+        gr = warp_sum(gr);
+        gi = warp_sum(gi);
+        const double g = hypot(gr, gi);
+        if (!(g > 1e-15 * sqrt(al) * sqrt(be))) continue;
+        const double zeta = (be - al) / (2.0 * g);
+        const double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+        const double c = 1.0 / sqrt(1.0 + t * t), sn = c * t;
+        const c128 ph = mk<double>(gr / g, -gi / g);  // e^{-i phi}
+        for (int k = lane; k < n; k += 32) {
+          c128 &x = X[int64_t(k) * ld + a];
+          c128 &y = X[int64_t(k) * ld + b];
+          const c128 xv = x, yv = cmul(y, ph);
+          x = mk<double>(c * xv.re - sn * yv.re, c * xv.im - sn * yv.im);
+          y = mk<double>(sn * xv.re + c * yv.re, sn * xv.im + c * yv.im);
+        }
+        if (lane == 0) *flag = 1;
+      }
+      __syncthreads();
+    }
+    const int rot = *flag;
+    __syncthreads();
+    if (!rot) break;
+  }
+  // column norms -> sigma_max, sigma_min
+  double smax = 0.0, smin = 1e308;
+  for (int j = wid; j < n; j += NW) {
+    double s2 = 0.0;
+    for (int k = lane; k < n; k += 32) s2 += cabs2(X[int64_t(k) * ld + j]);
+    s2 = warp_sum(s2);
+    smax = fmax(smax, s2);
+    smin = fmin(smin, s2);
+  }
+  // block max / min of the per-warp values (lane-uniform)
+  __syncthreads();
+  if (lane == 0) {
+    red[wid] = smax;
+    red[NW + wid] = smin;
+  }
+  __syncthreads();
+  double M = 0.0, m = 1e308;
+  for (int i = 0; i < NW; ++i) {
+    M = fmax(M, red[i]);
+    m = fmin(m, red[NW + i]);
+  }
+  __syncthreads();
+  return m > 0.0 ? sqrt(M) / sqrt(m) : INFINITY;
+}
+
+// Condition guard shared by direct_inverse (1e14) and the Woodbury aux (1e12),
+// deciding exactly like np.linalg.cond(X) > limit (lowrank.py:135,212):
+// ||X||_F ||X^-1||_F >= cond_2(X), so a bound at or below the limit accepts;
+// otherwise cond_2 is computed exactly by one-sided Jacobi on the writable
+// copy `work` (n x n, row stride ldw, destroyed; `red` needs 2 * warps doubles).
+LRZ_DEV bool cta_cond_ok(double fx, double fi, double limit, c128 *work, int n, int ldw,
+                         double *red, int *flag) {
   const double fb = sqrt(fx) * sqrt(fi);
   if (fb <= limit) return true;
   if (!isfinite(fx) || !isfinite(fi)) return false;
-  const double s1 = cta_sigma_max(X, K, ldx, v, w, red, 60);
-  const double s2 = cta_sigma_max(Xinv, K, ldi, v, w, red, 60);
-  const double c = s1 * s2;
+  const double c = cta_jacobi_cond(work, n, ldw, red, flag);
   return c <= limit;
 }
 
@@ -200,7 +285,19 @@ LRZ_DEV int cta_herm_inverse(const c128 *Ain, c128 *Aout, int K, c128 *M, double
     info = LRZ_INFO_SINGULAR;
   } else {
     const double fi = cta_fro2(W, K, K, sc.red);
-    if (!cta_cond_ok(Ain, W, K, K, K, fa, fi, limit, sc.v, sc.w, sc.red))
+    const double fb = sqrt(fa) * sqrt(fi);
+    bool ok = fb <= limit;
+    if (!ok && isfinite(fb)) {
+      // exact cond_2 of A (one-sided Jacobi on a copy in the output buffer, the
+      // accuracy class of np.linalg.cond), then invert again
+      for (int e = tid; e < K * K; e += NT) W[e] = Ain[e];
+      __syncthreads();
+      ok = cta_jacobi_cond(W, K, K, sc.red, sc.ired) <= limit;
+      for (int e = tid; e < K * K; e += NT) W[e] = Ain[e];
+      __syncthreads();
+      cta_gauss_jordan(W, K, K, indefinite, sc.colbuf, sc.rowbuf, sc.perm, sc.red, sc.ired);
+    }
+    if (!ok)
       info = LRZ_INFO_SINGULAR;
     else if (indefinite)
       info = LRZ_INFO_INDEFINITE;
@@ -270,7 +367,8 @@ LRZ_DEV int cta_woodbury(int K, int r, const c128 *__restrict__ Ainv_in, c128 *A
                             sc.inv.red, sc.inv.ired);
   if (st != 0) return LRZ_INFO_SINGULAR_AUX;
   const double fi = cta_fro2(sc.auxinv, r, r, sc.inv.red);
-  if (!cta_cond_ok(sc.aux, sc.auxinv, r, r, r, fa, fi, 1e12, sc.inv.v, sc.inv.w, sc.inv.red))
+  // (sc.aux is not needed after this point: the exact path rotates it in place)
+  if (!cta_cond_ok(fa, fi, 1e12, sc.aux, r, r, sc.inv.red, sc.inv.ired))
     return LRZ_INFO_SINGULAR_AUX;
   // 4. T = AiU aux^-1 (K x r)
   for (int e = tid; e < K * r; e += NT) {

@@ -432,7 +432,7 @@ def run_trajectory(H, noise, cfg: TrajectoryConfig, streams: OmegaStreams | None
         tdt = H.dtype
     B, T, K, Nn = H.shape
     chunk = T if chunk is None else chunk
-    nz = np.ascontiguousarray(np.broadcast_to(np.asarray(noise, dtype=np.float64), (B, K)))
+    nz = np.array(np.broadcast_to(np.asarray(noise, dtype=np.float64), (B, K)), order="C")
     noise_d = torch.from_numpy(nz).to(dev)
     runner = TrajectoryRunner(B, K, Nn, tdt, cfg, dev)
     outs = []
