@@ -22,6 +22,10 @@ int lrz_sketch_gemm(int64_t B, int K, int Dtot, const void *dA, int64_t a_stride
                     const uint8_t *mask, void *Y, void *W, void *stream);
 
 int lrz_use_dmma();
+int lrz_arsvd_tail_M(int64_t B, int K, int D, const void *dA, int64_t a_stride, const void *Q,
+                     void *M, int64_t wst, const uint8_t *tail, cudaStream_t s);
+int lrz_arsvd_tail_U(int64_t B, int K, int D, const void *Jp, const void *Q, int64_t wst,
+                     void *U, const uint8_t *tail, cudaStream_t s);
 int lrz_sketch_dmma_large(int64_t B, int K, int Dtot, const void *dA, int64_t a_stride,
                           const double *omega, int64_t omega_stride, const int32_t *omega_row,
                           int64_t orow_div, const int64_t *cursor, int k_init, int p,
@@ -51,6 +55,12 @@ struct ArsvdArgs {
   const int32_t *start_it;  // nullable: iteration to resume at (warp front end), < 0 = skip
   const c128 *ya;           // nullable: the front end's Y_all [item][K][ydtot]; a resumed
   int ydtot;                //   iteration takes its sketch Y from there
+  // K > 32 tail pipeline for items the front end resumed at the last iteration:
+  // phase 1 forms Q (Householder) and stops; M = dA^H Q runs as a batched DMMA
+  // GEMM; phase 2 takes M and finishes (SVD, rank, V); U = Q J_perm is a second
+  // GEMM.  tail[item]: 1 = in the pipeline, 2 = U wanted from the GEMM.
+  int phase;
+  uint8_t *tail;
   c128 *U, *V;
   double *S;
   int32_t *k_est, *iters, *fallback;
@@ -333,6 +343,8 @@ LRZ_DEV int64_t arsvd_item(const ArsvdArgs &g, const int64_t item, int64_t cur, 
   __shared__ int s_rot[2];
   __shared__ int s_r;
 
+  const bool tail = g.phase != 0 && g.ya && it0 == g.i_max - 1;
+  if (g.phase == 2 && !tail) return 0;
   const c128 *dA = g.dA + item * g.as;
   const int64_t orw = g.orow ? int64_t(g.orow[item]) : item / g.orow_div;
   const double *om = g.omega + orw * g.os;
@@ -383,6 +395,11 @@ LRZ_DEV int64_t arsvd_item(const ArsvdArgs &g, const int64_t item, int64_t cur, 
     const double *zre = om + cur;
     const double *zim = zre + int64_t(K) * d;
     cur += int64_t(2) * K * d;
+    const bool p2 = g.phase == 2 && it == it0;  // Q and M come from phase 1 + the GEMM
+    if (p2) {
+      Q = g.ws + item * (int64_t(2) * D * K + int64_t(D) * D) + int64_t(D) * K;
+      M = Q - int64_t(D) * K;
+    } else {
     // ---- Y = dA Omega  (threads: k slow, j fast -> Omega row contiguous); a
     //      resumed iteration takes the front end's Y block (same Omega, DMMA product)
     if (g.ya && it == it0) {
@@ -496,8 +513,16 @@ LRZ_DEV int64_t arsvd_item(const ArsvdArgs &g, const int64_t item, int64_t cur, 
       M = t;
     }
     __syncthreads();
+    if (g.phase == 1 && tail) {  // Q formed: M = dA^H Q runs as a batched GEMM
+      if (tid == 0) g.tail[item] = 1;
+      return 0;
+    }
+    }  // !p2
     // ---- M = dA^H Q  (B^H; threads: j slow, k fast -> dA row contiguous)
     double loc2 = 0.0;
+    if (p2) {
+      for (int e = tid; e < K * d; e += NT) loc2 += cabs2(M[e]);
+    } else
     for (int e = tid; e < K * d; e += NT) {
       const int j = e / K, k = e - j * K;
       c128 a = czero<double>();
@@ -583,7 +608,23 @@ LRZ_DEV int64_t arsvd_item(const ArsvdArgs &g, const int64_t item, int64_t cur, 
     }
   }
   // ---- outputs: S, V = M_perm / s, U = Q J_perm (all d columns, sorted)
-  if (have_sv && (g.want == 1 || 2 * r <= K)) {
+  if (tail && have_sv && (g.want == 1 || 2 * r <= K)) {
+    // phase 2: V here; J_perm (column-major d x d) into M's buffer once M is
+    // consumed, U = Q J_perm by the batched GEMM that follows
+    for (int e = tid; e < K * d; e += NT) {
+      const int j = e / K, k = e - j * K;
+      const int pj = perm[j];
+      const double sj = sval[pj];
+      const c128 m = M[int64_t(pj) * K + k];
+      V[int64_t(j) * K + k] = sj > 0.0 ? cscale(m, 1.0 / sj) : czero<double>();
+    }
+    __syncthreads();
+    for (int e = tid; e < d * d; e += NT) {
+      const int j = e / d, i = e - j * d;
+      M[e] = J[int64_t(perm[j]) * d + i];
+    }
+    if (tid == 0) g.tail[item] = 2;
+  } else if (have_sv && (g.want == 1 || 2 * r <= K)) {
     for (int e = tid; e < K * d; e += NT) {
       const int j = e / K, k = e - j * K;
       const int pj = perm[j];
@@ -1248,11 +1289,12 @@ extern "C" int lrz_cgemm(int dtype, int64_t batch, int M, int N, int Kd, int opA
 size_t lrz_arsvd_ws(int64_t B, int K, int D) {
   return size_t(B) * (size_t(2) * D * K + size_t(D) * D) * sizeof(c128);
 }
-// plus the screening front end: resume index and three [B][K][max(Dtot, 32)] blocks
+// plus the screening front end: resume index, three [B][K][max(Dtot, SCR_DMAX)] blocks and
+// the tail-pipeline flags
 size_t lrz_arsvd_ws_total(int64_t B, int K, int D) {
-  const size_t dt = size_t(std::max(4 * D, 32));  // Dtot <= 4 D bound is loose but safe
+  const size_t dt = size_t(std::max(4 * D, SCR_DMAX));  // >= max(Dtot, SCR_DMAX) (Dtot <= 4 D)
   return lrz_arsvd_ws(B, K, D) + ((size_t(B) * sizeof(int32_t) + 255) & ~size_t(255)) +
-         3 * size_t(B) * K * dt * sizeof(c128);
+         3 * size_t(B) * K * dt * sizeof(c128) + ((size_t(B) + 255) & ~size_t(255));
 }
 
 extern "C" int lrz_arsvd(int64_t B, int K, const void *dA, int64_t a_stride,
@@ -1301,6 +1343,8 @@ extern "C" int lrz_arsvd(int64_t B, int K, const void *dA, int64_t a_stride,
   g.start_it = nullptr;
   g.ya = nullptr;
   g.ydtot = 0;
+  g.phase = 0;
+  g.tail = nullptr;
   g.U = (c128 *)U;
   g.V = (c128 *)V;
   g.S = S;
@@ -1369,6 +1413,30 @@ extern "C" int lrz_arsvd(int64_t B, int K, const void *dA, int64_t a_stride,
     g.start_it = resume;
     g.ya = Ya;
     g.ydtot = Dtot;
+    if (large_dmma && g.D == dneed) {
+      // tail pipeline: the two K^2 d products of the resumed last iteration as
+      // batched DMMA GEMMs (dmma_tiled.cu) between the two halves of the item
+      g.tail = (uint8_t *)(wp + 3 * blk);
+      g.phase = 1;
+      cudaMemsetAsync(g.tail, 0, size_t(B), st);
+      {
+        LrzProf prof("arsvd_kernel", st);
+        arsvd_kernel<<<unsigned(B), ARSVD_THREADS, 0, st>>>(g);
+      }
+      if (int rc2 = lrz_launch_status("arsvd_kernel (phase 1)")) return rc2;
+      const int64_t wst = int64_t(2) * g.D * K + int64_t(g.D) * g.D;
+      c128 *w0 = (c128 *)workspace;
+      if (int rc2 = lrz_arsvd_tail_M(B, K, g.D, dA, a_stride, w0 + int64_t(g.D) * K, w0, wst,
+                                     g.tail, st))
+        return rc2;
+      g.phase = 2;
+      {
+        LrzProf prof("arsvd_kernel:tail", st);
+        arsvd_kernel<<<unsigned(B), ARSVD_THREADS, 0, st>>>(g);
+      }
+      if (int rc2 = lrz_launch_status("arsvd_kernel (phase 2)")) return rc2;
+      return lrz_arsvd_tail_U(B, K, g.D, w0, w0 + int64_t(g.D) * K, wst, U, g.tail, st);
+    }
   }
   LrzProf prof("arsvd_kernel", st);
   arsvd_kernel<<<unsigned(B), ARSVD_THREADS, 0, st>>>(g);
@@ -1413,6 +1481,8 @@ extern "C" int lrz_arsvd_seq(int64_t B, int T, int K, const void *dA, const doub
   g.start_it = nullptr;
   g.ya = nullptr;
   g.ydtot = 0;
+  g.phase = 0;
+  g.tail = nullptr;
   g.U = (c128 *)U;
   g.V = (c128 *)V;
   g.S = S;

@@ -476,3 +476,50 @@ int lrz_chain_apply_dmma(int64_t B, int T, int t, int K, int D, const uint8_t *a
   b.kss = int64_t(T) * D;
   return zgemm_dmma_launch<double, false, false, false, true, 2>(B, b, s, "chain:Aupdate_dmma");
 }
+
+// arSVD tail pipeline (arsvd.cu): M[j][k] = sum_m Q[j][m] conj(dA[m][k]) = (dA^H Q)
+// for the items phase 1 marked (tail == 1); Q, M: [D][K] column blocks inside
+// each item's workspace (stride wst elements).
+int lrz_arsvd_tail_M(int64_t B, int K, int D, const void *dA, int64_t a_stride, const void *Q,
+                     void *M, int64_t wst, const uint8_t *tail, cudaStream_t s) {
+  ZgArgs a{};
+  a.NN = D;
+  a.J = K;
+  a.Kd = K;
+  a.X = Q;
+  a.xs = wst;
+  a.ldx = K;
+  a.Y = (const c128 *)dA;
+  a.ys = a_stride;
+  a.ldy = K;
+  a.out = M;
+  a.os = wst;
+  a.ldo = K;
+  a.mask = tail;
+  a.mstride = 1;
+  a.mval = 1;
+  return zgemm_dmma_launch<double, true, false, false, true, 0>(B, a, s, "arsvd_tail:M_dmma");
+}
+
+// U[j][k] = sum_i Q[i][k] J_perm[i][j] for the items phase 2 marked (tail == 2);
+// J_perm column-major d x d (d = D) at the start of the item's M block.
+int lrz_arsvd_tail_U(int64_t B, int K, int D, const void *Jp, const void *Q, int64_t wst,
+                     void *U, const uint8_t *tail, cudaStream_t s) {
+  ZgArgs a{};
+  a.NN = D;
+  a.J = K;
+  a.Kd = D;
+  a.X = Jp;
+  a.xs = wst;
+  a.ldx = D;
+  a.Y = (const c128 *)Q;
+  a.ys = wst;
+  a.ldy = K;
+  a.out = U;
+  a.os = int64_t(D) * K;
+  a.ldo = K;
+  a.mask = tail;
+  a.mstride = 1;
+  a.mval = 2;
+  return zgemm_dmma_launch<double, true, false, false, false, 0>(B, a, s, "arsvd_tail:U_dmma");
+}
