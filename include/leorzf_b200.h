@@ -276,6 +276,50 @@ int lrz_campaign_reduce(int64_t B, int T, int t_base, int K, int n_reset, int co
                         const uint8_t *method, const int32_t *k_est, double *stats,
                         void *stream);
 
+/* ---- fused entry points: what a non-Python caller binds ---- */
+
+/* Alg. 2 dispatcher over B items (lowrank.py:319-373): dA = gram_delta(H, dH),
+ * arSVD of dA from item b's sketch stream (omega row b, starting at
+ * cursor[b]), then 'none' (k_est = 0: the state is copied), Woodbury
+ * (k_est <= K/2 and cond(aux) <= 1e12) or full (the true Gram of H + dH,
+ * inverted with the 1e14 guard) -- the reference's decisions.  H, dH:
+ * [B][K][N] dtype; A, A_inv (in) and A_out, A_inv_out (out): complex128
+ * [B][K][K] (A / A_out nullable: GramState.A not maintained).  method
+ * (LRZ_METHOD_*), k_est, consumed (normals drawn), cost (cost units,
+ * lowrank.py:101-118; nullable), info (LRZ_INFO_* of the full inversion).
+ * Workspace: lrz_update_inverse_ws(dtype, B, K, N, cfg->d_max) bytes. */
+size_t lrz_update_inverse_ws(int dtype, int64_t B, int K, int N, int d_max);
+int lrz_update_inverse(int dtype, int64_t B, int K, int N, const void *H, const void *dH,
+                       double alpha, const void *A, const void *A_inv, const double *omega,
+                       int64_t omega_stride, const int64_t *cursor, const lrz_arsvd_cfg *cfg,
+                       void *A_out, void *A_inv_out, uint8_t *method, int32_t *k_est,
+                       int64_t *consumed, double *cost, int32_t *info, void *workspace,
+                       void *stream);
+
+/* One time chunk of the per-trial sweep (harness._sweep_trial,
+ * harness.py:221-255), fully digital: for B trials x T steps, the Grams, the
+ * Gram corrections, the arSVD of every dispatcher step in order per trial at
+ * the exact sketch cursors, the dispatcher, the batched full inversions, the
+ * Woodbury chain, the precoder and the rates -- in stream order, no host
+ * synchronisation.  H [B][T][K][N] dtype, noise [B][K]; t0 = global index of
+ * the chunk's first step (resets at t % n_reset == 0); cfg NULL = the
+ * conventional method.  omega: [B] rows (stride omega_stride) starting at each
+ * trial's first unconsumed normal; consumed[b] = normals the chunk used.
+ * State in/out: A_inv_state, A_state (nullable) [B][K][K] complex128; G_prev
+ * = the previous chunk's last Gram (NULL at the start of a pass), G_last
+ * (nullable) receives this chunk's.  Outputs per (b, t): rates (sum-rate),
+ * per_ut [B][T][K], method, k_est, info; A_inv_seq nullable [B][T][K][K].
+ * Workspace: lrz_trajectory_ws(dtype, B, T, K, N, d_max) bytes (d_max = 1
+ * for the conventional method). */
+size_t lrz_trajectory_ws(int dtype, int64_t B, int T, int K, int N, int d_max);
+int lrz_trajectory(int dtype, int64_t B, int T, int K, int N, const void *H, double alpha,
+                   double P_t, const double *noise, int64_t t0, int n_reset,
+                   const lrz_arsvd_cfg *cfg, const double *omega, int64_t omega_stride,
+                   void *A_inv_state, void *A_state, const void *G_prev, void *G_last,
+                   double *rates, double *per_ut, uint8_t *method, int32_t *k_est,
+                   int32_t *info, int64_t *consumed, void *A_inv_seq, void *workspace,
+                   void *stream);
+
 /* Workspace sizing for the calls that take one. */
 #define LRZ_WS_INVERSE 0
 #define LRZ_WS_ARSVD 1

@@ -79,6 +79,13 @@ _SIGS = {
     "lrz_campaign_reduce": (C.c_int, [I64, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, P, P,
                                       P, P]),
     "lrz_workspace_bytes": (SZ, [C.c_int, C.c_int, I64, C.c_int, C.c_int, C.c_int]),
+    "lrz_update_inverse_ws": (SZ, [C.c_int, I64, C.c_int, C.c_int, C.c_int]),
+    "lrz_update_inverse": (C.c_int, [C.c_int, I64, C.c_int, C.c_int, P, P, F64, P, P, P, I64, P,
+                                     C.POINTER(ArsvdCfg), P, P, P, P, P, P, P, P, P]),
+    "lrz_trajectory_ws": (SZ, [C.c_int, I64, C.c_int, C.c_int, C.c_int, C.c_int]),
+    "lrz_trajectory": (C.c_int, [C.c_int, I64, C.c_int, C.c_int, C.c_int, P, F64, F64, P, I64,
+                                 C.c_int, C.POINTER(ArsvdCfg), P, I64, P, P, P, P, P, P, P, P,
+                                 P, P, P, P, P]),
     "lrz_spec_verify": (C.c_int, [I64, C.c_int, C.c_int, C.POINTER(ArsvdCfg), P, P, P, P, P, P,
                                   P, P, P]),
 }

@@ -1,8 +1,11 @@
 """Exception types of the drop-in API.
 
 Same names, hierarchy and meaning as the reference's
-``pkg/src/leorzf/errors.py:8-54``, so callers that catch
-``leorzf.errors.X`` can catch ``paper_2512_16543_b200.errors.X`` instead.
+``pkg/src/leorzf/errors.py:8-54``.  When the reference package is installed
+(``import leorzf`` works), every class here also SUBCLASSES the reference's
+class of the same name, so a caller that catches ``leorzf.errors.X`` -- the
+reference's CLI and harness (cli.py:290-299) -- catches what this package
+raises after the swap INTEGRATION.md shows.
 
 Device kernels never raise: they write a per-item status code into an
 ``int32 info[B]`` array (see ``include/leorzf_b200.h``) and the Python
@@ -10,51 +13,62 @@ layer maps the codes below onto these exceptions for single-item calls.
 """
 
 
-class ConfigError(Exception):
+try:  # the reference installed: be its exception classes too
+    from leorzf import errors as _ref
+except Exception:  # pragma: no cover - depends on the environment
+    _ref = None
+
+
+def _also(name: str) -> tuple:
+    """(the reference's class of that name,) when it is importable."""
+    return (getattr(_ref, name),) if _ref is not None and hasattr(_ref, name) else ()
+
+
+class ConfigError(*(_also("ConfigError") or (Exception,))):
     """Invalid scenario configuration (reference errors.py:8)."""
 
 
-class ParseError(ConfigError):
+class ParseError(ConfigError, *_also("ParseError")):
     """Config text could not be parsed (reference errors.py:12)."""
 
 
-class UnknownKeyError(ConfigError):
+class UnknownKeyError(ConfigError, *_also("UnknownKeyError")):
     """Unknown configuration key (reference errors.py:16)."""
 
 
-class RangeError(ConfigError):
+class RangeError(ConfigError, *_also("RangeError")):
     """Configuration value out of range (reference errors.py:20)."""
 
 
-class SimulationError(Exception):
+class SimulationError(*(_also("SimulationError") or (Exception,))):
     """Numerical failure while running the precoder update (errors.py:24)."""
 
 
-class DimensionMismatchError(SimulationError):
+class DimensionMismatchError(SimulationError, *_also("DimensionMismatchError")):
     """Operands have incompatible shapes (errors.py:28)."""
 
 
-class SingularMatrixError(SimulationError):
+class SingularMatrixError(SimulationError, *_also("SingularMatrixError")):
     """Condition estimate above 1e14 or non-finite (errors.py:32)."""
 
 
-class SingularAuxiliaryError(SimulationError):
+class SingularAuxiliaryError(SimulationError, *_also("SingularAuxiliaryError")):
     """Woodbury r x r auxiliary matrix condition above 1e12 (errors.py:36)."""
 
 
-class UnsupportedGeometryError(SimulationError):
+class UnsupportedGeometryError(SimulationError, *_also("UnsupportedGeometryError")):
     """Array geometry outside what an operation supports (errors.py:41)."""
 
 
-class BelowMinElevationError(SimulationError):
+class BelowMinElevationError(SimulationError, *_also("BelowMinElevationError")):
     """A served user terminal is below the elevation mask (errors.py:45)."""
 
 
-class ZeroPrecoderError(SimulationError):
+class ZeroPrecoderError(SimulationError, *_also("ZeroPrecoderError")):
     """Precoder has zero Frobenius norm (errors.py:49)."""
 
 
-class EmptyInputError(SimulationError):
+class EmptyInputError(SimulationError, *_also("EmptyInputError")):
     """Operation requires a non-empty input (errors.py:53)."""
 
 

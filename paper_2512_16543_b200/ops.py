@@ -520,3 +520,78 @@ def prof_collect(device=None) -> dict:
         ms, n = v.split(":")
         out[name] = (float(ms), int(n))
     return out
+
+
+# -- fused entry points (fused.cu) ---------------------------------------------------------
+
+def update_inverse_fused(H: torch.Tensor, dH: torch.Tensor, alpha: float, A: torch.Tensor,
+                         A_inv: torch.Tensor, omega: torch.Tensor, cursor: torch.Tensor, eta,
+                         k_init: int, p: int, i_max: int) -> dict:
+    """lrz_update_inverse over a flat batch: H, dH [B,K,N]; A, A_inv [B,K,K] c128;
+    omega [B,L] f64 (row b = item b's stream); cursor [B] i64."""
+    for t_, n_ in ((H, "H"), (dH, "dH"), (A, "A"), (A_inv, "A_inv"), (cursor, "cursor")):
+        _chk(t_, n_)
+    if not omega.is_cuda or omega.dim() != 2 or omega.stride(1) != 1:
+        raise ValueError("omega must be a [B, L] CUDA tensor with contiguous rows")
+    B, K, Nn = H.shape
+    dev = H.device
+    D = d_max_for(K, k_init, p, i_max)
+    cfg = _arsvd_cfg(eta, k_init, p, i_max, D, omega.shape[1])
+    lib = N.lib_for(dev)
+    out = dict(A=torch.empty_like(A), A_inv=torch.empty_like(A_inv),
+               method=torch.empty(B, dtype=torch.uint8, device=dev),
+               k_est=torch.empty(B, dtype=torch.int32, device=dev),
+               consumed=torch.empty(B, dtype=torch.int64, device=dev),
+               cost=torch.empty(B, dtype=torch.float64, device=dev),
+               info=torch.empty(B, dtype=torch.int32, device=dev))
+    ws = workspace(dev, lib.lrz_update_inverse_ws(_dt(H), B, K, Nn, D), "fused_ui")
+    N.check(lib.lrz_update_inverse(_dt(H), B, K, Nn, H.data_ptr(), dH.data_ptr(), float(alpha),
+                                   A.data_ptr(), A_inv.data_ptr(), omega.data_ptr(),
+                                   omega.stride(0), cursor.data_ptr(), C.byref(cfg),
+                                   out["A"].data_ptr(), out["A_inv"].data_ptr(),
+                                   out["method"].data_ptr(), out["k_est"].data_ptr(),
+                                   out["consumed"].data_ptr(), out["cost"].data_ptr(),
+                                   out["info"].data_ptr(), ws.data_ptr(), N.stream_ptr(dev)),
+            "lrz_update_inverse")
+    _count(8)
+    return out
+
+
+def trajectory_chunk(H: torch.Tensor, alpha: float, P_t: float, noise: torch.Tensor, t0: int,
+                     n_reset: int, eta, k_init: int, p: int, i_max: int,
+                     omega: torch.Tensor | None, A_inv_state: torch.Tensor,
+                     A_state: torch.Tensor | None, G_prev: torch.Tensor | None,
+                     keep_A_inv: bool = False) -> dict:
+    """lrz_trajectory: one chunk H [B,T,K,N] of the in-order sweep (eta None =
+    conventional).  A_inv_state / A_state are updated in place; returns the
+    per-step outputs and G_last for the next chunk."""
+    _chk(H, "H")
+    _chk(noise, "noise")
+    _chk(A_inv_state, "A_inv_state")
+    B, T, K, Nn = H.shape
+    dev = H.device
+    D = 1 if eta is None else d_max_for(K, k_init, p, i_max)
+    cfg = None if eta is None else _arsvd_cfg(eta, k_init, p, i_max, D, omega.shape[1])
+    lib = N.lib_for(dev)
+    out = dict(rates=torch.empty(B, T, dtype=torch.float64, device=dev),
+               per_ut=torch.empty(B, T, K, dtype=torch.float64, device=dev),
+               method=torch.empty(B, T, dtype=torch.uint8, device=dev),
+               k_est=torch.empty(B, T, dtype=torch.int32, device=dev),
+               info=torch.empty(B, T, dtype=torch.int32, device=dev),
+               consumed=torch.zeros(B, dtype=torch.int64, device=dev),
+               G_last=torch.empty(B, K, K, dtype=torch.complex128, device=dev),
+               A_inv=(torch.empty(B, T, K, K, dtype=torch.complex128, device=dev)
+                      if keep_A_inv else None))
+    ws = workspace(dev, lib.lrz_trajectory_ws(_dt(H), B, T, K, Nn, D), "fused_traj")
+    N.check(lib.lrz_trajectory(_dt(H), B, T, K, Nn, H.data_ptr(), float(alpha), float(P_t),
+                               noise.data_ptr(), int(t0), int(n_reset),
+                               C.byref(cfg) if cfg is not None else None,
+                               N.ptr(omega), omega.stride(0) if omega is not None else 0,
+                               A_inv_state.data_ptr(), N.ptr(A_state), N.ptr(G_prev),
+                               out["G_last"].data_ptr(), out["rates"].data_ptr(),
+                               out["per_ut"].data_ptr(), out["method"].data_ptr(),
+                               out["k_est"].data_ptr(), out["info"].data_ptr(),
+                               out["consumed"].data_ptr(), N.ptr(out["A_inv"]), ws.data_ptr(),
+                               N.stream_ptr(dev)), "lrz_trajectory")
+    _count(10)
+    return out

@@ -133,6 +133,19 @@ class TrajectoryRunner:
         self._in_order = False    # set once a chunk needed the in-order arSVD
         self._walk_first = False  # set once a chunk needed the cursor walk
 
+    def snapshot(self) -> dict:
+        """Copy of the chunk-to-chunk state (for re-running a sync=False chunk)."""
+        cl = lambda x: None if x is None else x.clone()  # noqa: E731
+        return dict(t=self.t, H_prev=cl(self.H_prev), G_prev=cl(self.G_prev),
+                    A_inv=self.A_inv.clone(), A=self.A.clone(), in_order=self._in_order,
+                    walk_first=self._walk_first)
+
+    def restore(self, snap: dict) -> None:
+        self.t, self.H_prev, self.G_prev = snap["t"], snap["H_prev"], snap["G_prev"]
+        self.A_inv.copy_(snap["A_inv"])
+        self.A.copy_(snap["A"])
+        self._in_order, self._walk_first = snap["in_order"], snap["walk_first"]
+
     def _ev(self):
         if self.prof is None:
             return None
@@ -245,7 +258,11 @@ class TrajectoryRunner:
         sync=False: no host round trip at all (CUDA-graph capture): the chunk is
         computed optimistically from the first arSVD pass and ``result.flags``
         (device int32[2]: unverified trials, short sketch windows) must be
-        checked by the caller -- nonzero means re-run the chunk with sync=True."""
+        checked by the caller.  Nonzero means the results are not the
+        reference's: the runner's state (t, H_prev, G_prev, A_inv, A) has
+        already advanced past this chunk, so the re-run with sync=True needs a
+        FRESH runner (or one restored with ``snapshot()`` / ``restore()`` taken
+        before the call) and the same sketch window."""
         c = self.cfg
         B, T, K, Nn = H.shape
         assert (B, K, Nn) == (self.B, self.K, self.N) and H.dtype == self.dtype
@@ -395,7 +412,10 @@ class TrajectoryRunner:
         self.H_prev = H[:, -1].contiguous().clone()
         self.G_prev = G[:, -1].contiguous().clone()
         self.t += T
-        info = torch.maximum(info, pr["info"].reshape(B, T))
+        # status per step: the inverse's code (singular / indefinite) wins over the
+        # precoder's (zero norm), so a singular step is never hidden by a later code
+        pinfo = pr["info"].reshape(B, T)
+        info = torch.where(info != 0, info, pinfo)
         return ChunkResult(rates=pr["sum"].reshape(B, T), per_ut=pr["rates"].reshape(B, T, K),
                            method=method, k_est=k_est, iters=iters, info=info,
                            A_inv=A_inv_seq if keep_A_inv else None,

@@ -6,6 +6,7 @@ import numpy as np
 import pytest
 import torch
 
+from conftest import ROOT
 from paper_2512_16543_b200 import _native, errors, lowrank, scenario as S
 from paper_2512_16543_b200.omega import (consumed_by, normals_per_call_max, sketch_widths)
 from paper_2512_16543_b200.trajectory import step_costs
@@ -155,3 +156,31 @@ def test_drift_is_small_per_step():
     H = S.channels(spec)[0]
     rel = np.linalg.norm(H[1] - H[0]) / np.linalg.norm(H[0])
     assert 1e-4 < rel < 0.2
+
+
+def test_exceptions_subclass_the_reference_classes_when_installed():
+    """With the reference installed (baseline/_ref, or any `import leorzf`),
+    a caller catching leorzf.errors.X catches this package's X
+    (errors.py:28-50; cli.py:290-299).  Run in a fresh interpreter so the
+    reference is importable before this package's errors module loads."""
+    import os
+    import subprocess
+    import sys
+    ref = ROOT / "baseline" / "_ref"
+    if not (ref / "leorzf").exists():
+        pytest.skip("reference not installed in baseline/_ref")
+    code = (
+        "import leorzf.errors as E\n"
+        "from paper_2512_16543_b200 import errors as X\n"
+        "for n in ('ConfigError', 'SimulationError', 'DimensionMismatchError',\n"
+        "          'SingularMatrixError', 'SingularAuxiliaryError', 'ZeroPrecoderError',\n"
+        "          'EmptyInputError', 'BelowMinElevationError'):\n"
+        "    assert issubclass(getattr(X, n), getattr(E, n)), n\n"
+        "try:\n"
+        "    raise X.SingularAuxiliaryError('x')\n"
+        "except E.SimulationError:\n"
+        "    print('ok')\n")
+    env = dict(os.environ, PYTHONPATH=os.pathsep.join([str(ref), str(ROOT)]))
+    out = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True,
+                         timeout=120)
+    assert out.returncode == 0 and out.stdout.strip() == "ok", out.stderr
