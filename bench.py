@@ -354,9 +354,9 @@ def measured_peaks(torch, dev):
     """FP64 / FP32 dense GEMM peaks measured now (cuBLAS via torch.matmul),
     since MEASURED_PEAKS.json only has HBM and bf16."""
     out = {}
-    for name, dt in (("fp64", torch.float64), ("fp32", torch.float32)):
-        n = 8192 if name == "fp64" else 8192
-        torch.backends.cuda.matmul.allow_tf32 = False
+    for name, dt in (("fp64", torch.float64), ("fp32", torch.float32), ("tf32", torch.float32)):
+        n = 8192
+        torch.backends.cuda.matmul.allow_tf32 = name == "tf32"
         a = torch.randn(n, n, dtype=dt, device=dev)
         b = torch.randn(n, n, dtype=dt, device=dev)
         for _ in range(2):
@@ -371,6 +371,9 @@ def measured_peaks(torch, dev):
             best = min(best, e0.elapsed_time(e1) / 1e3)
         out[name] = 2 * n ** 3 / best / 1e12
         del a, b
+    torch.backends.cuda.matmul.allow_tf32 = False
+    # 3xTF32 (hi*hi + hi*lo + lo*hi): three TF32 products per real product
+    out["tf32x3_effective"] = out["tf32"] / 3.0
     return out
 
 
@@ -385,6 +388,8 @@ def kernel_model(name: str, spec, items: int, D: int, Dtot: int, r_mean: float,
     nb = (K + 31) // 32
     if name == "dmma_hn_kernel:W":                 # W = H^H A^-1 + ||W||^2
         return (8 * K * K * N + 8 * N * K) * items, (K * N * c + K * K * 16 + N * K * c) * items
+    if name == "tc_w_kernel":                      # W on tcgen05 (3xTF32, complex64)
+        return (8 * K * K * N + 8 * N * K) * items, (K * N * c + N * K * c + 8 * (2 * K) ** 2) * items
     if name == "dmma_hn_kernel:coupling":          # (G - alpha I) A^-1, SURVEY A.6
         return 8 * K ** 3 * items, 3 * K * K * 16 * items
     if name == "precode_dmma32_kernel":            # W + norm + coupling + SINR fused
@@ -510,18 +515,25 @@ def run_b200(args):
     mp_path = ROOT / "MEASURED_PEAKS.json"
     hbm = json.loads(mp_path.read_text())["hbm_gbs"] if mp_path.exists() else 6650.0
 
-    def roofline_table(kprof, sp, steps, items_per_launch, summ, Dtot, D):
-        """Per-kernel (per launch) achieved vs roofline from CUDA-event times over
-        the timed region; the dominant kernel (largest total time) first."""
-        fpk = peaks["fp64"]   # every N-sized product runs on the FP64 pipe (DMMA / DFMA)
+    def roofline_table(kprof, sp, steps, items_per_pass, summ, Dtot, D):
+        """Per-kernel achieved vs roofline from CUDA-event times over the timed
+        region: a kernel's algorithmic work over one pass (items_per_pass
+        (trial, step) items; Woodbury / full-step counts for the chain and the
+        inversions) divided evenly over its launches in the pass; the dominant
+        kernel (largest total time) first."""
         rows = {}
         for name, (ms, n) in kprof.items():
+            # FP64 pipe (DMMA / DFMA) for everything but the tcgen05 precoder, whose
+            # 3xTF32 split runs three TF32 products per real product
+            fpk = peaks["tf32x3_effective"] if name == "tc_w_kernel" else peaks["fp64"]
             if n == 0 or ms <= 0:
                 continue
             per_launch = ms / n
             per_pass = n / max(steps, 1)
-            m = kernel_model(name, sp, items_per_launch, D, Dtot, summ["_r"],
-                             summ["_full"] / per_pass, summ["_wb"] / per_pass)
+            m = kernel_model(name, sp, items_per_pass, D, Dtot, summ["_r"], summ["_full"],
+                             summ["_wb"])
+            if m is not None:
+                m = (m[0] / per_pass, m[1] / per_pass)
             row = {"ms_total_per_step": ms / steps, "launches_per_step": n / steps,
                    "ms_per_launch": per_launch}
             if m is not None:
@@ -546,8 +558,11 @@ def run_b200(args):
                            launches_per_step=r["launches_per_step"],
                            algorithmic={"flops_per_launch": r["flops_per_launch"],
                                         "bytes_per_launch": r["bytes_per_launch"]},
-                           peak_source=("measured now: cuBLAS DGEMM 8192^3 via torch.matmul "
-                                        "(MEASURED_PEAKS.json has no FP64 entry)")
+                           peak_source=(("measured now: cuBLAS TF32 GEMM 8192^3 / 3 (3xTF32 "
+                                         "split), MEASURED_PEAKS.json has no TF32 entry")
+                                        if name == "tc_w_kernel" else
+                                        ("measured now: cuBLAS DGEMM 8192^3 via torch.matmul "
+                                         "(MEASURED_PEAKS.json has no FP64 entry)"))
                            if r["unit"] == "TFLOP/s" else "MEASURED_PEAKS.json hbm_gbs",
                            traffic=None)
                 return out
@@ -595,7 +610,7 @@ def run_b200(args):
     value = world * updates / (ms_wb / 1e3)
     value_full = world * updates / (ms_full / 1e3)
     Dtot, D = sketch_dims(spec)
-    ktab = roofline_table(kprof, spec, args.steps, B * chunk, summ, Dtot, D)
+    ktab = roofline_table(kprof, spec, args.steps, B * T, summ, Dtot, D)
     roof = dominant(ktab)
     # stage split: one more pass with events between the runner's stages
     prof = []
@@ -605,6 +620,7 @@ def run_b200(args):
     for name, a, b_ in prof:
         stages[name] = stages.get(name, 0.0) + a.elapsed_time(b_)
     del H_chunks
+    ops._WS.clear()
     torch.cuda.empty_cache()
 
     # ================================================================ e2e
@@ -705,6 +721,7 @@ def run_b200(args):
             configs[lab] = run_config(sp, etas, reps, rank, world, dev, one_pass, summarize,
                                       roofline_table, dominant, sketch_dims, timed, ops, S,
                                       DeviceOmegaStreams, torch)
+            ops._WS.clear()          # grow-only scratch of this config's shapes
             torch.cuda.empty_cache()
         if rank == 0 and world == 1 and not args.no_cpu:
             for lab, name, ov, etas, _ in runs:
@@ -718,6 +735,8 @@ def run_b200(args):
 
     leo = None
     if not args.no_extra:
+        ops._WS.clear()
+        torch.cuda.empty_cache()
         leo = leo_side(args, dev, world, max_over_ranks)
 
     cpu = None
@@ -799,7 +818,7 @@ def run_config(sp, etas, reps, rank, world, dev, one_pass, summarize, roofline_t
         runner_ms = sum(evs[i].elapsed_time(evs[i + 1]) for i in range(0, len(evs), 2)) / reps
         summ = summarize(outs)
         Dtot, D = sketch_dims(sp)
-        ktab = roofline_table(kprof, sp, reps, B * ch, summ, Dtot, D)
+        ktab = roofline_table(kprof, sp, reps, B * T, summ, Dtot, D)
         key = "conventional" if e is None else f"wb_eta{e:g}"
         out[key] = {
             "updates_per_s": world * B * T / (runner_ms / 1e3),

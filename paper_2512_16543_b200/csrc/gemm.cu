@@ -898,7 +898,7 @@ int lrz_dmma_hn(int dtype, int64_t B, int NN, int J, int Kd, const void *X, int6
                 cudaStream_t s, const uint8_t *mask = nullptr,
                 const char *what = "dmma_hn_kernel");
 int lrz_tc_w_ok(int K, int N, int64_t h_stride);
-int lrz_tc_w_tiles(int N);
+int lrz_tc_w_tiles(int N, int K);
 size_t lrz_tc_w_ws(int64_t B, int K);
 int lrz_tc_precoder_w(int64_t B, int K, int N, const void *H, const void *A_inv, int64_t ais,
                       void *W, double *parts, void *ws, cudaStream_t s);
@@ -1144,7 +1144,7 @@ extern "C" int lrz_precode_rate(int dtype, int64_t B, int K, int N, const void *
       if (dtype == LRZ_C64 && use_tc() && lrz_tc_w_ok(K, N, h_stride) &&
           w_stride == int64_t(N) * K) {
         // complex64: W = H^H A^-1 on tcgen05 (3xTF32, TMA tiles, TMEM accumulator)
-        np_w = lrz_tc_w_tiles(N);
+        np_w = lrz_tc_w_tiles(N, K);
         const int64_t G = tc_group(K);
         for (int64_t b0 = 0; b0 < B; b0 += G) {
           const int64_t g = std::min<int64_t>(G, B - b0);

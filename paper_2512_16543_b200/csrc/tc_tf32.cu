@@ -103,13 +103,19 @@ __host__ __device__ constexpr uint32_t tc_idesc(int n) {
 }
 LRZ_DEV float tf32_hi(float x) { return __uint_as_float(__float_as_uint(x) & 0xFFFFE000u); }
 
+// accumulator columns per CTA: all 2K when 2K <= 256, else one 256-column half
+// (two CTAs per n-tile, so TMEM (512 columns) and shared memory hold two CTAs
+// per SM and one CTA's epilogue overlaps the other's MMAs)
+__host__ __device__ inline int tc_pc(int K) { return 2 * K < 256 ? 2 * K : 256; }
+__host__ __device__ inline int tc_halves(int K) { return 2 * K > 256 ? 2 : 1; }
+
 template <int S>
 struct TcSmem {
-  // per stage: raw H slab (8 x 256 floats), Aop hi / lo (128 x 16), Bop hi / lo (2K x 16)
+  // per stage: raw H slab (8 x 256 floats), Aop hi / lo (128 x 16), Bop hi / lo (Pc x 16)
   static constexpr size_t raw = 8 * 256 * 4, aop = TC_M * TC_QC * 4;
-  __host__ __device__ static size_t bop(int K) { return size_t(2 * K) * TC_QC * 4; }
+  __host__ __device__ static size_t bop(int K) { return size_t(tc_pc(K)) * TC_QC * 4; }
   __host__ __device__ static size_t stage(int K) { return raw + 2 * aop + 2 * bop(K); }
-  __host__ __device__ static size_t bytes(int K) { return 1024 + S * stage(K) + 256; }
+  __host__ __device__ static size_t bytes(int K) { return 128 + S * stage(K) + 256; }
 };
 
 // Bop (hi, lo) of every item in the canonical chunk order: chunk c (q in
@@ -139,13 +145,13 @@ __global__ void tc_bop_kernel(int64_t B, int K, const c128 *__restrict__ Ainv, i
   }
 }
 
-template <int NH, int S>
-__global__ void __launch_bounds__(TC_THREADS, 1)
+template <int S>
+__global__ void __launch_bounds__(TC_THREADS, 2)
     tc_w_kernel(const __grid_constant__ CUtensorMap map_h, const __grid_constant__ CUtensorMap map_b,
                 int K, int N, int64_t B, c64 *__restrict__ W, double *__restrict__ parts) {
-  extern __shared__ __align__(1024) unsigned char tc_smem_raw[];
+  extern __shared__ __align__(128) unsigned char tc_smem_raw[];
   unsigned char *sm = reinterpret_cast<unsigned char *>(
-      (reinterpret_cast<uintptr_t>(tc_smem_raw) + 1023) & ~uintptr_t(1023));
+      (reinterpret_cast<uintptr_t>(tc_smem_raw) + 127) & ~uintptr_t(127));
   using L = TcSmem<S>;
   const size_t stage = L::stage(K);
   const size_t bop_b = L::bop(K);
@@ -154,16 +160,16 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 3 * S + 1);
   float *red = reinterpret_cast<float *>(bars + 3 * S + 2);  // 4 doubles as 8 floats
 
-  const int tiles = N / TC_M;
+  const int halves = tc_halves(K);
+  const int tiles = (N / TC_M) * halves;
   const int64_t item = blockIdx.x / tiles;
-  const int n0 = int(blockIdx.x - item * tiles) * TC_M;
+  const int tl = int(blockIdx.x - item * tiles);
+  const int n0 = (tl / halves) * TC_M, half = tl % halves;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nch = (2 * K) / TC_QC;
-  const int P = 2 * K;                       // accumulator columns
-  const int NI = P < 256 ? P : 256;          // UMMA N per instruction
-  constexpr uint32_t TMEM_COLS = NH == 2 ? 512 : 0;
-  const uint32_t tcols = NH == 2 ? 512u : (P <= 32 ? 32u : P <= 64 ? 64u : P <= 128 ? 128u : 256u);
-  (void)TMEM_COLS;
+  const int P = tc_pc(K);                    // accumulator columns of this CTA
+  const int NI = P;                          // UMMA N per instruction
+  const uint32_t tcols = P <= 32 ? 32u : P <= 64 ? 64u : P <= 128 ? 128u : 256u;
 
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < S; ++s) {
@@ -189,7 +195,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     // ---------------- TMA producer
     if (lane == 0) {
       const int64_t hrow = item * K;
-      const int64_t brow_hi = item * nch * int64_t(K);
+      // this CTA's half of each Bop chunk tile: rows of 128 B from half * P / 2
+      const int64_t brow_hi = item * nch * int64_t(K) + half * (P / 2);
       const int64_t brow_lo = B * nch * int64_t(K) + brow_hi;
       const uint32_t tx = uint32_t(L::raw + 2 * bop_b);
       for (int c = 0; c < nch; ++c) {
@@ -217,15 +224,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
 #pragma unroll
         for (int ks = 0; ks < 2; ++ks) {
           const uint64_t ah = sdesc(ahi + 256 * ks), al = sdesc(alo + 256 * ks);
-#pragma unroll
-          for (int h = 0; h < NH; ++h) {
-            const uint64_t bh = sdesc(bhi + 16384 * h + 256 * ks);
-            const uint64_t bl = sdesc(blo + 16384 * h + 256 * ks);
-            const uint32_t d = tmem + 256 * h;
-            tc_mma(d, ah, bh, idesc, (c > 0 || ks > 0) ? 1u : 0u);
-            tc_mma(d, ah, bl, idesc, 1u);
-            tc_mma(d, al, bh, idesc, 1u);
-          }
+          const uint64_t bh = sdesc(bhi + 256 * ks), bl = sdesc(blo + 256 * ks);
+          tc_mma(tmem, ah, bh, idesc, (c > 0 || ks > 0) ? 1u : 0u);
+          tc_mma(tmem, ah, bl, idesc, 1u);
+          tc_mma(tmem, al, bh, idesc, 1u);
         }
         tc_commit(&empty[s]);
         if (c == nch - 1) tc_commit(tmem_full);
@@ -264,7 +266,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     const int q4 = warp & 3;
     const int row = 32 * q4 + lane;
     const int n = n0 + row;
-    c64 *wrow = W + (item * int64_t(N) + n) * K;
+    c64 *wrow = W + (item * int64_t(N) + n) * K + half * 128;  // 256 real = 128 complex columns
     double nrm = 0.0;
     for (int col = 0; col < P; col += 32) {
       uint32_t r[32];
@@ -342,21 +344,21 @@ static int make_map_2d(CUtensorMap *m, const void *base, uint64_t cols, uint64_t
   return LRZ_OK;
 }
 
-template <int NH, int S>
+template <int S>
 static int tc_w_launch(const CUtensorMap &mh, const CUtensorMap &mb, int K, int N, int64_t B,
                        c64 *W, double *parts, cudaStream_t s) {
   const size_t sm = TcSmem<S>::bytes(K);
   static size_t reserved = 0;  // largest dynamic shared memory set so far (K-dependent)
   if (sm > reserved) {
-    if (cudaFuncSetAttribute(tc_w_kernel<NH, S>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    if (cudaFuncSetAttribute(tc_w_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              int(sm)) != cudaSuccess) {
       lrz_set_error("tc_w_kernel: cannot reserve %zu bytes of shared memory", sm);
       return LRZ_ELAUNCH;
     }
     reserved = sm;
   }
-  const int64_t grid = B * (N / TC_M);
-  tc_w_kernel<NH, S><<<unsigned(grid), TC_THREADS, sm, s>>>(mh, mb, K, N, B, W, parts);
+  const int64_t grid = B * (N / TC_M) * tc_halves(K);
+  tc_w_kernel<S><<<unsigned(grid), TC_THREADS, sm, s>>>(mh, mb, K, N, B, W, parts);
   return lrz_launch_status("tc_w_kernel");
 }
 
@@ -368,8 +370,8 @@ using namespace lrz;
 int lrz_tc_w_ok(int K, int N, int64_t h_stride) {
   return K >= 32 && K <= 256 && K % 8 == 0 && N % TC_M == 0 && h_stride == int64_t(K) * N;
 }
-// norm partials per item (one per 128-row tile)
-int lrz_tc_w_tiles(int N) { return N / TC_M; }
+// norm partials per item (one per CTA: 128-row tile x column half)
+int lrz_tc_w_tiles(int N, int K) { return (N / TC_M) * tc_halves(K); }
 // workspace: the pre-split Bop of every item
 size_t lrz_tc_w_ws(int64_t B, int K) { return size_t(B) * 2 * (2 * K) * (2 * K) * sizeof(float); }
 
@@ -388,8 +390,7 @@ int lrz_tc_precoder_w(int64_t B, int K, int N, const void *H, const void *A_inv,
   if (int rc = make_map_2d(&mh, H, uint64_t(2) * N, uint64_t(B) * K, uint64_t(N) * 8, 256, 8))
     return rc;
   const uint64_t brows = uint64_t(B) * 2 * ((2 * K) / TC_QC) * K;
-  if (int rc = make_map_2d(&mb, bop, 32, brows, 128, 32, uint32_t(K))) return rc;
+  if (int rc = make_map_2d(&mb, bop, 32, brows, 128, 32, uint32_t(tc_pc(K) / 2))) return rc;
   LrzProf prof("tc_w_kernel", s);
-  if (K > 128) return tc_w_launch<2, 2>(mh, mb, K, N, B, (c64 *)W, parts, s);
-  return tc_w_launch<1, 3>(mh, mb, K, N, B, (c64 *)W, parts, s);
+  return tc_w_launch<2>(mh, mb, K, N, B, (c64 *)W, parts, s);
 }
