@@ -377,6 +377,31 @@ def measured_peaks(torch, dev):
     return out
 
 
+def ncu_traffic(kernel: str, spec, B: int, chunk: int):
+    """DRAM bytes per launch (dram__bytes_read.sum + dram__bytes_write.sum) of the
+    dominant kernel from the committed ncu launch list of the same workload
+    (profiles/r02_traffic_<config>_<dtype>.json, scripts/ncu_summary.py traffic),
+    matched by kernel and grid size; (None, None) when not captured."""
+    path = ROOT / "profiles" / f"r02_traffic_{spec.name}_{spec.dtype}.json"
+    if not path.exists():
+        return None, None
+    tab = json.loads(path.read_text())
+    K, N = spec.K, spec.N
+    T = "double" if spec.dtype == "c128" else "float"
+    items = B * chunk
+    keys = {
+        "dmma_hn_kernel:W": f"void lrz::zgemm_dmma_kernel<{T}, 0, 1, 0, 0, 0> grid"
+                            f"({items * -(-N // 64) * -(-K // 64)},1,1)",
+        "gram_dmma_off_kernel": f"void lrz::gram_dmma_off_kernel<{T}> grid"
+                                f"({-(-items * (K // 32) * (K // 32 + 1) // 2 // 4)},1,1)",
+    }
+    k = keys.get(kernel)
+    if k is None or k not in tab:
+        return None, None
+    return tab[k]["dram_bytes_per_launch"], (
+        f"ncu dram__bytes_read.sum + dram__bytes_write.sum per launch, {path.relative_to(ROOT)}")
+
+
 def kernel_model(name: str, spec, items: int, D: int, Dtot: int, r_mean: float,
                  n_full: int, n_wb: int):
     """Algorithmic (flops, compulsory HBM bytes) of ONE launch of an
@@ -612,6 +637,8 @@ def run_b200(args):
     Dtot, D = sketch_dims(spec)
     ktab = roofline_table(kprof, spec, args.steps, B * T, summ, Dtot, D)
     roof = dominant(ktab)
+    if roof is not None:
+        roof["traffic"], roof["traffic_source"] = ncu_traffic(roof["kernel"], spec, B, chunk)
     # stage split: one more pass with events between the runner's stages
     prof = []
     one_pass(spec, eta, H_chunks, streams, noise, chunk, prof=prof)

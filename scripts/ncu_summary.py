@@ -90,12 +90,14 @@ def traffic(path, out=None):
     hi = [i for i, r in enumerate(rows) if "Kernel Name" in r][0]
     h, data = rows[hi], rows[hi + 1:]
     ki, ii = h.index("Kernel Name"), h.index("ID")
+    gi = h.index("Grid Size")
     mi, vi, ui = h.index("Metric Name"), h.index("Metric Value"), h.index("Metric Unit")
     per = {}
     for r in data:
         if len(r) <= vi:
             continue
-        key = (r[ii], r[ki].split("(")[0])
+        # one template instantiation serves several products: key by grid size too
+        key = (r[ii], r[ki].split("(")[0] + " grid" + r[gi].replace(" ", ""))
         d = per.setdefault(key, {})
         v = float(r[vi].replace(",", ""))
         unit = r[ui]
