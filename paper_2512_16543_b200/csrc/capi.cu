@@ -26,6 +26,7 @@ size_t lrz_arsvd_ws_total(int64_t B, int K, int D);
 size_t lrz_precode_ws(int dtype, int64_t B, int K, int N);
 size_t lrz_wb_ws(int64_t B, int K, int D);
 size_t lrz_rng_ws(int64_t B, int64_t L);
+size_t lrz_inverse_blocked_ws(int64_t B, int K);
 
 extern "C" int lrz_version(void) { return 1; }
 
@@ -49,7 +50,9 @@ extern "C" int lrz_device_check(int device) {
 extern "C" size_t lrz_workspace_bytes(int op, int dtype, int64_t B, int K, int N, int d_max) {
   switch (op) {
     case LRZ_WS_INVERSE:
-      return size_t(B);  // per-item redo flags of the warp fast path
+      // per-item redo flags of the fast paths (+ the blocked GJ buffers, K > 64)
+      return ((size_t(B) + 255) & ~size_t(255)) +
+             ((K > 64 && K <= 256 && K % 32 == 0) ? lrz_inverse_blocked_ws(B, K) : 0);
     case LRZ_WS_ARSVD:
       return lrz_arsvd_ws_total(B, K, d_max);
     case LRZ_WS_WOODBURY:

@@ -894,6 +894,12 @@ static int set_smem(const void *fn, size_t bytes) {
   return LRZ_OK;
 }
 
+int lrz_use_dmma();
+size_t lrz_inverse_blocked_ws(int64_t B, int K);
+int lrz_inverse_blocked(int64_t B, int K, const void *A, int64_t a_stride, void *A_inv,
+                        int64_t ai_stride, int32_t *info, double limit, const uint8_t *mask,
+                        uint8_t *redo, void *ws, cudaStream_t s);
+
 extern "C" int lrz_herm_inverse(int64_t B, int K, const void *A, int64_t a_stride,
                                 void *A_inv, int64_t ai_stride, int32_t *info, double cond_limit,
                                 const uint8_t *item_mask, void *workspace, void *stream) {
@@ -918,6 +924,15 @@ extern "C" int lrz_herm_inverse(int64_t B, int K, const void *A, int64_t a_strid
       herm_inverse_warp_kernel<32><<<unsigned((B + 3) / 4), 128, 0, st>>>(
           B, K, (const c128 *)A, a_stride, (c128 *)A_inv, ai_stride, info, cond_limit,
           item_mask, redo);
+    mask = redo;
+  } else if (K > INV_SMEM_KMAX && K <= 256 && K % 32 == 0 && workspace && lrz_use_dmma()) {
+    // blocked Gauss-Jordan with the rank-32 updates on DMMA (inverse_blocked.cu);
+    // flagged items (non-PD pivots, guard bound exceeded) go to the CTA kernel
+    uint8_t *redo = (uint8_t *)workspace;
+    void *bws = (char *)workspace + ((size_t(B) + 255) & ~size_t(255));
+    if (int rc = lrz_inverse_blocked(B, K, A, a_stride, A_inv, ai_stride, info, cond_limit,
+                                     item_mask, redo, bws, st))
+      return rc;
     mask = redo;
   } else if (K > INV_SMEM_KMAX && K <= 256 && workspace) {
     // cluster path: the matrix spread over CS CTAs' shared memory

@@ -523,3 +523,70 @@ int lrz_arsvd_tail_U(int64_t B, int K, int D, const void *Jp, const void *Q, int
   a.mval = 2;
   return zgemm_dmma_launch<double, true, false, false, false, 0>(B, a, s, "arsvd_tail:U_dmma");
 }
+
+// Blocked Gauss-Jordan rank-b update (inverse_blocked.cu):
+//   next[i][k] = cur[i][k] - sum_r Cp[i][r] cur[j0 + r][k]
+int lrz_gj_update_dmma(int64_t B, int K, int b, int j0, const void *Cp, const void *Acur,
+                       int64_t cst, void *Anext, int64_t nst, const uint8_t *mask,
+                       cudaStream_t s) {
+  ZgArgs a{};
+  a.NN = K;
+  a.J = K;
+  a.Kd = b;
+  a.X = Cp;
+  a.xs = int64_t(K) * b;
+  a.ldx = b;
+  a.Y = (const c128 *)Acur + int64_t(j0) * K;
+  a.ys = cst;
+  a.ldy = K;
+  a.out = Anext;
+  a.os = nst;
+  a.ldo = K;
+  a.base = (const c128 *)Acur;
+  a.bs = cst;
+  a.mask = mask;
+  a.mstride = 1;
+  a.mval = 1;
+  return zgemm_dmma_launch<double, true, false, false, false, 1>(B, a, s, "gj_update_dmma");
+}
+
+// Blocked Gauss-Jordan panels: Cp = A[:, j] Pinv (K x b), Rp = Pinv A[j, :] (b x K)
+int lrz_gj_panels_dmma(int64_t B, int K, int b, int j0, const void *Acur, int64_t cst,
+                       const void *Pinv, void *Cp, void *Rp, const uint8_t *mask,
+                       cudaStream_t s) {
+  ZgArgs a{};
+  a.NN = K;  // Cp[i][c] = sum_r A[i][j0 + r] Pinv[r][c]
+  a.J = b;
+  a.Kd = b;
+  a.X = (const c128 *)Acur + j0;
+  a.xs = cst;
+  a.ldx = K;
+  a.Y = (const c128 *)Pinv;
+  a.ys = int64_t(b) * b;
+  a.ldy = b;
+  a.out = Cp;
+  a.os = int64_t(K) * b;
+  a.ldo = b;
+  a.mask = mask;
+  a.mstride = 1;
+  a.mval = 1;
+  if (int rc = zgemm_dmma_launch<double, true, false, false, false, 0>(B, a, s, "gj_panel_dmma"))
+    return rc;
+  ZgArgs c{};
+  c.NN = b;  // Rp[r][k] = sum_c Pinv[r][c] A[j0 + c][k]
+  c.J = K;
+  c.Kd = b;
+  c.X = Pinv;
+  c.xs = int64_t(b) * b;
+  c.ldx = b;
+  c.Y = (const c128 *)Acur + int64_t(j0) * K;
+  c.ys = cst;
+  c.ldy = K;
+  c.out = Rp;
+  c.os = int64_t(K) * b;
+  c.ldo = K;
+  c.mask = mask;
+  c.mstride = 1;
+  c.mval = 1;
+  return zgemm_dmma_launch<double, true, false, false, false, 0>(B, c, s, "gj_panel_dmma");
+}
