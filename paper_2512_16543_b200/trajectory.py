@@ -99,6 +99,14 @@ class TrajectoryResult:
 
 
 _MASKS: dict = {}   # dispatcher-step masks by (B, reset pattern, device)
+
+
+class _nullctx:
+    def __enter__(self):
+        return None
+
+    def __exit__(self, *a):
+        return False
 _PINNED: list = []  # one pinned int32[2] readback buffer (page-locking per call is slow)
 
 
@@ -241,10 +249,28 @@ class TrajectoryRunner:
         self._stage("precode_rate", e0)
         return A_inv_seq, method, info, pr, W, iters, consumed
 
+    def _tail_on(self, stream, G, Hf, noise, is_sketch, *rest):
+        """_tail on `stream` after the current stream's work so far; the
+        tensors it reads are marked as used there (allocator safety)."""
+        cur = torch.cuda.current_stream(self.device)
+        ev = torch.cuda.Event()
+        ev.record(cur)
+        stream.wait_event(ev)
+        used = [G, Hf, noise, is_sketch]
+        for x in rest:
+            if isinstance(x, torch.Tensor):
+                used.append(x)
+            elif isinstance(x, dict):
+                used.extend(v for v in x.values() if isinstance(v, torch.Tensor))
+        for t_ in used:
+            t_.record_stream(stream)
+        with torch.cuda.stream(stream):
+            return self._tail(G, Hf, noise, is_sketch, *rest)
+
     # -- one chunk -------------------------------------------------------------
     def run_chunk(self, H: torch.Tensor, noise: torch.Tensor, omega: torch.Tensor | None = None,
                   keep_A_inv: bool = False, keep_W: bool = False, hybrid: dict | None = None,
-                  omega_ready=None, sync: bool = True) -> ChunkResult:
+                  omega_ready=None, sync: bool = True, back_stream=None) -> ChunkResult:
         """H [B, T, K, N] (device, self.dtype); noise [B, K] float64 (device);
         omega [B, L] float64 (device; row b = trial b's next unconsumed normals,
         L >= T * normals_per_step_max()).
@@ -262,7 +288,16 @@ class TrajectoryRunner:
         reference's: the runner's state (t, H_prev, G_prev, A_inv, A) has
         already advanced past this chunk, so the re-run with sync=True needs a
         FRESH runner (or one restored with ``snapshot()`` / ``restore()`` taken
-        before the call) and the same sketch window."""
+        before the call) and the same sketch window.
+
+        back_stream (with sync=False): stages 4-7 (dispatcher, inversions,
+        Woodbury chain, precoder + rate) run on that stream behind an event,
+        while the current stream returns to the caller for the next chunk's
+        Grams and arSVD -- the latency-bound chain of chunk c overlaps the
+        throughput-bound products of chunk c + 1.  The next chunk's front
+        stages depend only on this chunk's front stages (last Gram, sketch
+        consumption), the chain only on the previous chain (same stream).
+        The caller joins ``back_stream`` before reading the results."""
         c = self.cfg
         B, T, K, Nn = H.shape
         assert (B, K, Nn) == (self.B, self.K, self.N) and H.dtype == self.dtype
@@ -372,8 +407,17 @@ class TrajectoryRunner:
             passes = 1
             # optimistic: the rest of the chunk is queued behind the first pass and
             # only then is the verifier's answer read back (one sync per chunk)
-            tail = self._tail(G, Hf, noise, is_sketch, iters_pred, cursor, res, k_est, plan,
-                              hybrid, keep_W)
+            if back_stream is not None and not sync:
+                # this chunk's sketch consumption, on the front stream (the next
+                # chunk's window advance must not wait for the back stages)
+                front_consumed = cursor[:, -1] + \
+                    res["consumed"].reshape(B, T)[:, -1] * is_sketch[:, -1]
+                tail = self._tail_on(back_stream, G, Hf, noise, is_sketch, iters_pred, cursor,
+                                     res, k_est, plan, hybrid, keep_W)
+                tail = tail[:-1] + (front_consumed,)
+            else:
+                tail = self._tail(G, Hf, noise, is_sketch, iters_pred, cursor, res, k_est, plan,
+                                  hybrid, keep_W)
             chunk_flags = flags
             if sync:
                 pinned = _pinned_flags()
@@ -403,19 +447,24 @@ class TrajectoryRunner:
                                       plan, hybrid, keep_W)
                 if passes > n_spec:
                     self._in_order = True   # iteration counts track the sketch: skip speculation
+        elif back_stream is not None and not sync:
+            tail = self._tail_on(back_stream, G, Hf, noise, is_sketch, None, None, None, k_est,
+                                 plan, hybrid, keep_W)
         else:
             tail = self._tail(G, Hf, noise, is_sketch, None, None, None, k_est, plan, hybrid,
                               keep_W)
         A_inv_seq, method, info, pr, W, iters, consumed = tail
         # state for the next chunk
-        self.A_inv = A_inv_seq[:, -1].clone()
         self.H_prev = H[:, -1].contiguous().clone()
         self.G_prev = G[:, -1].contiguous().clone()
         self.t += T
-        # status per step: the inverse's code (singular / indefinite) wins over the
-        # precoder's (zero norm), so a singular step is never hidden by a later code
-        pinfo = pr["info"].reshape(B, T)
-        info = torch.where(info != 0, info, pinfo)
+        bs = back_stream if (back_stream is not None and not sync) else None
+        with torch.cuda.stream(bs) if bs is not None else _nullctx():
+            self.A_inv = A_inv_seq[:, -1].clone()
+            # status per step: the inverse's code (singular / indefinite) wins over the
+            # precoder's (zero norm), so a singular step is never hidden by a later code
+            pinfo = pr["info"].reshape(B, T)
+            info = torch.where(info != 0, info, pinfo)
         return ChunkResult(rates=pr["sum"].reshape(B, T), per_ut=pr["rates"].reshape(B, T, K),
                            method=method, k_est=k_est, iters=iters, info=info,
                            A_inv=A_inv_seq if keep_A_inv else None,
