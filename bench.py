@@ -636,6 +636,9 @@ def run_b200(args):
     # pass settles every chunk -- checked on a warm-up pass (verifier flags zero
     # and the same results as the synchronous pass)
     ref_sync = one_pass(spec, eta, H_chunks, streams, noise, chunk)
+    torch.cuda.synchronize(dev)
+    ops._WS.clear()
+    torch.cuda.empty_cache()
     pipe_flags.zero_()
     trial_pipe = one_pass(spec, eta, H_chunks, streams, noise, chunk, pipelined=True)
     torch.cuda.synchronize(dev)
@@ -768,7 +771,7 @@ def run_b200(args):
         runs = [
             ("C1_c128", "C1", {}, [spec_eta_default, None], 2),
             ("C2_c128", "C2", {}, [spec_eta_default, None], 3),
-            ("C2_c128_eta0.9", "C2", {}, [0.9], 3),
+            ("C2_c128_eta0.9", "C2", {}, [0.9], 3),      # chunk 50: cross-chunk pipelining
             ("C2_c64", "C2", {"dtype": "c64"}, [spec_eta_default, None], 3),
             ("C3_c64", "C3", {}, [spec_eta_default, None], 1),
             ("C5_c64", "C5", {"dtype": "c64"}, [spec_eta_default, None], 1),
@@ -781,11 +784,12 @@ def run_b200(args):
                              1))
         for lab, name, ov, etas, reps in runs:
             sp = S.CONFIGS[name].with_(**ov)
+            ch_over = 50 if lab == "C2_c128_eta0.9" else None   # walk(c+1) overlaps chain(c)
             if args.quick:
                 sp = sp.with_(T=min(sp.T, 2 * CHUNK[name]))
             configs[lab] = run_config(sp, etas, reps, rank, world, dev, one_pass, summarize,
                                       roofline_table, dominant, sketch_dims, timed, ops, S,
-                                      DeviceOmegaStreams, torch)
+                                      DeviceOmegaStreams, torch, pipe_flags, ch_over)
             ops._WS.clear()          # grow-only scratch of this config's shapes
             torch.cuda.empty_cache()
         if rank == 0 and world == 1 and not args.no_cpu:
@@ -850,15 +854,16 @@ spec_eta_default = "default"
 
 
 def run_config(sp, etas, reps, rank, world, dev, one_pass, summarize, roofline_table, dominant,
-               sketch_dims, timed, ops, S, DeviceOmegaStreams, torch):
+               sketch_dims, timed, ops, S, DeviceOmegaStreams, torch, pipe_flags, chunk=None):
     """One BASELINE config: full trial count and T, channels synthesised on the
     device per T-chunk (C4's 215 GB pass is streamed); each method timed over
     `reps` passes after one warm-up pass.  `updates_per_s` counts the runner
-    (CUDA events around every run_chunk), `updates_per_s_with_channels` the
-    whole pass including the channel synthesis."""
+    (CUDA events around every run_chunk; pipelined passes: the pass minus the
+    channel-synthesis kernels), `updates_per_s_with_channels` the whole pass
+    including the channel synthesis.""" 
     B, T = sp.B, sp.T
     trials = list(range(rank * B, (rank + 1) * B))
-    ch = min(T, CHUNK.get(sp.name, T))
+    ch = min(T, chunk or CHUNK.get(sp.name, T))
     chans = S.DeviceChannels(sp, trials, dev)
     noise = torch.full((B, sp.K), sp.noise_var, dtype=torch.float64, device=dev)
     stream = torch.cuda.current_stream(dev)
@@ -873,7 +878,23 @@ def run_config(sp, etas, reps, rank, world, dev, one_pass, summarize, roofline_t
             ev.record(stream)
             evs.append(ev)
 
-        run = lambda: one_pass(sp, e, chans.generate, streams, noise, ch, on_chunk=mark)  # noqa
+        # cross-chunk pipelining when a warm-up pass shows it reproduces the
+        # synchronous pass (verifier flags zero, same decisions and rates)
+        ref = one_pass(sp, e, chans.generate, streams, noise, ch)
+        torch.cuda.synchronize(dev)
+        ops._WS.clear()            # the synchronous pass's scratch (front stream)
+        torch.cuda.empty_cache()
+        pipe_flags.zero_()
+        tri = one_pass(sp, e, chans.generate, streams, noise, ch, pipelined=True)
+        torch.cuda.synchronize(dev)
+        pipelined = int(pipe_flags.abs().sum().item()) == 0 and all(
+            torch.equal(a.method, b_.method) and torch.equal(a.k_est, b_.k_est) and
+            torch.equal(a.rates, b_.rates) for a, b_ in zip(ref, tri))
+        del ref, tri
+        if pipelined:
+            torch.cuda.synchronize(dev)
+        run = lambda: one_pass(sp, e, chans.generate, streams, noise, ch,  # noqa: E731
+                               on_chunk=None if pipelined else mark, pipelined=pipelined)
         run()
         torch.cuda.synchronize(dev)
         evs.clear()
@@ -881,7 +902,12 @@ def run_config(sp, etas, reps, rank, world, dev, one_pass, summarize, roofline_t
         ms, outs = timed(run, reps)
         kprof = ops.prof_collect(dev)
         ops.prof_enable(False, dev)
-        runner_ms = sum(evs[i].elapsed_time(evs[i + 1]) for i in range(0, len(evs), 2)) / reps
+        if pipelined:
+            # the pass minus the on-device channel synthesis inside it
+            runner_ms = ms - kprof.get("channel_kernel", (0.0, 0))[0] / reps
+        else:
+            runner_ms = sum(evs[i].elapsed_time(evs[i + 1])
+                            for i in range(0, len(evs), 2)) / reps
         summ = summarize(outs)
         Dtot, D = sketch_dims(sp)
         ktab = roofline_table(kprof, sp, reps, B * T, summ, Dtot, D)
@@ -889,7 +915,7 @@ def run_config(sp, etas, reps, rank, world, dev, one_pass, summarize, roofline_t
         out[key] = {
             "updates_per_s": world * B * T / (runner_ms / 1e3),
             "updates_per_s_with_channels": world * B * T / (ms / 1e3),
-            "ms_per_pass": runner_ms, "roofline": dominant(ktab),
+            "ms_per_pass": runner_ms, "pipelined": pipelined, "roofline": dominant(ktab),
             "kernels_top": dict(list(ktab.items())[:6]),
             **{k: v for k, v in summ.items() if not k.startswith("_")}}
         out["workload"] = workload_desc(sp, e if e is not None else sp.eta)

@@ -1098,7 +1098,7 @@ size_t lrz_precode_ws(int dtype, int64_t B, int K, int N) {
   bytes = (bytes + 255) & ~size_t(255);
   bytes += size_t(B) * tiles * sizeof(double);
   bytes = (bytes + 255) & ~size_t(255);
-  bytes += size_t(B) * N * K * es;
+  bytes += size_t(B) * N * K * (dtype == LRZ_C64 ? 8 : 16);  // W (input precision)
   bytes = (bytes + 1023) & ~size_t(1023);
   if (dtype == LRZ_C64 && K > 32 && K <= 256)  // tcgen05 precoder: pre-split A^-1 operand
     bytes += lrz_tc_w_ws(std::min<int64_t>(B, tc_group(K)), K);
@@ -1128,7 +1128,8 @@ extern "C" int lrz_precode_rate(int dtype, int64_t B, int K, int N, const void *
     W = ws + off;
     w_stride = int64_t(N) * K;
   }
-  void *tc_ws = ws + ((off_w + size_t(B) * N * K * 16 + 1023) & ~size_t(1023));
+  void *tc_ws = ws + ((off_w + size_t(B) * N * K * (dtype == LRZ_C64 ? 8 : 16) + 1023) &
+                      ~size_t(1023));
   cudaStream_t s = (cudaStream_t)stream;
   const dim3 g1(unsigned(B * tm * tn)), g2(unsigned(B * tn * tn));
   if (G_true) {

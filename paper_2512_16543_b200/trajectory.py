@@ -364,7 +364,7 @@ class TrajectoryRunner:
             n_spec = 0 if self._in_order else c.spec_passes
             # cursor walk (K <= 32): resolves every step's cursor from the energy
             # screen alone, in order, so one more speculative pass settles the chunk
-            can_walk = sync and n_spec > 0 and ops.walk_ok(K, c.k_init, c.p, c.i_max)
+            can_walk = n_spec > 0 and ops.walk_ok(K, c.k_init, c.p, c.i_max)
 
             def walk():
                 e0 = self._ev()
