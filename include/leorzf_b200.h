@@ -320,6 +320,14 @@ int lrz_trajectory(int dtype, int64_t B, int T, int K, int N, const void *H, dou
                    int32_t *info, int64_t *consumed, void *A_inv_seq, void *workspace,
                    void *stream);
 
+/* Campaign summary on the device (harness.py:336-367) for M methods (method 0
+ * = the conventional baseline): rates [M][B][T] (per-step sum-rates), stats
+ * [M][B][6] (lrz_campaign_reduce) -> trial_mean [M][B], summary [M][6] =
+ * (pooled mean rate, mean cost units per trial, mean rank, n_full,
+ * n_woodbury, n_none), table [M][2] = (savings %, degradation %). */
+int lrz_campaign_summary(int M, int64_t B, int T, const double *rates, const double *stats,
+                         double *trial_mean, double *summary, double *table, void *stream);
+
 /* Workspace sizing for the calls that take one. */
 #define LRZ_WS_INVERSE 0
 #define LRZ_WS_ARSVD 1

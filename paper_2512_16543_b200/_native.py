@@ -79,6 +79,7 @@ _SIGS = {
     "lrz_campaign_reduce": (C.c_int, [I64, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, P, P,
                                       P, P]),
     "lrz_workspace_bytes": (SZ, [C.c_int, C.c_int, I64, C.c_int, C.c_int, C.c_int]),
+    "lrz_campaign_summary": (C.c_int, [C.c_int, I64, C.c_int, P, P, P, P, P, P]),
     "lrz_update_inverse_ws": (SZ, [C.c_int, I64, C.c_int, C.c_int, C.c_int]),
     "lrz_update_inverse": (C.c_int, [C.c_int, I64, C.c_int, C.c_int, P, P, F64, P, P, P, I64, P,
                                      C.POINTER(ArsvdCfg), P, P, P, P, P, P, P, P, P]),

@@ -394,9 +394,76 @@ __global__ void campaign_reduce_kernel(int64_t B, int T, int t_base, int K, int 
   }
 }
 
+// Campaign summary on the device (harness.py:336-367): per method m of M
+// (rates [M][B][T], stats [M][B][6] from campaign_reduce): per-trial mean
+// rates, the pooled mean rate, mean cost units per trial, the pooled mean
+// rank (k_sum / k_count) and the decision counts; fixed summation orders.
+// summary[m] = (mean_rate, mean_cost, mean_k, n_full, n_woodbury, n_none).
+__global__ void campaign_summary_kernel(int64_t B, int T, const double *__restrict__ rates,
+                                        const double *__restrict__ stats,
+                                        double *__restrict__ trial_mean,
+                                        double *__restrict__ summary) {
+  __shared__ double red[8];
+  const int m = blockIdx.x;
+  const double *r = rates + int64_t(m) * B * T;
+  double tot = 0.0;
+  for (int64_t b = 0; b < B; ++b) {
+    double loc = 0.0;
+    for (int t = threadIdx.x; t < T; t += blockDim.x) loc += r[b * T + t];
+    const double sb = block_sum(loc, red);
+    if (threadIdx.x == 0) trial_mean[int64_t(m) * B + b] = sb / T;
+    tot += sb;
+  }
+  if (threadIdx.x == 0) {
+    const double *st = stats + int64_t(m) * B * 6;
+    double cost = 0, ks = 0, kc = 0, nf = 0, nw = 0, nn = 0;
+    for (int64_t b = 0; b < B; ++b) {
+      cost += st[b * 6 + 0];
+      ks += st[b * 6 + 1];
+      kc += st[b * 6 + 2];
+      nf += st[b * 6 + 3];
+      nw += st[b * 6 + 4];
+      nn += st[b * 6 + 5];
+    }
+    double *o = summary + m * 6;
+    o[0] = tot / (double(B) * T);
+    o[1] = cost / double(B);
+    o[2] = kc > 0 ? ks / kc : 0.0;
+    o[3] = nf;
+    o[4] = nw;
+    o[5] = nn;
+  }
+}
+
+// the comparison table (harness.py:357-367): method 0 is the conventional
+// baseline; row m = (savings %, degradation %) = 100 (1 - cost_m / cost_0),
+// 100 (1 - rate_m / rate_0)
+__global__ void campaign_table_kernel(int M, const double *__restrict__ summary,
+                                      double *__restrict__ table) {
+  const int m = threadIdx.x;
+  if (m >= M) return;
+  const double c0 = summary[1], r0 = summary[0];
+  table[m * 2 + 0] = m == 0 ? 0.0 : 100.0 * (1.0 - summary[m * 6 + 1] / c0);
+  table[m * 2 + 1] = m == 0 ? 0.0 : 100.0 * (1.0 - summary[m * 6 + 0] / r0);
+}
+
 }  // namespace lrz
 
 using namespace lrz;
+
+extern "C" int lrz_campaign_summary(int M, int64_t B, int T, const double *rates,
+                                    const double *stats, double *trial_mean, double *summary,
+                                    double *table, void *stream) {
+  if (M < 1 || M > 1024 || B < 1 || T < 1 || !rates || !stats || !trial_mean || !summary ||
+      !table) {
+    lrz_set_error("lrz_campaign_summary: bad arguments");
+    return LRZ_EINVAL;
+  }
+  cudaStream_t s = (cudaStream_t)stream;
+  campaign_summary_kernel<<<unsigned(M), 256, 0, s>>>(B, T, rates, stats, trial_mean, summary);
+  campaign_table_kernel<<<1, 1024, 0, s>>>(M, summary, table);
+  return lrz_launch_status("lrz_campaign_summary");
+}
 
 static size_t leo_smem(int nx, int ny) {
   const int N = nx * ny;

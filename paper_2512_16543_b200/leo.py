@@ -206,9 +206,20 @@ def stream_seed(master_seed: int, label: str, trial_index: int) -> np.random.See
         [int(master_seed), zlib.crc32(label.encode("utf-8")), int(trial_index)])
 
 
-def ecdf(samples) -> np.ndarray:
+def ecdf(samples):
     """(value, cumulative probability) steps, duplicates collapsed onto their
-    last step (harness.py:95-104)."""
+    last step (harness.py:95-104).  A CUDA tensor is reduced on the device
+    (sort, run-length of equal values, cumulative counts) and returned as a
+    device tensor; array input keeps the host form."""
+    if isinstance(samples, torch.Tensor) and samples.is_cuda:
+        x = samples.reshape(-1).to(torch.float64)
+        if x.numel() == 0:
+            raise EmptyInputError("ecdf needs at least one sample")
+        xs, _ = torch.sort(x)
+        vals, cnt = torch.unique_consecutive(xs, return_counts=True)
+        # elementwise IEEE division (a scalar divisor may become a reciprocal multiply)
+        n = torch.full_like(vals, float(xs.numel()))
+        return torch.stack([vals, torch.cumsum(cnt, 0).to(torch.float64) / n], 1)
     x = np.asarray(samples, dtype=float).ravel()
     if x.size == 0:
         raise EmptyInputError("ecdf needs at least one sample")
@@ -422,11 +433,9 @@ def _simulate(cfg, specs, trials, seed, device, chunk, sketch_labels=None, keep_
         if keep_cols:
             cols.append(snap["cols"].cpu())
     out = {}
-    for gr in groups:
-        full = dict(rates=torch.cat(gr["rates"], 1).cpu().numpy(),
-                    method=torch.cat(gr["method"], 1).cpu().numpy(),
-                    k_est=torch.cat(gr["k_est"], 1).cpu().numpy(),
-                    stats=gr["stats"].cpu().numpy())
+    for gr in groups:   # device tensors; the callers reduce on the device
+        full = dict(rates=torch.cat(gr["rates"], 1), method=torch.cat(gr["method"], 1),
+                    k_est=torch.cat(gr["k_est"], 1), stats=gr["stats"])
         for i, lab in enumerate(gr["labels"]):
             out[lab] = {k: v[i * B:(i + 1) * B] for k, v in full.items()}
     if keep_cols:
@@ -471,36 +480,39 @@ def run_campaign(cfg, master_seed: int | None = None, workers: int = 1,
     trials = shard_trials(cfg.mc_runs, rank, world)
     if device is None and torch.cuda.is_available():
         device = torch.device("cuda", torch.cuda.current_device())
-    res = _simulate(cfg, specs, trials, seed, device, chunk)
+    dev = torch.device(device) if device is not None else torch.device("cuda", 0)
+    res = _simulate(cfg, specs, trials, seed, dev, chunk)
     if world > 1:
         local = {}
         for i, lab in enumerate(labels):
             for k in ("rates", "method", "k_est", "stats"):
-                local[f"{i}_{k}"] = res[lab][k]
-        merged = gather_results(local, trials, cfg.mc_runs,
-                                device=torch.device(device) if device is not None else None)
-        res = {lab: {k: merged[f"{i}_{k}"] for k in ("rates", "method", "k_est", "stats")}
+                local[f"{i}_{k}"] = res[lab][k].cpu().numpy()
+        merged = gather_results(local, trials, cfg.mc_runs, device=dev)
+        res = {lab: {k: torch.from_numpy(np.ascontiguousarray(merged[f"{i}_{k}"])).to(dev)
+                     for k in ("rates", "method", "k_est", "stats")}
                for i, lab in enumerate(labels)}
+    # pooled means, per-trial means, mean cost / rank, counts and the comparison
+    # table on the device (lrz_campaign_summary); only scalars come back
+    rates_d = torch.stack([res[lab]["rates"] for lab in labels]).contiguous()
+    stats_d = torch.stack([res[lab]["stats"] for lab in labels]).contiguous()
+    tm_d, sm_d, tb_d = ops.campaign_summary(rates_d, stats_d)
+    tm, sm, tb = tm_d.cpu().numpy(), sm_d.cpu().numpy(), tb_d.cpu().numpy()
     pooled, tmeans, mrate, mcost, mk, counts, decisions, per_step = {}, {}, {}, {}, {}, {}, {}, {}
-    for lab in labels:
-        r = res[lab]
-        pooled[lab] = r["rates"].reshape(-1)
-        tmeans[lab] = np.array([row.mean() for row in r["rates"]])
-        mrate[lab] = float(pooled[lab].mean())
-        st = r["stats"]
-        mcost[lab] = float(st[:, 0].mean())
-        kc = float(st[:, 2].sum())
-        mk[lab] = float(st[:, 1].sum()) / kc if kc else 0.0
-        counts[lab] = {name: int(st[:, 3 + j].sum()) for j, name in enumerate(_METHOD_NAMES)}
+    for i, lab in enumerate(labels):
+        r = {k: v.cpu().numpy() for k, v in res[lab].items()}
+        pooled[lab] = r["rates"].reshape(-1)          # the API returns the pooled samples
+        tmeans[lab] = tm[i]
+        mrate[lab] = float(sm[i, 0])
+        mcost[lab] = float(sm[i, 1])
+        mk[lab] = float(sm[i, 2])
+        counts[lab] = {name: int(sm[i, 3 + j]) for j, name in enumerate(_METHOD_NAMES)}
         if collect_decisions:
             decisions[lab] = [row.astype(np.uint8) for row in r["method"]]
         per_step[lab] = r
     conv = method_label(None)
     rows = [ComparisonRow(conv, None, 0.0, 0.0)]
-    for eta in etas:
-        lab = method_label(eta)
-        rows.append(ComparisonRow(lab, eta, 100.0 * (1.0 - mcost[lab] / mcost[conv]),
-                                  100.0 * (1.0 - mrate[lab] / mrate[conv])))
+    for i, eta in enumerate(etas, start=1):
+        rows.append(ComparisonRow(method_label(eta), eta, float(tb[i, 0]), float(tb[i, 1])))
     return CampaignResult(labels=labels, etas={method_label(e): e for e in etas} | {conv: None},
                           table=ComparisonTable(rows), pooled_rates=pooled,
                           trial_mean_rates=tmeans, mean_rate=mrate, mean_cost=mcost,
@@ -516,6 +528,7 @@ def run_trial(cfg, eta: float | None, trial_index: int, master_seed: int | None 
     label = method_label(eta)
     sl = {label: sketch_stream} if sketch_stream else None
     r = _simulate(cfg, [(label, eta)], [trial_index], seed, device, None, sketch_labels=sl)[label]
+    r = {k: v.cpu().numpy() for k, v in r.items()}
     T, K = cfg.n_snapshots, cfg.K
     tg = np.arange(T)
     sk = (tg > 0) & ~((cfg.n_reset > 0) & (tg % max(cfg.n_reset, 1) == 0)) if eta is not None \

@@ -595,3 +595,21 @@ def trajectory_chunk(H: torch.Tensor, alpha: float, P_t: float, noise: torch.Ten
                                N.stream_ptr(dev)), "lrz_trajectory")
     _count(10)
     return out
+
+
+def campaign_summary(rates: torch.Tensor, stats: torch.Tensor):
+    """lrz_campaign_summary: rates [M,B,T] f64, stats [M,B,6] f64 (device) ->
+    (trial_mean [M,B], summary [M,6], table [M,2]) on the device."""
+    _chk(rates, "rates")
+    _chk(stats, "stats")
+    M, B, T = rates.shape
+    dev = rates.device
+    tm = torch.empty(M, B, dtype=torch.float64, device=dev)
+    sm = torch.empty(M, 6, dtype=torch.float64, device=dev)
+    tb = torch.empty(M, 2, dtype=torch.float64, device=dev)
+    lib = N.lib_for(dev)
+    N.check(lib.lrz_campaign_summary(M, B, T, rates.data_ptr(), stats.data_ptr(), tm.data_ptr(),
+                                     sm.data_ptr(), tb.data_ptr(), N.stream_ptr(dev)),
+            "lrz_campaign_summary")
+    _count(2)
+    return tm, sm, tb

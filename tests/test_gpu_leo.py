@@ -101,7 +101,7 @@ def test_full_default_pass_matches_reference(cuda):
     out = L._simulate(cfg, specs, [0], cfg.seed, cuda, 400, keep_cols=True)
     assert np.array_equal(out["_cols"][0], g["cols"])
     for i, (lab, _) in enumerate(specs):
-        r = out[lab]
+        r = {k: v.cpu().numpy() for k, v in out[lab].items()}
         assert np.array_equal(r["method"][0], g[f"trial_method_{i}"]), lab
         assert np.array_equal(r["k_est"][0], g[f"trial_k_{i}"]), lab
         np.testing.assert_allclose(r["rates"][0], g[f"trial_rates_{i}"], rtol=RTOL_RATE)
@@ -164,3 +164,36 @@ def test_campaign_reduce_matches_step_costs(cuda):
     np.testing.assert_array_equal(st[:, 2], np.full(B, (~reset).sum()))
     for j in range(3):
         np.testing.assert_array_equal(st[:, 3 + j], (method == j).sum(1))
+
+
+def test_campaign_summary_and_ecdf_on_device(cuda):
+    """f4: the pooled means, per-trial means, counts, mean rank / cost and the
+    comparison table come from lrz_campaign_summary on the device; the ECDF of
+    a CUDA tensor is built on the device (harness.py:95-104, 336-367) -- both
+    equal the host computations on the same per-step results."""
+    import torch
+    from paper_2512_16543_b200 import ops
+    cfg = L.ScenarioConfig(K=4, n_x=4, n_y=4, N_RF=6, pass_s=3.0, update_rate_Hz=10.0,
+                           mc_runs=3, eta_list=(0.9, 0.65), n_reset=12).validate()
+    res = L.run_campaign(cfg, collect_decisions=True, device=cuda)
+    for lab in res.labels:
+        r = res.per_step[lab]
+        np.testing.assert_allclose(res.mean_rate[lab], r["rates"].mean(), rtol=1e-12)
+        np.testing.assert_allclose(res.trial_mean_rates[lab], r["rates"].mean(axis=1),
+                                   rtol=1e-12)
+        st = r["stats"]
+        assert res.mean_cost[lab] == pytest.approx(st[:, 0].mean(), rel=1e-14)
+        kc = st[:, 2].sum()
+        assert res.mean_k_est[lab] == pytest.approx(st[:, 1].sum() / kc if kc else 0.0,
+                                                    rel=1e-14)
+        assert sum(res.method_counts[lab].values()) == r["rates"].size
+        e_dev = L.ecdf(torch.from_numpy(res.pooled_rates[lab]).to(cuda)).cpu().numpy()
+        e_host = L.ecdf(res.pooled_rates[lab])
+        assert np.array_equal(e_dev, e_host)
+    conv = res.labels[0]
+    for row in res.table.rows[1:]:
+        lab = row.method_label
+        assert row.savings_pct == pytest.approx(
+            100.0 * (1.0 - res.mean_cost[lab] / res.mean_cost[conv]), rel=1e-12)
+        assert row.degradation_pct == pytest.approx(
+            100.0 * (1.0 - res.mean_rate[lab] / res.mean_rate[conv]), rel=1e-9, abs=1e-12)
