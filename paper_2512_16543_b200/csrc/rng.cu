@@ -24,6 +24,7 @@
 
 #include "common.cuh"
 #include "_gen/ziggurat_tables.h"
+#include "glibc_log1p.h"
 
 namespace lrz {
 
@@ -83,8 +84,8 @@ LRZ_DEV double zig_from(uint64_t r, u128 st, u128 inc, const ZigTables &t, int &
     if (rabs < t.ki[idx]) return x;
     if (idx == 0) {
       for (;;) {
-        const double xx = -0.27366123732975828 * log1p(-pcg_double(st, inc));
-        const double yy = -log1p(-pcg_double(st, inc));
+        const double xx = __dmul_rn(-0.27366123732975828, glibc_log1p(-pcg_double(st, inc)));
+        const double yy = -glibc_log1p(-pcg_double(st, inc));
         used += 2;
         if (yy + yy > xx * xx)
           return ((rabs >> 8) & 1) ? -(3.6541528853610088 + xx) : 3.6541528853610088 + xx;
@@ -93,7 +94,11 @@ LRZ_DEV double zig_from(uint64_t r, u128 st, u128 inc, const ZigTables &t, int &
     } else {
       const double u = pcg_double(st, inc);
       ++used;
-      if ((t.fi[idx - 1] - t.fi[idx]) * u + t.fi[idx] < exp(-0.5 * x * x)) return x;
+      // numpy's baseline build does not contract this (no FMA): unfused here too.
+      // exp: CUDA's and glibc's agree to 1 ulp, so the decision can differ only
+      // if the left side falls between the two (p ~ 2^-52 per wedge test)
+      const double lhs = __dadd_rn(__dmul_rn(__dsub_rn(t.fi[idx - 1], t.fi[idx]), u), t.fi[idx]);
+      if (lhs < exp(__dmul_rn(__dmul_rn(-0.5, x), x))) return x;
     }
     if (used > RNG_MAXC) return 0.0;
     r = pcg_next(st, inc);

@@ -184,3 +184,45 @@ def test_exceptions_subclass_the_reference_classes_when_installed():
     out = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True,
                          timeout=120)
     assert out.returncode == 0 and out.stdout.strip() == "ok", out.stderr
+
+
+def test_device_log1p_restatement_matches_libm(tmp_path):
+    """csrc/glibc_log1p.h (the device RNG's ziggurat-tail log1p) compiled for the
+    host with gcc equals the libm log1p numpy's Generator calls, bit for bit, on
+    the arguments the tail sees (-u, u in [0, 1)) and on every branch's range."""
+    import ctypes
+    import shutil
+    import subprocess
+    gcc = shutil.which("gcc")
+    if gcc is None:
+        pytest.skip("gcc not available")
+    src = tmp_path / "l1p.c"
+    src.write_text('#include "glibc_log1p.h"\n'
+                   'void l1p(const double *x, double *y, long n)'
+                   '{ for (long i = 0; i < n; ++i) y[i] = glibc_log1p(x[i]); }\n')
+    so = tmp_path / "l1p.so"
+    subprocess.run([gcc, "-O2", "-ffp-contract=off", "-shared", "-fPIC", "-I",
+                    str(ROOT / "paper_2512_16543_b200" / "csrc"), str(src), "-o", str(so), "-lm"],
+                   check=True)
+    twin = ctypes.CDLL(str(so))
+    libm = ctypes.CDLL("libm.so.6")
+    libm.log1p.restype = ctypes.c_double
+    libm.log1p.argtypes = [ctypes.c_double]
+    rng = np.random.default_rng(7)
+    n = 400_000
+    u = np.concatenate([
+        rng.random(n),                                        # the tail's arguments
+        rng.random(n) * 1e-6,                                 # k = 0, tiny |x|
+        1.0 - rng.random(n) * 1e-3,                           # x -> -1
+        np.ldexp(rng.random(n), -rng.integers(0, 60, n)),     # every exponent
+        (1.0 + np.ldexp(rng.integers(0, 1 << 20, n).astype(np.float64), -52)) - 1.0,
+        np.array([0.0, 2.0 ** -54, 2.0 ** -29, 0.2929, 0.5, 1.0 - 2.0 ** -53]),
+    ])
+    x = np.ascontiguousarray(-u)
+    y = np.empty_like(x)
+    twin.l1p(x.ctypes.data_as(ctypes.c_void_p), y.ctypes.data_as(ctypes.c_void_p),
+             ctypes.c_long(x.size))
+    # libm through ctypes, call by call (numpy's np.log1p ufunc may be a SIMD
+    # variant, not the libm routine the Generator calls)
+    want = np.array([libm.log1p(v) for v in x.tolist()])
+    assert np.array_equal(y.view(np.uint64), want.view(np.uint64))
