@@ -101,7 +101,12 @@ int lrz_herm_inverse(int64_t B, int K, const void *A, int64_t a_stride, void *A_
  *   dispatcher's Woodbury candidates) -- the batched runner's mode, which
  *   lets iterations that cannot reach the energy target skip the SVD.
  *   hermitian 1 promises dA == dA^H exactly (Gram corrections are): with
- *   want_factor 0 and K <= 32 a warp-per-item front end runs first. */
+ *   want_factor 0 and K <= 32 a warp-per-item front end runs first.
+ *   want_factor 2 (hermitian, d_max <= 40): cursor-resolution mode -- only
+ *   the screening front end runs and writes iters / consumed from the
+ *   screened energies (estimates inside the CholeskyQR error band; no
+ *   factors, k_est untouched).  The batched runner alternates it with
+ *   lrz_spec_verify to settle the sketch cursors before the exact pass. */
 typedef struct {
   double eta;
   int k_init, p, i_max;
@@ -375,6 +380,20 @@ int lrz_spec_verify(int64_t B, int T, int K, const lrz_arsvd_cfg *cfg,
                     const int32_t *iters_act, int64_t *cursor, const int64_t *cursor0,
                     int32_t *first_unverified, uint8_t *active, int32_t *pending,
                     void *stream);
+
+/* The same with a per-step tally of the iteration counts observed so far
+ * (votes: uint8 [B][T][LRZ_SPEC_VOTE_W], nullable = lrz_spec_verify): the
+ * suffix behind the first mismatch is re-predicted by majority instead of by
+ * the last observation.  Counts that hinge on the sketch drawn (not on the
+ * step's spectrum) are then not carried over from a pass at shifted cursors.
+ * iters_act == NULL also clears the tally (the prediction counts as one vote).
+ * Used by the runner's screen-only rounds (lrz_arsvd want_factor 2). */
+#define LRZ_SPEC_VOTE_W 16
+int lrz_spec_verify_vote(int64_t B, int T, int K, const lrz_arsvd_cfg *cfg,
+                         const uint8_t *is_sketch, int32_t *iters_pred,
+                         const int32_t *iters_act, int64_t *cursor, const int64_t *cursor0,
+                         int32_t *first_unverified, uint8_t *active, int32_t *pending,
+                         uint8_t *votes, void *stream);
 
 #ifdef __cplusplus
 }

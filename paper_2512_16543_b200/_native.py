@@ -89,6 +89,8 @@ _SIGS = {
                                  P, P, P, P, P]),
     "lrz_spec_verify": (C.c_int, [I64, C.c_int, C.c_int, C.POINTER(ArsvdCfg), P, P, P, P, P, P,
                                   P, P, P]),
+    "lrz_spec_verify_vote": (C.c_int, [I64, C.c_int, C.c_int, C.POINTER(ArsvdCfg), P, P, P, P, P,
+                                       P, P, P, P, P]),
 }
 
 _lib = None

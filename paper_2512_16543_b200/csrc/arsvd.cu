@@ -60,6 +60,7 @@ struct ArsvdArgs {
   // GEMM; phase 2 takes M and finishes (SVD, rank, V); U = Q J_perm is a second
   // GEMM.  tail[item]: 1 = in the pipeline, 2 = U wanted from the GEMM.
   int phase;
+  int smem_ws;  // 1: per-item Q / M / J live in dynamic shared memory (no tail pipeline)
   uint8_t *tail;
   c128 *U, *V;
   double *S;
@@ -75,9 +76,11 @@ LRZ_DEV void rr_pair(int rnd, int pi, int dp, int &a, int &b) {
   if (pi == 0) {
     a = rnd;
     b = n1;
-  } else {
-    a = (rnd + pi) % n1;
-    b = (rnd - pi + n1) % n1;
+  } else {  // rnd < n1, 0 < pi <= n1 / 2: one conditional wrap instead of a modulo
+    a = rnd + pi;
+    if (a >= n1) a -= n1;
+    b = rnd - pi;
+    if (b < 0) b += n1;
   }
   if (a > b) {
     const int t = a;
@@ -132,13 +135,16 @@ LRZ_DEV void jacobi_sv(c128 *M, c128 *J, int K, int d, double *sval, int *perm, 
         gr = grp_sum(gr);
         gi = grp_sum(gi);
         if (!act) continue;
-        const double gabs = hypot(gr, gi);
-        if (!(gabs > JACOBI_TOL * sqrt(al) * sqrt(be)) || gabs == 0.0) continue;
-        // one divide for the three quotients by |g|, rsqrt for the cosine
-        const double ig = 1.0 / gabs;
+        // |g|^2 against (tol ||a|| ||b||)^2: no square roots on the skip path; 1 / |g|
+        // by rsqrt, the tangent's quotient by a reciprocal (the rotation only has to
+        // be unitary to rounding, which c and s from one rsqrt are)
+        const double g2 = fma(gr, gr, gi * gi);
+        if (!(g2 > (JACOBI_TOL * JACOBI_TOL) * al * be) || !(g2 > 0.0)) continue;
+        const double ig = rsqrt(g2);
         const double zeta = (be - al) * (0.5 * ig);
-        const double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
-        const double c = rsqrt(1.0 + t * t), s = c * t;
+        const double z1 = fma(zeta, zeta, 1.0);
+        const double t = copysign(__drcp_rn(fabs(zeta) + z1 * rsqrt(z1)), zeta);
+        const double c = rsqrt(fma(t, t, 1.0)), s = c * t;
         const c128 ph = mk<double>(gr * ig, -gi * ig);  // e^{-i phi}
         c128 *wa = M + int64_t(a) * K, *wb = M + int64_t(b) * K;
         for (int k = gl; k < K; k += JG) {
@@ -349,7 +355,11 @@ LRZ_DEV int64_t arsvd_item(const ArsvdArgs &g, const int64_t item, int64_t cur, 
   const int64_t orw = g.orow ? int64_t(g.orow[item]) : item / g.orow_div;
   const double *om = g.omega + orw * g.os;
   const int64_t cur0 = cur;
-  c128 *Q = g.ws + item * (int64_t(2) * D * K + int64_t(D) * D);  // [D][K]
+  // small problems keep Q / M / J in shared memory (g.smem_ws: the launch reserved
+  // (2 D K + D^2) complex of dynamic shared memory), the rest in the global workspace
+  extern __shared__ __align__(16) char arsvd_dyn_smem[];
+  c128 *Q = g.smem_ws ? (c128 *)arsvd_dyn_smem
+                      : g.ws + item * (int64_t(2) * D * K + int64_t(D) * D);  // [D][K]
   c128 *M = Q + int64_t(D) * K;                                    // [D][K]
   c128 *J = M + int64_t(D) * K;                                    // [D][D] col-major
   c128 *U = g.U + item * int64_t(D) * K;
@@ -656,6 +666,19 @@ __global__ void __launch_bounds__(ARSVD_THREADS) arsvd_kernel(ArsvdArgs g) {
   arsvd_item(g, item, g.cursor ? g.cursor[item] : 0, it0);
 }
 
+// The same item code for small problems (K <= 32): 128 threads per item and a
+// register budget that keeps ARSVD_SMALL_CTAS items resident per SM -- the item is
+// latency bound (one barrier and one scalar chain per reflector / Jacobi round),
+// so throughput comes from the number of items in flight.
+template <int CTAS>
+__global__ void __launch_bounds__(128, CTAS) arsvd_small_kernel(ArsvdArgs g) {
+  const int64_t item = blockIdx.x;
+  if (g.mask && !g.mask[item]) return;
+  const int it0 = g.start_it ? g.start_it[item] : 0;
+  if (it0 < 0) return;
+  arsvd_item(g, item, g.cursor ? g.cursor[item] : 0, it0);
+}
+
 // In-order resolution of the unverified suffix of every trial: one CTA per
 // trial walks its sketch steps t >= first[b] and feeds each call the cursor
 // the previous one ended at -- the reference's sequential use of one
@@ -954,7 +977,13 @@ __global__ void __launch_bounds__(128, 4) arsvd_screen_kernel(ArsvdArgs g, int64
     // CholeskyQR error bound on the captured energy (relative)
     const double tol = 64.0 * d * EPS64 * kap2 + 1e-12;
     if (!ok || kap2 > 1e8) {
-      if (lane == 0) resume[item] = it;
+      if (lane == 0) {
+        resume[item] = it;
+        if (g.want == 2) {  // estimate only: the exact pass decides
+          g.iters[item] = it + 1;
+          g.consumed[item] = used;
+        }
+      }
       return;
     }
     // X = W_i L^-H row by row (lane = row), ||X||_F^2
@@ -965,6 +994,21 @@ __global__ void __launch_bounds__(128, 4) arsvd_screen_kernel(ArsvdArgs g, int64
                         (last || d > 24) ? X + int64_t(k) * SCR_DMAX : nullptr);
     const double mf = warp_sum(loc);
     __syncwarp();
+    if (g.want == 2) {
+      // cursor-resolution rounds: iteration count from the screened energy alone
+      // (best estimate inside the error band; the exact pass verifies it later)
+      if (mf < target && !last) {
+        k0 *= 2;
+        o += d;
+        continue;
+      }
+      if (lane == 0) {
+        g.iters[item] = it + 1;
+        g.consumed[item] = used;
+        resume[item] = it;
+      }
+      return;
+    }
     if (mf < target * (1.0 - tol)) {  // no prefix of the spectrum reaches the target
       if (!last) {
         k0 *= 2;
@@ -1286,6 +1330,19 @@ extern "C" int lrz_cgemm(int dtype, int64_t batch, int M, int N, int Kd, int opA
                          int64_t lda, int64_t sA, int opB, const void *Bm, int64_t ldb,
                          int64_t sB, void *C, int64_t ldc, int64_t sC, void *stream);
 
+// Threads per item of the exact kernel: small problems are latency bound (barrier
+// and scalar chains per reflector / Jacobi round), so K <= 32 runs narrow CTAs
+// and many items per SM instead of one wide CTA per item.
+static int arsvd_threads(int K) {
+  static int env = -1;
+  if (env < 0) {
+    const char *e = getenv("LRZ_ARSVD_THREADS");
+    env = e ? atoi(e) : 0;
+  }
+  if (env >= 32 && env <= ARSVD_THREADS && env % 32 == 0) return env;
+  return K <= 32 ? 128 : ARSVD_THREADS;
+}
+
 size_t lrz_arsvd_ws(int64_t B, int K, int D) {
   return size_t(B) * (size_t(2) * D * K + size_t(D) * D) * sizeof(c128);
 }
@@ -1344,6 +1401,7 @@ extern "C" int lrz_arsvd(int64_t B, int K, const void *dA, int64_t a_stride,
   g.ya = nullptr;
   g.ydtot = 0;
   g.phase = 0;
+  g.smem_ws = 0;
   g.tail = nullptr;
   g.U = (c128 *)U;
   g.V = (c128 *)V;
@@ -1373,7 +1431,13 @@ extern "C" int lrz_arsvd(int64_t B, int K, const void *dA, int64_t a_stride,
                        }
                        return need <= cfg->omega_len;
                      }();
-  if (hermitian && want_factor == 0 && g.D <= SCR_DMAX && Dtot <= 4 * g.D && whole) {
+  const bool front_ok = hermitian && g.D <= SCR_DMAX && Dtot <= 4 * g.D && whole;
+  if (want_factor == 2 && !front_ok) {
+    lrz_set_error("lrz_arsvd: screen-only mode needs the screening front end (hermitian dA, "
+                  "d_max <= %d, the whole sketch window)", (int)SCR_DMAX);
+    return LRZ_EINVAL;
+  }
+  if (front_ok && want_factor != 1) {
     // screening front end (see arsvd_screen_kernel); workspace layout after the
     // CTA kernel's part: resume[B] int32 | Om/X [B][K][Dtot] | Y [B][K][Dtot] | W
     char *wp = (char *)workspace + lrz_arsvd_ws(B, K, cfg->d_max);
@@ -1410,6 +1474,7 @@ extern "C" int lrz_arsvd(int64_t B, int K, const void *dA, int64_t a_stride,
       arsvd_screen_kernel<<<unsigned((B + 3) / 4), 128, sm, st>>>(g, B, Dtot, Ya, Wa, Om,
                                                                   resume);
     }
+    if (want_factor == 2) return lrz_launch_status("lrz_arsvd (screen only)");
     g.start_it = resume;
     g.ya = Ya;
     g.ydtot = Dtot;
@@ -1438,8 +1503,38 @@ extern "C" int lrz_arsvd(int64_t B, int K, const void *dA, int64_t a_stride,
       return lrz_arsvd_tail_U(B, K, g.D, w0, w0 + int64_t(g.D) * K, wst, U, g.tail, st);
     }
   }
+  size_t dyn = 0;
+  {
+    const size_t need = (size_t(2) * g.D * K + size_t(g.D) * g.D) * sizeof(c128);
+    static int use_smem = -1;
+    if (use_smem < 0) {
+      const char *e = getenv("LRZ_ARSVD_SMEM");
+      use_smem = e ? atoi(e) : 1;
+    }
+    if (use_smem && need <= 48 * 1024) {
+      g.smem_ws = 1;
+      dyn = need;
+    }
+  }
   LrzProf prof("arsvd_kernel", st);
-  arsvd_kernel<<<unsigned(B), ARSVD_THREADS, 0, st>>>(g);
+  if (arsvd_threads(K) == 128) {
+    static int ctas = -1;
+    if (ctas < 0) {
+      const char *e = getenv("LRZ_ARSVD_CTAS");
+      ctas = e ? atoi(e) : 6;
+    }
+    auto launch = [&](auto kern) {
+      if (dyn) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(dyn));
+      kern<<<unsigned(B), 128, dyn, st>>>(g);
+    };
+    if (ctas >= 8) launch(arsvd_small_kernel<8>);
+    else if (ctas >= 6) launch(arsvd_small_kernel<6>);
+    else launch(arsvd_small_kernel<4>);
+  } else {
+    if (dyn) cudaFuncSetAttribute(arsvd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  int(dyn));
+    arsvd_kernel<<<unsigned(B), arsvd_threads(K), dyn, st>>>(g);
+  }
   return lrz_launch_status("lrz_arsvd");
 }
 
@@ -1482,6 +1577,7 @@ extern "C" int lrz_arsvd_seq(int64_t B, int T, int K, const void *dA, const doub
   g.ya = nullptr;
   g.ydtot = 0;
   g.phase = 0;
+  g.smem_ws = 0;
   g.tail = nullptr;
   g.U = (c128 *)U;
   g.V = (c128 *)V;

@@ -655,12 +655,14 @@ __global__ void __launch_bounds__(INV_THREADS)
 struct ConsumedTab {
   int64_t v[33];
 };
+constexpr int SPEC_VOTE_W = LRZ_SPEC_VOTE_W;  // tally slots per step (iteration counts 0 .. 15)
 
 __global__ void spec_verify_kernel(int64_t B, int T, int K, ConsumedTab consumed_tab,
                                    const uint8_t *is_sketch, int32_t *iters_pred,
                                    const int32_t *iters_act, int64_t *cursor,
                                    const int64_t *cursor0, int32_t *first_unverified,
-                                   uint8_t *active, int32_t *pending) {
+                                   uint8_t *active, int32_t *pending,
+                                   uint8_t *__restrict__ votes) {
   // one warp per trial: ballots find the first mispredicted step, a warp scan
   // rebuilds the cursors (32 steps per iteration instead of one)
   const int lane = threadIdx.x & 31;
@@ -668,6 +670,22 @@ __global__ void spec_verify_kernel(int64_t B, int T, int K, ConsumedTab consumed
   if (b >= B) return;
   const int64_t base = b * T;
   int t = first_unverified[b];
+  if (votes) {
+    // per-step tally of the iteration counts seen so far (every sketch step >= t
+    // was evaluated by the last pass, each time with another sketch): the suffix
+    // is re-predicted by majority, the first prediction counting as one vote
+    for (int s = t + lane; s < T; s += 32) {
+      uint8_t *v = votes + (base + s) * SPEC_VOTE_W;
+      if (!iters_act) {
+        for (int i = 0; i < SPEC_VOTE_W; ++i) v[i] = 0;
+        if (is_sketch[base + s]) v[min(iters_pred[base + s], SPEC_VOTE_W - 1)] = 1;
+      } else if (is_sketch[base + s]) {
+        uint8_t &c = v[min(max(iters_act[base + s], 0), SPEC_VOTE_W - 1)];
+        if (c < 255) ++c;
+      }
+    }
+    __syncwarp();
+  }
   if (iters_act) {
     // accept the verified prefix: the first sketch step s >= t whose observed
     // iteration count differs from the prediction is corrected and ends it
@@ -709,7 +727,19 @@ __global__ void spec_verify_kernel(int64_t B, int T, int K, ConsumedTab consumed
     if (s < T) {
       const int64_t bt = base + s;
       const bool sk = is_sketch[bt];
-      if (iters_act && s >= t && sk) iters_pred[bt] = max(iters_act[bt], 0);
+      if (iters_act && s >= t && sk) {
+        int pred = max(iters_act[bt], 0);
+        if (votes) {  // majority; ties keep the standing prediction, else the latest count
+          const uint8_t *v = votes + bt * SPEC_VOTE_W;
+          const int cur_p = min(iters_pred[bt], SPEC_VOTE_W - 1);
+          int best = min(pred, SPEC_VOTE_W - 1);
+          if (v[cur_p] >= v[best]) best = cur_p;
+          for (int i = 0; i < SPEC_VOTE_W; ++i)
+            if (v[i] > v[best]) best = i;
+          pred = best;
+        }
+        iters_pred[bt] = pred;
+      }
       active[bt] = (s >= t && sk) ? 1 : 0;
       if (sk) inc = consumed_tab.v[iters_pred[bt]];
     }
@@ -1120,8 +1150,19 @@ extern "C" int lrz_spec_verify(int64_t B, int T, int K, const lrz_arsvd_cfg *cfg
                                const int32_t *iters_act, int64_t *cursor, const int64_t *cursor0,
                                int32_t *first_unverified, uint8_t *active, int32_t *pending,
                                void *stream) {
+  return lrz_spec_verify_vote(B, T, K, cfg, is_sketch, iters_pred, iters_act, cursor, cursor0,
+                              first_unverified, active, pending, nullptr, stream);
+}
+
+extern "C" int lrz_spec_verify_vote(int64_t B, int T, int K, const lrz_arsvd_cfg *cfg,
+                                    const uint8_t *is_sketch, int32_t *iters_pred,
+                                    const int32_t *iters_act, int64_t *cursor,
+                                    const int64_t *cursor0, int32_t *first_unverified,
+                                    uint8_t *active, int32_t *pending, uint8_t *votes,
+                                    void *stream) {
   if (B < 0 || T < 1 || K < 1 || !cfg || !is_sketch || !iters_pred || !cursor ||
-      !cursor0 || !first_unverified || !active || !pending || cfg->i_max > 30) {
+      !cursor0 || !first_unverified || !active || !pending || cfg->i_max > 30 ||
+      (votes && cfg->i_max >= LRZ_SPEC_VOTE_W)) {
     lrz_set_error("lrz_spec_verify: bad arguments");
     return LRZ_EINVAL;
   }
@@ -1137,6 +1178,7 @@ extern "C" int lrz_spec_verify(int64_t B, int T, int K, const lrz_arsvd_cfg *cfg
   const unsigned nb = unsigned((B + 3) / 4);  // one warp per trial
   spec_verify_kernel<<<nb, 128, 0, (cudaStream_t)stream>>>(B, T, K, tab, is_sketch, iters_pred,
                                                            iters_act, cursor, cursor0,
-                                                           first_unverified, active, pending);
+                                                           first_unverified, active, pending,
+                                                           votes);
   return lrz_launch_status("lrz_spec_verify");
 }

@@ -158,9 +158,10 @@ def _arsvd_cfg(eta, k_init: int, p: int, i_max: int, D: int, omega_len: int = 0)
 def arsvd(dA: torch.Tensor, omega: torch.Tensor, cursor: torch.Tensor, eta, k_init: int,
           p: int, i_max: int, omega_row: torch.Tensor | None = None,
           mask: torch.Tensor | None = None, out: dict | None = None,
-          want_factor: bool = True, hermitian: bool = False) -> dict:
+          want_factor: bool | int = True, hermitian: bool = False) -> dict:
     """K2+K3 over a flat batch of items.  dA [B,K,K] c128; omega [R,L] f64;
-    cursor [B] int64; omega_row [B] int32 (row of omega per item, default = item)."""
+    cursor [B] int64; omega_row [B] int32 (row of omega per item, default = item).
+    want_factor 2: screen-only cursor-resolution mode (iters / consumed estimates)."""
     _chk(dA, "dA")
     if not omega.is_cuda or omega.dim() != 2 or omega.stride(1) != 1:
         raise ValueError("omega must be a [R, L] CUDA tensor with contiguous rows")
@@ -189,10 +190,11 @@ def arsvd(dA: torch.Tensor, omega: torch.Tensor, cursor: torch.Tensor, eta, k_in
                           out["consumed"].data_ptr(), N.ptr(mask), int(want_factor),
                           int(hermitian), ws.data_ptr(), N.stream_ptr(dev)), "lrz_arsvd")
     # screening front end (sketch GEMM [+ W GEMM for K > 32] + screen) + the exact kernel
-    front = hermitian and not want_factor and D <= 40
+    front = hermitian and int(want_factor) != 1 and D <= 40
     # K <= 32: fused sketch + screen + exact; K > 32: Omega gather + Y + W GEMMs on
-    # DMMA (SIMT: sketch + W GEMM) + screen + exact
-    _count((3 if K <= 32 else (5 if dmma_active() else 4)) if front else 1)
+    # DMMA (SIMT: sketch + W GEMM) + screen + exact; want_factor 2: no exact kernel
+    _count(((3 if K <= 32 else (5 if dmma_active() else 4)) if front else 1)
+           - (1 if int(want_factor) == 2 else 0))
     out["D"] = D
     return out
 
@@ -416,16 +418,24 @@ def plan(is_sketch: torch.Tensor, k_est: torch.Tensor, K: int, out: torch.Tensor
     return pl
 
 
+SPEC_VOTE_W = 16   # LRZ_SPEC_VOTE_W
+
+
 def spec_verify(is_sketch, iters_pred, iters_act, cursor, cursor0, first_unverified, active,
-                pending, K, eta, k_init, p, i_max):
+                pending, K, eta, k_init, p, i_max, votes=None):
+    """votes: optional uint8 [B, T, SPEC_VOTE_W] tally (majority re-prediction)."""
     B, T = is_sketch.shape
     dev = is_sketch.device
     cfg = _arsvd_cfg(eta, k_init, p, i_max, d_max_for(K, k_init, p, i_max))
     lib = N.lib_for(dev)
-    N.check(lib.lrz_spec_verify(B, T, K, C.byref(cfg), is_sketch.data_ptr(),
-                                iters_pred.data_ptr(), N.ptr(iters_act), cursor.data_ptr(),
-                                cursor0.data_ptr(), first_unverified.data_ptr(),
-                                active.data_ptr(), pending.data_ptr(), N.stream_ptr(dev)),
+    if votes is not None:
+        _chk(votes, "votes")
+        assert votes.shape == (B, T, SPEC_VOTE_W) and votes.dtype == torch.uint8
+    N.check(lib.lrz_spec_verify_vote(B, T, K, C.byref(cfg), is_sketch.data_ptr(),
+                                     iters_pred.data_ptr(), N.ptr(iters_act), cursor.data_ptr(),
+                                     cursor0.data_ptr(), first_unverified.data_ptr(),
+                                     active.data_ptr(), pending.data_ptr(), N.ptr(votes),
+                                     N.stream_ptr(dev)),
             "lrz_spec_verify")
     _count(1)
 

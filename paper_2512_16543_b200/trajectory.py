@@ -65,6 +65,10 @@ class TrajectoryConfig:
     # (ranks then usually hit before the iteration cap, so iteration counts follow
     # the sketch and a first speculative pass at predicted cursors is wasted)
     walk_first: bool | None = None
+    # screen-only cursor-resolution rounds run by that walk before the in-order
+    # kernel: -1 = 16 (an idle round costs ~40 us; C2 at eta = 0.9 needs up to ~12:
+    # a trial's borderline steps settle one per round), 0 = none (warp walk only)
+    screen_rounds: int = -1
 
 
 @dataclass
@@ -364,12 +368,39 @@ class TrajectoryRunner:
             n_spec = 0 if self._in_order else c.spec_passes
             # cursor walk (K <= 32): resolves every step's cursor from the energy
             # screen alone, in order, so one more speculative pass settles the chunk
-            can_walk = n_spec > 0 and ops.walk_ok(K, c.k_init, c.p, c.i_max)
+            walk_kernel = ops.walk_ok(K, c.k_init, c.p, c.i_max)
+            can_screen = D <= 40 and c.screen_rounds != 0
+            can_walk = n_spec > 0 and (walk_kernel or can_screen)
 
             def walk():
                 e0 = self._ev()
-                ops.arsvd_walk(dA, omega, is_sketch, first, cursor, iters_pred, self._eta,
-                               c.k_init, c.p, c.i_max)
+                first0 = first.clone()   # steps before it hold verified exact factors
+                if can_screen:
+                    # screen-only rounds, batched over every unsettled step: each round
+                    # takes the iteration counts the CholeskyQR energy screen sees at
+                    # the current cursors, accepts every trial's prefix up to its first
+                    # changed count and re-bases the cursors behind it (no host sync)
+                    rounds = c.screen_rounds if c.screen_rounds > 0 else 16
+                    # counts that hinge on the sketch drawn are not carried over from a
+                    # pass at shifted cursors: the suffix is re-predicted by majority
+                    votes = torch.empty(B, T, ops.SPEC_VOTE_W, dtype=torch.uint8, device=dev)
+                    pending.zero_()
+                    ops.spec_verify(is_sketch, iters_pred, None, cursor, cursor0, first, active,
+                                    pending, K, self._eta, c.k_init, c.p, c.i_max, votes=votes)
+                    for _ in range(rounds):
+                        ops.arsvd(dAf, omega, cursor.reshape(BT), self._eta, c.k_init, c.p,
+                                  c.i_max, omega_row=row, mask=active.reshape(BT), out=res,
+                                  want_factor=2, hermitian=True)
+                        pending.zero_()
+                        ops.spec_verify(is_sketch, iters_pred, res["iters"], cursor, cursor0,
+                                        first, active, pending, K, self._eta, c.k_init, c.p,
+                                        c.i_max, votes=votes)
+                if walk_kernel:
+                    # trials the rounds left unsettled (the kernel returns at once for
+                    # the others): in order, one warp per trial
+                    ops.arsvd_walk(dA, omega, is_sketch, first, cursor, iters_pred, self._eta,
+                                   c.k_init, c.p, c.i_max)
+                first.copy_(first0)
                 pending.zero_()
                 ops.spec_verify(is_sketch, iters_pred, None, cursor, cursor0, first, active,
                                 pending, K, self._eta, c.k_init, c.p, c.i_max)

@@ -116,6 +116,30 @@ def test_rng_locate_matches_host_stream(cuda):
     assert (d == host.window(1000)).mean() > 0.999
 
 
+@pytest.mark.parametrize("rounds,T,eta", [(-1, 200, 0.9), (1, 200, 0.9), (2, 120, 0.8), (0, 60, 0.9)])
+def test_screen_rounds_settle_the_cursors(cuda, rounds, T, eta):
+    """Screen-only cursor-resolution rounds (lrz_arsvd want_factor 2 + lrz_spec_verify,
+    then the in-order warp walk for what is left) against the in-order exact
+    trajectory on full-length Woodbury-regime C2 trials: iteration counts,
+    consumption, ranks, methods identical; settled in one exact pass."""
+    spec = S.C2.with_(B=4, T=T)
+    trials = list(range(4))
+    H, noise, _ = _setup(cuda, spec, None, trials)
+    outs = []
+    for sp, r in ((0, 0), (2, rounds)):
+        cfg = TrajectoryConfig(alpha=spec.alpha, eta=eta, k_init=spec.k_init, p=spec.p,
+                               i_max=spec.i_max, spec_passes=sp, walk_first=True,
+                               screen_rounds=r)
+        rn = TrajectoryRunner(4, spec.K, spec.N, torch.complex128, cfg, cuda)
+        st = DeviceOmegaStreams.for_method(spec.seed, eta, trials, cuda)
+        outs.append(rn.run_chunk(H, noise, st.window(spec.T * rn.normals_per_step_max())))
+    a, b = outs
+    assert torch.equal(a.iters, b.iters) and torch.equal(a.consumed, b.consumed)
+    assert torch.equal(a.k_est, b.k_est) and torch.equal(a.method, b.method)
+    assert b.spec_passes == 1
+    torch.testing.assert_close(a.rates, b.rates, rtol=1e-10, atol=0)
+
+
 @pytest.mark.parametrize("walk_first", [True, False])
 def test_cursor_walk_equals_in_order(cuda, walk_first):
     """The energy-screen cursor walk (lrz_arsvd_walk) followed by one speculative
