@@ -5,7 +5,10 @@
 
 #include <cooperative_groups.h>
 
+#include "dmma.cuh"
 #include "linalg.cuh"
+
+int lrz_use_dmma();
 
 namespace lrz {
 
@@ -44,21 +47,23 @@ constexpr int WB_SMEM_DMAX = 40;  // aux / aux^-1 in shared memory up to this ra
 __host__ __device__ inline int64_t wb_ws_elems(int K, int D) {
   // AiU, T, VhAi (K x D each) [+ aux, aux^-1 when they do not fit shared memory]
   // + the DMMA chain's aux and aux^-1 in global memory (D x D each)
-  return 3 * int64_t(K) * D + (D > WB_SMEM_DMAX ? 2 * int64_t(D) * D : 0) + 2 * int64_t(D) * D;
+  return 3 * int64_t(K) * D + (D > WB_SMEM_DMAX ? 2 * int64_t(D) * (D + 1) : 0) +
+         2 * int64_t(D) * D;
 }
 // offset of the DMMA chain's global aux (then aux^-1) inside a trial's workspace
 __host__ __device__ inline int64_t wb_ws_aux_off(int K, int D) {
-  return 3 * int64_t(K) * D + (D > WB_SMEM_DMAX ? 2 * int64_t(D) * D : 0);
+  return 3 * int64_t(K) * D + (D > WB_SMEM_DMAX ? 2 * int64_t(D) * (D + 1) : 0);
 }
 __host__ __device__ inline size_t wb_aux_smem(int D) {
-  return D > WB_SMEM_DMAX ? 0 : 2 * size_t(D) * D * sizeof(c128);
+  // D x (D + 1) each: the resident chain keeps aux / aux^-1 at an odd row stride
+  return D > WB_SMEM_DMAX ? 0 : 2 * size_t(D) * (D + 1) * sizeof(c128);
 }
 LRZ_DEV void carve_wb(WbScratch &sc, char *aux_smem, c128 *w, int K, int D) {
   sc.AiU = w;
   sc.T = w + int64_t(K) * D;
   sc.VhAi = w + 2 * int64_t(K) * D;
   sc.aux = D > WB_SMEM_DMAX ? w + 3 * int64_t(K) * D : (c128 *)aux_smem;
-  sc.auxinv = sc.aux + D * D;
+  sc.auxinv = sc.aux + D * (D + 1);
 }
 
 __global__ void __launch_bounds__(INV_THREADS)
@@ -285,6 +290,240 @@ __global__ void __launch_bounds__(INV_THREADS)
   if (threadIdx.x == 0) info[item] = st;
 }
 
+// ---------------------------------------------------------------------------
+// Resident Woodbury step on the FP64 tensor pipe (K <= 32, r <= 32; every
+// operand in shared memory).  The step of cta_woodbury (lowrank.py:208-220)
+// with each product cut into 8 x 8 complex output blocks that the CTA's warps
+// take round robin (mma.sync m8n8k4 f64, four real DMMAs per complex k-step,
+// fragments straight from the resident tiles), and the r x r auxiliary inverse
+// -- pivoted Gauss-Jordan, as cta_gauss_jordan -- done by one warp on
+// __syncwarp while the other warps apply A += (U S) V^H.  One CTA issued ~1
+// instruction per cycle on the SIMT version (ncu: pivot search over CTA
+// barriers 20 %, LDS-bound cfma loops); this one is bound by the DMMA pipe.
+// ---------------------------------------------------------------------------
+template <class FA, class FB>
+LRZ_DEV void blk_zmma(int ksteps, FA a, FB b, double (&cr)[2], double (&ci)[2]) {
+  const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+  for (int c = 0; c < ksteps; ++c) {
+    const c128 av = a(g, 4 * c + t), bv = b(4 * c + t, g);
+    dmma(cr, av.re, bv.re);
+    dmma(cr, -av.im, bv.im);
+    dmma(ci, av.re, bv.im);
+    dmma(ci, av.im, bv.re);
+  }
+}
+
+// In-place inverse of the r x r matrix M (row stride ldm, shared memory) by one
+// warp: Gauss-Jordan with partial row pivoting, the arithmetic of
+// cta_gauss_jordan (lane i owns row i; the column permutation is undone at the
+// end).  perm: r ints of scratch.  Returns 0, or 2 on a zero / non-finite
+// pivot; fro2 = ||M^-1||_F^2.  Warp-uniform; all 32 lanes must call.
+LRZ_DEV int warp_gj_pivot(c128 *M, int r, int ldm, int *perm, double &fro2) {
+  const int lane = threadIdx.x & 31;
+  for (int k = 0; k < r; ++k) {
+    double best = -1.0;
+    int bi = r;
+    if (lane >= k && lane < r) {
+      best = cabs2(M[lane * ldm + k]);
+      bi = lane;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (ob > best || (ob == best && oi < bi)) {  // smallest index on ties
+        best = ob;
+        bi = oi;
+      }
+    }
+    if (!(best > 0.0) || bi >= r) return 2;
+    if (bi != k && lane < r) {
+      const c128 x = M[k * ldm + lane];
+      M[k * ldm + lane] = M[bi * ldm + lane];
+      M[bi * ldm + lane] = x;
+    }
+    if (lane == 0) perm[k] = bi;
+    __syncwarp();
+    const c128 piv = M[k * ldm + k];
+    if (!(isfinite(piv.re) && isfinite(piv.im))) return 2;
+    const c128 pinv = cinv(piv);
+    c128 rj = czero<double>(), ck = czero<double>();
+    if (lane < r) {
+      rj = (lane == k) ? pinv : cmul(M[k * ldm + lane], pinv);  // row k of the result
+      ck = M[lane * ldm + k];                                   // my row's column-k entry
+    }
+    __syncwarp();
+    if (lane < r) M[k * ldm + lane] = rj;
+    __syncwarp();
+    if (lane < r && lane != k) {
+      c128 *row = M + lane * ldm;
+      const c128 *rk = M + k * ldm;
+      for (int j = 0; j < r; ++j) {
+        if (j == k) {
+          row[j] = cmul(mk<double>(-ck.re, -ck.im), pinv);
+        } else {
+          const c128 rr = rk[j];
+          c128 m = row[j];
+          m.re = fma(-ck.re, rr.re, m.re);
+          m.re = fma(ck.im, rr.im, m.re);
+          m.im = fma(-ck.re, rr.im, m.im);
+          m.im = fma(-ck.im, rr.re, m.im);
+          row[j] = m;
+        }
+      }
+    }
+    __syncwarp();
+  }
+  for (int k = r - 1; k >= 0; --k) {
+    const int p = perm[k];
+    if (p != k && lane < r) {
+      const c128 x = M[lane * ldm + k];
+      M[lane * ldm + k] = M[lane * ldm + p];
+      M[lane * ldm + p] = x;
+    }
+  }
+  __syncwarp();
+  double loc = 0.0;
+  if (lane < r)
+    for (int j = 0; j < r; ++j) loc += cabs2(M[lane * ldm + j]);
+  fro2 = warp_sum(loc);
+  return 0;
+}
+
+// Ainv_in / Ainv_out: K x K at row stride ld; U, V, sc.AiU, sc.T: column j at
+// j * ld; sc.VhAi: row j at j * ld; A (nullable, in place): K x K at stride K.
+// Returns LRZ_INFO_OK or LRZ_INFO_SINGULAR_AUX (then Ainv_out is untouched and
+// A is garbage: the caller's full branch overwrites both).
+LRZ_DEV int cta_woodbury_dmma(int K, int r, const c128 *__restrict__ Ai, c128 *Ainv_out, c128 *A,
+                              const c128 *__restrict__ U, const c128 *__restrict__ V,
+                              const double *__restrict__ S, const WbScratch &sc, int ld) {
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, NW = blockDim.x >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  const int KB = (K + 7) >> 3, RB = (r + 7) >> 3, ksK = (K + 3) >> 2, ksr = (r + 3) >> 2;
+  const int lda = r | 1;  // odd row stride of aux / aux^-1 (bank spread for lane = row)
+  const c128 Z = czero<double>();
+  __shared__ double s_fi;
+  __shared__ int s_st;
+  // 1. AiU = A^-1 U (K x r), VhAi = V^H A^-1 (r x K)
+  for (int blk = wid; blk < 2 * KB * RB; blk += NW) {
+    double cr[2] = {0.0, 0.0}, ci[2] = {0.0, 0.0};
+    if (blk < KB * RB) {
+      const int k0 = 8 * (blk / RB), j0 = 8 * (blk % RB);
+      blk_zmma(
+          ksK,
+          [&](int i, int m) { return (k0 + i < K && m < K) ? Ai[(k0 + i) * ld + m] : Z; },
+          [&](int m, int j) { return (m < K && j0 + j < r) ? U[(j0 + j) * ld + m] : Z; }, cr, ci);
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int k = k0 + g, j = j0 + 2 * t + e;
+        if (k < K && j < r) sc.AiU[j * ld + k] = mk<double>(cr[e], ci[e]);
+      }
+    } else {
+      const int b2 = blk - KB * RB, j0 = 8 * (b2 / KB), m0 = 8 * (b2 % KB);
+      blk_zmma(
+          ksK,
+          [&](int i, int k) { return (j0 + i < r && k < K) ? cconj(V[(j0 + i) * ld + k]) : Z; },
+          [&](int k, int m) { return (k < K && m0 + m < K) ? Ai[k * ld + m0 + m] : Z; }, cr, ci);
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int j = j0 + g, m = m0 + 2 * t + e;
+        if (j < r && m < K) sc.VhAi[j * ld + m] = mk<double>(cr[e], ci[e]);
+      }
+    }
+  }
+  __syncthreads();
+  // 2. aux = diag(1/S) + V^H AiU  (r x r, both copies at stride lda)
+  double loc = 0.0;
+  for (int blk = wid; blk < RB * RB; blk += NW) {
+    const int i0 = 8 * (blk / RB), j0 = 8 * (blk % RB);
+    double cr[2] = {0.0, 0.0}, ci[2] = {0.0, 0.0};
+    blk_zmma(
+        ksK, [&](int i, int k) { return (i0 + i < r && k < K) ? cconj(V[(i0 + i) * ld + k]) : Z; },
+        [&](int k, int j) { return (k < K && j0 + j < r) ? sc.AiU[(j0 + j) * ld + k] : Z; }, cr, ci);
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const int i = i0 + g, j = j0 + 2 * t + e;
+      if (i < r && j < r) {
+        c128 a = mk<double>(cr[e], ci[e]);
+        if (i == j) a.re = 1.0 / S[i] + a.re;
+        sc.aux[i * lda + j] = a;
+        sc.auxinv[i * lda + j] = a;
+        loc += cabs2(a);
+      }
+    }
+  }
+  const double fa = block_sum(loc, sc.inv.red);
+  __syncthreads();
+  // 3. warp 0: aux^-1; the other warps: A += (U S) V^H (overwritten by the
+  //    caller's full branch if the step turns out singular)
+  if (wid == 0) {
+    double fi = 0.0;
+    const int st = warp_gj_pivot(sc.auxinv, r, lda, sc.inv.perm, fi);
+    if (lane == 0) {
+      s_st = st;
+      s_fi = fi;
+    }
+  } else if (A) {
+    for (int blk = wid - 1; blk < KB * KB; blk += NW - 1) {
+      const int k0 = 8 * (blk / KB), m0 = 8 * (blk % KB);
+      double cr[2] = {0.0, 0.0}, ci[2] = {0.0, 0.0};
+      blk_zmma(
+          ksr,
+          [&](int i, int j) {
+            return (k0 + i < K && j < r) ? cscale(U[j * ld + k0 + i], S[j]) : Z;
+          },
+          [&](int j, int m) { return (j < r && m0 + m < K) ? cconj(V[j * ld + m0 + m]) : Z; }, cr,
+          ci);
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int k = k0 + g, m = m0 + 2 * t + e;
+        if (k < K && m < K) {
+          c128 &x = A[k * K + m];
+          x = mk<double>(x.re + cr[e], x.im + ci[e]);
+        }
+      }
+    }
+  }
+  __syncthreads();
+  if (s_st != 0) return LRZ_INFO_SINGULAR_AUX;
+  // the 1e12 condition guard (lowrank.py:212-217); sc.aux is free after this
+  if (!cta_cond_ok(fa, s_fi, 1e12, sc.aux, r, lda, sc.inv.red, sc.inv.ired))
+    return LRZ_INFO_SINGULAR_AUX;
+  // 4. T = AiU aux^-1 (K x r)
+  for (int blk = wid; blk < KB * RB; blk += NW) {
+    const int k0 = 8 * (blk / RB), j0 = 8 * (blk % RB);
+    double cr[2] = {0.0, 0.0}, ci[2] = {0.0, 0.0};
+    blk_zmma(
+        ksr, [&](int kk, int i) { return (k0 + kk < K && i < r) ? sc.AiU[i * ld + k0 + kk] : Z; },
+        [&](int i, int j) { return (i < r && j0 + j < r) ? sc.auxinv[i * lda + j0 + j] : Z; }, cr,
+        ci);
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const int k = k0 + g, j = j0 + 2 * t + e;
+      if (k < K && j < r) sc.T[j * ld + k] = mk<double>(cr[e], ci[e]);
+    }
+  }
+  __syncthreads();
+  // 5. A^-1 - T VhAi
+  for (int blk = wid; blk < KB * KB; blk += NW) {
+    const int k0 = 8 * (blk / KB), m0 = 8 * (blk % KB);
+    double cr[2] = {0.0, 0.0}, ci[2] = {0.0, 0.0};
+    blk_zmma(
+        ksr, [&](int kk, int j) { return (k0 + kk < K && j < r) ? sc.T[j * ld + k0 + kk] : Z; },
+        [&](int j, int m) { return (j < r && m0 + m < K) ? sc.VhAi[j * ld + m0 + m] : Z; }, cr, ci);
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const int k = k0 + g, m = m0 + 2 * t + e;
+      if (k < K && m < K) {
+        const c128 o = Ai[k * ld + m];
+        Ainv_out[k * ld + m] = mk<double>(o.re - cr[e], o.im - ci[e]);
+      }
+    }
+  }
+  __syncthreads();
+  return LRZ_INFO_OK;
+}
+
 // Per-trial chain over T steps (harness.py:228-241 semantics):
 //   plan 0 (full):     A_inv_seq[t] already holds inv(G_t); A_state = G_t
 //   plan 1 (Woodbury): A_inv_seq[t] = woodbury(A_inv_seq[t-1]); on SingularAux
@@ -328,6 +567,7 @@ __global__ void __launch_bounds__(INV_THREADS)
   WbScratch sc;
   sc.inv = carve_inv(smem, n, &M, K, K <= INV_SMEM_KMAX);
   const bool res = resident != 0;
+  const bool dmma_step = resident == 2;  // the step's products on the FP64 tensor pipe
   c128 *sAi = nullptr, *sA = nullptr, *sU = nullptr, *sV = nullptr;
   const int ld = K + 1;                   // resident stride (bank spread)
   const int64_t KL = int64_t(K) * ld;     // one resident A^-1 buffer
@@ -382,8 +622,10 @@ __global__ void __launch_bounds__(INV_THREADS)
         asm volatile("cp.async.commit_group;\n" ::);
         asm volatile("cp.async.wait_group 0;\n" ::);
         __syncthreads();
-        st = cta_woodbury(K, r[bt], sAi + cb * KL, sAi + (cb ^ 1) * KL, Acur, Acur, sU, sV,
-                          S + bt * D, sc, ld);
+        st = dmma_step ? cta_woodbury_dmma(K, r[bt], sAi + cb * KL, sAi + (cb ^ 1) * KL, Acur, sU,
+                                           sV, S + bt * D, sc, ld)
+                       : cta_woodbury(K, r[bt], sAi + cb * KL, sAi + (cb ^ 1) * KL, Acur, Acur, sU,
+                                      sV, S + bt * D, sc, ld);
         if (st == LRZ_INFO_OK) {
           cb ^= 1;
           for (int64_t e = tid; e < KK; e += NT) out[e] = sAi[cb * KL + (e / K) * ld + e % K];
@@ -1040,7 +1282,13 @@ extern "C" int lrz_chain(int64_t B, int T, int K, int d_max, const uint8_t *plan
     if (c) cudaFuncSetAttribute((const void *)chain_kernel,
                                 cudaFuncAttributePreferredSharedMemoryCarveout, atoi(c));
   }
-  const int resident = mode && chain_resident(K, d_max);
+  // resident: 2 = the DMMA step (LRZ_CHAIN_RESIDENT=1 selects the SIMT resident step)
+  static int simt = -1;
+  if (simt < 0) {
+    const char *e = getenv("LRZ_CHAIN_RESIDENT");
+    simt = (e && e[0] == '1') ? 1 : 0;
+  }
+  const int resident = (mode && chain_resident(K, d_max)) ? (simt || !lrz_use_dmma() ? 1 : 2) : 0;
   const size_t sm = resident ? lrz_chain_smem(K, d_max)
                              : InvSmem::bytes(K, d_max, K <= INV_SMEM_KMAX) + wb_aux_smem(d_max);
   if (set_smem((const void *)chain_kernel, sm)) return LRZ_ELAUNCH;
