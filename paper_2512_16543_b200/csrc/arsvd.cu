@@ -336,16 +336,19 @@ LRZ_DEV void hh_apply(const c128 *X, int K, int d, const double *tau, c128 *C, i
 
 // One arsvd call (item) by the whole CTA, sketch stream read from `cur`,
 // resuming at iteration it0.  Returns the normals consumed (block-uniform).
+// DM: bound on the sketch width d (sizes the per-item shared scratch: the small
+// kernel's items leave the SM's shared memory to the kernels they overlap with).
+template <int DM = ARSVD_DMAX>
 LRZ_DEV int64_t arsvd_item(const ArsvdArgs &g, const int64_t item, int64_t cur, const int it0) {
   const int K = g.K, D = g.D;
   const int tid = threadIdx.x, NT = blockDim.x, lane = tid & 31, wid = tid >> 5, NW = NT >> 5;
 
   __shared__ double red[ARSVD_THREADS / 32];
-  __shared__ double sval[ARSVD_DMAX];
-  __shared__ int perm[ARSVD_DMAX];
-  __shared__ c128 rbuf[ARSVD_DMAX];
-  __shared__ double s_tau[ARSVD_DMAX];
-  __shared__ c128 s_ph[ARSVD_DMAX];
+  __shared__ double sval[DM];
+  __shared__ int perm[DM];
+  __shared__ c128 rbuf[DM];
+  __shared__ double s_tau[DM];
+  __shared__ c128 s_ph[DM];
   __shared__ int s_rot[2];
   __shared__ int s_r;
 
@@ -676,7 +679,7 @@ __global__ void __launch_bounds__(128, CTAS) arsvd_small_kernel(ArsvdArgs g) {
   if (g.mask && !g.mask[item]) return;
   const int it0 = g.start_it ? g.start_it[item] : 0;
   if (it0 < 0) return;
-  arsvd_item(g, item, g.cursor ? g.cursor[item] : 0, it0);
+  arsvd_item<32>(g, item, g.cursor ? g.cursor[item] : 0, it0);
 }
 
 // In-order resolution of the unverified suffix of every trial: one CTA per
@@ -1517,7 +1520,7 @@ extern "C" int lrz_arsvd(int64_t B, int K, const void *dA, int64_t a_stride,
     }
   }
   LrzProf prof("arsvd_kernel", st);
-  if (arsvd_threads(K) == 128) {
+  if (arsvd_threads(K) == 128 && g.D <= 32 && K <= 32) {
     static int ctas = -1;
     if (ctas < 0) {
       const char *e = getenv("LRZ_ARSVD_CTAS");

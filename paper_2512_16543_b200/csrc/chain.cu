@@ -314,29 +314,34 @@ LRZ_DEV void blk_zmma(int ksteps, FA a, FB b, double (&cr)[2], double (&ci)[2]) 
 }
 
 // In-place inverse of the r x r matrix M (row stride ldm, shared memory) by one
-// warp: Gauss-Jordan with partial row pivoting, the arithmetic of
-// cta_gauss_jordan (lane i owns row i; the column permutation is undone at the
-// end).  perm: r ints of scratch.  Returns 0, or 2 on a zero / non-finite
+// warp: Gauss-Jordan with partial row pivoting (the algorithm of
+// cta_gauss_jordan: largest |m|^2 in the column, smallest row on ties; the
+// column permutation is undone at the end).  The warp is latency bound, so the
+// pivot search is two integer redux steps on the (ordered) bit pattern of
+// |m|^2 plus a ballot instead of five shuffle rounds, the pivot's reciprocal is
+// conj(p) / |p|^2 with one division, and the rank-1 update runs over all r^2
+// entries spread across the 32 lanes (column k and the scaled row k
+// snapshotted in colbuf / rowbuf), independent iterations the scheduler can
+// overlap.  perm: r ints of scratch.  Returns 0, or 2 on a zero / non-finite
 // pivot; fro2 = ||M^-1||_F^2.  Warp-uniform; all 32 lanes must call.
-LRZ_DEV int warp_gj_pivot(c128 *M, int r, int ldm, int *perm, double &fro2) {
+LRZ_DEV int warp_gj_pivot(c128 *M, int r, int ldm, int *perm, c128 *colbuf, c128 *rowbuf,
+                          double &fro2) {
   const int lane = threadIdx.x & 31;
+  const int rr2 = r * r;
+  const float inv_r = 1.0f / float(r);
   for (int k = 0; k < r; ++k) {
-    double best = -1.0;
-    int bi = r;
-    if (lane >= k && lane < r) {
-      best = cabs2(M[lane * ldm + k]);
-      bi = lane;
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      const double ob = __shfl_xor_sync(0xffffffffu, best, o);
-      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-      if (ob > best || (ob == best && oi < bi)) {  // smallest index on ties
-        best = ob;
-        bi = oi;
-      }
-    }
-    if (!(best > 0.0) || bi >= r) return 2;
+    // pivot: argmax |M[i][k]|^2 over i >= k (non-negative doubles order like their bits)
+    double mag = 0.0;
+    if (lane >= k && lane < r) mag = cabs2(M[lane * ldm + k]);
+    const unsigned long long bits = (mag == mag) ? (unsigned long long)__double_as_longlong(mag)
+                                                 : 0xFFFFFFFFFFFFFFFFull;  // NaN: fail below
+    const unsigned hi = unsigned(bits >> 32), lo = unsigned(bits);
+    const unsigned mh = __reduce_max_sync(0xffffffffu, hi);
+    const unsigned ml = __reduce_max_sync(0xffffffffu, hi == mh ? lo : 0u);
+    const bool cand = lane >= k && lane < r && hi == mh && lo == ml;
+    const unsigned bal = __ballot_sync(0xffffffffu, cand);
+    if (bal == 0u || (mh == 0u && ml == 0u) || mh >= 0x7FF00000u) return 2;  // zero / inf / NaN
+    const int bi = __ffs(bal) - 1;
     if (bi != k && lane < r) {
       const c128 x = M[k * ldm + lane];
       M[k * ldm + lane] = M[bi * ldm + lane];
@@ -345,32 +350,33 @@ LRZ_DEV int warp_gj_pivot(c128 *M, int r, int ldm, int *perm, double &fro2) {
     if (lane == 0) perm[k] = bi;
     __syncwarp();
     const c128 piv = M[k * ldm + k];
-    if (!(isfinite(piv.re) && isfinite(piv.im))) return 2;
-    const c128 pinv = cinv(piv);
-    c128 rj = czero<double>(), ck = czero<double>();
+    const double id = 1.0 / cabs2(piv);
+    const c128 pinv = mk<double>(piv.re * id, -piv.im * id);
+    if (!(isfinite(pinv.re) && isfinite(pinv.im))) return 2;
     if (lane < r) {
-      rj = (lane == k) ? pinv : cmul(M[k * ldm + lane], pinv);  // row k of the result
-      ck = M[lane * ldm + k];                                   // my row's column-k entry
+      colbuf[lane] = M[lane * ldm + k];
+      rowbuf[lane] = (lane == k) ? pinv : cmul(M[k * ldm + lane], pinv);
     }
     __syncwarp();
-    if (lane < r) M[k * ldm + lane] = rj;
-    __syncwarp();
-    if (lane < r && lane != k) {
-      c128 *row = M + lane * ldm;
-      const c128 *rk = M + k * ldm;
-      for (int j = 0; j < r; ++j) {
+    for (int e = lane; e < rr2; e += 32) {
+      const int i = int((float(e) + 0.5f) * inv_r), j = e - i * r;  // exact: e < 1024
+      const c128 rj = rowbuf[j];
+      c128 m;
+      if (i == k) {
+        m = rj;
+      } else {
+        const c128 c = colbuf[i];
         if (j == k) {
-          row[j] = cmul(mk<double>(-ck.re, -ck.im), pinv);
+          m = cmul(mk<double>(-c.re, -c.im), pinv);
         } else {
-          const c128 rr = rk[j];
-          c128 m = row[j];
-          m.re = fma(-ck.re, rr.re, m.re);
-          m.re = fma(ck.im, rr.im, m.re);
-          m.im = fma(-ck.re, rr.im, m.im);
-          m.im = fma(-ck.im, rr.re, m.im);
-          row[j] = m;
+          m = M[i * ldm + j];
+          m.re = fma(-c.re, rj.re, m.re);
+          m.re = fma(c.im, rj.im, m.re);
+          m.im = fma(-c.re, rj.im, m.im);
+          m.im = fma(-c.im, rj.re, m.im);
         }
       }
+      M[i * ldm + j] = m;
     }
     __syncwarp();
   }
@@ -384,8 +390,10 @@ LRZ_DEV int warp_gj_pivot(c128 *M, int r, int ldm, int *perm, double &fro2) {
   }
   __syncwarp();
   double loc = 0.0;
-  if (lane < r)
-    for (int j = 0; j < r; ++j) loc += cabs2(M[lane * ldm + j]);
+  for (int e = lane; e < rr2; e += 32) {
+    const int i = int((float(e) + 0.5f) * inv_r), j = e - i * r;
+    loc += cabs2(M[i * ldm + j]);
+  }
   fro2 = warp_sum(loc);
   return 0;
 }
@@ -458,7 +466,7 @@ LRZ_DEV int cta_woodbury_dmma(int K, int r, const c128 *__restrict__ Ai, c128 *A
   //    caller's full branch if the step turns out singular)
   if (wid == 0) {
     double fi = 0.0;
-    const int st = warp_gj_pivot(sc.auxinv, r, lda, sc.inv.perm, fi);
+    const int st = warp_gj_pivot(sc.auxinv, r, lda, sc.inv.perm, sc.inv.colbuf, sc.inv.rowbuf, fi);
     if (lane == 0) {
       s_st = st;
       s_fi = fi;
@@ -540,8 +548,9 @@ __host__ __device__ inline size_t chain_base_smem(int K, int D) {
   return (InvSmem::bytes(K, D, K <= INV_SMEM_KMAX) + wb_aux_smem(D) + 15) & ~size_t(15);
 }
 __host__ __device__ inline size_t chain_resident_smem(int K, int D) {
-  // A^-1 x 2 and U, V, A^-1 U, T, V^H A^-1 at stride K + 1; A at stride K
-  return (2 * size_t(K) * (K + 1) + size_t(K) * K + 5 * size_t(K + 1) * D) * sizeof(c128);
+  // A^-1 x 2 and (U, V) x 2 (the next step's factors are prefetched), A^-1 U, T,
+  // V^H A^-1 at stride K + 1; A at stride K
+  return (2 * size_t(K) * (K + 1) + size_t(K) * K + 7 * size_t(K + 1) * D) * sizeof(c128);
 }
 
 LRZ_DEV void chain_cp16(void *smem, const void *gmem) {
@@ -574,15 +583,18 @@ __global__ void __launch_bounds__(INV_THREADS)
   if (res) {
     sAi = (c128 *)(smem + chain_base_smem(K, D));  // [2][K][ld]
     sA = sAi + 2 * KL;                             // [K][K]
-    sU = sA + KK;                                  // [D][ld]
+    sU = sA + KK;                                  // [2][U | V][D][ld]
     sV = sU + int64_t(ld) * D;
-    carve_wb(sc, smem + InvSmem::bytes(K, D, K <= INV_SMEM_KMAX), sV + int64_t(ld) * D, ld, D);
+    carve_wb(sc, smem + InvSmem::bytes(K, D, K <= INV_SMEM_KMAX), sU + 4 * int64_t(ld) * D, ld,
+             D);
   } else {
     carve_wb(sc, smem + InvSmem::bytes(K, D, K <= INV_SMEM_KMAX), ws + b * wb_ws_elems(K, D),
              K, D);
   }
   c128 *Ast = A_state ? A_state + b * KK : nullptr;
   int cb = 0;  // resident: sAi + cb KL holds A^-1 of the previous step
+  int ub = 0;            // resident: the (U, V) buffer pair of the current Woodbury step
+  bool uv_ready = false; // its factors were requested by the previous step
   // resident tiles are filled lazily (a chunk of full inversions never reads them)
   bool have_ai = false, have_a = false;
   c128 *Acur = res ? (Ast ? sA : nullptr) : Ast;  // where the A state lives
@@ -613,19 +625,37 @@ __global__ void __launch_bounds__(INV_THREADS)
     if (pl == 1) {
       const c128 *Ub = U + bt * int64_t(D) * K, *Vb = V + bt * int64_t(D) * K;
       if (res) {
-        const int rk = r[bt] * K;
-        for (int e = tid; e < rk; e += NT) {
-          const int o = (e / K) * ld + e % K;
-          chain_cp16(sU + o, Ub + e);
-          chain_cp16(sV + o, Vb + e);
+        // this step's factors (unless the previous step prefetched them), then the
+        // next Woodbury step's into the other buffer pair: its load latency
+        // overlaps this step's arithmetic
+        const int64_t UV2 = 2 * int64_t(ld) * D;
+        auto fetch = [&](int64_t bt2, int buf) {
+          const int rk = r[bt2] * K;
+          const c128 *Ug = U + bt2 * int64_t(D) * K, *Vg = V + bt2 * int64_t(D) * K;
+          c128 *du = sU + buf * UV2, *dv = sV + buf * UV2;
+          for (int e = tid; e < rk; e += NT) {
+            const int o = (e / K) * ld + e % K;
+            chain_cp16(du + o, Ug + e);
+            chain_cp16(dv + o, Vg + e);
+          }
+          asm volatile("cp.async.commit_group;\n" ::);
+        };
+        if (!uv_ready) fetch(bt, ub);
+        const bool nxt = t + 1 < T && s_plan[t % CH_PLAN_BLK + 1] == 1;
+        if (nxt) {
+          fetch(bt + 1, ub ^ 1);
+          asm volatile("cp.async.wait_group 1;\n" ::);
+        } else {
+          asm volatile("cp.async.wait_group 0;\n" ::);
         }
-        asm volatile("cp.async.commit_group;\n" ::);
-        asm volatile("cp.async.wait_group 0;\n" ::);
         __syncthreads();
-        st = dmma_step ? cta_woodbury_dmma(K, r[bt], sAi + cb * KL, sAi + (cb ^ 1) * KL, Acur, sU,
-                                           sV, S + bt * D, sc, ld)
-                       : cta_woodbury(K, r[bt], sAi + cb * KL, sAi + (cb ^ 1) * KL, Acur, Acur, sU,
-                                      sV, S + bt * D, sc, ld);
+        const c128 *cU = sU + ub * UV2, *cV = sV + ub * UV2;
+        st = dmma_step ? cta_woodbury_dmma(K, r[bt], sAi + cb * KL, sAi + (cb ^ 1) * KL, Acur, cU,
+                                           cV, S + bt * D, sc, ld)
+                       : cta_woodbury(K, r[bt], sAi + cb * KL, sAi + (cb ^ 1) * KL, Acur, Acur, cU,
+                                      cV, S + bt * D, sc, ld);
+        uv_ready = nxt;
+        if (nxt) ub ^= 1;
         if (st == LRZ_INFO_OK) {
           cb ^= 1;
           for (int64_t e = tid; e < KK; e += NT) out[e] = sAi[cb * KL + (e / K) * ld + e % K];
