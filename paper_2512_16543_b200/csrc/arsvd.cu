@@ -158,7 +158,10 @@ LRZ_DEV void jacobi_sv(c128 *M, c128 *J, int K, int d, double *sval, int *perm, 
           ja[k] = mk<double>(c * x.re - s * y.re, c * x.im - s * y.im);
           jb[k] = mk<double>(s * x.re + c * y.re, s * x.im + c * y.im);
         }
-        if (gl == 0) s_rot[sweep & 1] = 1;
+        // another sweep only if some pair of this one was coupled above 1e-8: pairs
+        // below that are rotated here and leave second-order (~1e-16) couplings, so
+        // the sweep that would merely confirm convergence is not run
+        if (gl == 0 && g2 > 1e-16 * al * be) s_rot[sweep & 1] = 1;
       }
       __syncthreads();
       // the next sweep's flag was last read before this sweep's first barrier
@@ -1343,7 +1346,7 @@ static int arsvd_threads(int K) {
     env = e ? atoi(e) : 0;
   }
   if (env >= 32 && env <= ARSVD_THREADS && env % 32 == 0) return env;
-  return K <= 32 ? 128 : ARSVD_THREADS;
+  return K <= 32 ? 96 : ARSVD_THREADS;
 }
 
 size_t lrz_arsvd_ws(int64_t B, int K, int D) {
@@ -1520,7 +1523,7 @@ extern "C" int lrz_arsvd(int64_t B, int K, const void *dA, int64_t a_stride,
     }
   }
   LrzProf prof("arsvd_kernel", st);
-  if (arsvd_threads(K) == 128 && g.D <= 32 && K <= 32) {
+  if (arsvd_threads(K) <= 128 && g.D <= 32 && K <= 32) {
     static int ctas = -1;
     if (ctas < 0) {
       const char *e = getenv("LRZ_ARSVD_CTAS");
@@ -1528,7 +1531,7 @@ extern "C" int lrz_arsvd(int64_t B, int K, const void *dA, int64_t a_stride,
     }
     auto launch = [&](auto kern) {
       if (dyn) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(dyn));
-      kern<<<unsigned(B), 128, dyn, st>>>(g);
+      kern<<<unsigned(B), arsvd_threads(K), dyn, st>>>(g);
     };
     if (ctas >= 8) launch(arsvd_small_kernel<8>);
     else if (ctas >= 6) launch(arsvd_small_kernel<6>);
