@@ -771,7 +771,7 @@ def run_b200(args):
         runs = [
             ("C1_c128", "C1", {}, [spec_eta_default, None], 2),
             ("C2_c128", "C2", {}, [spec_eta_default, None], 3),
-            ("C2_c128_eta0.9", "C2", {}, [0.9], 3),      # chunk 50: cross-chunk pipelining
+            ("C2_c128_eta0.9", "C2", {}, [0.9], 3),      # chunk 100: cross-chunk pipelining
             ("C2_c64", "C2", {"dtype": "c64"}, [spec_eta_default, None], 3),
             ("C3_c64", "C3", {}, [spec_eta_default, None], 1),
             ("C5_c64", "C5", {"dtype": "c64"}, [spec_eta_default, None], 1),
@@ -784,7 +784,8 @@ def run_b200(args):
                              1))
         for lab, name, ov, etas, reps in runs:
             sp = S.CONFIGS[name].with_(**ov)
-            ch_over = 50 if lab == "C2_c128_eta0.9" else None   # walk(c+1) overlaps chain(c)
+            # the next chunk's Grams / screen rounds overlap this chunk's chain
+            ch_over = 100 if lab == "C2_c128_eta0.9" else None
             if args.quick:
                 sp = sp.with_(T=min(sp.T, 2 * CHUNK[name]))
             configs[lab] = run_config(sp, etas, reps, rank, world, dev, one_pass, summarize,

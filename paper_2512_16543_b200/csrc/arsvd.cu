@@ -61,6 +61,7 @@ struct ArsvdArgs {
   // GEMM.  tail[item]: 1 = in the pipeline, 2 = U wanted from the GEMM.
   int phase;
   int smem_ws;  // 1: per-item Q / M / J live in dynamic shared memory (no tail pipeline)
+  int smem_j;   // 1: J and the preconditioned Jacobi's R live in dynamic shared memory
   uint8_t *tail;
   c128 *U, *V;
   double *S;
@@ -368,6 +369,15 @@ LRZ_DEV int64_t arsvd_item(const ArsvdArgs &g, const int64_t item, int64_t cur, 
                       : g.ws + item * (int64_t(2) * D * K + int64_t(D) * D);  // [D][K]
   c128 *M = Q + int64_t(D) * K;                                    // [D][K]
   c128 *J = M + int64_t(D) * K;                                    // [D][D] col-major
+  // K >= 64: the QR-preconditioned Jacobi's d x d operands (rotation matrix J and
+  // the triangular factor) in dynamic shared memory (g.smem_j: 2 D^2 complex) --
+  // every round re-reads the columns the last one wrote, which from global memory
+  // is an L2 round trip per round
+  c128 *Rsm = nullptr;
+  if (g.smem_j) {
+    J = (c128 *)arsvd_dyn_smem;
+    Rsm = J + int64_t(D) * D;
+  }
   c128 *U = g.U + item * int64_t(D) * K;
   c128 *V = g.V + item * int64_t(D) * K;
   double *S = g.S + item * D;
@@ -569,7 +579,7 @@ LRZ_DEV int64_t arsvd_item(const ArsvdArgs &g, const int64_t item, int64_t cur, 
       // QR-preconditioned one-sided Jacobi: M = Q2 R2 (Householder), rotate the
       // d x d R2 (columns of length d instead of K), then M J = Q2 (R2 J).  The
       // rotations and singular values are those of M (M^H M = R2^H R2).
-      c128 *Rb = V, *Ub = U;   // the item's factor outputs as scratch (written below)
+      c128 *Rb = Rsm ? Rsm : V, *Ub = U;   // the item's factor outputs as scratch (written below)
       hh_qr(M, K, d, s_tau, s_ph, rbuf);
       for (int e = tid; e < d * d; e += NT) {
         const int c = e / d, r = e - c * d;
@@ -1408,6 +1418,7 @@ extern "C" int lrz_arsvd(int64_t B, int K, const void *dA, int64_t a_stride,
   g.ydtot = 0;
   g.phase = 0;
   g.smem_ws = 0;
+  g.smem_j = 0;
   g.tail = nullptr;
   g.U = (c128 *)U;
   g.V = (c128 *)V;
@@ -1502,8 +1513,16 @@ extern "C" int lrz_arsvd(int64_t B, int K, const void *dA, int64_t a_stride,
         return rc2;
       g.phase = 2;
       {
+        const size_t dj = size_t(2) * g.D * g.D * sizeof(c128);
+        const bool sj = K >= 64 && dj <= 96 * 1024;
+        if (sj) {
+          g.smem_j = 1;
+          cudaFuncSetAttribute(arsvd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               int(dj));
+        }
         LrzProf prof("arsvd_kernel:tail", st);
-        arsvd_kernel<<<unsigned(B), ARSVD_THREADS, 0, st>>>(g);
+        arsvd_kernel<<<unsigned(B), ARSVD_THREADS, sj ? dj : 0, st>>>(g);
+        g.smem_j = 0;
       }
       if (int rc2 = lrz_launch_status("arsvd_kernel (phase 2)")) return rc2;
       return lrz_arsvd_tail_U(B, K, g.D, w0, w0 + int64_t(g.D) * K, wst, U, g.tail, st);
@@ -1584,6 +1603,7 @@ extern "C" int lrz_arsvd_seq(int64_t B, int T, int K, const void *dA, const doub
   g.ydtot = 0;
   g.phase = 0;
   g.smem_ws = 0;
+  g.smem_j = 0;
   g.tail = nullptr;
   g.U = (c128 *)U;
   g.V = (c128 *)V;
