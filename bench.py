@@ -680,10 +680,19 @@ def run_b200(args):
     roof = dominant(ktab)
     if roof is not None:
         roof["traffic"], roof["traffic_source"] = ncu_traffic(roof["kernel"], spec, B, chunk)
-    # stage split: one more pass with events between the runner's stages
+    # stage split: one more pass with events between the runner's stages; when the
+    # timed passes overlap two streams, the per-kernel table is taken from this
+    # unpipelined pass too (a kernel's event time then excludes the other stream's
+    # kernels it shared the SMs with); the dominant kernel's `roofline` stays the
+    # timed region's measurement
     prof = []
+    if pipelined:
+        ops.prof_enable(True, dev)
     one_pass(spec, eta, H_chunks, streams, noise, chunk, prof=prof)
     torch.cuda.synchronize(dev)
+    if pipelined:
+        ktab = roofline_table(ops.prof_collect(dev), spec, 1, B * T, summ, Dtot, D)
+        ops.prof_enable(False, dev)
     stages = {}
     for name, a, b_ in prof:
         stages[name] = stages.get(name, 0.0) + a.elapsed_time(b_)
@@ -835,6 +844,9 @@ def run_b200(args):
                              "gpu_launches": launches_full},
             "roofline": roof,
             "kernels": ktab,
+            "kernels_timing": ("CUDA events per launch, one unpipelined pass (the timed passes "
+                               "overlap two streams); `roofline` is the timed region's") if pipelined
+                              else "CUDA events per launch over the timed passes",
             "stages_ms_per_step": stages,
             "peaks_measured": peaks,
             "cpu_baseline": cpu,

@@ -52,7 +52,7 @@ extern "C" size_t lrz_workspace_bytes(int op, int dtype, int64_t B, int K, int N
     case LRZ_WS_INVERSE:
       // per-item redo flags of the fast paths (+ the blocked GJ buffers, K > 64)
       return ((size_t(B) + 255) & ~size_t(255)) +
-             ((K > 64 && K <= 256 && K % 32 == 0) ? lrz_inverse_blocked_ws(B, K) : 0);
+             ((K >= 64 && K <= 256 && K % 32 == 0) ? lrz_inverse_blocked_ws(B, K) : 0);
     case LRZ_WS_ARSVD:
       return lrz_arsvd_ws_total(B, K, d_max);
     case LRZ_WS_WOODBURY:

@@ -1290,6 +1290,16 @@ int lrz_inverse_blocked(int64_t B, int K, const void *A, int64_t a_stride, void 
                         int64_t ai_stride, int32_t *info, double limit, const uint8_t *mask,
                         uint8_t *redo, void *ws, cudaStream_t s);
 
+// smallest K the blocked DMMA Gauss-Jordan takes (LRZ_INV_BLOCKED_MIN overrides)
+static int inv_blocked_min() {
+  static int v = -1;
+  if (v < 0) {
+    const char *e = getenv("LRZ_INV_BLOCKED_MIN");
+    v = e ? atoi(e) : INV_SMEM_KMAX;  // K = 64: 7.9 -> 5.9 ms per 12,800 items (C3)
+  }
+  return v;
+}
+
 extern "C" int lrz_herm_inverse(int64_t B, int K, const void *A, int64_t a_stride,
                                 void *A_inv, int64_t ai_stride, int32_t *info, double cond_limit,
                                 const uint8_t *item_mask, void *workspace, void *stream) {
@@ -1315,7 +1325,7 @@ extern "C" int lrz_herm_inverse(int64_t B, int K, const void *A, int64_t a_strid
           B, K, (const c128 *)A, a_stride, (c128 *)A_inv, ai_stride, info, cond_limit,
           item_mask, redo);
     mask = redo;
-  } else if (K > INV_SMEM_KMAX && K <= 256 && K % 32 == 0 && workspace && lrz_use_dmma()) {
+  } else if (K >= inv_blocked_min() && K <= 256 && K % 32 == 0 && workspace && lrz_use_dmma()) {
     // blocked Gauss-Jordan with the rank-32 updates on DMMA (inverse_blocked.cu);
     // flagged items (non-PD pivots, guard bound exceeded) go to the CTA kernel
     uint8_t *redo = (uint8_t *)workspace;

@@ -18,24 +18,26 @@ spec = S.CONFIGS[name].with_(dtype=dt)
 if len(sys.argv) > 4:
     spec = spec.with_(B=int(sys.argv[4]))
 nch = int(sys.argv[5]) if len(sys.argv) > 5 else 3
+conv = len(sys.argv) > 6 and sys.argv[6] == "conv"
 dev = torch.device("cuda", 0)
 trials = list(range(spec.B))
 chans = S.DeviceChannels(spec, trials, dev)
 tdt = torch.complex64 if dt == "c64" else torch.complex128
 noise = torch.full((spec.B, spec.K), spec.noise_var, dtype=torch.float64, device=dev)
-cfg = TrajectoryConfig(alpha=spec.alpha, eta=spec.eta, k_init=spec.k_init, p=spec.p,
+cfg = TrajectoryConfig(alpha=spec.alpha, eta=None if conv else spec.eta, k_init=spec.k_init, p=spec.p,
                        i_max=spec.i_max)
 rn = TrajectoryRunner(spec.B, spec.K, spec.N, tdt, cfg, dev)
 st = DeviceOmegaStreams.for_method(spec.seed, spec.eta, trials, dev)
 for c in range(nch):
     H = chans.generate(c * chunk, (c + 1) * chunk)
-    om = st.window(chunk * rn.normals_per_step_max())
+    om = None if conv else st.window(chunk * rn.normals_per_step_max())
     if c == 1:
         torch.cuda.synchronize()
         ops.prof_enable(True, dev)
         rn.prof = []
     r = rn.run_chunk(H, noise, om)
-    st.advance(r.consumed)
+    if not conv:
+        st.advance(r.consumed)
     del H
 torch.cuda.synchronize()
 k = ops.prof_collect(dev)
