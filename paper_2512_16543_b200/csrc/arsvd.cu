@@ -1521,7 +1521,21 @@ extern "C" int lrz_arsvd(int64_t B, int K, const void *dA, int64_t a_stride,
                                int(dj));
         }
         LrzProf prof("arsvd_kernel:tail", st);
-        arsvd_kernel<<<unsigned(B), ARSVD_THREADS, sj ? dj : 0, st>>>(g);
+        static int tail_small = -1;
+        if (tail_small < 0) {
+          const char *e = getenv("LRZ_ARSVD_TAIL_SMALL");
+          tail_small = e ? atoi(e) : 96;
+        }
+        if (tail_small && g.D <= 32) {
+          // narrow items, more of them per SM (the d x d Jacobi is latency bound):
+          // C3 (K 64, d 21) 8.5 -> 6.5 ms per 12,800 items at 96 threads
+          if (sj)
+            cudaFuncSetAttribute(arsvd_small_kernel<6>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, int(dj));
+          arsvd_small_kernel<6><<<unsigned(B), tail_small, sj ? dj : 0, st>>>(g);
+        } else {  // (d = 37 at C5: 1280 items, 128-192 thread items measured no faster)
+          arsvd_kernel<<<unsigned(B), ARSVD_THREADS, sj ? dj : 0, st>>>(g);
+        }
         g.smem_j = 0;
       }
       if (int rc2 = lrz_launch_status("arsvd_kernel (phase 2)")) return rc2;

@@ -631,15 +631,37 @@ LRZ_DEV int cta_woodbury_dmma(int K, int r, const c128 *__restrict__ Ai, c128 *A
 // instead of one per dependent product; the arithmetic and its order are the
 // global-memory path's, so the results are bit-identical.
 constexpr int CH_PLAN_BLK = 1024;  // plan entries staged per block of steps
-__host__ __device__ inline bool chain_resident(int K, int D) { return K <= 32 && D <= 32; }
-__host__ __device__ inline size_t chain_base_smem(int K, int D) {
-  return (InvSmem::bytes(K, D, K <= INV_SMEM_KMAX) + wb_aux_smem(D) + 15) & ~size_t(15);
+// Resident layouts.  K <= 32: A^-1 double buffered, A resident, (U, V) double
+// buffered.  32 < K <= 64 (DMMA step only): one A^-1 buffer updated in place,
+// A stays in global memory (its update is off the critical path), the fallback
+// inverse factorises in place in global memory, (U, V) double buffered when
+// that still fits the SM's shared memory.
+struct ChainPlan {
+  int aibufs, uvbufs;
+  bool a_res, matrix, ok;
+  size_t base, bytes;
+};
+constexpr size_t CHAIN_SMEM_MAX = 227 * 1024;
+__host__ __device__ inline ChainPlan chain_plan(int K, int D) {
+  ChainPlan p{};
+  p.ok = K <= 64 && D <= 32;
+  if (!p.ok) return p;
+  const bool small = K <= 32;
+  p.aibufs = small ? 2 : 1;
+  p.a_res = small;
+  p.matrix = small;
+  p.base = (InvSmem::bytes(K, D, p.matrix) + wb_aux_smem(D) + 15) & ~size_t(15);
+  const size_t ld = size_t(K) + 1;
+  auto total = [&](int uv) {
+    return p.base + (p.aibufs * size_t(K) * ld + (p.a_res ? size_t(K) * K : 0) +
+                     (2 * uv + 3) * ld * D) * sizeof(c128);
+  };
+  p.uvbufs = total(2) <= CHAIN_SMEM_MAX ? 2 : 1;
+  p.bytes = total(p.uvbufs);
+  p.ok = p.bytes <= CHAIN_SMEM_MAX;
+  return p;
 }
-__host__ __device__ inline size_t chain_resident_smem(int K, int D) {
-  // A^-1 x 2 and (U, V) x 2 (the next step's factors are prefetched), A^-1 U, T,
-  // V^H A^-1 at stride K + 1; A at stride K
-  return (2 * size_t(K) * (K + 1) + size_t(K) * K + 7 * size_t(K + 1) * D) * sizeof(c128);
-}
+__host__ __device__ inline bool chain_resident(int K, int D) { return chain_plan(K, D).ok; }
 
 LRZ_DEV void chain_cp16(void *smem, const void *gmem) {
   const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
@@ -662,18 +684,21 @@ __global__ void __launch_bounds__(INV_THREADS)
   const int tid = threadIdx.x, NT = blockDim.x;
   c128 *M;
   WbScratch sc;
-  sc.inv = carve_inv(smem, n, &M, K, K <= INV_SMEM_KMAX);
   const bool res = resident != 0;
   const bool dmma_step = resident == 2;  // the step's products on the FP64 tensor pipe
+  const ChainPlan cp = res ? chain_plan(K, D) : ChainPlan{};
+  const bool want_m = res ? cp.matrix : K <= INV_SMEM_KMAX;
+  sc.inv = carve_inv(smem, n, &M, K, want_m);
   c128 *sAi = nullptr, *sA = nullptr, *sU = nullptr, *sV = nullptr;
   const int ld = K + 1;                   // resident stride (bank spread)
-  const int64_t KL = int64_t(K) * ld;     // one resident A^-1 buffer
+  // one resident A^-1 buffer; 0 when the single buffer is updated in place
+  const int64_t KL = (res && cp.aibufs == 2) ? int64_t(K) * ld : 0;
   if (res) {
-    sAi = (c128 *)(smem + chain_base_smem(K, D));  // [2][K][ld]
-    sA = sAi + 2 * KL;                             // [K][K]
-    sU = sA + KK;                                  // [2][U | V][D][ld]
+    sAi = (c128 *)(smem + cp.base);                // [aibufs][K][ld]
+    sA = sAi + cp.aibufs * int64_t(K) * ld;        // [K][K] when A is resident
+    sU = sA + (cp.a_res ? KK : 0);                 // [uvbufs][U | V][D][ld]
     sV = sU + int64_t(ld) * D;
-    carve_wb(sc, smem + InvSmem::bytes(K, D, K <= INV_SMEM_KMAX), sU + 4 * int64_t(ld) * D, ld,
+    carve_wb(sc, smem + InvSmem::bytes(K, D, want_m), sU + 2 * cp.uvbufs * int64_t(ld) * D, ld,
              D);
   } else {
     carve_wb(sc, smem + InvSmem::bytes(K, D, K <= INV_SMEM_KMAX), ws + b * wb_ws_elems(K, D),
@@ -685,7 +710,9 @@ __global__ void __launch_bounds__(INV_THREADS)
   bool uv_ready = false; // its factors were requested by the previous step
   // resident tiles are filled lazily (a chunk of full inversions never reads them)
   bool have_ai = false, have_a = false;
-  c128 *Acur = res ? (Ast ? sA : nullptr) : Ast;  // where the A state lives
+  // where the A state lives (resident only for K <= 32)
+  const bool a_res = res && cp.a_res;
+  c128 *Acur = a_res ? (Ast ? sA : nullptr) : Ast;
   // the trial's plan row is staged in shared memory block by block (with one
   // entry of lookahead): a chunk of full inversions then costs no dependent
   // global load per step
@@ -704,7 +731,7 @@ __global__ void __launch_bounds__(INV_THREADS)
     bool reload = false;  // resident: A^-1 of this step is in `out` (global)
     if (res && pl != 0 && !have_ai) {  // A^-1 of the previous step, from global
       for (int64_t e = tid; e < KK; e += NT) sAi[cb * KL + (e / K) * ld + e % K] = prev[e];
-      if (Ast && !have_a)
+      if (a_res && Ast && !have_a)
         for (int64_t e = tid; e < KK; e += NT) sA[e] = Ast[e];
       have_ai = true;
       have_a = true;
@@ -716,7 +743,7 @@ __global__ void __launch_bounds__(INV_THREADS)
         // this step's factors (unless the previous step prefetched them), then the
         // next Woodbury step's into the other buffer pair: its load latency
         // overlaps this step's arithmetic
-        const int64_t UV2 = 2 * int64_t(ld) * D;
+        const int64_t UV2 = cp.uvbufs == 2 ? 2 * int64_t(ld) * D : 0;
         auto fetch = [&](int64_t bt2, int buf) {
           const int rk = r[bt2] * K;
           const c128 *Ug = U + bt2 * int64_t(D) * K, *Vg = V + bt2 * int64_t(D) * K;
@@ -729,7 +756,7 @@ __global__ void __launch_bounds__(INV_THREADS)
           asm volatile("cp.async.commit_group;\n" ::);
         };
         if (!uv_ready) fetch(bt, ub);
-        const bool nxt = t + 1 < T && s_plan[t % CH_PLAN_BLK + 1] == 1;
+        const bool nxt = cp.uvbufs == 2 && t + 1 < T && s_plan[t % CH_PLAN_BLK + 1] == 1;
         if (nxt) {
           fetch(bt + 1, ub ^ 1);
           asm volatile("cp.async.wait_group 1;\n" ::);
@@ -787,7 +814,7 @@ __global__ void __launch_bounds__(INV_THREADS)
       if (info && pl != 0) info[bt] = st;
     }
   }
-  if (res && Ast && have_a) {
+  if (a_res && Ast && have_a) {
     for (int64_t e = tid; e < KK; e += NT) Ast[e] = sA[e];
   }
 }
@@ -1262,7 +1289,7 @@ extern "C" int lrz_plan(int64_t n, int K, const uint8_t *is_sketch, const int32_
 size_t lrz_inverse_smem(int K) { return InvSmem::bytes(K, K, K <= INV_SMEM_KMAX); }
 size_t lrz_woodbury_smem(int D) { return InvSmem::bytes(D, D, false) + wb_aux_smem(D); }
 size_t lrz_chain_smem(int K, int D) {
-  return chain_resident(K, D) ? chain_base_smem(K, D) + chain_resident_smem(K, D)
+  return chain_resident(K, D) ? chain_plan(K, D).bytes
                               : InvSmem::bytes(K, D, K <= INV_SMEM_KMAX) + wb_aux_smem(D);
 }
 size_t lrz_wb_ws(int64_t B, int K, int D) {
@@ -1416,7 +1443,10 @@ extern "C" int lrz_chain(int64_t B, int T, int K, int d_max, const uint8_t *plan
     const char *e = getenv("LRZ_CHAIN_RESIDENT");
     simt = (e && e[0] == '1') ? 1 : 0;
   }
-  const int resident = (mode && chain_resident(K, d_max)) ? (simt || !lrz_use_dmma() ? 1 : 2) : 0;
+  // (K > 32 is resident only with the DMMA step, which updates A^-1 in place)
+  const bool dm = !simt && lrz_use_dmma();
+  const int resident =
+      (mode && chain_resident(K, d_max) && (K <= 32 || dm)) ? (dm ? 2 : 1) : 0;
   const size_t sm = resident ? lrz_chain_smem(K, d_max)
                              : InvSmem::bytes(K, d_max, K <= INV_SMEM_KMAX) + wb_aux_smem(d_max);
   if (set_smem((const void *)chain_kernel, sm)) return LRZ_ELAUNCH;

@@ -351,9 +351,10 @@ extern "C" int lrz_trajectory(int dtype, int64_t B, int T, int K, int N, const v
   traj_fullmask_kernel<<<unsigned((BT + 255) / 256), 256, 0, s>>>(BT, plan, is_sketch);
   if ((rc = lrz_herm_inverse(BT, K, G, KK, Aseq, KK, info, 1e14, is_sketch, ws_inv, stream)))
     return rc;
-  // 6. the Woodbury chain per trial (lowrank.py:182-227; step-parallel for K > 32)
+  // 6. the Woodbury chain per trial (lowrank.py:182-227; step-parallel for K > 64,
+  //    resident per-trial CTAs up to K = 64)
   if (cfg) {
-    rc = K > 32 ? lrz_chain_steps(B, T, K, D, plan, G, A_inv_state, Aseq, A_state, U, V, S,
+    rc = K > 64 ? lrz_chain_steps(B, T, K, D, plan, G, A_inv_state, Aseq, A_state, U, V, S,
                                   k_est, method, info, ws_ch, stream)
                 : lrz_chain(B, T, K, D, plan, G, A_inv_state, Aseq, A_state, U, V, S, k_est,
                             method, info, ws_ch, stream);

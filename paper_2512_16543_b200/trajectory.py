@@ -229,11 +229,11 @@ class TrajectoryRunner:
         # 6. sequential Woodbury recurrence per trial
         method = torch.zeros(B, T, dtype=torch.uint8, device=dev)
         e0 = self._ev()
-        # large K: the step-parallel chain (products batched over trials) when there
-        # are dispatcher steps (measured slower at K = 32: launch bound); otherwise
-        # one CTA per trial
+        # K > 64: the step-parallel chain (products batched over trials) when there are
+        # dispatcher steps; up to K = 64 one CTA per trial with the trial's A^-1
+        # resident in shared memory (the step's products on DMMA)
         ops.chain(plan, G, self.A_inv, A_inv_seq, self.A if c.maintain_A else None, U, V, S,
-                  k_est, method, info, steps=(res is not None and K > 32))
+                  k_est, method, info, steps=(res is not None and K > 64))
         self._stage("chain", e0)
         # 7. precoder and rate
         e0 = self._ev()
