@@ -991,7 +991,9 @@ __global__ void __launch_bounds__(128, 4) arsvd_screen_kernel(ArsvdArgs g, int64
     }
     const double kap2 = ok ? (lmax / lmin) * (lmax / lmin) : 1e300;
     // CholeskyQR error bound on the captured energy (relative)
-    const double tol = 64.0 * d * EPS64 * kap2 + 1e-12;
+    // (kap2 comes from diag(L), a lower bound on cond(Y)^2: one more factor d covers
+    // the usual gap between the diagonal ratio and cond(L))
+    const double tol = 64.0 * d * d * EPS64 * kap2 + 1e-12;
     if (!ok || kap2 > 1e8) {
       if (lane == 0) {
         resume[item] = it;
@@ -1313,7 +1315,7 @@ __global__ void __launch_bounds__(32)
       double loc = 0.0;
       for (int k = lane; k < K; k += 32) loc += scr_xrow_d(d, Ws + k * WK_LD, L, LDL, nullptr);
       const double mf = warp_sum(loc);
-      const double tol = 64.0 * d * EPS64 * kap2 + 1e-12;
+      const double tol = 64.0 * d * d * EPS64 * kap2 + 1e-12;
       used += int64_t(2) * K * d;
       if (mf < target * (1.0 - tol)) {  // certainly no hit: next, wider sketch
         k0 *= 2;
@@ -1503,7 +1505,15 @@ extern "C" int lrz_arsvd(int64_t B, int K, const void *dA, int64_t a_stride,
       cudaMemsetAsync(g.tail, 0, size_t(B), st);
       {
         LrzProf prof("arsvd_kernel", st);
-        arsvd_kernel<<<unsigned(B), ARSVD_THREADS, 0, st>>>(g);
+        static int p1_small = -1;
+        if (p1_small < 0) {
+          const char *e = getenv("LRZ_ARSVD_P1_SMALL");
+          p1_small = e ? atoi(e) : 128;  // d <= 32: C3 2.80 -> 2.45 ms, C4 7.98 -> 7.47 ms
+        }
+        if (p1_small && g.D <= 32)
+          arsvd_small_kernel<6><<<unsigned(B), p1_small, 0, st>>>(g);
+        else
+          arsvd_kernel<<<unsigned(B), ARSVD_THREADS, 0, st>>>(g);
       }
       if (int rc2 = lrz_launch_status("arsvd_kernel (phase 1)")) return rc2;
       const int64_t wst = int64_t(2) * g.D * K + int64_t(g.D) * g.D;

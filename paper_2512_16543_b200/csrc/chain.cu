@@ -992,7 +992,8 @@ __global__ void __launch_bounds__(256)
         // U S (rows) and V (cols): A += (U S) V^H (lowrank.py:220)
         Ts[ty][tx] = (j < rr && row < K) ? cscale(Ub[int64_t(j) * K + row], Sb[j])
                                         : czero<double>();
-        Ws[ty][tx] = (j < D && col < K) ? Vb[int64_t(j) * K + col] : czero<double>();
+        // rows j >= rr of V were never written by arsvd: 0 * NaN must not reach A
+        Ws[ty][tx] = (j < rr && col < K) ? Vb[int64_t(j) * K + col] : czero<double>();
       }
       __syncthreads();
 #pragma unroll
