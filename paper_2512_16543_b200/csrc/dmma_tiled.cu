@@ -28,14 +28,20 @@ struct DtPad {
   static constexpr int X = sizeof(T) == 8 ? 2 : 4;  // row pad (elements) of the X slab
 };
 
-template <typename T>
+// WNS warps along n (x 8 / WNS along j): 4 = the 64 n x 64 j tile, 2 = 32 n x 128 j
+// for products with few output rows (the chain's D x K products, the arSVD tail's
+// M = dA^H Q with NN = d <= 32: a 64-row tile would be one third full).
+template <typename T, int WNS = 4>
 struct DtSmem {
-  static constexpr int XLD = DT_BN + DtPad<T>::X;
-  static constexpr int YLD = DT_BJ + 2;
+  static constexpr int BN = 16 * WNS, BJ = 32 * (8 / WNS);
+  static constexpr int XLD = BN + DtPad<T>::X;
+  static constexpr int YLD = BJ + 2;
   static constexpr size_t xbytes = size_t(DT_KC) * XLD * sizeof(cplx<T>);
   static constexpr size_t ybytes = size_t(DT_KC) * YLD * sizeof(c128);
   static constexpr size_t stage = xbytes + ybytes;
-  static constexpr size_t bytes = stage * DT_ST + 16 * sizeof(double);
+  // the 32 x 128 tile's Y slab is twice as wide: two stages keep two CTAs per SM
+  static constexpr int ST = WNS == 4 ? DT_ST : 2;
+  static constexpr size_t bytes = stage * ST + 16 * sizeof(double);
 };
 
 LRZ_DEV void cpa(void *smem, const void *gmem, int bytes, bool pred) {
@@ -77,18 +83,19 @@ struct ZgArgs {
   int tiles_n, tiles_j;
 };
 
-template <typename T, bool XT, bool XC, bool YT, bool YC, int MODE>
+template <typename T, bool XT, bool XC, bool YT, bool YC, int MODE, int WNS = 4>
 __global__ void __launch_bounds__(DT_THREADS, 2) zgemm_dmma_kernel(ZgArgs a) {
-  using S = DtSmem<T>;
+  using S = DtSmem<T, WNS>;
+  constexpr int BN = S::BN, BJ = S::BJ, ST = S::ST;
   extern __shared__ __align__(16) unsigned char dt_smem[];
   __shared__ double s_ks[DT_ST][DT_KC];
   const int ntile = a.tiles_n * a.tiles_j;
   const int64_t item = blockIdx.x / ntile;
   if (a.mask && a.mask[item * a.mstride] != a.mval) return;
   const int tile = int(blockIdx.x - item * ntile);
-  const int n0 = (tile / a.tiles_j) * DT_BN, j0 = (tile % a.tiles_j) * DT_BJ;
+  const int n0 = (tile / a.tiles_j) * BN, j0 = (tile % a.tiles_j) * BJ;
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5, g = lane >> 2, t = lane & 3;
-  const int wn = w & 3, wj = w >> 2;
+  const int wn = w % WNS, wj = w / WNS;
   const int NN = a.NN, J = a.J;
   const int Kd = a.kd_item ? min(a.Kd, int(a.kd_item[item * a.kstride])) : a.Kd;
   const cplx<T> *x = reinterpret_cast<const cplx<T> *>(a.X) + item * a.xs;
@@ -105,18 +112,18 @@ __global__ void __launch_bounds__(DT_THREADS, 2) zgemm_dmma_kernel(ZgArgs a) {
     cplx<T> *xsl = xslab(s);
     c128 *ysl = yslab(s);
 #pragma unroll
-    for (int i = 0; i < (DT_KC * DT_BN) / DT_THREADS; ++i) {
+    for (int i = 0; i < (DT_KC * BN) / DT_THREADS; ++i) {
       const int e = tid + i * DT_THREADS;
-      const int r = XT ? e % DT_KC : e / DT_BN, c = XT ? e / DT_KC : e % DT_BN;
+      const int r = XT ? e % DT_KC : e / BN, c = XT ? e / DT_KC : e % BN;
       const int k = k0 + r, n = n0 + c;
       const bool ok = k < Kd && n < NN;
       const int64_t off = XT ? int64_t(n) * a.ldx + k : int64_t(k) * a.ldx + n;
       cpa(xsl + r * S::XLD + c, x + (ok ? off : 0), sizeof(cplx<T>), ok);
     }
 #pragma unroll
-    for (int i = 0; i < (DT_KC * DT_BJ) / DT_THREADS; ++i) {
+    for (int i = 0; i < (DT_KC * BJ) / DT_THREADS; ++i) {
       const int e = tid + i * DT_THREADS;
-      const int r = YT ? e % DT_KC : e / DT_BJ, c = YT ? e / DT_KC : e % DT_BJ;
+      const int r = YT ? e % DT_KC : e / BJ, c = YT ? e / DT_KC : e % BJ;
       const int k = k0 + r, j = j0 + c;
       const bool ok = k < Kd && j < J;
       const int64_t off = YT ? int64_t(j) * a.ldy + k : int64_t(k) * a.ldy + j;
@@ -133,18 +140,18 @@ __global__ void __launch_bounds__(DT_THREADS, 2) zgemm_dmma_kernel(ZgArgs a) {
 
   const int nslab = (Kd + DT_KC - 1) / DT_KC;
 #pragma unroll
-  for (int s = 0; s < DT_ST - 1; ++s) {
+  for (int s = 0; s < ST - 1; ++s) {
     if (s < nslab) load(s, s * DT_KC);
     asm volatile("cp.async.commit_group;\n" ::);
   }
   for (int it = 0; it < nslab; ++it) {
-    asm volatile("cp.async.wait_group %0;\n" ::"n"(DT_ST - 2));
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(ST - 2));
     __syncthreads();
-    const int nxt = it + DT_ST - 1;
-    if (nxt < nslab) load(nxt % DT_ST, nxt * DT_KC);
+    const int nxt = it + ST - 1;
+    if (nxt < nslab) load(nxt % ST, nxt * DT_KC);
     asm volatile("cp.async.commit_group;\n" ::);
-    const cplx<T> *xsl = xslab(it % DT_ST);
-    const c128 *ysl = yslab(it % DT_ST);
+    const cplx<T> *xsl = xslab(it % ST);
+    const c128 *ysl = yslab(it % ST);
 #pragma unroll
     for (int kk = 0; kk < DT_KC; kk += 4) {
       double hr[2], hi[2], br[4], bi[4];
@@ -154,7 +161,7 @@ __global__ void __launch_bounds__(DT_THREADS, 2) zgemm_dmma_kernel(ZgArgs a) {
         hr[nb] = double(v.re);
         hi[nb] = XC ? double(v.im) : -double(v.im);  // the product below conjugates x
       }
-      const double ks = ksc ? s_ks[it % DT_ST][kk + t] : 1.0;
+      const double ks = ksc ? s_ks[it % ST][kk + t] : 1.0;
 #pragma unroll
       for (int jb = 0; jb < 4; ++jb) {
         const c128 v = ysl[(kk + t) * S::YLD + 32 * wj + 8 * jb + g];
@@ -207,21 +214,22 @@ __global__ void __launch_bounds__(DT_THREADS, 2) zgemm_dmma_kernel(ZgArgs a) {
       }
   }
   if (a.parts) {
-    double *red = reinterpret_cast<double *>(dt_smem + S::stage * DT_ST);
+    double *red = reinterpret_cast<double *>(dt_smem + S::stage * ST);
     const double s = block_sum(nrm, red);
     if (tid == 0) a.parts[item * ntile + tile] = s;
   }
 }
 
-template <typename T, bool XT, bool XC, bool YT, bool YC, int MODE>
-static int zgemm_dmma_launch(int64_t B, ZgArgs a, cudaStream_t s, const char *what) {
+template <typename T, bool XT, bool XC, bool YT, bool YC, int MODE, int WNS>
+static int zgemm_dmma_launch_w(int64_t B, ZgArgs a, cudaStream_t s, const char *what) {
   LrzProf prof(what, s);
-  a.tiles_n = (a.NN + DT_BN - 1) / DT_BN;
-  a.tiles_j = (a.J + DT_BJ - 1) / DT_BJ;
-  const size_t sm = DtSmem<T>::bytes;
+  using S = DtSmem<T, WNS>;
+  a.tiles_n = (a.NN + S::BN - 1) / S::BN;
+  a.tiles_j = (a.J + S::BJ - 1) / S::BJ;
+  const size_t sm = S::bytes;
   static bool attr = false;
   if (!attr) {
-    if (cudaFuncSetAttribute(zgemm_dmma_kernel<T, XT, XC, YT, YC, MODE>,
+    if (cudaFuncSetAttribute(zgemm_dmma_kernel<T, XT, XC, YT, YC, MODE, WNS>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)) != cudaSuccess) {
       lrz_set_error("zgemm_dmma_kernel: cannot reserve %zu bytes of shared memory", sm);
       return LRZ_ELAUNCH;
@@ -241,9 +249,22 @@ static int zgemm_dmma_launch(int64_t B, ZgArgs a, cudaStream_t s, const char *wh
     if (a.mask) c.mask = a.mask + b0 * a.mstride;
     if (a.kd_item) c.kd_item = a.kd_item + b0 * a.kstride;
     if (a.kscale) c.kscale = a.kscale + b0 * a.kss;
-    zgemm_dmma_kernel<T, XT, XC, YT, YC, MODE><<<unsigned(bb * nt), DT_THREADS, sm, s>>>(c);
+    zgemm_dmma_kernel<T, XT, XC, YT, YC, MODE, WNS><<<unsigned(bb * nt), DT_THREADS, sm, s>>>(c);
   }
   return lrz_launch_status(what);
+}
+
+// few output rows (NN <= 32) and no norm partials: the 32 n x 128 j tile
+template <typename T, bool XT, bool XC, bool YT, bool YC, int MODE>
+static int zgemm_dmma_launch(int64_t B, ZgArgs a, cudaStream_t s, const char *what) {
+  static int narrow = -1;
+  if (narrow < 0) {
+    const char *e = getenv("LRZ_ZGEMM_NARROW");
+    narrow = e ? atoi(e) : 1;
+  }
+  if (narrow && a.NN <= 32 && !a.parts)
+    return zgemm_dmma_launch_w<T, XT, XC, YT, YC, MODE, 2>(B, a, s, what);
+  return zgemm_dmma_launch_w<T, XT, XC, YT, YC, MODE, 4>(B, a, s, what);
 }
 
 template <typename T>
