@@ -313,100 +313,17 @@ LRZ_DEV void blk_zmma(int ksteps, FA a, FB b, double (&cr)[2], double (&ci)[2]) 
   }
 }
 
-// In-place inverse of the r x r matrix M (row stride ldm, shared memory) by one
-// warp: Gauss-Jordan with partial row pivoting (the algorithm of
-// cta_gauss_jordan: largest |m|^2 in the column, smallest row on ties; the
-// column permutation is undone at the end).  The warp is latency bound, so the
-// pivot search is two integer redux steps on the (ordered) bit pattern of
-// |m|^2 plus a ballot instead of five shuffle rounds, the pivot's reciprocal is
-// conj(p) / |p|^2 with one division, and the rank-1 update runs over all r^2
-// entries spread across the 32 lanes (column k and the scaled row k
-// snapshotted in colbuf / rowbuf), independent iterations the scheduler can
-// overlap.  perm: r ints of scratch.  Returns 0, or 2 on a zero / non-finite
-// pivot; fro2 = ||M^-1||_F^2.  Warp-uniform; all 32 lanes must call.
-LRZ_DEV int warp_gj_pivot(c128 *M, int r, int ldm, int *perm, c128 *colbuf, c128 *rowbuf,
-                          double &fro2) {
-  const int lane = threadIdx.x & 31;
-  const int rr2 = r * r;
-  const float inv_r = 1.0f / float(r);
-  for (int k = 0; k < r; ++k) {
-    // pivot: argmax |M[i][k]|^2 over i >= k (non-negative doubles order like their bits)
-    double mag = 0.0;
-    if (lane >= k && lane < r) mag = cabs2(M[lane * ldm + k]);
-    const unsigned long long bits = (mag == mag) ? (unsigned long long)__double_as_longlong(mag)
-                                                 : 0xFFFFFFFFFFFFFFFFull;  // NaN: fail below
-    const unsigned hi = unsigned(bits >> 32), lo = unsigned(bits);
-    const unsigned mh = __reduce_max_sync(0xffffffffu, hi);
-    const unsigned ml = __reduce_max_sync(0xffffffffu, hi == mh ? lo : 0u);
-    const bool cand = lane >= k && lane < r && hi == mh && lo == ml;
-    const unsigned bal = __ballot_sync(0xffffffffu, cand);
-    if (bal == 0u || (mh == 0u && ml == 0u) || mh >= 0x7FF00000u) return 2;  // zero / inf / NaN
-    const int bi = __ffs(bal) - 1;
-    if (bi != k && lane < r) {
-      const c128 x = M[k * ldm + lane];
-      M[k * ldm + lane] = M[bi * ldm + lane];
-      M[bi * ldm + lane] = x;
-    }
-    if (lane == 0) perm[k] = bi;
-    __syncwarp();
-    const c128 piv = M[k * ldm + k];
-    const double id = 1.0 / cabs2(piv);
-    const c128 pinv = mk<double>(piv.re * id, -piv.im * id);
-    if (!(isfinite(pinv.re) && isfinite(pinv.im))) return 2;
-    if (lane < r) {
-      colbuf[lane] = M[lane * ldm + k];
-      rowbuf[lane] = (lane == k) ? pinv : cmul(M[k * ldm + lane], pinv);
-    }
-    __syncwarp();
-    for (int e = lane; e < rr2; e += 32) {
-      const int i = int((float(e) + 0.5f) * inv_r), j = e - i * r;  // exact: e < 1024
-      const c128 rj = rowbuf[j];
-      c128 m;
-      if (i == k) {
-        m = rj;
-      } else {
-        const c128 c = colbuf[i];
-        if (j == k) {
-          m = cmul(mk<double>(-c.re, -c.im), pinv);
-        } else {
-          m = M[i * ldm + j];
-          m.re = fma(-c.re, rj.re, m.re);
-          m.re = fma(c.im, rj.im, m.re);
-          m.im = fma(-c.re, rj.im, m.im);
-          m.im = fma(-c.im, rj.re, m.im);
-        }
-      }
-      M[i * ldm + j] = m;
-    }
-    __syncwarp();
-  }
-  for (int k = r - 1; k >= 0; --k) {
-    const int p = perm[k];
-    if (p != k && lane < r) {
-      const c128 x = M[lane * ldm + k];
-      M[lane * ldm + k] = M[lane * ldm + p];
-      M[lane * ldm + p] = x;
-    }
-  }
-  __syncwarp();
-  double loc = 0.0;
-  for (int e = lane; e < rr2; e += 32) {
-    const int i = int((float(e) + 0.5f) * inv_r), j = e - i * r;
-    loc += cabs2(M[i * ldm + j]);
-  }
-  fro2 = warp_sum(loc);
-  return 0;
-}
-
-// The same inverse for r <= 16 with the matrix in registers: lane l holds row
-// l / 2, columns 8 (l & 1) .. + 7.  Implicit row pivoting (no swaps: the pivot
+// In-place inverse of the r x r matrix M (r <= 16, row stride ldm, shared memory)
+// by one warp with the matrix in registers: lane l holds row l / 2, columns
+// 8 (l & 1) .. + 7.  Gauss-Jordan with implicit row pivoting (no swaps: the pivot
 // of column k is the largest |m|^2 among the rows not used yet, smallest row on
 // ties; the row and column permutations are applied when the result is written
 // back), the pivot loop fully unrolled so every register index is static, one
 // warp-wide exchange per pivot (the scaled pivot row through rowbuf, the
 // reciprocal and the column-k entries by shuffles).  ~170 instructions per
-// pivot against ~390 of warp_gj_pivot -- the warp is bound by instruction
-// count x latency.  Returns like warp_gj_pivot.
+// pivot against ~390 of a shared-memory warp version -- the warp is bound by
+// instruction count x latency.  Returns 0, or 2 on a zero / non-finite pivot;
+// fro2 = ||M^-1||_F^2.  Warp-uniform; all 32 lanes must call.
 LRZ_DEV int warp_gj_reg16(c128 *M, int r, int ldm, c128 *rowbuf, double &fro2) {
   const int lane = threadIdx.x & 31, row = lane >> 1, half = lane & 1, c0 = 8 * half;
   c128 m[8];
@@ -550,17 +467,19 @@ LRZ_DEV int cta_woodbury_dmma(int K, int r, const c128 *__restrict__ Ai, c128 *A
   __syncthreads();
   // 3. warp 0: aux^-1; the other warps: A += (U S) V^H (overwritten by the
   //    caller's full branch if the step turns out singular)
-  if (wid == 0) {
+  // r <= 16: warp 0 inverts in registers while the other warps update A; wider
+  // aux matrices take the whole CTA (cta_gj_pivot_small: two barriers per pivot,
+  // the rank-1 update spread over all threads), so every warp updates A first
+  const bool wide = r > 16;
+  if (!wide && wid == 0) {
     double fi = 0.0;
-    const int st = r <= 16 ? warp_gj_reg16(sc.auxinv, r, lda, sc.inv.rowbuf, fi)
-                           : warp_gj_pivot(sc.auxinv, r, lda, sc.inv.perm, sc.inv.colbuf,
-                                           sc.inv.rowbuf, fi);
+    const int st = warp_gj_reg16(sc.auxinv, r, lda, sc.inv.rowbuf, fi);
     if (lane == 0) {
       s_st = st;
       s_fi = fi;
     }
   } else if (A) {
-    for (int blk = wid - 1; blk < KB * KB; blk += NW - 1) {
+    for (int blk = wide ? wid : wid - 1; blk < KB * KB; blk += wide ? NW : NW - 1) {
       const int k0 = 8 * (blk / KB), m0 = 8 * (blk % KB);
       double cr[2] = {0.0, 0.0}, ci[2] = {0.0, 0.0};
       blk_zmma(
@@ -581,9 +500,18 @@ LRZ_DEV int cta_woodbury_dmma(int K, int r, const c128 *__restrict__ Ai, c128 *A
     }
   }
   __syncthreads();
-  if (s_st != 0) return LRZ_INFO_SINGULAR_AUX;
+  double fi_all;
+  if (wide) {
+    if (cta_gauss_jordan(sc.auxinv, r, lda, true, sc.inv.colbuf, sc.inv.rowbuf, sc.inv.perm,
+                         sc.inv.red, sc.inv.ired) != 0)
+      return LRZ_INFO_SINGULAR_AUX;
+    fi_all = cta_fro2(sc.auxinv, r, lda, sc.inv.red);
+  } else {
+    if (s_st != 0) return LRZ_INFO_SINGULAR_AUX;
+    fi_all = s_fi;
+  }
   // the 1e12 condition guard (lowrank.py:212-217); sc.aux is free after this
-  if (!cta_cond_ok(fa, s_fi, 1e12, sc.aux, r, lda, sc.inv.red, sc.inv.ired))
+  if (!cta_cond_ok(fa, fi_all, 1e12, sc.aux, r, lda, sc.inv.red, sc.inv.ired))
     return LRZ_INFO_SINGULAR_AUX;
   // 4. T = AiU aux^-1 (K x r)
   for (int blk = wid; blk < KB * RB; blk += NW) {
