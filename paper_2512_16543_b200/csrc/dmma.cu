@@ -106,25 +106,13 @@ __global__ void __launch_bounds__(32 * GD_WARPS, 3)
 // (item, block): 16 8 x 8 tiles, A fragments from the rows of block I, B
 // fragments from the rows of block J, 8 columns of H per step; written with
 // the mirrored upper block.
-template <typename T>
-__global__ void __launch_bounds__(32 * GD_WARPS)
-    gram_dmma_off_kernel(int64_t B, int K, int N, const cplx<T> *__restrict__ H, int64_t hs,
-                         c128 *__restrict__ A, int64_t as, int npair, double alpha,
-                         int diag) {
+// One lower 32 x 32 block (I, J) of the Gram by one warp.  DIAG (I == J): only
+// the 10 of 16 8 x 8 tiles on or below the diagonal are accumulated (the same
+// fragment loads, 40 instead of 64 DMMAs per k-step).
+template <typename T, bool DIAG>
+LRZ_DEV void gram_block32(int K, int N, const cplx<T> *__restrict__ h, c128 *__restrict__ a,
+                          int I, int J, double alpha) {
   const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
-  const int64_t wid = int64_t(blockIdx.x) * GD_WARPS + (threadIdx.x >> 5);
-  if (wid >= B * npair) return;
-  const int64_t item = wid / npair;
-  // pairs (I, J) in row order: J < I, or J <= I with diag (the diagonal blocks
-  // as full 32 x 32 products: for N in the thousands the 16-tile warp streams
-  // H at the DMMA rate, the 10-tile diagonal kernel does not)
-  int p = int(wid - item * npair), I = diag ? 0 : 1;
-  while (p >= I + diag) {
-    p -= I + diag;
-    ++I;
-  }
-  const int J = p;
-  const cplx<T> *h = H + item * hs;
   bool iok[4], jok[4];
   const cplx<T> *hi[4], *hj[4];
 #pragma unroll
@@ -146,7 +134,7 @@ __global__ void __launch_bounds__(32 * GD_WARPS)
       for (int s = 0; s < 2; ++s) {
         const int n = n0 + 4 * s + t;
         vi[b][s] = (iok[b] && n < N) ? ldg_c(hi[b] + n) : czero<double>();
-        vj[b][s] = (jok[b] && n < N) ? ldg_c(hj[b] + n) : czero<double>();
+        vj[b][s] = DIAG ? vi[b][s] : ((jok[b] && n < N) ? ldg_c(hj[b] + n) : czero<double>());
       }
 #pragma unroll
     for (int s = 0; s < 2; ++s)
@@ -155,6 +143,7 @@ __global__ void __launch_bounds__(32 * GD_WARPS)
         const double ar = vi[ib][s].re, ai = vi[ib][s].im, nar = -ar;
 #pragma unroll
         for (int jb = 0; jb < 4; ++jb) {
+          if (DIAG && jb > ib) continue;  // strictly upper tile of a diagonal block
           const double br = vj[jb][s].re, bi = vj[jb][s].im;
           dmma(cr[4 * ib + jb], ar, br);
           dmma(cr[4 * ib + jb], ai, bi);
@@ -163,11 +152,11 @@ __global__ void __launch_bounds__(32 * GD_WARPS)
         }
       }
   }
-  c128 *a = A + item * as;
 #pragma unroll
   for (int ib = 0; ib < 4; ++ib)
 #pragma unroll
-    for (int jb = 0; jb < 4; ++jb)
+    for (int jb = 0; jb < 4; ++jb) {
+      if (DIAG && jb > ib) continue;
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
         const int row = 32 * I + 8 * ib + g, col = 32 * J + 8 * jb + 2 * t + e;
@@ -183,6 +172,39 @@ __global__ void __launch_bounds__(32 * GD_WARPS)
           }
         }
       }
+    }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(32 * GD_WARPS)
+    gram_dmma_off_kernel(int64_t B, int K, int N, const cplx<T> *__restrict__ H, int64_t hs,
+                         c128 *__restrict__ A, int64_t as, int npair, double alpha,
+                         int diag) {
+  const int64_t wid = int64_t(blockIdx.x) * GD_WARPS + (threadIdx.x >> 5);
+  if (wid >= B * npair) return;
+  const int64_t item = wid / npair;
+  // pairs (I, J) in row order: J < I, or J <= I with diag
+  int p = int(wid - item * npair), I = diag ? 0 : 1;
+  while (p >= I + diag) {
+    p -= I + diag;
+    ++I;
+  }
+  const int J = p;
+  gram_block32<T, false>(K, N, H + item * hs, A + item * as, I, J, alpha);
+}
+
+// The diagonal 32 x 32 blocks (I, I), 10 of their 16 tiles each, one warp per
+// (item, block).  A kernel of its own: sharing one with the full-block warps
+// costs the complex64 instantiation 30 registers and ~6 % of its rate.
+template <typename T>
+__global__ void __launch_bounds__(32 * GD_WARPS)
+    gram_dmma_diag_kernel(int64_t B, int K, int N, const cplx<T> *__restrict__ H, int64_t hs,
+                          c128 *__restrict__ A, int64_t as, int nb, double alpha) {
+  const int64_t wid = int64_t(blockIdx.x) * GD_WARPS + (threadIdx.x >> 5);
+  if (wid >= B * nb) return;
+  const int64_t item = wid / nb;
+  const int I = int(wid - item * nb);
+  gram_block32<T, true>(K, N, H + item * hs, A + item * as, I, I, alpha);
 }
 
 // ---------------------------------------------------------------------------
@@ -373,7 +395,21 @@ static void gram_dmma_launch(int64_t B, int K, int N, const cplx<T> *h, int64_t 
   const int nb = (K + 31) / 32;
   if (nb > 1) {
     // K > 32: every lower 32 x 32 block (diagonal ones included) by the 16-tile kernel
+    static int split = -1;  // LRZ_GRAM_DIAG=0: diagonal blocks as full blocks (one launch)
+    if (split < 0) {
+      const char *e = getenv("LRZ_GRAM_DIAG");
+      split = e ? atoi(e) : 1;
+    }
     LrzProf prof_o("gram_dmma_off_kernel", s);
+    if (split) {
+      // the diagonal blocks first: they are the shorter warps (10 of 16 tiles)
+      const unsigned ndg = unsigned((B * nb + GD_WARPS - 1) / GD_WARPS);
+      gram_dmma_diag_kernel<T><<<ndg, 32 * GD_WARPS, 0, s>>>(B, K, N, h, hs, a, as, nb, alpha);
+      const int np = nb * (nb - 1) / 2;
+      const unsigned no = unsigned((B * np + GD_WARPS - 1) / GD_WARPS);
+      gram_dmma_off_kernel<T><<<no, 32 * GD_WARPS, 0, s>>>(B, K, N, h, hs, a, as, np, alpha, 0);
+      return;
+    }
     const int np = nb * (nb + 1) / 2;
     const unsigned no = unsigned((B * np + GD_WARPS - 1) / GD_WARPS);
     gram_dmma_off_kernel<T><<<no, 32 * GD_WARPS, 0, s>>>(B, K, N, h, hs, a, as, np, alpha, 1);
