@@ -392,8 +392,10 @@ def ncu_traffic(kernel: str, spec, B: int, chunk: int):
     keys = {
         "dmma_hn_kernel:W": f"void lrz::zgemm_dmma_kernel<{T}, 0, 1, 0, 0, 0> grid"
                             f"({items * -(-N // 64) * -(-K // 64)},1,1)",
+        "w_dmma_direct_kernel": f"void lrz::w_dmma_direct_kernel<{T}, 1> grid"
+                                f"({items * -(-N // 32) * -(-(-(-K // 32)) // 4)},1,1)",
         "gram_dmma_off_kernel": f"void lrz::gram_dmma_off_kernel<{T}> grid"
-                                f"({-(-items * (K // 32) * (K // 32 + 1) // 2 // 4)},1,1)",
+                                f"({-(-items * (K // 32) * (K // 32 - 1) // 2 // 4)},1,1)",
     }
     k = keys.get(kernel)
     if k is None or k not in tab:
@@ -411,7 +413,7 @@ def kernel_model(name: str, spec, items: int, D: int, Dtot: int, r_mean: float,
     K, N = spec.K, spec.N
     c = 8 if spec.dtype == "c64" else 16
     nb = (K + 31) // 32
-    if name == "dmma_hn_kernel:W":                 # W = H^H A^-1 + ||W||^2
+    if name in ("dmma_hn_kernel:W", "w_dmma_direct_kernel"):   # W = H^H A^-1 + ||W||^2
         return (8 * K * K * N + 8 * N * K) * items, (K * N * c + K * K * 16 + N * K * c) * items
     if name == "tc_w_kernel":                      # W on tcgen05 (3xTF32, complex64)
         return (8 * K * K * N + 8 * N * K) * items, (K * N * c + N * K * c + 8 * (2 * K) ** 2) * items

@@ -208,6 +208,89 @@ __global__ void __launch_bounds__(32 * GD_WARPS)
 }
 
 // ---------------------------------------------------------------------------
+// K6 for K > 32, complex128: W = H^H A^-1 (N x K, precoding.py:47) with the Gram
+// kernel's structure -- one warp per 32 n x 32 j output block, 16 complex 8 x 8
+// accumulator tiles, both fragments straight from global memory: lane (g, t)
+// reads conj(H)[4c + t][n0 + 8b + g] and A^-1[4c + t][j0 + 8b + g], a warp load
+// is four 128-byte row segments.  64 DMMAs per 8 fragment loads against the
+// tiled kernel's 32 per 6 (shared-memory slabs, 16 x 32 warp tiles).  The four
+// warps of a CTA share the n block (their H loads hit L1) and take four j
+// blocks.  ||W||_F^2 goes out as one partial per warp, summed in a fixed order.
+// ---------------------------------------------------------------------------
+template <typename T, int NBW>  // NBW n blocks per CTA (x 4 j blocks): 32 NBW x 128 of W
+__global__ void __launch_bounds__(128 * NBW)
+    w_dmma_direct_kernel(int64_t B, int K, int N, const cplx<T> *__restrict__ H, int64_t hs,
+                         const c128 *__restrict__ Ainv, int64_t ais, cplx<T> *__restrict__ W,
+                         int64_t wstr, double *__restrict__ parts, int nnb, int njb, int njq) {
+  const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3, w = threadIdx.x >> 5;
+  const int nng = (nnb + NBW - 1) / NBW;
+  const int64_t per = int64_t(nng) * njq;
+  const int64_t item = blockIdx.x / per;
+  const int rem = int(blockIdx.x - item * per);
+  const int nb = NBW * (rem / njq) + (w >> 2), jb0 = 4 * (rem % njq) + (w & 3);
+  if (jb0 >= njb || nb >= nnb) return;
+  const int n0 = 32 * nb, j0 = 32 * jb0;
+  const cplx<T> *h = H + item * hs;
+  const c128 *y = Ainv + item * ais;
+  bool nok[4], jok[4];
+#pragma unroll
+  for (int b = 0; b < 4; ++b) {
+    nok[b] = n0 + 8 * b + g < N;
+    jok[b] = j0 + 8 * b + g < K;
+  }
+  double cr[16][2], ci[16][2];
+#pragma unroll
+  for (int x = 0; x < 16; ++x) cr[x][0] = cr[x][1] = ci[x][0] = ci[x][1] = 0.0;
+  for (int k0 = 0; k0 < K; k0 += 8) {
+    c128 vx[4][2], vy[4][2];
+#pragma unroll
+    for (int s = 0; s < 2; ++s) {
+      const int k = k0 + 4 * s + t;
+      const bool kok = k < K;
+      const cplx<T> *hr = h + int64_t(kok ? k : 0) * N + n0 + g;
+      const c128 *yr = y + int64_t(kok ? k : 0) * K + j0 + g;
+#pragma unroll
+      for (int b = 0; b < 4; ++b) {
+        vx[b][s] = (kok && nok[b]) ? ldg_c(hr + 8 * b) : czero<double>();
+        vy[b][s] = (kok && jok[b]) ? ldg_c(yr + 8 * b) : czero<double>();
+      }
+    }
+#pragma unroll
+    for (int s = 0; s < 2; ++s)
+#pragma unroll
+      for (int ib = 0; ib < 4; ++ib) {
+        const double xr = vx[ib][s].re, xi = vx[ib][s].im, nxi = -xi;
+#pragma unroll
+        for (int jb = 0; jb < 4; ++jb) {
+          // conj(x) y = (xr yr + xi yi) + i (xr yi - xi yr)
+          const double yr_ = vy[jb][s].re, yi_ = vy[jb][s].im;
+          dmma(cr[4 * ib + jb], xr, yr_);
+          dmma(cr[4 * ib + jb], xi, yi_);
+          dmma(ci[4 * ib + jb], xr, yi_);
+          dmma(ci[4 * ib + jb], nxi, yr_);
+        }
+      }
+  }
+  cplx<T> *o = W + item * wstr;
+  double nrm = 0.0;
+#pragma unroll
+  for (int ib = 0; ib < 4; ++ib)
+#pragma unroll
+    for (int jb = 0; jb < 4; ++jb)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int n = n0 + 8 * ib + g, j = j0 + 8 * jb + 2 * t + e;
+        if (n < N && j < K) {
+          const cplx<T> z = mk<T>(T(cr[4 * ib + jb][e]), T(ci[4 * ib + jb][e]));
+          o[int64_t(n) * K + j] = z;
+          nrm += double(z.re) * double(z.re) + double(z.im) * double(z.im);
+        }
+      }
+  nrm = warp_sum(nrm);
+  if (parts && lane == 0) parts[item * (int64_t(nnb) * njb) + int64_t(nb) * njb + jb0] = nrm;
+}
+
+// ---------------------------------------------------------------------------
 // K6 fused, K <= 32, one item per CTA of 4 warps:
 //   W = H^H A^-1 (N x K, unscaled, precoding.py:47), ||W||_F^2,
 //   C = G A^-1 - alpha A^-1 = H W for F_RF = I, s = sqrt(P_t)/||W||,
@@ -451,4 +534,38 @@ int lrz_precode_dmma32(int dtype, int64_t B, int K, int N, const void *H, int64_
         int64_t(K) * K, alpha, P_t, noise, noise_div, (c128 *)W, wst, scale, rates, sinr,
         sum_rate, info);
   return lrz_launch_status("precode_dmma32_kernel");
+}
+
+// W = H^H A^-1 by w_dmma_direct_kernel; parts (nullable): ceil(N/32) ceil(K/32)
+// norm partials per item.
+int lrz_w_dmma_direct(int dtype, int64_t B, int K, int N, const void *H, int64_t hs,
+                      const void *A_inv, int64_t ais, void *W, int64_t wstr, double *parts,
+                      cudaStream_t s) {
+  const int nnb = (N + 31) / 32, njb = (K + 31) / 32, njq = (njb + 3) / 4;
+  static int nbw = -1;
+  if (nbw < 0) {
+    const char *e = getenv("LRZ_W_NBW");
+    nbw = e ? atoi(e) : 1;
+  }
+  const int NB_ = nbw == 2 ? 2 : 1;
+  const int64_t per = int64_t((nnb + NB_ - 1) / NB_) * njq;
+  const int64_t chunk = (int64_t(1) << 30) / per;
+  LrzProf prof("w_dmma_direct_kernel", s);
+  for (int64_t b0 = 0; b0 < B; b0 += chunk) {
+    const int64_t bb = B - b0 < chunk ? B - b0 : chunk;
+    double *pp = parts ? parts + b0 * int64_t(nnb) * njb : nullptr;
+    auto go = [&](auto kern, auto hp, auto wp) {
+      kern<<<unsigned(bb * per), 128 * NB_, 0, s>>>(bb, K, N, hp + b0 * hs, hs,
+                                                    (const c128 *)A_inv + b0 * ais, ais,
+                                                    wp + b0 * wstr, wstr, pp, nnb, njb, njq);
+    };
+    if (dtype == LRZ_C64) {
+      if (NB_ == 2) go(w_dmma_direct_kernel<float, 2>, (const c64 *)H, (c64 *)W);
+      else go(w_dmma_direct_kernel<float, 1>, (const c64 *)H, (c64 *)W);
+    } else {
+      if (NB_ == 2) go(w_dmma_direct_kernel<double, 2>, (const c128 *)H, (c128 *)W);
+      else go(w_dmma_direct_kernel<double, 1>, (const c128 *)H, (c128 *)W);
+    }
+  }
+  return lrz_launch_status("w_dmma_direct_kernel");
 }

@@ -1105,6 +1105,18 @@ size_t lrz_precode_ws(int dtype, int64_t B, int K, int N) {
   return bytes;
 }
 
+int lrz_w_dmma_direct(int dtype, int64_t B, int K, int N, const void *H, int64_t hs,
+                      const void *A_inv, int64_t ais, void *W, int64_t wstr, double *parts,
+                      cudaStream_t s);
+static int w_direct() {  // LRZ_W_DIRECT=0: the shared-memory tiled kernel (dmma_tiled.cu)
+  static int v = -1;
+  if (v < 0) {
+    const char *e = getenv("LRZ_W_DIRECT");
+    v = e ? atoi(e) : 1;
+  }
+  return v;
+}
+
 extern "C" int lrz_precode_rate(int dtype, int64_t B, int K, int N, const void *H,
                                 int64_t h_stride, const void *A_inv, int64_t ai_stride,
                                 double P_t, const double *noise, int64_t noise_div, void *W,
@@ -1154,6 +1166,12 @@ extern "C" int lrz_precode_rate(int dtype, int64_t B, int K, int N, const void *
                                          (c64 *)W + b0 * w_stride, parts + b0 * np_w, tc_ws, s))
             return rc;
         }
+      } else if (w_direct() && w_stride == int64_t(N) * K) {
+        // one warp per 32 x 32 block of W, fragments straight from global memory
+        np_w = ((N + 31) / 32) * ((K + 31) / 32);
+        if (int rc = lrz_w_dmma_direct(dtype, B, K, N, H, h_stride, A_inv, ai_stride, W, w_stride,
+                                       parts, s))
+          return rc;
       } else if (int rc = lrz_dmma_hn(dtype, B, N, K, K, H, h_stride, N, A_inv, ai_stride, W,
                                       w_stride, parts, s, nullptr, "dmma_hn_kernel:W")) {
         // FP64 tensor pipe, 64 x 64 output tiles, k streamed (dmma_tiled.cu):
