@@ -540,7 +540,7 @@ int lrz_precode_dmma32(int dtype, int64_t B, int K, int N, const void *H, int64_
 // norm partials per item.
 int lrz_w_dmma_direct(int dtype, int64_t B, int K, int N, const void *H, int64_t hs,
                       const void *A_inv, int64_t ais, void *W, int64_t wstr, double *parts,
-                      cudaStream_t s) {
+                      cudaStream_t s, const char *what) {
   const int nnb = (N + 31) / 32, njb = (K + 31) / 32, njq = (njb + 3) / 4;
   static int nbw = -1;
   if (nbw < 0) {
@@ -550,7 +550,7 @@ int lrz_w_dmma_direct(int dtype, int64_t B, int K, int N, const void *H, int64_t
   const int NB_ = nbw == 2 ? 2 : 1;
   const int64_t per = int64_t((nnb + NB_ - 1) / NB_) * njq;
   const int64_t chunk = (int64_t(1) << 30) / per;
-  LrzProf prof("w_dmma_direct_kernel", s);
+  LrzProf prof(what, s);
   for (int64_t b0 = 0; b0 < B; b0 += chunk) {
     const int64_t bb = B - b0 < chunk ? B - b0 : chunk;
     double *pp = parts ? parts + b0 * int64_t(nnb) * njb : nullptr;

@@ -1107,7 +1107,7 @@ size_t lrz_precode_ws(int dtype, int64_t B, int K, int N) {
 
 int lrz_w_dmma_direct(int dtype, int64_t B, int K, int N, const void *H, int64_t hs,
                       const void *A_inv, int64_t ais, void *W, int64_t wstr, double *parts,
-                      cudaStream_t s);
+                      cudaStream_t s, const char *what = "w_dmma_direct_kernel");
 static int w_direct() {  // LRZ_W_DIRECT=0: the shared-memory tiled kernel (dmma_tiled.cu)
   static int v = -1;
   if (v < 0) {
@@ -1178,9 +1178,14 @@ extern "C" int lrz_precode_rate(int dtype, int64_t B, int K, int N, const void *
         // W = H^H A^-1 with per-CTA norm partials, then the coupling G A^-1
         return rc;
       }
-      if (int rc = lrz_dmma_hn(LRZ_C128, B, K, K, K, G_true, int64_t(K) * K, K, A_inv,
-                               ai_stride, Gc, int64_t(K) * K, nullptr, s, nullptr,
-                               "dmma_hn_kernel:coupling"))
+      // the coupling G A^-1 = conj(G)^T A^-1 (G Hermitian): the same product with N = K
+      if (w_direct()) {
+        if (int rc = lrz_w_dmma_direct(LRZ_C128, B, K, K, G_true, int64_t(K) * K, A_inv,
+                                       ai_stride, Gc, int64_t(K) * K, nullptr, s, "coupling_dmma_direct"))
+          return rc;
+      } else if (int rc = lrz_dmma_hn(LRZ_C128, B, K, K, K, G_true, int64_t(K) * K, K, A_inv,
+                                      ai_stride, Gc, int64_t(K) * K, nullptr, s, nullptr,
+                                      "dmma_hn_kernel:coupling"))
         return rc;
       LrzProf prof("sinr_kernel", s);
       sinr_kernel<double><<<unsigned(B), 256, 0, s>>>(
