@@ -1,0 +1,5 @@
+mkdir -p gpurun_out
+timeout 2400 python -m pytest tests -m gpu -x -q --timeout=900 > gpurun_out/g63_tests.txt 2>&1; echo "tests rc=$?"; tail -4 gpurun_out/g63_tests.txt
+python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -2
+timeout 2400 python bench.py > gpurun_out/g63_bench.json 2> gpurun_out/g63_bench.err; echo "bench rc=$?"; tail -3 gpurun_out/g63_bench.err
+timeout 900 python bench.py --impl reference > gpurun_out/g63_ref.json 2> gpurun_out/g63_ref.err; echo "ref rc=$?"
