@@ -375,7 +375,9 @@ int lrz_sketch_dmma_large(int64_t B, int K, int Dtot, const void *dA, int64_t a_
     const char *e = getenv("LRZ_SKETCH_DIRECT");
     direct = e ? atoi(e) : 1;
   }
-  if (direct && a_stride == int64_t(K) * K) {
+  // (K >= 256 only: at K = 64 / 128 the short reduction does not amortise a 32 x 32
+  // register tile -- measured 2x slower than the tiled kernel at C3 / C4)
+  if (direct && K >= 256 && a_stride == int64_t(K) * K) {
     // dA Hermitian: dA Omega = conj(dA)^T Omega, one warp per 32 x 32 output block
     if (int rc = lrz_hn_dmma_direct(LRZ_C128, B, K, K, Dtot, dA, a_stride, Om, st, Y, st, nullptr,
                                     mask, s, "dmma_hn_kernel:sketch_Y"))
