@@ -219,15 +219,13 @@ __global__ void __launch_bounds__(32 * GD_WARPS)
 // ---------------------------------------------------------------------------
 template <typename T, int NBW>  // NBW n blocks per CTA (x 4 j blocks): 32 NBW x 128 of W
 __global__ void __launch_bounds__(128 * NBW)
-    w_dmma_direct_kernel(int64_t B, int K, int N, int J, const cplx<T> *__restrict__ H,
-                         int64_t hs, const c128 *__restrict__ Ainv, int64_t ais,
-                         cplx<T> *__restrict__ W, int64_t wstr, double *__restrict__ parts,
-                         const uint8_t *__restrict__ mask, int nnb, int njb, int njq) {
+    w_dmma_direct_kernel(int64_t B, int K, int N, const cplx<T> *__restrict__ H, int64_t hs,
+                         const c128 *__restrict__ Ainv, int64_t ais, cplx<T> *__restrict__ W,
+                         int64_t wstr, double *__restrict__ parts, int nnb, int njb, int njq) {
   const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3, w = threadIdx.x >> 5;
   const int nng = (nnb + NBW - 1) / NBW;
   const int64_t per = int64_t(nng) * njq;
   const int64_t item = blockIdx.x / per;
-  if (mask && !mask[item]) return;
   const int rem = int(blockIdx.x - item * per);
   const int nb = NBW * (rem / njq) + (w >> 2), jb0 = 4 * (rem % njq) + (w & 3);
   if (jb0 >= njb || nb >= nnb) return;
@@ -238,7 +236,7 @@ __global__ void __launch_bounds__(128 * NBW)
 #pragma unroll
   for (int b = 0; b < 4; ++b) {
     nok[b] = n0 + 8 * b + g < N;
-    jok[b] = j0 + 8 * b + g < J;
+    jok[b] = j0 + 8 * b + g < K;
   }
   double cr[16][2], ci[16][2];
 #pragma unroll
@@ -250,7 +248,7 @@ __global__ void __launch_bounds__(128 * NBW)
       const int k = k0 + 4 * s + t;
       const bool kok = k < K;
       const cplx<T> *hr = h + int64_t(kok ? k : 0) * N + n0 + g;
-      const c128 *yr = y + int64_t(kok ? k : 0) * J + j0 + g;
+      const c128 *yr = y + int64_t(kok ? k : 0) * K + j0 + g;
 #pragma unroll
       for (int b = 0; b < 4; ++b) {
         vx[b][s] = (kok && nok[b]) ? ldg_c(hr + 8 * b) : czero<double>();
@@ -282,9 +280,9 @@ __global__ void __launch_bounds__(128 * NBW)
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
         const int n = n0 + 8 * ib + g, j = j0 + 8 * jb + 2 * t + e;
-        if (n < N && j < J) {
+        if (n < N && j < K) {
           const cplx<T> z = mk<T>(T(cr[4 * ib + jb][e]), T(ci[4 * ib + jb][e]));
-          o[int64_t(n) * J + j] = z;
+          o[int64_t(n) * K + j] = z;
           nrm += double(z.re) * double(z.re) + double(z.im) * double(z.im);
         }
       }
@@ -538,13 +536,12 @@ int lrz_precode_dmma32(int dtype, int64_t B, int K, int N, const void *H, int64_
   return lrz_launch_status("precode_dmma32_kernel");
 }
 
-// out[n][j] = sum_k conj(X[k][n]) Y[k][j] by w_dmma_direct_kernel: X (K x N, of
-// dtype), Y (K x J, complex128), out (N x J, of dtype); parts (nullable):
-// ceil(N/32) ceil(J/32) norm partials per item; mask (nullable): active items.
-int lrz_hn_dmma_direct(int dtype, int64_t B, int K, int N, int J, const void *H, int64_t hs,
-                       const void *A_inv, int64_t ais, void *W, int64_t wstr, double *parts,
-                       const uint8_t *mask, cudaStream_t s, const char *what) {
-  const int nnb = (N + 31) / 32, njb = (J + 31) / 32, njq = (njb + 3) / 4;
+// W = H^H A^-1 by w_dmma_direct_kernel; parts (nullable): ceil(N/32) ceil(K/32)
+// norm partials per item.
+int lrz_w_dmma_direct(int dtype, int64_t B, int K, int N, const void *H, int64_t hs,
+                      const void *A_inv, int64_t ais, void *W, int64_t wstr, double *parts,
+                      cudaStream_t s, const char *what) {
+  const int nnb = (N + 31) / 32, njb = (K + 31) / 32, njq = (njb + 3) / 4;
   static int nbw = -1;
   if (nbw < 0) {
     const char *e = getenv("LRZ_W_NBW");
@@ -558,10 +555,9 @@ int lrz_hn_dmma_direct(int dtype, int64_t B, int K, int N, int J, const void *H,
     const int64_t bb = B - b0 < chunk ? B - b0 : chunk;
     double *pp = parts ? parts + b0 * int64_t(nnb) * njb : nullptr;
     auto go = [&](auto kern, auto hp, auto wp) {
-      kern<<<unsigned(bb * per), 128 * NB_, 0, s>>>(bb, K, N, J, hp + b0 * hs, hs,
+      kern<<<unsigned(bb * per), 128 * NB_, 0, s>>>(bb, K, N, hp + b0 * hs, hs,
                                                     (const c128 *)A_inv + b0 * ais, ais,
-                                                    wp + b0 * wstr, wstr, pp,
-                                                    mask ? mask + b0 : nullptr, nnb, njb, njq);
+                                                    wp + b0 * wstr, wstr, pp, nnb, njb, njq);
     };
     if (dtype == LRZ_C64) {
       if (NB_ == 2) go(w_dmma_direct_kernel<float, 2>, (const c64 *)H, (c64 *)W);
@@ -572,12 +568,4 @@ int lrz_hn_dmma_direct(int dtype, int64_t B, int K, int N, int J, const void *H,
     }
   }
   return lrz_launch_status("w_dmma_direct_kernel");
-}
-
-// W = H^H A^-1 (J = K)
-int lrz_w_dmma_direct(int dtype, int64_t B, int K, int N, const void *H, int64_t hs,
-                      const void *A_inv, int64_t ais, void *W, int64_t wstr, double *parts,
-                      cudaStream_t s, const char *what) {
-  return lrz_hn_dmma_direct(dtype, B, K, N, K, H, hs, A_inv, ais, W, wstr, parts, nullptr, s,
-                            what);
 }

@@ -312,10 +312,6 @@ int lrz_dmma_hn(int dtype, int64_t B, int NN, int J, int Kd, const void *X, int6
                                 (c128 *)out, os, parts, mask, s, what);
 }
 
-int lrz_hn_dmma_direct(int dtype, int64_t B, int K, int N, int J, const void *H, int64_t hs,
-                       const void *A_inv, int64_t ais, void *W, int64_t wstr, double *parts,
-                       const uint8_t *mask, cudaStream_t s, const char *what);
-
 // Omega_all [B][K][Dtot] (complex128) gathered from the normal window: column c
 // of block i (offset o_i, width d_i) is sqrt(1/2) (zre[k d_i + j] + i zim[k d_i + j])
 // at the item's cursor, blocks back to back in the stream (lowrank.py:284-286).
@@ -370,21 +366,6 @@ int lrz_sketch_dmma_large(int64_t B, int K, int Dtot, const void *dA, int64_t a_
   }
   if (int rc = lrz_launch_status("omega_gather_kernel")) return rc;
   const int64_t st = int64_t(K) * Dtot;
-  static int direct = -1;  // LRZ_SKETCH_DIRECT=0: the tiled kernel
-  if (direct < 0) {
-    const char *e = getenv("LRZ_SKETCH_DIRECT");
-    direct = e ? atoi(e) : 1;
-  }
-  // (K >= 256 only: at K = 64 / 128 the short reduction does not amortise a 32 x 32
-  // register tile -- measured 2x slower than the tiled kernel at C3 / C4)
-  if (direct && K >= 256 && a_stride == int64_t(K) * K) {
-    // dA Hermitian: dA Omega = conj(dA)^T Omega, one warp per 32 x 32 output block
-    if (int rc = lrz_hn_dmma_direct(LRZ_C128, B, K, K, Dtot, dA, a_stride, Om, st, Y, st, nullptr,
-                                    mask, s, "dmma_hn_kernel:sketch_Y"))
-      return rc;
-    return lrz_hn_dmma_direct(LRZ_C128, B, K, K, Dtot, dA, a_stride, Y, st, W, st, nullptr, mask,
-                              s, "dmma_hn_kernel:sketch_W");
-  }
   if (int rc = dmma_hn_launch<double>(B, K, Dtot, K, (const c128 *)dA, a_stride, K,
                                       (const c128 *)Om, st, (c128 *)Y, st, nullptr, mask, s,
                                       "dmma_hn_kernel:sketch_Y"))
