@@ -482,6 +482,14 @@ LRZ_DEV int cta_woodbury_dmma(int K, int r, const c128 *__restrict__ Ai, c128 *A
     for (int blk = wide ? wid : wid - 1; blk < KB * KB; blk += wide ? NW : NW - 1) {
       const int k0 = 8 * (blk / KB), m0 = 8 * (blk % KB);
       double cr[2] = {0.0, 0.0}, ci[2] = {0.0, 0.0};
+      // A's entries first: for K > 32 they come from global memory, and the load
+      // then overlaps the block's DMMAs instead of stalling the write-back
+      c128 x[2];
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int k = k0 + g, m = m0 + 2 * t + e;
+        x[e] = (k < K && m < K) ? A[k * K + m] : Z;
+      }
       blk_zmma(
           ksr,
           [&](int i, int j) {
@@ -492,10 +500,7 @@ LRZ_DEV int cta_woodbury_dmma(int K, int r, const c128 *__restrict__ Ai, c128 *A
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
         const int k = k0 + g, m = m0 + 2 * t + e;
-        if (k < K && m < K) {
-          c128 &x = A[k * K + m];
-          x = mk<double>(x.re + cr[e], x.im + ci[e]);
-        }
+        if (k < K && m < K) A[k * K + m] = mk<double>(x[e].re + cr[e], x[e].im + ci[e]);
       }
     }
   }
