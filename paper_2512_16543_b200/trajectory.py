@@ -200,9 +200,11 @@ class TrajectoryRunner:
         return dev_mask, int((~reset).sum())
 
     def _tail(self, G, Hf, noise, is_sketch, iters_pred, cursor, res, k_est, plan, hybrid,
-              keep_W):
+              keep_W, precode_stream=None):
         """Stages 4-7 of a chunk (dispatcher, batched full inversions, Woodbury
-        chain, precoder + rate) from the arSVD results."""
+        chain, precoder + rate) from the arSVD results.  precode_stream: stage 7
+        (the throughput-bound products W = H^H A^-1 and the coupling) is queued
+        on that stream behind an event; stages 4-6 stay on the current one."""
         c = self.cfg
         B, T, K = G.shape[0], G.shape[1], self.K
         BT, Nn, dev = B * T, Hf.shape[-1], self.device
@@ -237,6 +239,26 @@ class TrajectoryRunner:
         self._stage("chain", e0)
         # 7. precoder and rate
         e0 = self._ev()
+        ctx = _nullctx()
+        if precode_stream is not None:
+            ev = torch.cuda.Event()
+            ev.record(torch.cuda.current_stream(dev))
+            precode_stream.wait_event(ev)
+            used = [G, Hf, noise, A_inv_seq]
+            if hybrid is not None:
+                used.extend(v for v in hybrid.values() if isinstance(v, torch.Tensor))
+            for t_ in used:
+                t_.record_stream(precode_stream)
+            ctx = torch.cuda.stream(precode_stream)
+        with ctx:
+            pr, W = self._precode(G, Hf, noise, A_inv_seq, hybrid, keep_W, T)
+        self._stage("precode_rate", e0)
+        return A_inv_seq, method, info, pr, W, iters, consumed
+
+    def _precode(self, G, Hf, noise, A_inv_seq, hybrid, keep_W, T):
+        c = self.cfg
+        K, dev = self.K, self.device
+        BT, Nn = Hf.shape[0], Hf.shape[-1]
         if hybrid is not None:
             pr = ops.hybrid_precode_rate(Hf, A_inv_seq.reshape(BT, K, K),
                                          hybrid["H_rf"].reshape(BT, K, Nn),
@@ -250,8 +272,26 @@ class TrajectoryRunner:
                                   want_sinr=False,
                                   G_true=G.reshape(BT, K, K) if c.rate_via_gram else None,
                                   alpha=c.alpha)
-        self._stage("precode_rate", e0)
-        return A_inv_seq, method, info, pr, W, iters, consumed
+        return pr, W
+
+    def gram_async(self, H: torch.Tensor, heavy_stream):
+        """Stage 1 of a chunk (the true Grams) queued on ``heavy_stream`` behind
+        the current stream's work so far; returns (G, event) for
+        ``run_chunk(gram=...)``.  The pipelined caller issues chunk c + 1's Grams
+        before ``run_chunk`` of chunk c, so that they precede chunk c's precoder
+        on the heavy stream."""
+        B, T, K, Nn = H.shape
+        cur = torch.cuda.current_stream(self.device)
+        ev = torch.cuda.Event()
+        ev.record(cur)
+        heavy_stream.wait_event(ev)
+        H.record_stream(heavy_stream)
+        with torch.cuda.stream(heavy_stream):
+            G = ops.gram(H.reshape(B * T, K, Nn), self.cfg.alpha).reshape(B, T, K, K)
+            done = torch.cuda.Event()
+            done.record(heavy_stream)
+        G.record_stream(cur)
+        return G, done
 
     def _tail_on(self, stream, G, Hf, noise, is_sketch, *rest):
         """_tail on `stream` after the current stream's work so far; the
@@ -274,7 +314,8 @@ class TrajectoryRunner:
     # -- one chunk -------------------------------------------------------------
     def run_chunk(self, H: torch.Tensor, noise: torch.Tensor, omega: torch.Tensor | None = None,
                   keep_A_inv: bool = False, keep_W: bool = False, hybrid: dict | None = None,
-                  omega_ready=None, sync: bool = True, back_stream=None) -> ChunkResult:
+                  omega_ready=None, sync: bool = True, back_stream=None,
+                  heavy_stream=None, gram=None) -> ChunkResult:
         """H [B, T, K, N] (device, self.dtype); noise [B, K] float64 (device);
         omega [B, L] float64 (device; row b = trial b's next unconsumed normals,
         L >= T * normals_per_step_max()).
@@ -301,7 +342,18 @@ class TrajectoryRunner:
         throughput-bound products of chunk c + 1.  The next chunk's front
         stages depend only on this chunk's front stages (last Gram, sketch
         consumption), the chain only on the previous chain (same stream).
-        The caller joins ``back_stream`` before reading the results."""
+        The caller joins ``back_stream`` before reading the results.
+
+        heavy_stream (with sync=False; instead of back_stream): the two
+        throughput-bound stages -- the Grams (stage 1) and the precoder products
+        (stage 7), both at the FP64 tensor-pipe peak from K = 64 -- are queued on
+        that (low-priority) stream, everything between them (Gram corrections,
+        arSVD, inversions, chain: latency-bound launches) stays on the current
+        stream, which the caller gives the higher priority.  With
+        ``gram=self.gram_async(H_next, heavy_stream)`` issued before this call the
+        heavy stream runs  G(c+1) | W(c) | G(c+2) | W(c+1) ...  back to back while
+        the light stages of chunk c + 1 run beside W(c) on the SMs' spare
+        registers.  The caller joins ``heavy_stream`` before reading rates / W."""
         c = self.cfg
         B, T, K, Nn = H.shape
         assert (B, K, Nn) == (self.B, self.K, self.N) and H.dtype == self.dtype
@@ -310,9 +362,16 @@ class TrajectoryRunner:
         Hf = H.reshape(BT, K, Nn)
         is_sketch, n_sketch = self._is_sketch(T)
 
+        if heavy_stream is not None:
+            assert not sync and back_stream is None
         # 1. true Grams of every step
         e0 = self._ev()
-        G = ops.gram(Hf, c.alpha).reshape(B, T, K, K)
+        if heavy_stream is not None:
+            G, g_ready = gram if gram is not None else self.gram_async(H, heavy_stream)
+            assert G.shape == (B, T, K, K)
+            torch.cuda.current_stream(dev).wait_event(g_ready)
+        else:
+            G = ops.gram(Hf, c.alpha).reshape(B, T, K, K)
         self._stage("gram", e0)
         plan = torch.zeros(B, T, dtype=torch.uint8, device=dev)
         k_est = torch.zeros(B, T, dtype=torch.int32, device=dev)
@@ -438,7 +497,10 @@ class TrajectoryRunner:
             passes = 1
             # optimistic: the rest of the chunk is queued behind the first pass and
             # only then is the verifier's answer read back (one sync per chunk)
-            if back_stream is not None and not sync:
+            if heavy_stream is not None:
+                tail = self._tail(G, Hf, noise, is_sketch, iters_pred, cursor, res, k_est, plan,
+                                  hybrid, keep_W, precode_stream=heavy_stream)
+            elif back_stream is not None and not sync:
                 # this chunk's sketch consumption, on the front stream (the next
                 # chunk's window advance must not wait for the back stages)
                 front_consumed = cursor[:, -1] + \
@@ -478,6 +540,9 @@ class TrajectoryRunner:
                                       plan, hybrid, keep_W)
                 if passes > n_spec:
                     self._in_order = True   # iteration counts track the sketch: skip speculation
+        elif heavy_stream is not None:
+            tail = self._tail(G, Hf, noise, is_sketch, None, None, None, k_est, plan, hybrid,
+                              keep_W, precode_stream=heavy_stream)
         elif back_stream is not None and not sync:
             tail = self._tail_on(back_stream, G, Hf, noise, is_sketch, None, None, None, k_est,
                                  plan, hybrid, keep_W)
@@ -492,6 +557,10 @@ class TrajectoryRunner:
         bs = back_stream if (back_stream is not None and not sync) else None
         with torch.cuda.stream(bs) if bs is not None else _nullctx():
             self.A_inv = A_inv_seq[:, -1].clone()
+        if heavy_stream is not None:
+            bs = heavy_stream     # the precoder's status is produced there
+            info.record_stream(heavy_stream)
+        with torch.cuda.stream(bs) if bs is not None else _nullctx():
             # status per step: the inverse's code (singular / indefinite) wins over the
             # precoder's (zero norm), so a singular step is never hidden by a later code
             pinfo = pr["info"].reshape(B, T)
