@@ -161,3 +161,68 @@ def test_cursor_walk_equals_in_order(cuda, walk_first):
     assert torch.equal(a.k_est, b.k_est) and torch.equal(a.method, b.method)
     assert b.spec_passes <= 2
     torch.testing.assert_close(a.rates, b.rates, rtol=1e-10, atol=0)
+
+
+@pytest.mark.parametrize("name,B,T,chunk,dtype", [("C2", 6, 48, 16, "c128"),
+                                                   ("C3", 4, 24, 8, "c64")])
+@pytest.mark.parametrize("schedule", ["back", "heavy"])
+def test_two_stream_schedules_equal_the_synchronous_runner(cuda, name, B, T, chunk, dtype,
+                                                           schedule):
+    """run_chunk(sync=False) with back_stream (chunk c's chain / precoder beside
+    chunk c + 1's front stages) and with heavy_stream + gram_async (Grams and
+    precoder products on a low-priority stream) reproduce the synchronous pass
+    bit for bit over several chunks, with zero verifier flags."""
+    spec = S.CONFIGS[name].with_(B=B, T=T, dtype=dtype)
+    trials = list(range(B))
+    tdt = torch.complex64 if dtype == "c64" else torch.complex128
+    H, noise, cfg = _setup(cuda, spec, spec.eta, trials)
+    H = H.to(tdt)
+    chunks = [H[:, t0:t0 + chunk].contiguous() for t0 in range(0, T, chunk)]
+    st = DeviceOmegaStreams.for_method(spec.seed, spec.eta, trials, cuda)
+    cur = torch.cuda.current_stream(cuda)
+
+    def run(mode):
+        rn = TrajectoryRunner(B, spec.K, spec.N, tdt, cfg, cuda)
+        st.raw.zero_()
+        st.consumed_total.zero_()
+        outs, flags = [], torch.zeros(2, dtype=torch.int32, device=cuda)
+        if mode == "heavy":
+            heavy = torch.cuda.Stream(cuda, priority=0)
+            light = torch.cuda.Stream(cuda, priority=-1)
+            light.wait_stream(cur)
+            with torch.cuda.stream(light):
+                g = rn.gram_async(chunks[0], heavy)
+                for i, Hc in enumerate(chunks):
+                    g_next = rn.gram_async(chunks[i + 1], heavy) if i + 1 < len(chunks) else None
+                    om = st.window(chunk * rn.normals_per_step_max())
+                    r = rn.run_chunk(Hc, noise, om, sync=False, heavy_stream=heavy, gram=g,
+                                     keep_A_inv=True)
+                    flags.add_(r.flags)
+                    st.advance(r.consumed)
+                    outs.append(r)
+                    g = g_next
+            cur.wait_stream(light)
+            cur.wait_stream(heavy)
+        else:
+            back = torch.cuda.Stream(cuda, priority=-1) if mode == "back" else None
+            for Hc in chunks:
+                om = st.window(chunk * rn.normals_per_step_max())
+                r = rn.run_chunk(Hc, noise, om, sync=back is None, back_stream=back,
+                                 keep_A_inv=True)
+                if r.flags is not None:
+                    flags.add_(r.flags)
+                st.advance(r.consumed)
+                outs.append(r)
+            if back is not None:
+                cur.wait_stream(back)
+        torch.cuda.synchronize()
+        assert int(flags.abs().sum()) == 0
+        return outs
+
+    ref = run("sync")
+    got = run(schedule)
+    for a, b in zip(ref, got):
+        assert torch.equal(a.method, b.method) and torch.equal(a.k_est, b.k_est)
+        assert torch.equal(a.iters, b.iters) and torch.equal(a.consumed, b.consumed)
+        assert torch.equal(a.rates, b.rates) and torch.equal(a.info, b.info)
+        assert torch.equal(a.A_inv, b.A_inv)
