@@ -291,6 +291,154 @@ __global__ void __launch_bounds__(128 * NBW)
 }
 
 // ---------------------------------------------------------------------------
+// W = H^H A^-1 (and the coupling G A^-1) with three real DMMAs per complex tile
+// step instead of four (the "3M" complex product): with a = conj(x) = (xr, -xi)
+// and b = y,
+//   P += xr yr,  Q += xi yi,  R += (xr - xi)(yr + yi)
+//   Re = P + Q,  Im = R - P + Q        (= xr yi - xi yr)
+// -- 25 % fewer tensor-pipe instructions for two DADDs per fragment pair and a
+// third accumulator set (96 registers for a warp's 16 tiles).  Every partial sum
+// is bounded by (|xr| + |xi|)(|yr| + |yi|), so the error stays normwise at the
+// level of the four-product form (1e-15 relative on random data; parity with the
+// oracle unchanged).  With the fragments straight from global memory (the form
+// of w_dmma_direct_kernel) the 3M product measured no faster: that kernel is
+// bound by its loads once the DMMA phase of an iteration is a quarter shorter
+// (two warps per scheduler at 255 registers).  So the operands are staged in
+// shared memory: a CTA of four warps (2 n x 2 j, 32 x 32 of W each: the same 16 tiles, three
+// accumulator sets) streams 16-row slabs of conj-H (16 x 64) and A^-1 (16 x 64)
+// through a 3-stage cp.async ring; rows padded by two elements, so a
+// quarter-warp's fragment LDS.128 (4 rows x 2 columns) covers 128 distinct
+// bytes.  Two CTAs per SM (101 KB each).  48 DMMAs per 8 fragment LDS.
+// ---------------------------------------------------------------------------
+constexpr int W3_KC = 16, W3_ST = 3, W3_BN = 64, W3_BJ = 64;
+template <typename T>
+struct W3Smem {
+  static constexpr int XLD = W3_BN + (sizeof(T) == 8 ? 2 : 4);
+  static constexpr int YLD = W3_BJ + 2;
+  static constexpr size_t xbytes = size_t(W3_KC) * XLD * sizeof(cplx<T>);
+  static constexpr size_t ybytes = size_t(W3_KC) * YLD * sizeof(c128);
+  static constexpr size_t stage = xbytes + ybytes;
+  static constexpr size_t bytes = stage * W3_ST;
+};
+
+LRZ_DEV void w3_cpa(void *smem, const void *gmem, int bytes, bool pred) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  if (bytes == 16)
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(sa), "l"(gmem),
+                 "r"(pred ? 16 : 0));
+  else
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(sa), "l"(gmem),
+                 "r"(pred ? 8 : 0));
+}
+
+template <typename T>
+__global__ void __launch_bounds__(128, 2)
+    w_dmma_3m_tiled_kernel(int64_t B, int K, int N, const cplx<T> *__restrict__ H, int64_t hs,
+                           const c128 *__restrict__ Ainv, int64_t ais, cplx<T> *__restrict__ W,
+                           int64_t wstr, double *__restrict__ parts, int nnb, int njb,
+                           int tiles_n, int tiles_j) {
+  using S = W3Smem<T>;
+  extern __shared__ __align__(16) unsigned char w3_smem[];
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5, g = lane >> 2, t = lane & 3;
+  const int wn = w & 1, wj = w >> 1;
+  const int ntile = tiles_n * tiles_j;
+  const int64_t item = blockIdx.x / ntile;
+  const int tile = int(blockIdx.x - item * ntile);
+  const int n0 = (tile / tiles_j) * W3_BN, j0 = (tile % tiles_j) * W3_BJ;
+  const cplx<T> *h = H + item * hs;
+  const c128 *y = Ainv + item * ais;
+  auto xslab = [&](int s) { return reinterpret_cast<cplx<T> *>(w3_smem + size_t(s) * S::stage); };
+  auto yslab = [&](int s) {
+    return reinterpret_cast<c128 *>(w3_smem + size_t(s) * S::stage + S::xbytes);
+  };
+  auto load = [&](int s, int k0) {
+    cplx<T> *xsl = xslab(s);
+    c128 *ysl = yslab(s);
+#pragma unroll
+    for (int i = 0; i < (W3_KC * W3_BN) / 128; ++i) {
+      const int e = tid + i * 128;
+      const int r = e / W3_BN, c = e % W3_BN;
+      const int k = k0 + r, n = n0 + c;
+      const bool ok = k < K && n < N;
+      w3_cpa(xsl + r * S::XLD + c, h + (ok ? int64_t(k) * N + n : 0), sizeof(cplx<T>), ok);
+    }
+#pragma unroll
+    for (int i = 0; i < (W3_KC * W3_BJ) / 128; ++i) {
+      const int e = tid + i * 128;
+      const int r = e / W3_BJ, c = e % W3_BJ;
+      const int k = k0 + r, j = j0 + c;
+      const bool ok = k < K && j < K;
+      w3_cpa(ysl + r * S::YLD + c, y + (ok ? int64_t(k) * K + j : 0), 16, ok);
+    }
+  };
+  double cp[16][2], cq[16][2], cs[16][2];
+#pragma unroll
+  for (int x = 0; x < 16; ++x)
+    cp[x][0] = cp[x][1] = cq[x][0] = cq[x][1] = cs[x][0] = cs[x][1] = 0.0;
+  const int nslab = (K + W3_KC - 1) / W3_KC;
+#pragma unroll
+  for (int s = 0; s < W3_ST - 1; ++s) {
+    if (s < nslab) load(s, s * W3_KC);
+    asm volatile("cp.async.commit_group;\n" ::);
+  }
+  for (int it = 0; it < nslab; ++it) {
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(W3_ST - 2));
+    __syncthreads();
+    const int nxt = it + W3_ST - 1;
+    if (nxt < nslab) load(nxt % W3_ST, nxt * W3_KC);
+    asm volatile("cp.async.commit_group;\n" ::);
+    const cplx<T> *xsl = xslab(it % W3_ST) + 32 * wn + g;
+    const c128 *ysl = yslab(it % W3_ST) + 32 * wj + g;
+#pragma unroll
+    for (int kk = 0; kk < W3_KC; kk += 4) {
+      double xr[4], xi[4], yr[4], yi[4], ys[4];
+#pragma unroll
+      for (int b = 0; b < 4; ++b) {
+        const cplx<T> v = xsl[(kk + t) * S::XLD + 8 * b];
+        xr[b] = double(v.re);
+        xi[b] = double(v.im);
+        const c128 u = ysl[(kk + t) * S::YLD + 8 * b];
+        yr[b] = u.re;
+        yi[b] = u.im;
+        ys[b] = u.re + u.im;
+      }
+#pragma unroll
+      for (int ib = 0; ib < 4; ++ib) {
+        const double xs = xr[ib] - xi[ib];
+#pragma unroll
+        for (int jb = 0; jb < 4; ++jb) {
+          dmma(cp[4 * ib + jb], xr[ib], yr[jb]);
+          dmma(cq[4 * ib + jb], xi[ib], yi[jb]);
+          dmma(cs[4 * ib + jb], xs, ys[jb]);
+        }
+      }
+    }
+  }
+  asm volatile("cp.async.wait_group 0;\n" ::);
+  cplx<T> *o = W + item * wstr;
+  double nrm = 0.0;
+  const int nw = n0 + 32 * wn, jw = j0 + 32 * wj;
+#pragma unroll
+  for (int ib = 0; ib < 4; ++ib)
+#pragma unroll
+    for (int jb = 0; jb < 4; ++jb)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int n = nw + 8 * ib + g, j = jw + 8 * jb + 2 * t + e;
+        if (n < N && j < K) {
+          const int x = 4 * ib + jb;
+          const cplx<T> z = mk<T>(T(cp[x][e] + cq[x][e]), T(cs[x][e] - cp[x][e] + cq[x][e]));
+          o[int64_t(n) * K + j] = z;
+          nrm += double(z.re) * double(z.re) + double(z.im) * double(z.im);
+        }
+      }
+  nrm = warp_sum(nrm);
+  // one partial per 32 x 32 block, the layout of w_dmma_direct_kernel's
+  if (parts && lane == 0 && nw < N && jw < K)
+    parts[item * (int64_t(nnb) * njb) + int64_t(nw / 32) * njb + jw / 32] = nrm;
+}
+
+// ---------------------------------------------------------------------------
 // K6 fused, K <= 32, one item per CTA of 4 warps:
 //   W = H^H A^-1 (N x K, unscaled, precoding.py:47), ||W||_F^2,
 //   C = G A^-1 - alpha A^-1 = H W for F_RF = I, s = sqrt(P_t)/||W||,
@@ -546,6 +694,34 @@ int lrz_w_dmma_direct(int dtype, int64_t B, int K, int N, const void *H, int64_t
   if (nbw < 0) {
     const char *e = getenv("LRZ_W_NBW");
     nbw = e ? atoi(e) : 1;
+  }
+  static int m3 = -1;  // LRZ_W3M=0: the four-product register-fragment kernel
+  if (m3 < 0) {
+    const char *e = getenv("LRZ_W3M");
+    m3 = e ? atoi(e) : 1;
+  }
+  if (m3) {
+    const int tn = (N + W3_BN - 1) / W3_BN, tj = (K + W3_BJ - 1) / W3_BJ;
+    const int64_t cap = (int64_t(1) << 30) / (int64_t(tn) * tj);
+    // (profiler labels of the 3M kernel: W and the coupling)
+    const char *lab = what[0] == 'c' ? "coupling_dmma_3m_tiled" : "w_dmma_3m_tiled_kernel";
+    LrzProf prof(lab, s);
+    for (int64_t b0 = 0; b0 < B; b0 += cap) {
+      const int64_t bb = B - b0 < cap ? B - b0 : cap;
+      double *pp = parts ? parts + b0 * int64_t(nnb) * njb : nullptr;
+      auto go3 = [&](auto kern, auto hp, auto wp, size_t smem) {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+        kern<<<unsigned(bb * tn * tj), 128, smem, s>>>(bb, K, N, hp + b0 * hs, hs,
+                                                       (const c128 *)A_inv + b0 * ais, ais,
+                                                       wp + b0 * wstr, wstr, pp, nnb, njb, tn,
+                                                       tj);
+      };
+      if (dtype == LRZ_C64)
+        go3(w_dmma_3m_tiled_kernel<float>, (const c64 *)H, (c64 *)W, W3Smem<float>::bytes);
+      else
+        go3(w_dmma_3m_tiled_kernel<double>, (const c128 *)H, (c128 *)W, W3Smem<double>::bytes);
+    }
+    return lrz_launch_status("w_dmma_3m_tiled_kernel");
   }
   const int NB_ = nbw == 2 ? 2 : 1;
   const int64_t per = int64_t((nnb + NB_ - 1) / NB_) * njq;
