@@ -438,6 +438,8 @@ def kernel_model(name: str, spec, items: int, D: int, Dtot: int, r_mean: float,
     if name == "gram_dmma_off_kernel":             # K > 32: every lower 32 x 32 block
         # algorithmic Hermitian count 4 K (K + 1) N (executed: nb (nb + 1) / 2 full blocks)
         return 4 * K * (K + 1) * N * items, (K * N * c + K * K * 16) * items
+    if name == "gram_dmma_3m_tiled_kernel":        # 3M product: 3 K (K + 1) N executed flops
+        return 3 * K * (K + 1) * N * items, (K * N * c + K * K * 16) * items
     if name in ("dmma_hn_kernel:sketch_Y", "dmma_hn_kernel:sketch_W"):
         return 8 * K * K * Dtot * items, (K * K * 16 + 2 * K * Dtot * 16) * items
     if name == "sketch_dmma_kernel":               # Y = dA Omega and W = dA Y, K <= 32
@@ -674,14 +676,16 @@ def run_b200(args):
                 row["bytes_per_launch"] = b_
                 if "3m_tiled" in name:
                     # against SURVEY 8(d)'s four-product count (complex MAC = 8 flops)
-                    f4 = f + 2 * sp.K * sp.K * (sp.N if name.startswith("w_") else sp.K) \
-                        * items_per_pass / per_pass
+                    extra = {"w_dmma_3m_tiled_kernel": 2 * sp.K * sp.K * sp.N,
+                             "coupling_dmma_3m_tiled": 2 * sp.K ** 3,
+                             "gram_dmma_3m_tiled_kernel": sp.K * (sp.K + 1) * sp.N}[name]
+                    f4 = f + extra * items_per_pass / per_pass
                     row["four_product_equivalent"] = {
                         "flops_per_launch": f4, "achieved": f4 / t / 1e12,
                         "frac": f4 / t / 1e12 / fpk,
                         "note": "3M complex product: 3 real DMMA products per complex one; "
                                 "`achieved` counts the executed flops, this entry SURVEY "
-                                "8(d)'s 8 K^2 N"}
+                                "8(d)'s count (complex MAC = 8 flops)"}
             rows[name] = row
         return dict(sorted(rows.items(), key=lambda kv: -kv[1]["ms_total_per_step"]))
 

@@ -321,16 +321,6 @@ struct W3Smem {
   static constexpr size_t bytes = stage * W3_ST;
 };
 
-LRZ_DEV void w3_cpa(void *smem, const void *gmem, int bytes, bool pred) {
-  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
-  if (bytes == 16)
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(sa), "l"(gmem),
-                 "r"(pred ? 16 : 0));
-  else
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(sa), "l"(gmem),
-                 "r"(pred ? 8 : 0));
-}
-
 template <typename T>
 __global__ void __launch_bounds__(128, 2)
     w_dmma_3m_tiled_kernel(int64_t B, int K, int N, const cplx<T> *__restrict__ H, int64_t hs,
@@ -351,24 +341,37 @@ __global__ void __launch_bounds__(128, 2)
   auto yslab = [&](int s) {
     return reinterpret_cast<c128 *>(w3_smem + size_t(s) * S::stage + S::xbytes);
   };
+  // slab loads: thread tid copies element (row r0 + 2 i, column c0) of both slabs,
+  // i = 0 .. 7 -- one global pointer per operand advanced by a constant, one
+  // shared-memory offset, the column bounds decided once
+  const int r0 = tid >> 6, c0 = tid & 63;
+  const bool xok = n0 + c0 < N, yok = j0 + c0 < K;
+  const cplx<T> *xg = h + int64_t(r0) * N + (xok ? n0 + c0 : 0);
+  const c128 *yg = y + int64_t(r0) * K + (yok ? j0 + c0 : 0);
+  const int64_t xstep = int64_t(2) * N, ystep = int64_t(2) * K;
+  const unsigned xso = unsigned(r0 * S::XLD + c0) * unsigned(sizeof(cplx<T>));
+  const unsigned yso = unsigned(S::xbytes) + unsigned(r0 * S::YLD + c0) * 16u;
+  const unsigned smem0 = (unsigned)__cvta_generic_to_shared(w3_smem);
   auto load = [&](int s, int k0) {
-    cplx<T> *xsl = xslab(s);
-    c128 *ysl = yslab(s);
+    const unsigned sb = smem0 + unsigned(s) * unsigned(S::stage);
+    const cplx<T> *xp = xg + int64_t(k0) * N;
+    const c128 *yp = yg + int64_t(k0) * K;
 #pragma unroll
-    for (int i = 0; i < (W3_KC * W3_BN) / 128; ++i) {
-      const int e = tid + i * 128;
-      const int r = e / W3_BN, c = e % W3_BN;
-      const int k = k0 + r, n = n0 + c;
-      const bool ok = k < K && n < N;
-      w3_cpa(xsl + r * S::XLD + c, h + (ok ? int64_t(k) * N + n : 0), sizeof(cplx<T>), ok);
-    }
-#pragma unroll
-    for (int i = 0; i < (W3_KC * W3_BJ) / 128; ++i) {
-      const int e = tid + i * 128;
-      const int r = e / W3_BJ, c = e % W3_BJ;
-      const int k = k0 + r, j = j0 + c;
-      const bool ok = k < K && j < K;
-      w3_cpa(ysl + r * S::YLD + c, y + (ok ? int64_t(k) * K + j : 0), 16, ok);
+    for (int i = 0; i < W3_KC / 2; ++i) {
+      const bool kok = k0 + r0 + 2 * i < K;
+      const bool px = kok && xok, py = kok && yok;
+      const unsigned xd = sb + xso + unsigned(2 * i * S::XLD) * unsigned(sizeof(cplx<T>));
+      const unsigned yd = sb + yso + unsigned(2 * i * S::YLD) * 16u;
+      const void *xs_ = px ? (const void *)(xp + i * xstep) : (const void *)h;
+      const void *ys_ = py ? (const void *)(yp + i * ystep) : (const void *)y;
+      if (sizeof(cplx<T>) == 16)
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(xd), "l"(xs_),
+                     "r"(px ? 16 : 0));
+      else
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(xd), "l"(xs_),
+                     "r"(px ? 8 : 0));
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(yd), "l"(ys_),
+                   "r"(py ? 16 : 0));
     }
   };
   double cp[16][2], cq[16][2], cs[16][2];
@@ -436,6 +439,199 @@ __global__ void __launch_bounds__(128, 2)
   // one partial per 32 x 32 block, the layout of w_dmma_direct_kernel's
   if (parts && lane == 0 && nw < N && jw < K)
     parts[item * (int64_t(nnb) * njb) + int64_t(nw / 32) * njb + jw / 32] = nrm;
+}
+
+// ---------------------------------------------------------------------------
+// Gram, K > 32, on the same 3M product and slab ring: A = H H^H + alpha I by
+// 64 x 64 tiles of the lower triangle, a CTA of four warps each.  With
+// a = h_i = (ar, ai) and b = conj(h_j) = (br, -bi):
+//   P += ar br,  Q += ai bi,  R += (ar + ai)(br - bi),  Re = P + Q,  Im = R - P + Q.
+// Slabs are 16 antennas x 64 rows of H, transposed on the way into shared memory
+// (a thread copies 16-byte pieces of 16 consecutive antennas of a row: 256-byte
+// global segments).  Off-diagonal tiles: warp (wn, wj) owns a 32 x 32 block, 16
+// tiles.  Diagonal tiles need the 36 8 x 8 tiles on or below the diagonal of
+// their 8 x 8 tile grid: warp w takes tile rows w and 7 - w (9 tiles each), so
+// the four warps finish together and no tile above the diagonal is computed.
+// ---------------------------------------------------------------------------
+template <typename T, int ROLE>  // ROLE 0..3: warp of a diagonal tile, 4: off-diagonal
+LRZ_DEV void gram3_body(int K, int N, const cplx<T> *__restrict__ h, c128 *__restrict__ a,
+                        int i0, int j0, double alpha, unsigned char *smem) {
+  using S = W3Smem<T>;
+  constexpr bool DIAG = ROLE < 4;
+  constexpr int NT = DIAG ? 9 : 16;
+  constexpr int RA = ROLE, RB = 7 - ROLE;  // the diagonal warp's two tile rows
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5, g = lane >> 2, t = lane & 3;
+  const int wn = w & 1, wj = w >> 1;
+  // slab loads: thread tid copies antenna r0 of rows c0 + 8 i, i = 0 .. 7.  Eight
+  // consecutive threads take 4 antennas x 2 rows: 64-byte global pieces, and in
+  // shared memory (row stride 66 elements) eight distinct 16-byte bank groups
+  const int r0 = (tid & 3) | (((tid >> 3) & 3) << 2), c0 = ((tid >> 2) & 1) | ((tid >> 5) << 1);
+  const cplx<T> *xg = h + int64_t(i0 + c0) * N + r0;
+  const cplx<T> *yg = h + int64_t(j0 + c0) * N + r0;
+  const int64_t rstep = int64_t(8) * N;
+  const unsigned xso = unsigned(r0 * S::XLD + c0) * unsigned(sizeof(cplx<T>));
+  // the Y slab holds H elements as well (XLD layout); a diagonal tile reads its X slab
+  const unsigned yso = unsigned(S::xbytes) + xso;
+  const unsigned smem0 = (unsigned)__cvta_generic_to_shared(smem);
+  auto load = [&](int s, int n0) {
+    const unsigned sb = smem0 + unsigned(s) * unsigned(S::stage);
+    const bool nok = n0 + r0 < N;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const bool px = nok && i0 + c0 + 8 * i < K;
+      const void *xs_ = px ? (const void *)(xg + n0 + i * rstep) : (const void *)h;
+      const unsigned xd = sb + xso + unsigned(8 * i) * unsigned(sizeof(cplx<T>));
+      if (sizeof(cplx<T>) == 16)
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(xd), "l"(xs_),
+                     "r"(px ? 16 : 0));
+      else
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(xd), "l"(xs_),
+                     "r"(px ? 8 : 0));
+      if (!DIAG) {
+        const bool py = nok && j0 + c0 + 8 * i < K;
+        const void *ys_ = py ? (const void *)(yg + n0 + i * rstep) : (const void *)h;
+        const unsigned yd = sb + yso + unsigned(8 * i) * unsigned(sizeof(cplx<T>));
+        if (sizeof(cplx<T>) == 16)
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(yd), "l"(ys_),
+                       "r"(py ? 16 : 0));
+        else
+          asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(yd), "l"(ys_),
+                       "r"(py ? 8 : 0));
+      }
+    }
+  };
+  double cp[NT][2], cq[NT][2], cs[NT][2];
+#pragma unroll
+  for (int x = 0; x < NT; ++x)
+    cp[x][0] = cp[x][1] = cq[x][0] = cq[x][1] = cs[x][0] = cs[x][1] = 0.0;
+  const int nslab = (N + W3_KC - 1) / W3_KC;
+#pragma unroll
+  for (int s = 0; s < W3_ST - 1; ++s) {
+    if (s < nslab) load(s, s * W3_KC);
+    asm volatile("cp.async.commit_group;\n" ::);
+  }
+  for (int it = 0; it < nslab; ++it) {
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(W3_ST - 2));
+    __syncthreads();
+    const int nxt = it + W3_ST - 1;
+    if (nxt < nslab) load(nxt % W3_ST, nxt * W3_KC);
+    asm volatile("cp.async.commit_group;\n" ::);
+    const cplx<T> *xsl =
+        reinterpret_cast<const cplx<T> *>(smem + size_t(it % W3_ST) * S::stage) + g;
+    const cplx<T> *ysl = DIAG ? xsl
+                              : reinterpret_cast<const cplx<T> *>(
+                                    smem + size_t(it % W3_ST) * S::stage + S::xbytes) + g;
+#pragma unroll
+    for (int kk = 0; kk < W3_KC; kk += 4) {
+      if (DIAG) {
+        double br[RB + 1], bi[RB + 1], bd[RB + 1];
+#pragma unroll
+        for (int b = 0; b <= RB; ++b) {
+          const cplx<T> u = ysl[(kk + t) * S::XLD + 8 * b];
+          br[b] = double(u.re);
+          bi[b] = double(u.im);
+          bd[b] = br[b] - bi[b];
+        }
+        // tile rows RA (tiles 0 .. RA) and RB (tiles RA + 1 .. 8): the A fragments are
+        // the B fragments of the same rows
+        {
+          const double ar = br[RA], ai = bi[RA], as_ = ar + ai;
+#pragma unroll
+          for (int jb = 0; jb <= RA; ++jb) {
+            dmma(cp[jb], ar, br[jb]);
+            dmma(cq[jb], ai, bi[jb]);
+            dmma(cs[jb], as_, bd[jb]);
+          }
+        }
+        {
+          const double ar = br[RB], ai = bi[RB], as_ = ar + ai;
+#pragma unroll
+          for (int jb = 0; jb <= RB; ++jb) {
+            dmma(cp[RA + 1 + jb], ar, br[jb]);
+            dmma(cq[RA + 1 + jb], ai, bi[jb]);
+            dmma(cs[RA + 1 + jb], as_, bd[jb]);
+          }
+        }
+      } else {
+        double ar[4], ai[4], br[4], bi[4], bd[4];
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+          const cplx<T> v = xsl[(kk + t) * S::XLD + 32 * wn + 8 * b];
+          ar[b] = double(v.re);
+          ai[b] = double(v.im);
+          const cplx<T> u = ysl[(kk + t) * S::XLD + 32 * wj + 8 * b];
+          br[b] = double(u.re);
+          bi[b] = double(u.im);
+          bd[b] = br[b] - bi[b];
+        }
+#pragma unroll
+        for (int ib = 0; ib < 4; ++ib) {
+          const double as_ = ar[ib] + ai[ib];
+#pragma unroll
+          for (int jb = 0; jb < 4; ++jb) {
+            dmma(cp[4 * ib + jb], ar[ib], br[jb]);
+            dmma(cq[4 * ib + jb], ai[ib], bi[jb]);
+            dmma(cs[4 * ib + jb], as_, bd[jb]);
+          }
+        }
+      }
+    }
+  }
+  asm volatile("cp.async.wait_group 0;\n" ::);
+  // write-back: the lower element and its mirrored conjugate (exactly Hermitian),
+  // real diagonal + alpha (lowrank.py:160-162)
+  auto put = [&](int row, int col, double re, double im) {
+    if (row < K && col < K && col <= row) {
+      if (row == col) {
+        a[int64_t(row) * K + col] = mk<double>(re + alpha, 0.0);
+      } else {
+        a[int64_t(row) * K + col] = mk<double>(re, im);
+        a[int64_t(col) * K + row] = mk<double>(re, -im);
+      }
+    }
+  };
+#pragma unroll
+  for (int x = 0; x < NT; ++x) {
+    int tr, tc;  // tile coordinates in the 64 x 64 tile's 8 x 8 grid
+    if (DIAG) {
+      tr = x <= RA ? RA : RB;
+      tc = x <= RA ? x : x - RA - 1;
+    } else {
+      tr = 4 * wn + x / 4;
+      tc = 4 * wj + x % 4;
+    }
+#pragma unroll
+    for (int e = 0; e < 2; ++e)
+      put(i0 + 8 * tr + g, j0 + 8 * tc + 2 * t + e, cp[x][e] + cq[x][e],
+          cs[x][e] - cp[x][e] + cq[x][e]);
+  }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(128, 2)
+    gram_dmma_3m_tiled_kernel(int64_t B, int K, int N, const cplx<T> *__restrict__ H, int64_t hs,
+                              c128 *__restrict__ A, int64_t as, int npair, double alpha) {
+  extern __shared__ __align__(16) unsigned char g3_smem[];
+  const int64_t item = blockIdx.x / npair;
+  // the diagonal tiles (the shorter CTAs) last: pairs in row order, J <= I
+  int p = int(blockIdx.x - item * npair), I = 0;
+  while (p > I) {
+    p -= I + 1;
+    ++I;
+  }
+  const int J = p;
+  const cplx<T> *h = H + item * hs;
+  c128 *a = A + item * as;
+  if (I != J) {
+    gram3_body<T, 4>(K, N, h, a, 64 * I, 64 * J, alpha, g3_smem);
+    return;
+  }
+  switch (threadIdx.x >> 5) {
+    case 0: gram3_body<T, 0>(K, N, h, a, 64 * I, 64 * I, alpha, g3_smem); break;
+    case 1: gram3_body<T, 1>(K, N, h, a, 64 * I, 64 * I, alpha, g3_smem); break;
+    case 2: gram3_body<T, 2>(K, N, h, a, 64 * I, 64 * I, alpha, g3_smem); break;
+    default: gram3_body<T, 3>(K, N, h, a, 64 * I, 64 * I, alpha, g3_smem); break;
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -630,6 +826,29 @@ static void gram_dmma_launch(int64_t B, int K, int N, const cplx<T> *h, int64_t 
     if (split < 0) {
       const char *e = getenv("LRZ_GRAM_DIAG");
       split = e ? atoi(e) : 1;
+    }
+    // complex64 H: the 3M tiled kernel (K = 64 .. 256: 23 - 28 % faster than the
+    // register-fragment kernels below, e.g. C5 c64 23.9 -> 17.2 ms per 640 items);
+    // complex128 H: the register-fragment kernels stay ahead (21.3 vs 21.7 ms at C5,
+    // 5.4 vs 5.8 at K = 128).  LRZ_GRAM3M = 0 / 1 forces one of them
+    static int g3 = -1;
+    if (g3 < 0) {
+      const char *e = getenv("LRZ_GRAM3M");
+      g3 = e ? atoi(e) : 2;
+    }
+    if (g3 == 1 || (g3 == 2 && sizeof(T) == 4)) {
+      const int nt = (K + 63) / 64, npair = nt * (nt + 1) / 2;
+      const size_t smem = W3Smem<T>::bytes;
+      cudaFuncSetAttribute(gram_dmma_3m_tiled_kernel<T>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+      LrzProf prof_g("gram_dmma_3m_tiled_kernel", s);
+      const int64_t cap = (int64_t(1) << 30) / npair;
+      for (int64_t b0 = 0; b0 < B; b0 += cap) {
+        const int64_t bb = B - b0 < cap ? B - b0 : cap;
+        gram_dmma_3m_tiled_kernel<T><<<unsigned(bb * npair), 128, smem, s>>>(
+            bb, K, N, h + b0 * hs, hs, a + b0 * as, as, npair, alpha);
+      }
+      return;
     }
     LrzProf prof_o("gram_dmma_off_kernel", s);
     if (split) {

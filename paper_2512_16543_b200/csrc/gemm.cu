@@ -1110,6 +1110,14 @@ int lrz_w_dmma_direct(int dtype, int64_t B, int K, int N, const void *H, int64_t
                       cudaStream_t s, const char *what = "w_dmma_direct_kernel");
 // (used for K >= 256: with a short reduction the 32 x 32 register tile's prologue and
 // epilogue dominate -- the coupling at K = 128 measured 11.5 -> 14 ms per 20,480 items)
+static int w_kmin() {  // smallest K of the direct / 3M kernels (LRZ_W_KMIN)
+  static int v = -1;
+  if (v < 0) {
+    const char *e = getenv("LRZ_W_KMIN");
+    v = e ? atoi(e) : 33;  // the 3M tiled kernel measured faster from K = 64 (dmma.cu)
+  }
+  return v;
+}
 static int w_direct() {  // LRZ_W_DIRECT=0: the shared-memory tiled kernel (dmma_tiled.cu)
   static int v = -1;
   if (v < 0) {
@@ -1168,7 +1176,7 @@ extern "C" int lrz_precode_rate(int dtype, int64_t B, int K, int N, const void *
                                          (c64 *)W + b0 * w_stride, parts + b0 * np_w, tc_ws, s))
             return rc;
         }
-      } else if (w_direct() && K >= 256 && w_stride == int64_t(N) * K) {
+      } else if (w_direct() && K >= w_kmin() && w_stride == int64_t(N) * K) {
         // one warp per 32 x 32 block of W, fragments straight from global memory
         np_w = ((N + 31) / 32) * ((K + 31) / 32);
         if (int rc = lrz_w_dmma_direct(dtype, B, K, N, H, h_stride, A_inv, ai_stride, W, w_stride,
@@ -1181,7 +1189,7 @@ extern "C" int lrz_precode_rate(int dtype, int64_t B, int K, int N, const void *
         return rc;
       }
       // the coupling G A^-1 = conj(G)^T A^-1 (G Hermitian): the same product with N = K
-      if (w_direct() && K >= 256) {
+      if (w_direct() && K >= w_kmin()) {
         if (int rc = lrz_w_dmma_direct(LRZ_C128, B, K, K, G_true, int64_t(K) * K, A_inv,
                                        ai_stride, Gc, int64_t(K) * K, nullptr, s, "coupling_dmma_direct"))
           return rc;
