@@ -81,6 +81,37 @@ def test_fused_precoder_vs_reference_formulas(cuda, K, N, dtype):
         assert np.allclose(pr["sinr"][b].cpu().numpy(), sinr, rtol=rtol, atol=0)
 
 
+@pytest.mark.parametrize("K,N", [(40, 100), (64, 200), (100, 500), (160, 520), (256, 320)])
+@pytest.mark.parametrize("dtype", [np.complex64, np.complex128])
+def test_large_K_precoder_ragged_shapes(cuda, K, N, dtype):
+    """K > 32: W = H^H A^-1 (3M tiled DMMA kernel at complex128, tcgen05 at
+    complex64), the coupling G A^-1 (3M tiled at both dtypes), norm and rates at
+    shapes that are not multiples of the 64 x 64 tile or the 16-row slab."""
+    rng = np.random.default_rng(7 * K + N)
+    B, alpha = 5, K / 10.0
+    H = crandn(rng, B, K, N).astype(dtype)
+    Hd = H.astype(np.complex128)
+    G = Hd @ Hd.conj().transpose(0, 2, 1) + alpha * np.eye(K)
+    Ainv = np.linalg.inv(G)
+    noise = np.full((B, K), 0.1)
+    Ht = torch.from_numpy(H).to(cuda)
+    W = torch.empty(B, N, K, dtype=Ht.dtype, device=cuda)
+    pr = ops.precode_rate(Ht, torch.from_numpy(Ainv).to(cuda), 1.0,
+                          torch.from_numpy(noise).to(cuda), 1, W=W,
+                          G_true=torch.from_numpy(G).to(cuda), alpha=alpha)
+    wtol, rtol = (1e-12, 1e-10) if dtype == np.complex128 else (2e-5, 1e-4)
+    for b in range(B):
+        F_raw = Hd[b].conj().T @ Ainv[b]                     # precoding.py:47
+        s = 1.0 / np.linalg.norm(F_raw, "fro")               # precoding.py:48-51
+        P = np.abs(Hd[b] @ (s * F_raw)) ** 2                 # precoding.py:74
+        sig = np.diag(P)
+        rates = np.log2(1.0 + sig / (P.sum(axis=1) - sig + noise[b]))
+        assert np.linalg.norm(W[b].cpu().numpy() - F_raw) / np.linalg.norm(F_raw) < wtol
+        assert abs(pr["scale"][b].item() - s) / s < rtol
+        assert np.allclose(pr["rates"][b].cpu().numpy(), rates, rtol=rtol, atol=rtol)
+        assert np.allclose(pr["sum"][b].item(), rates.sum(), rtol=rtol, atol=0)
+
+
 @pytest.mark.parametrize("K,D", [(48, 9), (64, 21), (128, 13)])
 def test_chain_steps_equals_per_trial_chain(cuda, K, D):
     rng = np.random.default_rng(K)
