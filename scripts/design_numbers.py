@@ -7,18 +7,18 @@ e = d["e2e"]
 st = d["stages_ms_per_step"]
 print("  | Measurement | B200 | CPU port (%d cores, %s) |" % (cpu["cores"], cpu.get("cpu_model", "?")))
 print("  |---|---|---|")
-print("  | C5 c128 WB-arSVD (headline) | **%s updates/s** (%.3f s/step; round 1: 3,933 incl. channels) | %.0f updates/s |"
+print("  | C5 c128 WB-arSVD (headline) | **%s updates/s** (%.3f s/step; round 1: 3,933 incl. channels; start of this session: 7,885) | %.0f updates/s |"
       % (f"{d['value']:,.0f}", d["ms_per_step"] / 1e3, cpu["value"]))
 print("  | C5 c128 full inversion | %s updates/s | — |" % f"{d['full_inverse']['value']:,.0f}")
 print("  | C5 c128 e2e (pinned host H, %d trials × 100 steps, H2D overlapped) | %s updates/s (PCIe: %.0f GB H2D per step) | — |"
       % (e["trials_per_gpu"], f"{e['value']:,.0f}", e["h2d_bytes_per_step"] / 1e9))
-print("  | dominant kernel | %s: %.1f %s = **%.2f of FP64 peak**, DRAM %.2f GB/launch vs %.2f GB algorithmic | — |"
-      % (r["kernel"], r["achieved"], r["unit"], r["frac"], (r.get("traffic") or 0) / 1e9,
-         r["algorithmic"]["bytes_per_launch"] / 1e9))
+fp = r.get("four_product_equivalent")
+print("  | dominant kernel | %s: %.1f %s executed = **%.2f of FP64 peak**%s, DRAM %.2f GB/launch vs %.2f GB algorithmic | — |"
+      % (r["kernel"], r["achieved"], r["unit"], r["frac"],
+         (" (%.1f TFLOP/s = %.2f of it in SURVEY 8(d)'s four-product flops)" % (fp["achieved"], fp["frac"])) if fp else "",
+         (r.get("traffic") or 0) / 1e9, r["algorithmic"]["bytes_per_launch"] / 1e9))
 print()
-print("  Per-config keys (runner time; channels synthesised on the device between")
-print("  chunks; dominant-kernel roofline from an unpipelined pass; CPU port):")
-print()
+
 print("  | Config | WB updates/s | Full updates/s | Dominant kernel (frac) | CPU |")
 print("  |---|---|---|---|---|")
 def fmt(v):
