@@ -430,6 +430,7 @@ def kernel_model(name: str, spec, items: int, D: int, Dtot: int, r_mean: float,
     if name in ("dmma_hn_kernel:coupling", "coupling_dmma_direct"):   # (G - alpha I) A^-1, SURVEY A.6
         return 8 * K ** 3 * items, 3 * K * K * 16 * items
     if name == "precode_dmma32_kernel":            # W + norm + coupling + SINR fused
+        # (SURVEY 8(d)'s four-product count; the W slabs execute 6 K^2 N on the 3M product)
         return ((8 * K * K * N + 8 * N * K + 8 * K ** 3 + 8 * K * K) * items,
                 (K * N * c + N * K * c + 2 * K * K * 16) * items)
     if name == "gram_dmma_kernel":                 # diagonal 32-row blocks (lower incl. diag)
