@@ -430,8 +430,8 @@ def kernel_model(name: str, spec, items: int, D: int, Dtot: int, r_mean: float,
     if name in ("dmma_hn_kernel:coupling", "coupling_dmma_direct"):   # (G - alpha I) A^-1, SURVEY A.6
         return 8 * K ** 3 * items, 3 * K * K * 16 * items
     if name == "precode_dmma32_kernel":            # W + norm + coupling + SINR fused
-        # (SURVEY 8(d)'s four-product count; the W slabs execute 6 K^2 N on the 3M product)
-        return ((8 * K * K * N + 8 * N * K + 8 * K ** 3 + 8 * K * K) * items,
+        # (executed flops: the W slabs run the 3M product, 6 K^2 N for SURVEY 8(d)'s 8 K^2 N)
+        return ((6 * K * K * N + 8 * N * K + 8 * K ** 3 + 8 * K * K) * items,
                 (K * N * c + N * K * c + 2 * K * K * 16) * items)
     if name == "gram_dmma_kernel":                 # diagonal 32-row blocks (lower incl. diag)
         kd = min(K, 32)
@@ -675,9 +675,10 @@ def run_b200(args):
                 row["frac"] = row["achieved"] / row["peak"]
                 row["flops_per_launch"] = f
                 row["bytes_per_launch"] = b_
-                if "3m_tiled" in name:
+                if "3m_tiled" in name or name == "precode_dmma32_kernel":
                     # against SURVEY 8(d)'s four-product count (complex MAC = 8 flops)
                     extra = {"w_dmma_3m_tiled_kernel": 2 * sp.K * sp.K * sp.N,
+                             "precode_dmma32_kernel": 2 * sp.K * sp.K * sp.N,
                              "coupling_dmma_3m_tiled": 2 * sp.K ** 3,
                              "gram_dmma_3m_tiled_kernel": sp.K * (sp.K + 1) * sp.N}[name]
                     f4 = f + extra * items_per_pass / per_pass
