@@ -605,8 +605,9 @@ def run_b200(args):
             # one pass each is a noisy comparison)
             if best_ms is None or tried[str(mode)] < 0.97 * best_ms:
                 best, best_ms = mode, tried[str(mode)]
-        ops._WS.clear()          # per-stream scratch of the schedules not kept
-        torch.cuda.empty_cache()
+        if len(modes) > 1:
+            ops._WS.clear()      # per-stream scratch of the schedules not kept
+            torch.cuda.empty_cache()
         return best, tried
 
     def summarize(outs):
@@ -876,9 +877,9 @@ def run_b200(args):
         cores = _cores()
         runs = [
             ("C1_c128", "C1", {}, [spec_eta_default, None], 2),
-            ("C2_c128", "C2", {}, [spec_eta_default, None], 3),
-            ("C2_c128_eta0.9", "C2", {}, [0.9], 3),      # chunk 100: cross-chunk pipelining
-            ("C2_c64", "C2", {"dtype": "c64"}, [spec_eta_default, None], 3),
+            ("C2_c128", "C2", {}, [spec_eta_default, None], 5),
+            ("C2_c128_eta0.9", "C2", {}, [0.9], 5),      # chunk 100: cross-chunk pipelining
+            ("C2_c64", "C2", {"dtype": "c64"}, [spec_eta_default, None], 5),
             ("C3_c64", "C3", {}, [spec_eta_default, None], 1),
             ("C5_c64", "C5", {"dtype": "c64"}, [spec_eta_default, None], 1),
         ]
@@ -1033,7 +1034,11 @@ def run_config(sp, etas, reps, rank, world, dev, one_pass, summarize, roofline_t
             torch.cuda.synchronize(dev)
         run = lambda: one_pass(sp, e, Hsrc, streams, noise, ch,  # noqa: E731
                                on_chunk=None if pipelined else mark, pipelined=pipelined)
+        # warm-up: two passes for the short ones (the caching allocator settles its
+        # cross-stream reuse only on the second pipelined pass)
         run()
+        if min((v for v in tried.values() if v), default=1e9) < 500.0:
+            run()
         torch.cuda.synchronize(dev)
         evs.clear()
         ops.prof_enable(True, dev)
